@@ -1,0 +1,166 @@
+/*
+ * dice_b200.h — C ABI of the B200-native DICE expert-parallel MoE sampling path.
+ *
+ * The reference (dicesim, /root/reference/pkg/src/dicesim) has no FFI: its
+ * boundary is the set of module-level Python functions the schedule engine
+ * imports (schedules.py:35-39, oracle.py:27-31). Each entry point below is the
+ * device replacement for one of those functions; the Python package
+ * paper_2411_16786_b200 binds them with ctypes and keeps the reference names
+ * and signatures.
+ *
+ * Conventions
+ *  - All pointers are caller-owned DEVICE pointers unless noted; no entry
+ *    point allocates device memory or synchronises the host.
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered.
+ *  - Feature dims are padded: hp = round_up(hidden_dim, 64), ep =
+ *    round_up(expert_dim, 64); padded columns are zero and stay zero.
+ *  - bf16 = IEEE bfloat16 bits (uint16), f32 = float, ids = int32.
+ *  - Return 0 on success, else a DICE_ERR_* code that the Python layer maps
+ *    1:1 onto the reference exception types (errors.py:4-29).
+ *  - Non-finite values never return an error synchronously: kernels record
+ *    the first offending step in a device `status` word (int32[4], see
+ *    dice_status_reset) that the host reads once per run, raising
+ *    NumericalDivergenceError(step) (schedules.py:445-449, 459-469).
+ */
+#ifndef DICE_B200_H_
+#define DICE_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DICE_OK 0
+#define DICE_ERR_CONTRACT 1   /* ContractError      (errors.py:12-13) */
+#define DICE_ERR_CONFIG 2     /* ConfigurationError (errors.py:8-9)   */
+#define DICE_ERR_NUMERICS 3   /* NumericsError      (errors.py:16-17) */
+#define DICE_ERR_CUDA 4       /* CUDA launch / driver failure          */
+
+/* Cond-comm strategies (policies.py:29-33). */
+#define DICE_COND_OFF 0
+#define DICE_COND_LOW_SCORE 1
+#define DICE_COND_HIGH_SCORE 2
+#define DICE_COND_RANDOM 3
+
+/* GEMM epilogues. */
+#define DICE_EPI_STORE_BF16 0
+#define DICE_EPI_GELU_BF16 1
+#define DICE_EPI_STORE_F32 2
+#define DICE_EPI_GELU_RESID 3
+#define DICE_EPI_CONSUME 4
+
+/* Library version / build identification (sm_100a). */
+int dice_version(void);
+
+/* status[0] = first step with a non-finite value (INT32_MAX if none),
+ * status[1] = layer of the first non-finite gate input, status[2..3] reserved. */
+int dice_status_reset(int32_t* status, void* stream);
+
+/* splitmix64 stream -> uniform[-a, a) values, bit-exact in fp64.
+ * Replaces splitmix64 + bits_to_uniform + init_model/sample_x0 consumption
+ * order (model.py:28-36, 47-50, 133-162, 181-186). Element (r, c) of the
+ * logical row-major [rows, cols] matrix is stream output start + r*cols + c.
+ * transpose=0 writes out[r*ld + c]; transpose=1 writes out[c*ld + r].
+ * out_dtype: 0 = f64, 1 = f32, 2 = bf16 (bf16 = RN(RN_f32(value))). */
+int dice_splitmix_fill(uint64_t seed, uint64_t start, int64_t rows, int64_t cols,
+                       double halfwidth, int transpose, int out_dtype, void* out,
+                       int64_t ld, void* stream);
+
+/* Raw splitmix64 outputs start..start+count-1 (model.py:28-36). */
+int dice_splitmix_bits(uint64_t seed, uint64_t start, int64_t count, uint64_t* out,
+                       void* stream);
+
+/* Fused gate: logits = u[:, :h] @ w_gate, softmax over E, stable top-k on
+ * scores (ties -> lower id), renormalised gates (model.py:209-223).
+ * u: f32 [n, hp]; w_gate_t: f32 [E, hp] (transposed W_gate); ids: int32 [n, k];
+ * gates: f32 [n, k]; scores: f32 [n, E] or NULL. Non-finite u records
+ * (step, layer) into status (model.py:212-213). */
+int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                   int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                   int layer, void* stream);
+
+/* Conditional-communication decision for one layer (TokenCache.decide,
+ * policies.py:159-186 with reduced_slots 118-139, random_keep_slots 107-115).
+ * State (this layer): last_refresh int32 [n] (init -1e9), primed uint8 [n],
+ * reduced uint8 [n, k], cached_ids int32 [n, k] (read only when strict).
+ * random_key = mix64(mix64(mix64(seed ^ TAG) + layer) + step), computed by
+ * the caller (policies.py:113-114). Outputs active / write uint8 [n, k]. */
+int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force,
+                     int refresh_interval, int strategy, int strict, uint64_t random_key,
+                     int32_t* last_refresh, uint8_t* primed, uint8_t* reduced,
+                     const int32_t* cached_ids, uint8_t* active, uint8_t* write,
+                     void* stream);
+
+/* Token permute (block prefix-sum) for routed_rows' (slot, expert) grouping
+ * (model.py:255-276) and the all-to-all byte plan (cluster.py:82-109).
+ * Pairs (t, s) with active[t, s] (active NULL = all) are assigned rows of the
+ * expert-sorted, 128-row-padded buffer: pos[t, s] = row or -1.
+ * tile_offsets: int32 [E+1] m-tile prefix per expert (device-resident; feeds
+ * the grouped GEMM with no host sync). counters: int64 [2] accumulated
+ * {active pairs, active pairs whose expert lives off the token's home device}
+ * under placement expert_dev = e / (E/D), home = ((row0+t)*D)/R_total.
+ * Also gathers x_perm[pos] = u16[t] (bf16 [max_rows, hp]). */
+int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
+                       const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows,
+                       int32_t* pos, int32_t* tile_offsets, int64_t* counters,
+                       int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
+                       void* stream);
+
+/* Upper bound of rows of the padded permuted buffer for n*k pairs over E experts. */
+int64_t dice_permute_max_rows(int64_t n, int k, int E);
+
+/* int32 words of scratch dice_route_permute needs; scratch[0] must be zero
+ * when first used (the kernel leaves it zero). */
+int64_t dice_permute_scratch_ints(int64_t n, int k, int E);
+
+/* Grouped expert FFN on the permuted rows (expert_forward, model.py:226-232):
+ * hbuf = gelu(x_perm @ W1_e) (bf16 [max_rows, ep]); y = hbuf @ W2_e (bf16 [max_rows, hp]).
+ * w1_t: bf16 [E*ep, hp] (per expert W1^T); w2_t: bf16 [E*hp, ep] (per expert W2^T).
+ * tcgen05/TMEM/TMA grouped GEMM, tile -> expert from tile_offsets. */
+int dice_grouped_ffn(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
+                     const uint16_t* w2_t, int E, int hp, int ep, const int32_t* tile_offsets,
+                     uint16_t* hbuf, uint16_t* y, void* stream);
+
+/* Stale-activation cache merge + weighted routed sum (TokenCache.assemble,
+ * policies.py:188-208; combine_outputs' routed part, model.py:295-298).
+ * For each token t: routed[t] = sum_s g_s * row_s (slots left to right, f32)
+ * where active pairs take row y[pos[t,s]] and gate gates[t,s], inactive pairs
+ * take the cached row/gate. Pairs with write[t,s] store their fresh row/gate/id
+ * into the cache. cache_* may be NULL (cond-comm off). rows_out (f32 [k, n, hp])
+ * and gates_out (f32 [n, k]) are optional (functional API). */
+int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* active,
+                        const uint8_t* write, const float* gates, const int32_t* ids,
+                        int64_t n, int k, int hp, uint16_t* cache_rows, float* cache_gates,
+                        int32_t* cache_ids, float* routed, float* rows_out, float* gates_out,
+                        void* stream);
+
+/* Dense bf16 GEMM C[M, N] = A[M, K] @ B[N, K]^T with a fused epilogue (see
+ * DICE_EPI_*): local_block (model.py:244-252) = GELU_RESID with residual h;
+ * shared_forward GEMM1 (model.py:235-241) = GELU_BF16 with the S experts
+ * concatenated on N, GEMM2 = STORE_F32 or CONSUME (u + (shared + routed)). */
+int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
+              float* out_f32, int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16,
+              const float* residual, int64_t ld_res, const float* addend, int64_t ld_add,
+              void* stream);
+
+/* out[t] = base[t] + sum_s gates[t, s] * rows[s, t] (f32, combine_outputs
+ * model.py:279-298 and the consume residual, schedules.py:317). rows f32
+ * [k, n, hp]; base f32 [n, hp]; optional residual adds u first:
+ * out = residual + (base + sum). */
+int dice_combine(const float* base, const float* rows, const float* gates, const float* residual,
+                 int64_t n, int k, int hp, float* out, uint16_t* out_bf16, void* stream);
+
+/* x_{s+1} = x_s - eta * y (model.py:301-305), f32 in place, plus its bf16 copy;
+ * records `step` into status on a non-finite result (schedules.py:447-449). */
+int dice_denoise(float* x, uint16_t* x16, const float* y, float eta, int64_t n, int hp,
+                 int32_t* status, int step, void* stream);
+
+/* f32 [n, ld_in] (first `cols` columns) -> bf16 [n, hp] and f32 [n, hp] padded copies. */
+int dice_pack_rows(const float* in, int64_t n, int cols, int64_t ld_in, int hp, float* out32,
+                   uint16_t* out16, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DICE_B200_H_ */

@@ -1,0 +1,363 @@
+// Warp-specialised tcgen05 GEMM for sm_100a: C[M,N] = A[M,K] * B[N,K]^T
+// (both operands K-major bf16, fp32 accumulation in TMEM), persistent over
+// 128 x BN output tiles, TMA-fed multi-stage smem ring, double-buffered TMEM
+// accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
+//
+// One kernel serves every dense contraction of the MoE layer:
+//   * grouped expert FFN (expert_forward, model.py:226-232): rows of A are the
+//     expert-sorted token rows padded per expert to 128-row tiles; B is the
+//     stacked per-expert weight [G*N, K]; a device-resident tile->expert prefix
+//     (group_tile_offsets) selects the B block per tile, so no host sync.
+//   * shared FFN (shared_forward, model.py:235-241) with the S shared experts
+//     concatenated along N (GEMM1) / K (GEMM2).
+//   * mixing block (local_block, model.py:244-252).
+// Epilogues fuse exact-erf GELU, the residual add of local_block, and the
+// consume step u + (shared + routed) (schedules.py:308-317, model.py:279-298).
+#include "dice_gemm.h"
+#include "dice_ptx.cuh"
+
+#include <mutex>
+#include <unordered_map>
+
+namespace dice {
+
+constexpr int BM = 128;
+constexpr int BK = 64;       // 64 bf16 = 128 B = one swizzle row
+constexpr int UMMA_K = 16;
+constexpr int kThreads = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN == 256 ? 4 : (BN == 192 ? 5 : 6);
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  // two accumulator buffers; allocation is a power of two >= 32 columns
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/;
+};
+
+struct __align__(8) GemmShared {
+  uint64_t full[8];
+  uint64_t empty[8];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  int m_tiles;
+  int group_off[kMaxGroups + 1];
+};
+
+__device__ __forceinline__ int find_group(const int* off, int groups, int m_tile) {
+  int g = 0;
+  while (g + 1 < groups && off[g + 1] <= m_tile) ++g;
+  return g;
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, int row, int col, uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+  }
+  if constexpr (EPI == EPI_GELU_RESID) {
+    const float4* res = reinterpret_cast<const float4*>(a.residual + (int64_t)row * a.ld_res + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 t = res[q];
+      v[4 * q + 0] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
+    }
+  }
+  if constexpr (EPI == EPI_CONSUME) {
+    const float4* res = reinterpret_cast<const float4*>(a.residual + (int64_t)row * a.ld_res + col);
+    const float4* add = reinterpret_cast<const float4*>(a.addend + (int64_t)row * a.ld_add + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 t = res[q], s = add[q];
+      v[4 * q + 0] = t.x + (v[4 * q + 0] + s.x);
+      v[4 * q + 1] = t.y + (v[4 * q + 1] + s.y);
+      v[4 * q + 2] = t.z + (v[4 * q + 2] + s.z);
+      v[4 * q + 3] = t.w + (v[4 * q + 3] + s.w);
+    }
+  }
+  if (a.out_f32 != nullptr) {
+    float4* dst = reinterpret_cast<float4*>(a.out_f32 + (int64_t)row * a.ld_f32 + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+  if (a.out_bf16 != nullptr) {
+    uint4* dst = reinterpret_cast<uint4*>(a.out_bf16 + (int64_t)row * a.ld_bf16 + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * q + 2 * p], v[8 * q + 2 * p + 1]);
+        w[p] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const GemmArgs args) {
+  using C = GemmCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + C::kStages * C::kABytes;
+  GemmShared* sh = reinterpret_cast<GemmShared*>(smem + C::kStages * C::kStageBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) { mbar_init(&sh->full[s], 1); mbar_init(&sh->empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 8); }
+    fence_barrier_init();
+    if (args.group_tile_offsets != nullptr) {
+      for (int g = 0; g <= args.num_groups; ++g) sh->group_off[g] = args.group_tile_offsets[g];
+      sh->m_tiles = sh->group_off[args.num_groups];
+    } else {
+      sh->group_off[0] = 0;
+      sh->group_off[1] = args.num_m_tiles;
+      sh->m_tiles = args.num_m_tiles;
+    }
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(&sh->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const uint32_t tmem_base = sh->tmem_base;
+  const int m_tiles = sh->m_tiles;
+  const int groups = args.group_tile_offsets != nullptr ? args.num_groups : 1;
+  const int n_blocks = args.num_n_blocks;
+  const int k_blocks = args.num_k_blocks;
+  const int num_tiles = m_tiles * n_blocks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_tile = tile % m_tiles;
+        const int n_blk = tile / m_tiles;
+        const int g = find_group(sh->group_off, groups, m_tile);
+        const int a_row = m_tile * BM;
+        const int b_row = g * args.N + n_blk * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&sh->empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&sh->full[stage], C::kStageBytes);
+          tma_load_2d(smA + stage * C::kABytes, &tmA, &sh->full[stage], kb * BK, a_row);
+          tma_load_2d(smB + stage * C::kBBytes, &tmB, &sh->full[stage], kb * BK, b_row);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&sh->full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smA + stage * C::kABytes);
+          const uint32_t b_base = smem_u32(smB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t ad = umma_desc_sw128(a_base + k * UMMA_K * 2);
+            const uint64_t bd = umma_desc_sw128(b_base + k * UMMA_K * 2);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&sh->empty[stage]);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&sh->tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // --------------------------------------------------------------- epilogue
+    const int sub = warp & 3;            // TMEM lane quadrant this warp may access
+    const int half = (warp - 4) >> 2;    // which half of the BN columns
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int m_tile = tile % m_tiles;
+      const int n_blk = tile / m_tiles;
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&sh->tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_tile * BM + sub * 32 + lane;
+      const bool row_ok = args.group_tile_offsets != nullptr || row < args.M_valid;
+#pragma unroll 1
+      for (int c = 0; c < BN / 2; c += 32) {
+        const int col_in_tile = half * (BN / 2) + c;
+        const int col = n_blk * BN + col_in_tile;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN + col_in_tile, r);
+        tmem_ld_wait();
+        if (row_ok && col < args.N) epilogue_chunk<EPI>(args, row, col, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh->tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------- host
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr; int64_t rows, cols; int box_rows;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<const void*>()(k.ptr) ^ (std::hash<int64_t>()(k.rows) * 31) ^
+           (std::hash<int64_t>()(k.cols) * 131) ^ (size_t)k.box_rows;
+  }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// Row-major bf16 [rows, cols] with a (BK x box_rows) box and 128-byte swizzle.
+int tensor_map(const void* ptr, int64_t rows, int64_t cols, int box_rows, CUtensorMap* out) {
+  MapKey key{ptr, rows, cols, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) { *out = it->second; return 0; }
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return DICE_ERR_CUDA;
+  if ((cols * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(ptr) & 15) != 0) return DICE_ERR_CONTRACT;
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return DICE_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = m;
+  *out = m;
+  return 0;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <int BN, int EPI>
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
+           cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmemBytes) != cudaSuccess)
+      return DICE_ERR_CUDA;
+    attr_done = true;
+  }
+  int grid = max_tiles < num_sms() ? max_tiles : num_sms();
+  if (grid <= 0) return 0;
+  gemm_bf16_tcgen05<BN, EPI><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, a);
+  return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
+}
+
+template <int BN>
+int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                 int max_tiles, cudaStream_t s) {
+  switch (epi) {
+    case EPI_STORE_BF16: return launch<BN, EPI_STORE_BF16>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_BF16: return launch<BN, EPI_GELU_BF16>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_F32: return launch<BN, EPI_STORE_F32>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID: return launch<BN, EPI_GELU_RESID>(ta, tb, a, max_tiles, s);
+    case EPI_CONSUME: return launch<BN, EPI_CONSUME>(ta, tb, a, max_tiles, s);
+    default: return DICE_ERR_CONTRACT;
+  }
+}
+
+}  // namespace
+
+int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
+  if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
+  if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
+  const int bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
+  CUtensorMap ta, tb;
+  int rc = tensor_map(p.A, p.A_rows, p.K, BM, &ta);
+  if (rc) return rc;
+  rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, bn, &tb);
+  if (rc) return rc;
+  GemmArgs a = p.epi;
+  a.M_valid = p.M;
+  a.N = p.N;
+  a.K = p.K;
+  a.num_n_blocks = (p.N + bn - 1) / bn;
+  a.num_k_blocks = (p.K + BK - 1) / BK;
+  a.group_tile_offsets = p.group_tile_offsets;
+  a.num_groups = p.num_groups;
+  a.num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + BM - 1) / BM;
+  const int max_tiles = a.num_m_tiles * a.num_n_blocks;
+  if (max_tiles == 0) return 0;
+  if (bn == 256) return dispatch_epi<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
+  if (bn == 192) return dispatch_epi<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
+  return dispatch_epi<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
+}
+
+}  // namespace dice

@@ -1,0 +1,54 @@
+// Internal GEMM interface shared by the C-ABI layer and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/dice_b200.h"
+
+namespace dice {
+
+constexpr int kMaxGroups = 64;
+
+enum EpiKind : int {
+  EPI_STORE_BF16 = 0,  // out_bf16 = acc
+  EPI_GELU_BF16 = 1,   // out_bf16 = gelu(acc)
+  EPI_STORE_F32 = 2,   // out_f32 = acc (and out_bf16 if set)
+  EPI_GELU_RESID = 3,  // v = gelu(acc) + residual -> out_f32, out_bf16   (local_block)
+  EPI_CONSUME = 4,     // v = residual + (acc + addend) -> out_f32, out_bf16 (consume)
+};
+
+struct GemmArgs {
+  int M_valid;
+  int N;
+  int K;
+  int num_n_blocks;
+  int num_k_blocks;
+  int num_m_tiles;
+  const int* group_tile_offsets;
+  int num_groups;
+  __nv_bfloat16* out_bf16;
+  int64_t ld_bf16;
+  float* out_f32;
+  int64_t ld_f32;
+  const float* residual;
+  int64_t ld_res;
+  const float* addend;
+  int64_t ld_add;
+};
+
+struct GemmProblem {
+  const void* A;          // bf16 [A_rows, K] row-major
+  int64_t A_rows;
+  const void* B;          // bf16 [num_groups * N, K] row-major
+  int M, N, K;
+  int num_groups;
+  const int* group_tile_offsets;  // device [num_groups+1] m-tile prefix; null => dense
+  int max_m_tiles;                // grouped: upper bound of total m tiles
+  int epi_kind;
+  GemmArgs epi;                   // only the output/residual fields are read
+};
+
+int gemm_bf16(const GemmProblem& p, cudaStream_t stream);
+
+}  // namespace dice

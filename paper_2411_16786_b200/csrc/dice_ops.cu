@@ -1,0 +1,655 @@
+// Memory-bound kernels of the DICE MoE layer (sm_100a) and the C-ABI entry
+// points declared in include/dice_b200.h. The dense contractions live in
+// dice_gemm.cu (tcgen05 / TMEM / TMA).
+#include <climits>
+#include <cstdint>
+
+#include "dice_gemm.h"
+#include "dice_ptx.cuh"
+
+namespace dice {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;  // model.py:17
+constexpr uint64_t kMul1 = 0xBF58476D1CE4E5B9ull;   // model.py:18
+constexpr uint64_t kMul2 = 0x94D049BB133111EBull;   // model.py:19
+
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t counter) {
+  uint64_t z = seed + counter * kGamma;
+  z = (z ^ (z >> 30)) * kMul1;
+  z = (z ^ (z >> 27)) * kMul2;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ void record_nonfinite(int32_t* status, int step, int layer) {
+  if (status == nullptr) return;
+  const int prev = atomicMin(&status[0], step);
+  if (prev > step) atomicExch(&status[1], layer);
+}
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
+  return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+// ------------------------------------------------------------------ status
+__global__ void status_reset_kernel(int32_t* s) {
+  s[0] = INT_MAX;
+  s[1] = -1;
+  s[2] = 0;
+  s[3] = 0;
+}
+
+// ----------------------------------------------------------- splitmix fill
+// Element (r, c) of the logical row-major [rows, cols] stream block is output
+// start + r*cols + c, i.e. counter start + r*cols + c + 1 (model.py:32-33).
+// Value = a * (2 * ((bits >> 11) * 2^-53) - 1) in fp64 (model.py:47-50).
+__global__ void splitmix_fill_kernel(uint64_t seed, uint64_t start, int64_t rows, int64_t cols,
+                                     double a, int transpose, int out_dtype, void* out,
+                                     int64_t ld) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r, c, o;
+    if (transpose) { c = i / rows; r = i - c * rows; o = c * ld + r; }
+    else { r = i / cols; c = i - r * cols; o = r * ld + c; }
+    const uint64_t bits = splitmix_at(seed, start + (uint64_t)(r * cols + c) + 1);
+    const double unit = __dmul_rn((double)(bits >> 11), 1.1102230246251565e-16);  // 2^-53
+    const double v = __dmul_rn(a, __dsub_rn(__dmul_rn(2.0, unit), 1.0));
+    if (out_dtype == 0) {
+      static_cast<double*>(out)[o] = v;
+    } else if (out_dtype == 1) {
+      static_cast<float*>(out)[o] = __double2float_rn(v);
+    } else {
+      static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(__double2float_rn(v));
+    }
+  }
+}
+
+__global__ void splitmix_bits_kernel(uint64_t seed, uint64_t start, int64_t count, uint64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = splitmix_at(seed, start + (uint64_t)i + 1);
+}
+
+// -------------------------------------------------------------------- gate
+// One warp per token row. W_gate^T staged in shared memory; fp32 dot products
+// reduced with butterfly shuffles; softmax; stable top-k by (score desc, id asc)
+// (model.py:215-222).
+template <int EMAX>
+__global__ void gate_topk_kernel(const float* __restrict__ u, const float* __restrict__ wt,
+                                 int64_t n, int hp, int E, int k, int32_t* __restrict__ ids,
+                                 float* __restrict__ gates, float* __restrict__ scores,
+                                 int32_t* status, int step, int layer) {
+  extern __shared__ float sw[];  // [E, hp]
+  for (int i = threadIdx.x; i < E * hp; i += blockDim.x) sw[i] = wt[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  for (int64_t t = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5); t < n;
+       t += (int64_t)gridDim.x * warps) {
+    float acc[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
+    bool finite = true;
+    const float* row = u + t * hp;
+    for (int c = lane * 4; c < hp; c += 128) {
+      const float4 x = *reinterpret_cast<const float4*>(row + c);
+      finite &= isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w);
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e) {
+        if (e < E) {
+          const float4 w = *reinterpret_cast<const float4*>(sw + e * hp + c);
+          acc[e] = fmaf(x.x, w.x, acc[e]);
+          acc[e] = fmaf(x.y, w.y, acc[e]);
+          acc[e] = fmaf(x.z, w.z, acc[e]);
+          acc[e] = fmaf(x.w, w.w, acc[e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+      if (e < E) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+      }
+    }
+    finite = __all_sync(0xffffffffu, finite);
+    if (!finite && lane == 0) record_nonfinite(status, step, layer);
+    // softmax over the E logits (model.py:216-218)
+    float mx = acc[0];
+#pragma unroll
+    for (int e = 1; e < EMAX; ++e) if (e < E) mx = fmaxf(mx, acc[e]);
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) if (e < E) { acc[e] = expf(acc[e] - mx); sum += acc[e]; }
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) if (e < E) acc[e] = acc[e] / sum;
+    if (scores != nullptr) {
+      for (int e = lane; e < E; e += 32) {
+        float v = 0.f;
+#pragma unroll
+        for (int q = 0; q < EMAX; ++q) if (q == e) v = acc[q];
+        scores[t * E + e] = v;
+      }
+    }
+    if (lane == 0) {
+      uint64_t taken = 0;
+      int pick[EMAX];
+      float psum = 0.f;
+      for (int j = 0; j < k; ++j) {
+        int best = -1;
+        float bv = 0.f;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          if (e < E && !((taken >> e) & 1ull) && (best < 0 || acc[e] > bv)) { best = e; bv = acc[e]; }
+        }
+        taken |= 1ull << best;
+        pick[j] = best;
+        psum += bv;
+        ids[t * k + j] = best;
+      }
+      for (int j = 0; j < k; ++j) {
+        float v = 0.f;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) if (e == pick[j]) v = acc[e];
+        gates[t * k + j] = v / psum;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ cond decide
+// Per token (policies.py:159-186): due = force | !primed | (step - last) >= R;
+// due tokens redraw the reduced-slot subset (policies.py:118-139) and reset the
+// cadence; active = !reduced | due; write = reduced & due; strict adds pairs
+// whose expert moved since the cached refresh.
+__global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, int k, int step,
+                                   int force, int R, int strategy, int strict, uint64_t key,
+                                   int32_t* last, uint8_t* primed, uint8_t* reduced,
+                                   const int32_t* __restrict__ cached_ids, uint8_t* active,
+                                   uint8_t* write) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (strategy == DICE_COND_OFF) {
+      for (int s = 0; s < k; ++s) { active[t * k + s] = 1; write[t * k + s] = 0; }
+      continue;
+    }
+    const bool due = force || !primed[t] || (step - last[t]) >= R;
+    if (due) {
+      int keep = -1;
+      if (strategy == DICE_COND_RANDOM) keep = (int)(splitmix_at(key, (uint64_t)t + 1) % (uint64_t)k);
+      for (int s = 0; s < k; ++s) {
+        bool red;
+        if (strategy == DICE_COND_LOW_SCORE) red = s >= 1;
+        else if (strategy == DICE_COND_HIGH_SCORE) red = s == 0;
+        else red = s != keep;
+        reduced[t * k + s] = red;
+      }
+      last[t] = step;
+      primed[t] = 1;
+    }
+    for (int s = 0; s < k; ++s) {
+      const bool red = reduced[t * k + s] != 0;
+      bool a = !red || due;
+      bool w = red && due;
+      if (strict && red && !due && ids[t * k + s] != cached_ids[t * k + s]) { a = true; w = true; }
+      active[t * k + s] = a;
+      write[t * k + s] = w;
+    }
+  }
+}
+
+// ------------------------------------------------------------- permute
+// Pairs are visited in slot-major order p = s*n + t, so positions within an
+// expert follow routed_rows' (slot, token-ascending) grouping (model.py:267-275).
+// Block b owns pairs [b*1024, (b+1)*1024). Pass 1 counts per (block, expert)
+// and the last block to finish turns the counts into per-block prefixes and
+// 128-row-padded expert bases; pass 2 recomputes in-block ranks and scatters.
+constexpr int kPermBlock = 1024;
+
+struct PermScratch {
+  // scratch layout (int32): [0] done counter, [1..1+E] expert row base,
+  // [2+E .. 2+E+nb*E) per-block prefix, followed by nothing.
+  __device__ static int* done(int32_t* s) { return s; }
+  __device__ static int* base(int32_t* s) { return s + 1; }
+  __device__ static int* blk(int32_t* s, int E, int b) { return s + 2 + E + (int64_t)b * E; }
+};
+
+__device__ __forceinline__ bool pair_of(int64_t p, int64_t n, int k, const int32_t* ids,
+                                        const uint8_t* active, int& e, int64_t& t, int& s) {
+  s = (int)(p / n);
+  t = p - (int64_t)s * n;
+  e = ids[t * k + s];
+  return active == nullptr || active[t * k + s] != 0;
+}
+
+// Rank of this thread's pair among earlier pairs of the same expert in its
+// block; fills wcnt[warp][e] with per-warp counts turned into exclusive
+// prefixes over warps. Returns rank within the block.
+__device__ __forceinline__ int block_rank(bool valid, int e, int E, int (*wcnt)[64]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
+  __syncthreads();
+  const int key = valid ? e : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
+  if (valid && rank_in_warp == 0) wcnt[warp][e] = __popc(peers);
+  __syncthreads();
+  if (threadIdx.x < E) {
+    int acc = 0;
+    for (int w = 0; w < 32; ++w) { const int c = wcnt[w][threadIdx.x]; wcnt[w][threadIdx.x] = acc; acc += c; }
+  }
+  __syncthreads();
+  return valid ? wcnt[warp][e] + rank_in_warp : 0;
+}
+
+__global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
+    const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
+    int32_t* tile_offsets, long long* counters, int devices, int64_t row0, int64_t rows_total,
+    int32_t* scratch) {
+  __shared__ int cnt[64];
+  __shared__ unsigned long long red[2];
+  __shared__ bool is_last;
+  if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 2) red[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t P = n * k;
+  const int64_t p = (int64_t)blockIdx.x * kPermBlock + threadIdx.x;
+  int e = 0, s = 0;
+  int64_t t = 0;
+  bool valid = false;
+  if (p < P) valid = pair_of(p, n, k, ids, active, e, t, s);
+  const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : -1);
+  const int lane = threadIdx.x & 31;
+  if (valid && __popc(peers & ((1u << lane) - 1)) == 0) atomicAdd(&cnt[e], __popc(peers));
+  // byte plan: active pairs whose expert device differs from the token home (cluster.py:75-90)
+  bool remote = false;
+  if (valid && devices > 1) {
+    const int home = (int)(((row0 + t) * devices) / rows_total);
+    const int edev = e / (E / devices);
+    remote = home != edev;
+  }
+  const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
+  const unsigned nr = __popc(__ballot_sync(0xffffffffu, remote));
+  if (lane == 0) { atomicAdd(&red[0], (unsigned long long)nv); atomicAdd(&red[1], (unsigned long long)nr); }
+  __syncthreads();
+  if (threadIdx.x < E) PermScratch::blk(scratch, E, blockIdx.x)[threadIdx.x] = cnt[threadIdx.x];
+  if (threadIdx.x == 0 && counters != nullptr) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&counters[0]), red[0]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&counters[1]), red[1]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(PermScratch::done(scratch), 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // last block: per-expert exclusive prefix over blocks, padded bases, tile offsets
+  if (threadIdx.x < E) {
+    const int ex = threadIdx.x;
+    int acc = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      volatile int* q = PermScratch::blk(scratch, E, b);
+      const int c = q[ex];
+      q[ex] = acc;
+      acc += c;
+    }
+    cnt[ex] = acc;  // total pairs of expert ex
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tiles = 0;
+    for (int ex = 0; ex < E; ++ex) {
+      tile_offsets[ex] = tiles;
+      PermScratch::base(scratch)[ex] = tiles * 128;
+      tiles += (cnt[ex] + 127) / 128;
+    }
+    tile_offsets[E] = tiles;
+    *PermScratch::done(scratch) = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
+    const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
+    const uint16_t* __restrict__ u16, int hp, uint16_t* __restrict__ x_perm, int32_t* pos,
+    const int32_t* __restrict__ scratch) {
+  __shared__ int wcnt[32][64];
+  __shared__ int rows_of[kPermBlock];
+  __shared__ int src_of[kPermBlock];
+  const int64_t P = n * k;
+  const int64_t p = (int64_t)blockIdx.x * kPermBlock + threadIdx.x;
+  int e = 0, s = 0;
+  int64_t t = 0;
+  bool valid = false;
+  const bool in_range = p < P;
+  if (in_range) valid = pair_of(p, n, k, ids, active, e, t, s);
+  const int r = block_rank(valid, e, E, wcnt);
+  int dst = -1;
+  if (valid) {
+    dst = scratch[1 + e] + scratch[2 + E + (int64_t)blockIdx.x * E + e] + r;
+  }
+  if (in_range) pos[t * k + s] = dst;
+  rows_of[threadIdx.x] = dst;
+  src_of[threadIdx.x] = (int)t;
+  __syncthreads();
+  // gather: each warp copies rows of the block's pairs, 16 B per lane per step
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int vec = hp / 8;
+  for (int i = warp; i < kPermBlock; i += kPermBlock / 32) {
+    const int d = rows_of[i];
+    if (d < 0) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(u16 + (int64_t)src_of[i] * hp);
+    uint4* out = reinterpret_cast<uint4*>(x_perm + (int64_t)d * hp);
+    for (int c = lane; c < vec; c += 32) out[c] = src[c];
+  }
+}
+
+// ------------------------------------------------------- cache assemble
+// One thread per (token, 8 columns). Slots are visited left to right and
+// accumulated in fp32 (model.py:295-297). Active pairs read the fresh expert
+// row; inactive pairs read the cached row and gate (policies.py:197-202);
+// write pairs persist row / gate / id (policies.py:203-207). write implies
+// active, so no thread reads a cache entry another thread writes.
+__global__ void cache_assemble_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos,
+                                      const uint8_t* __restrict__ active,
+                                      const uint8_t* __restrict__ write,
+                                      const float* __restrict__ gates, const int32_t* __restrict__ ids,
+                                      int64_t n, int k, int hp, uint16_t* cache_rows,
+                                      float* cache_gates, int32_t* cache_ids, float* routed,
+                                      float* rows_out, float* gates_out) {
+  const int vec = hp / 8;
+  const int64_t total = n * vec;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / vec;
+    const int c = (int)(i - t * vec) * 8;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int s = 0; s < k; ++s) {
+      const int64_t ps = t * k + s;
+      const bool act = active == nullptr || active[ps] != 0;
+      uint4 raw;
+      float g;
+      if (act) {
+        raw = *reinterpret_cast<const uint4*>(y + (int64_t)pos[ps] * hp + c);
+        g = gates[ps];
+        if (write != nullptr && write[ps]) {
+          *reinterpret_cast<uint4*>(cache_rows + ((int64_t)s * n + t) * hp + c) = raw;
+          if (c == 0) { cache_gates[ps] = g; cache_ids[ps] = ids[ps]; }
+        }
+      } else {
+        raw = *reinterpret_cast<const uint4*>(cache_rows + ((int64_t)s * n + t) * hp + c);
+        g = cache_gates[ps];
+      }
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw);
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { v[j] = bf16_bits_to_f32(h[j]); acc[j] = fmaf(g, v[j], acc[j]); }
+      if (rows_out != nullptr) {
+        float4* ro = reinterpret_cast<float4*>(rows_out + ((int64_t)s * n + t) * hp + c);
+        ro[0] = make_float4(v[0], v[1], v[2], v[3]);
+        ro[1] = make_float4(v[4], v[5], v[6], v[7]);
+      }
+      if (gates_out != nullptr && c == 0) gates_out[ps] = g;
+    }
+    float4* o = reinterpret_cast<float4*>(routed + t * hp + c);
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// ---------------------------------------------------------------- combine
+__global__ void combine_kernel(const float* __restrict__ base, const float* __restrict__ rows,
+                               const float* __restrict__ gates, const float* __restrict__ residual,
+                               int64_t n, int k, int hp, float* out, __nv_bfloat16* out16) {
+  const int vec = hp / 4;
+  const int64_t total = n * vec;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / vec;
+    const int c = (int)(i - t * vec) * 4;
+    float4 a = *reinterpret_cast<const float4*>(base + t * hp + c);
+    for (int s = 0; s < k; ++s) {
+      const float g = gates[t * k + s];
+      const float4 r = *reinterpret_cast<const float4*>(rows + ((int64_t)s * n + t) * hp + c);
+      a.x += g * r.x; a.y += g * r.y; a.z += g * r.z; a.w += g * r.w;
+    }
+    if (residual != nullptr) {
+      const float4 u = *reinterpret_cast<const float4*>(residual + t * hp + c);
+      a = make_float4(u.x + a.x, u.y + a.y, u.z + a.z, u.w + a.w);
+    }
+    *reinterpret_cast<float4*>(out + t * hp + c) = a;
+    if (out16 != nullptr) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+      uint2 w = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      *reinterpret_cast<uint2*>(out16 + t * hp + c) = w;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- denoise
+__global__ void denoise_kernel(float* x, __nv_bfloat16* x16, const float* __restrict__ y, float eta,
+                               int64_t count4, int32_t* status, int step) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(x)[i];
+    const float4 b = reinterpret_cast<const float4*>(y)[i];
+    a.x = a.x - eta * b.x; a.y = a.y - eta * b.y; a.z = a.z - eta * b.z; a.w = a.w - eta * b.w;
+    bad |= !(isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w));
+    reinterpret_cast<float4*>(x)[i] = a;
+    if (x16 != nullptr) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+      reinterpret_cast<uint2*>(x16)[i] =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) record_nonfinite(status, step, -1);
+}
+
+__global__ void pack_rows_kernel(const float* __restrict__ in, int64_t n, int cols, int64_t ld_in,
+                                 int hp, float* out32, __nv_bfloat16* out16) {
+  const int64_t total = n * hp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / hp;
+    const int c = (int)(i - t * hp);
+    const float v = c < cols ? in[t * ld_in + c] : 0.f;
+    if (out32 != nullptr) out32[i] = v;
+    if (out16 != nullptr) out16[i] = __float2bfloat16_rn(v);
+  }
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  const int64_t cap = 148 * 16;
+  if (g > cap) g = cap;
+  return g < 1 ? 1 : (int)g;
+}
+
+static inline int launch_ok() { return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA; }
+
+}  // namespace dice
+
+using namespace dice;
+
+extern "C" {
+
+int dice_version(void) { return 100; }
+
+int dice_status_reset(int32_t* status, void* stream) {
+  status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status);
+  return launch_ok();
+}
+
+int dice_splitmix_fill(uint64_t seed, uint64_t start, int64_t rows, int64_t cols, double halfwidth,
+                       int transpose, int out_dtype, void* out, int64_t ld, void* stream) {
+  if (rows < 0 || cols < 0 || out_dtype < 0 || out_dtype > 2) return DICE_ERR_CONTRACT;
+  if (rows * cols == 0) return DICE_OK;
+  splitmix_fill_kernel<<<grid_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
+      seed, start, rows, cols, halfwidth, transpose, out_dtype, out, ld);
+  return launch_ok();
+}
+
+int dice_splitmix_bits(uint64_t seed, uint64_t start, int64_t count, uint64_t* out, void* stream) {
+  if (count < 0) return DICE_ERR_CONFIG;
+  if (count == 0) return DICE_OK;
+  splitmix_bits_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(seed, start, count, out);
+  return launch_ok();
+}
+
+int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                   int32_t* ids, float* gates, float* scores, int32_t* status, int step, int layer,
+                   void* stream) {
+  if (E < 1 || E > 64 || k < 1 || k > E || hp % 64 != 0) return DICE_ERR_CONTRACT;
+  if (n == 0) return DICE_OK;
+  const size_t smem = (size_t)E * hp * sizeof(float);
+  const int threads = 256;
+  const int grid = grid_for(n, threads / 32);
+  cudaStream_t s = (cudaStream_t)stream;
+#define DICE_GATE(EM)                                                                          \
+  {                                                                                            \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(gate_topk_kernel<EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           200 * 1024);                                                        \
+      attr = true;                                                                             \
+    }                                                                                          \
+    gate_topk_kernel<EM><<<grid, threads, smem, s>>>(u, w_gate_t, n, hp, E, k, ids, gates,     \
+                                                     scores, status, step, layer);             \
+  }
+  if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
+  if (E <= 8) DICE_GATE(8)
+  else if (E <= 16) DICE_GATE(16)
+  else DICE_GATE(64)
+#undef DICE_GATE
+  return launch_ok();
+}
+
+int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, int refresh_interval,
+                     int strategy, int strict, uint64_t random_key, int32_t* last_refresh,
+                     uint8_t* primed, uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
+                     uint8_t* write, void* stream) {
+  if (k < 1 || refresh_interval < 1 || strategy < 0 || strategy > 3) return DICE_ERR_CONFIG;
+  if (n == 0) return DICE_OK;
+  cond_decide_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      ids, n, k, step, force, refresh_interval, strategy, strict, random_key, last_refresh, primed,
+      reduced, cached_ids, active, write);
+  return launch_ok();
+}
+
+int64_t dice_permute_max_rows(int64_t n, int k, int E) {
+  const int64_t tiles = (n * k + 127 * (int64_t)E + 127) / 128;
+  return (tiles < 1 ? 1 : tiles) * 128;
+}
+
+int64_t dice_permute_scratch_ints(int64_t n, int k, int E) {
+  const int64_t blocks = (n * k + kPermBlock - 1) / kPermBlock;
+  return 2 + E + (blocks < 1 ? 1 : blocks) * E;
+}
+
+int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
+                       const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows, int32_t* pos,
+                       int32_t* tile_offsets, int64_t* counters, int devices, int64_t row0,
+                       int64_t rows_total, int32_t* scratch, void* stream) {
+  if (E < 1 || E > 64 || k < 1 || hp % 64 != 0 || devices < 1 || E % devices != 0)
+    return DICE_ERR_CONTRACT;
+  if (max_rows < dice_permute_max_rows(n, k, E)) return DICE_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t P = n * k;
+  const int blocks = (int)((P + kPermBlock - 1) / kPermBlock);
+  if (blocks == 0) {
+    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (E + 1), s);
+    return launch_ok();
+  }
+  permute_count_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, tile_offsets,
+                                                     reinterpret_cast<long long*>(counters), devices,
+                                                     row0, rows_total, scratch);
+  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, u16, hp, x_perm, pos,
+                                                       scratch);
+  return launch_ok();
+}
+
+int dice_grouped_ffn(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
+                     const uint16_t* w2_t, int E, int hp, int ep, const int32_t* tile_offsets,
+                     uint16_t* hbuf, uint16_t* y, void* stream) {
+  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % 128 != 0)
+    return DICE_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  GemmProblem p{};
+  p.A = x_perm; p.A_rows = max_rows; p.B = w1_t; p.M = (int)max_rows; p.N = ep; p.K = hp;
+  p.num_groups = E; p.group_tile_offsets = tile_offsets; p.max_m_tiles = (int)(max_rows / 128);
+  p.epi_kind = EPI_GELU_BF16;
+  p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(hbuf); p.epi.ld_bf16 = ep;
+  int rc = gemm_bf16(p, s);
+  if (rc) return rc;
+  GemmProblem q{};
+  q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
+  q.num_groups = E; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / 128);
+  q.epi_kind = EPI_STORE_BF16;
+  q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(y); q.epi.ld_bf16 = hp;
+  return gemm_bf16(q, s);
+}
+
+int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* active,
+                        const uint8_t* write, const float* gates, const int32_t* ids, int64_t n, int k,
+                        int hp, uint16_t* cache_rows, float* cache_gates, int32_t* cache_ids,
+                        float* routed, float* rows_out, float* gates_out, void* stream) {
+  if (hp % 64 != 0 || k < 1) return DICE_ERR_CONTRACT;
+  if (active != nullptr && cache_rows == nullptr) {
+    // inactive pairs need a cache to read from unless every pair is active
+  }
+  if (n == 0) return DICE_OK;
+  cache_assemble_kernel<<<grid_for(n * (hp / 8), 256), 256, 0, (cudaStream_t)stream>>>(
+      y, pos, active, write, gates, ids, n, k, hp, cache_rows, cache_gates, cache_ids, routed,
+      rows_out, gates_out);
+  return launch_ok();
+}
+
+int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, int K, float* out_f32,
+              int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16, const float* residual,
+              int64_t ld_res, const float* addend, int64_t ld_add, void* stream) {
+  if (M < 0 || M > INT_MAX) return DICE_ERR_CONTRACT;
+  if (M == 0) return DICE_OK;
+  GemmProblem p{};
+  p.A = A; p.A_rows = M; p.B = B; p.M = (int)M; p.N = N; p.K = K;
+  p.num_groups = 1; p.group_tile_offsets = nullptr; p.max_m_tiles = 0;
+  p.epi_kind = epi;
+  p.epi.out_f32 = out_f32; p.epi.ld_f32 = ld_f32;
+  p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out_bf16); p.epi.ld_bf16 = ld_bf16;
+  p.epi.residual = residual; p.epi.ld_res = ld_res;
+  p.epi.addend = addend; p.epi.ld_add = ld_add;
+  if ((epi == EPI_GELU_RESID || epi == EPI_CONSUME) && residual == nullptr) return DICE_ERR_CONTRACT;
+  if (epi == EPI_CONSUME && addend == nullptr) return DICE_ERR_CONTRACT;
+  return gemm_bf16(p, (cudaStream_t)stream);
+}
+
+int dice_combine(const float* base, const float* rows, const float* gates, const float* residual,
+                 int64_t n, int k, int hp, float* out, uint16_t* out_bf16, void* stream) {
+  if (hp % 4 != 0) return DICE_ERR_CONTRACT;
+  if (n == 0) return DICE_OK;
+  combine_kernel<<<grid_for(n * (hp / 4), 256), 256, 0, (cudaStream_t)stream>>>(
+      base, rows, gates, residual, n, k, hp, out, reinterpret_cast<__nv_bfloat16*>(out_bf16));
+  return launch_ok();
+}
+
+int dice_denoise(float* x, uint16_t* x16, const float* y, float eta, int64_t n, int hp,
+                 int32_t* status, int step, void* stream) {
+  if (hp % 4 != 0) return DICE_ERR_CONTRACT;
+  const int64_t c4 = n * hp / 4;
+  if (c4 == 0) return DICE_OK;
+  denoise_kernel<<<grid_for(c4, 256), 256, 0, (cudaStream_t)stream>>>(
+      x, reinterpret_cast<__nv_bfloat16*>(x16), y, eta, c4, status, step);
+  return launch_ok();
+}
+
+int dice_pack_rows(const float* in, int64_t n, int cols, int64_t ld_in, int hp, float* out32,
+                   uint16_t* out16, void* stream) {
+  if (cols > hp) return DICE_ERR_CONTRACT;
+  if (n == 0) return DICE_OK;
+  pack_rows_kernel<<<grid_for(n * hp, 256), 256, 0, (cudaStream_t)stream>>>(
+      in, n, cols, ld_in, hp, out32, reinterpret_cast<__nv_bfloat16*>(out16));
+  return launch_ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,138 @@
+"""Tensor-level wrappers over the C-ABI (torch CUDA tensors in, CUDA kernels out).
+
+torch is used only for device memory and the current stream; every value is
+computed by the sm_100a library. Shapes use padded feature dims (multiples of
+64, zero padding) as include/dice_b200.h specifies.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import ContractError
+
+EPI_STORE_BF16, EPI_GELU_BF16, EPI_STORE_F32, EPI_GELU_RESID, EPI_CONSUME = range(5)
+COND_CODES = {"off": 0, "low_score": 1, "high_score": 2, "random": 3}
+
+
+def pad64(x: int) -> int:
+    return (x + 63) // 64 * 64
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need(t, dtype, what):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise ContractError(f"{what}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise ContractError(f"{what}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ContractError(f"{what}: expected a contiguous tensor")
+
+
+def status_reset(status):
+    _lib.call("dice_status_reset", _ptr(status), _stream())
+
+
+def splitmix_fill(out, seed, start, rows, cols, halfwidth, transpose=False):
+    """Fill `out` (f64/f32/bf16, row stride out.shape[-1]) from the splitmix64 stream."""
+    code = {torch.float64: 0, torch.float32: 1, torch.bfloat16: 2}[out.dtype]
+    _lib.call("dice_splitmix_fill", seed & 0xFFFFFFFFFFFFFFFF, start, rows, cols,
+              float(halfwidth), int(transpose), code, _ptr(out), out.shape[-1], _stream())
+
+
+def splitmix_bits(seed, start, count, device="cuda"):
+    out = torch.empty(count, dtype=torch.int64, device=device)
+    _lib.call("dice_splitmix_bits", seed & 0xFFFFFFFFFFFFFFFF, start, count, _ptr(out), _stream())
+    return out
+
+
+def gate_topk(u32, w_gate_t, k, ids, gates, scores=None, status=None, step=0, layer=0):
+    n, hp = u32.shape
+    E = w_gate_t.shape[0]
+    _need(u32, torch.float32, "gate u")
+    _lib.call("dice_gate_topk", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids), _ptr(gates),
+              _ptr(scores), _ptr(status), step, layer, _stream())
+
+
+def cond_decide(ids, step, force, refresh_interval, strategy, strict, random_key, last, primed,
+                reduced, cached_ids, active, write):
+    n, k = ids.shape
+    _lib.call("dice_cond_decide", _ptr(ids), n, k, step, int(force), refresh_interval,
+              COND_CODES[strategy], int(strict), random_key & 0xFFFFFFFFFFFFFFFF, _ptr(last),
+              _ptr(primed), _ptr(reduced), _ptr(cached_ids), _ptr(active), _ptr(write), _stream())
+
+
+def permute_max_rows(n, k, E):
+    return int(_lib.load().dice_permute_max_rows(n, k, E))
+
+
+def permute_scratch_ints(n, k, E):
+    return int(_lib.load().dice_permute_scratch_ints(n, k, E))
+
+
+def route_permute(ids, active, u16, x_perm, pos, tile_offsets, counters, scratch, E,
+                  devices=1, row0=0, rows_total=None):
+    n, k = ids.shape
+    hp = u16.shape[1]
+    _lib.call("dice_route_permute", _ptr(ids), _ptr(active), n, k, E, _ptr(u16), hp,
+              _ptr(x_perm), x_perm.shape[0], _ptr(pos), _ptr(tile_offsets), _ptr(counters),
+              devices, row0, n if rows_total is None else rows_total, _ptr(scratch), _stream())
+
+
+def grouped_ffn(x_perm, w1_t, w2_t, E, tile_offsets, hbuf, y):
+    max_rows, hp = x_perm.shape
+    ep = hbuf.shape[1]
+    _lib.call("dice_grouped_ffn", _ptr(x_perm), max_rows, _ptr(w1_t), _ptr(w2_t), E, hp, ep,
+              _ptr(tile_offsets), _ptr(hbuf), _ptr(y), _stream())
+
+
+def cache_assemble(y, pos, active, write, gates, ids, routed, cache_rows=None, cache_gates=None,
+                   cache_ids=None, rows_out=None, gates_out=None):
+    n, k = pos.shape
+    hp = routed.shape[1]
+    _lib.call("dice_cache_assemble", _ptr(y), _ptr(pos), _ptr(active), _ptr(write), _ptr(gates),
+              _ptr(ids), n, k, hp, _ptr(cache_rows), _ptr(cache_gates), _ptr(cache_ids),
+              _ptr(routed), _ptr(rows_out), _ptr(gates_out), _stream())
+
+
+def gemm(epi, A, B, out_f32=None, out_bf16=None, residual=None, addend=None):
+    """C[M, N] = A[M, K] @ B[N, K]^T (bf16 operands, fp32 accumulate) + fused epilogue."""
+    _need(A, torch.bfloat16, "gemm A")
+    _need(B, torch.bfloat16, "gemm B")
+    M, K = A.shape
+    N = B.shape[0]
+    if B.shape[1] != K:
+        raise ContractError(f"gemm: A {tuple(A.shape)} vs B {tuple(B.shape)}")
+    ld = lambda t: 0 if t is None else t.shape[-1]
+    _lib.call("dice_gemm", epi, _ptr(A), M, _ptr(B), N, K, _ptr(out_f32), ld(out_f32),
+              _ptr(out_bf16), ld(out_bf16), _ptr(residual), ld(residual), _ptr(addend),
+              ld(addend), _stream())
+
+
+def combine(base, rows, gates, out, residual=None, out_bf16=None):
+    n, hp = base.shape
+    k = gates.shape[1]
+    _lib.call("dice_combine", _ptr(base), _ptr(rows), _ptr(gates), _ptr(residual), n, k, hp,
+              _ptr(out), _ptr(out_bf16), _stream())
+
+
+def denoise(x32, x16, y, eta, status=None, step=0):
+    n, hp = x32.shape
+    _lib.call("dice_denoise", _ptr(x32), _ptr(x16), _ptr(y), float(eta), n, hp, _ptr(status),
+              step, _stream())
+
+
+def pack_rows(src, hp, out32=None, out16=None):
+    n, cols = src.shape
+    _need(src, torch.float32, "pack_rows src")
+    _lib.call("dice_pack_rows", _ptr(src), n, cols, src.stride(0), hp, _ptr(out32), _ptr(out16),
+              _stream())
