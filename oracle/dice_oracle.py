@@ -136,6 +136,14 @@ def init_layer(g: Geometry, seed: int, layer: int) -> LayerParams:
     return LayerParams(w_mix, w_gate, experts, shared)
 
 
+def gate_weight(g: Geometry, seed: int, layer: int) -> np.ndarray:
+    """Only W_gate of one layer, from its stream offset (model.py:157)."""
+    h = g.hidden_dim
+    start = layer * layer_value_count(g) + h * h
+    bits = stream_bits(seed, start, h * g.num_experts)
+    return to_uniform(bits, float(np.sqrt(1.0 / h))).reshape(h, g.num_experts)
+
+
 def init_params(g: Geometry, seed: int) -> list:
     return [init_layer(g, seed, l) for l in range(g.num_layers)]
 

@@ -377,9 +377,12 @@ __global__ void cache_assemble_kernel(const uint16_t* __restrict__ y, const int3
           *reinterpret_cast<uint4*>(cache_rows + ((int64_t)s * n + t) * hp + c) = raw;
           if (c == 0) { cache_gates[ps] = g; cache_ids[ps] = ids[ps]; }
         }
-      } else {
+      } else if (cache_rows != nullptr) {
         raw = *reinterpret_cast<const uint4*>(cache_rows + ((int64_t)s * n + t) * hp + c);
         g = cache_gates[ps];
+      } else {  // no cache: inactive pairs stay zero (routed_rows, model.py:262)
+        raw = make_uint4(0, 0, 0, 0);
+        g = 0.f;
       }
       const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw);
       float v[8];
@@ -596,9 +599,6 @@ int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* ac
                         int hp, uint16_t* cache_rows, float* cache_gates, int32_t* cache_ids,
                         float* routed, float* rows_out, float* gates_out, void* stream) {
   if (hp % 64 != 0 || k < 1) return DICE_ERR_CONTRACT;
-  if (active != nullptr && cache_rows == nullptr) {
-    // inactive pairs need a cache to read from unless every pair is active
-  }
   if (n == 0) return DICE_OK;
   cache_assemble_kernel<<<grid_for(n * (hp / 8), 256), 256, 0, (cudaStream_t)stream>>>(
       y, pos, active, write, gates, ids, n, k, hp, cache_rows, cache_gates, cache_ids, routed,

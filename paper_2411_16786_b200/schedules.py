@@ -1,0 +1,387 @@
+"""Execution schedules on the GPU — drop-in for dicesim.schedules
+(/root/reference/pkg/src/dicesim/schedules.py).
+
+``run_sampling`` keeps the reference signature and RunResult fields. The
+per-layer stage logic (synchronous / displaced / interweaved, selective and
+periodic sync, conditional communication; schedules.py:319-457) is host
+control flow; every value is produced by the sm_100a library, stream-ordered,
+with no host synchronisation inside the run. Device-side counters and the
+non-finite status word are read once at the end of the run.
+
+Buffers (all HBM-resident, allocated once per runner):
+* a dispatch payload = gate ids/gates, cond masks, permute positions/tile
+  offsets and the expert-sorted bf16 token rows (DispatchPayload, 48-57);
+* one combine slot per layer = the gate-weighted routed sum in f32
+  (CombinePayload + LayerBuffers, 60-79). It is consumed by the fused
+  shared-FFN epilogue u + (shared + routed).
+"""
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+from collections import Counter
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import ops
+from .cluster import ClusterConfig, build_placement
+from .errors import ContractError, NumericalDivergenceError
+from .model import ActivationBlock, RouteDecision, ToyModel, model_hash
+from .policies import (CondStrategy, PolicyConfig, TokenCache, is_sync_step,
+                       select_sync_layers)
+
+INT32_MAX = 2 ** 31 - 1
+
+
+class Strategy(Enum):
+    SYNCHRONOUS = "synchronous"
+    DISPLACED = "displaced"
+    INTERWEAVED = "interweaved"
+
+
+@dataclass(frozen=True)
+class StalenessRecord:
+    layer: int
+    used_step: int
+    generated_step: int
+
+    @property
+    def staleness(self) -> int:
+        return self.used_step - self.generated_step
+
+
+@dataclass
+class RunResult:
+    """Same fields as schedules.py:92-129. ``timeline`` holds measured CUDA-event
+    stage timings when the run was timed (else None)."""
+    final: ActivationBlock
+    timeline: object
+    staleness_records: list
+    strategy: Strategy
+    policy: PolicyConfig
+    seed: int
+    model_hash: str
+    x0_hash: str
+    config: object
+    cluster: ClusterConfig
+    dispatch_bytes: int
+    combine_bytes: int
+    peak_buffer_bytes: int
+    active_pairs: int
+    total_pairs: int
+    per_step_active_pairs: list
+    per_step_total_pairs: list
+    step_inputs: list | None = None
+    step_routes: list | None = None
+    gpu_seconds: float | None = None
+
+    @property
+    def total_comm_bytes(self) -> int:
+        return self.dispatch_bytes + self.combine_bytes
+
+    @property
+    def makespan_seconds(self) -> float | None:
+        return self.gpu_seconds
+
+    @property
+    def comm_stall_seconds(self) -> float:
+        return 0.0 if self.timeline is None else self.timeline.get("exposed_comm_seconds", 0.0)
+
+    def staleness_histogram(self) -> dict:
+        counts = Counter(rec.staleness for rec in self.staleness_records)
+        return dict(sorted(counts.items()))
+
+
+class _Payload:
+    """Device buffers of one dispatch (DispatchPayload, schedules.py:48-57)."""
+
+    def __init__(self, n, k, E, hp, max_rows, device):
+        self.ids = torch.zeros(n, k, dtype=torch.int32, device=device)
+        self.gates = torch.zeros(n, k, dtype=torch.float32, device=device)
+        self.active = torch.ones(n, k, dtype=torch.uint8, device=device)
+        self.write = torch.zeros(n, k, dtype=torch.uint8, device=device)
+        self.pos = torch.zeros(n, k, dtype=torch.int32, device=device)
+        self.tiles = torch.zeros(E + 1, dtype=torch.int32, device=device)
+        self.x_perm = torch.empty(max_rows, hp, dtype=torch.bfloat16, device=device)
+        self.layer = -1
+        self.gen = -1
+
+
+class DeviceRunner:
+    """One sampling run on one GPU: owns buffers, cache, counters (ScheduleRunner,
+    schedules.py:142-490)."""
+
+    def __init__(self, model: ToyModel, x0: ActivationBlock, strategy: Strategy,
+                 policy: PolicyConfig, cluster: ClusterConfig, seed: int, *,
+                 record_inputs: bool = False, record_routes: bool = False,
+                 time_experts: bool = False):
+        cfg = model.config
+        if not isinstance(strategy, Strategy):
+            raise ContractError(f"strategy must be a Strategy, got {strategy!r}")
+        if x0.generated_step != 0:
+            raise ContractError(f"x0 must carry generated_step 0, got {x0.generated_step}")
+        expected = (cfg.total_rows, cfg.hidden_dim)
+        if tuple(x0.values.shape) != expected:
+            raise ContractError(f"x0 shape {tuple(x0.values.shape)} does not match model {expected}")
+        if model.num_local_experts != cfg.num_experts:
+            raise ContractError("single-device runner needs every routed expert resident")
+        if policy.cond_strategy is CondStrategy.RANDOM and policy.cond_seed is None:
+            policy = dataclasses.replace(policy, cond_seed=seed)   # schedules.py:158-159
+        build_placement(cfg.num_experts, cluster.num_devices, cfg.total_rows)  # validates E % D
+        self.model, self.cfg, self.x0 = model, cfg, x0
+        self.strategy, self.policy, self.cluster, self.seed = strategy, policy, cluster, seed
+        self.record_inputs, self.record_routes = record_inputs, record_routes
+        self.time_experts = time_experts
+        dev = model.device
+        self.dev = dev
+        n, k, E, S = cfg.total_rows, cfg.top_k, cfg.num_experts, cfg.num_shared
+        hp, ep = model.hp, model.ep
+        self.n, self.k, self.E, self.S, self.hp, self.ep = n, k, E, S, hp, ep
+        self.max_rows = ops.permute_max_rows(n, k, E)
+        f32, bf = torch.float32, torch.bfloat16
+        self.x32 = torch.zeros(n, hp, dtype=f32, device=dev)
+        self.x16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        self.h32 = torch.zeros(n, hp, dtype=f32, device=dev)
+        self.h16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        self.u32 = torch.zeros(n, hp, dtype=f32, device=dev)
+        self.u16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        self.hbuf = torch.empty(self.max_rows, ep, dtype=bf, device=dev)
+        self.y = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
+        self.hsh = torch.empty(n, max(S, 1) * ep, dtype=bf, device=dev)
+        self.scores = torch.empty(n, E, dtype=f32, device=dev) if record_routes else None
+        L = cfg.num_layers
+        nslots = 1 if strategy is Strategy.SYNCHRONOUS else L
+        self.slots = torch.zeros(nslots, n, hp, dtype=f32, device=dev)
+        if strategy is Strategy.SYNCHRONOUS:
+            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev)]
+        elif strategy is Strategy.INTERWEAVED:
+            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(2)]
+        else:
+            self.payloads = [[_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(2)]
+                             for _ in range(L)]
+        self.cache = None
+        if policy.cond_strategy is not CondStrategy.OFF:
+            self.cache = TokenCache(L, n, k, cfg.hidden_dim, device=dev)
+        self.scratch = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+        self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
+        self.status = torch.empty(4, dtype=torch.int32, device=dev)
+        self.sync_layers = select_sync_layers(policy.sync_strategy, L, policy.explicit_layers)
+        self._expert_events = []
+
+    # ------------------------------------------------------------ helpers
+    def _reset_state(self):
+        cfg = self.cfg
+        ops.status_reset(self.status)
+        self.counters.zero_()
+        x0 = torch.as_tensor(self.x0.values).to(device=self.dev, dtype=torch.float32).contiguous()
+        ops.pack_rows(x0, self.hp, self.x32, self.x16)
+        if self.cache is not None:
+            c = self.cache
+            c.rows.zero_(); c.gates.zero_(); c.expert_ids.fill_(-1)
+            c.last_refresh.fill_(-(10 ** 9)); c.reduced_mask.zero_(); c.has_subset.zero_()
+        L = cfg.num_layers
+        self.slot_gen = [None] * L          # generating step of each combine slot
+        self.dispatch_slot = [None] * L     # displaced only
+        self.pending = None                 # interweaved only
+        self.occupied = set()
+        self.peak_buffer_bytes = 0
+        self.ring = 0
+        self.records = []
+        self.dispatch_log = []
+        self.combine_log = []
+        self.step_inputs, self.step_routes = [], []
+        self._expert_events = []
+
+    def _track(self, kind, layer):
+        self.occupied.add((kind, layer))
+        slot_bytes = self.cfg.total_rows * self.cfg.hidden_dim * self.cluster.bytes_per_element
+        self.peak_buffer_bytes = max(self.peak_buffer_bytes, len(self.occupied) * slot_bytes)
+
+    def _stage_is_sync(self, step, layer) -> bool:
+        """schedules.py:406-416."""
+        if self.strategy is Strategy.SYNCHRONOUS:
+            return True
+        if is_sync_step(step, self.policy.warmup, self.policy.period):
+            return True
+        if layer in self.sync_layers:
+            return True
+        if self.strategy is Strategy.DISPLACED:
+            return self.dispatch_slot[layer] is None or self.slot_gen[layer] is None
+        return self.slot_gen[layer] is None
+
+    def _next_payload(self, layer):
+        if self.strategy is Strategy.SYNCHRONOUS:
+            return self.payloads[0]
+        if self.strategy is Strategy.INTERWEAVED:
+            p = self.payloads[self.ring]
+            self.ring ^= 1
+            return p
+        pair = self.payloads[layer]
+        return pair[1] if self.dispatch_slot[layer] is pair[0] else pair[0]
+
+    def _slot(self, layer):
+        return self.slots[0] if self.strategy is Strategy.SYNCHRONOUS else self.slots[layer]
+
+    # -------------------------------------------------------------- stages
+    def _dispatch(self, step, layer, p: _Payload, force: bool):
+        """decide (policies.py:159-186) + permute/pack of the token rows that travel."""
+        if self.cache is not None:
+            self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write)
+            act = p.active
+        else:
+            act = None
+        ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
+                          self.counters[step, layer], self.scratch, self.E,
+                          devices=self.cluster.num_devices, row0=0, rows_total=self.n)
+        p.layer, p.gen = layer, step
+        self.dispatch_log.append((step, layer))
+
+    def _process(self, p: _Payload):
+        """Expert FFN on a dispatched payload + stale-cache merge into its
+        combine slot (_process_dispatch, schedules.py:388-397)."""
+        lw = self.model.layers[p.layer]
+        if self.time_experts:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
+        if self.time_experts:
+            e1.record()
+            self._expert_events.append((e0, e1, p.gen, p.layer))
+        c = self.cache
+        ops.cache_assemble(self.y, p.pos, None if c is None else p.active,
+                           None if c is None else p.write, p.gates, p.ids, self._slot(p.layer),
+                           None if c is None else c.rows[p.layer],
+                           None if c is None else c.gates[p.layer],
+                           None if c is None else c.expert_ids[p.layer])
+        self.slot_gen[p.layer] = p.gen
+        self.combine_log.append((p.gen, p.layer))
+
+    def _flush_pending(self):
+        prev, self.pending = self.pending, None
+        if prev is not None:
+            self._process(prev)
+            self._track("c", prev.layer)
+
+    def _consume(self, layer, step, gen):
+        """u + (shared + routed) fused into the shared-FFN GEMM2 epilogue
+        (_consume, schedules.py:308-317; combine_outputs, model.py:279-298)."""
+        lw = self.model.layers[layer]
+        slot = self._slot(layer)
+        if self.S > 0:
+            ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
+            ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
+                     residual=self.u32, addend=slot)
+        else:
+            empty = slot.new_empty(self.n, 0)
+            ops.combine(slot, slot, empty, self.h32, residual=self.u32, out_bf16=self.h16)
+        self.records.append(StalenessRecord(layer=layer, used_step=step, generated_step=gen))
+
+    def _run_step(self, step):
+        cfg = self.cfg
+        inputs_here, routes_here = [], []
+        for layer in range(cfg.num_layers):
+            lw = self.model.layers[layer]
+            hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
+            ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32, out_bf16=self.u16,
+                     residual=hin32)
+            sync = self._stage_is_sync(step, layer)
+            if sync and self.strategy is Strategy.INTERWEAVED:
+                self._flush_pending()
+            p = self._next_payload(layer)
+            ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores, self.status,
+                          step, layer)
+            if self.record_inputs:
+                inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu())
+            if self.record_routes:
+                routes_here.append(RouteDecision(p.ids.long().cpu(), p.gates.cpu(),
+                                                 self.scores.cpu()))
+            if sync:
+                self._dispatch(step, layer, p, force=True)
+                self._process(p)
+                if self.strategy is Strategy.DISPLACED:
+                    self.dispatch_slot[layer] = p
+                    self._track("d", layer)
+                    self._track("c", layer)
+                elif self.strategy is Strategy.INTERWEAVED:
+                    self._track("c", layer)
+                self._consume(layer, step, step)
+            elif self.strategy is Strategy.DISPLACED:
+                self._dispatch(step, layer, p, force=False)
+                old = self.dispatch_slot[layer]
+                self.dispatch_slot[layer] = p
+                self._track("d", layer)
+                gen = self.slot_gen[layer]
+                # consume the slot before the old dispatch overwrites it; cache
+                # ops keep the reference order decide(new) -> assemble(old)
+                self._consume(layer, step, gen)
+                self._process(old)
+                self._track("c", layer)
+            else:
+                self._dispatch(step, layer, p, force=False)
+                prev, self.pending = self.pending, p
+                if prev is not None:
+                    self._process(prev)
+                    self._track("c", prev.layer)
+                self._consume(layer, step, self.slot_gen[layer])
+        self._flush_pending()
+        ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
+        if self.record_inputs:
+            self.step_inputs.append(inputs_here)
+        if self.record_routes:
+            self.step_routes.append(routes_here)
+
+    def launch(self):
+        """Enqueue the whole run (no host sync)."""
+        self._reset_state()
+        for step in range(self.cfg.num_steps):
+            self._run_step(step)
+
+    def finish(self, gpu_seconds=None) -> RunResult:
+        """One device->host read of status + counters; build the RunResult."""
+        cfg = self.cfg
+        status = self.status.cpu().tolist()
+        if status[0] != INT32_MAX:
+            raise NumericalDivergenceError(
+                f"non-finite values at step {status[0]} (layer {status[1]})", step=status[0])
+        cnt = self.counters.cpu().numpy()
+        row_bytes = cfg.hidden_dim * self.cluster.bytes_per_element
+        dispatch_bytes = int(sum(cnt[s, l, 1] for s, l in self.dispatch_log)) * row_bytes
+        combine_bytes = int(sum(cnt[s, l, 1] for s, l in self.combine_log)) * row_bytes
+        per_step_active = [int(v) for v in cnt[:, :, 0].sum(axis=1)]
+        per_step_total = [cfg.num_layers * self.n * self.k] * cfg.num_steps
+        final = ActivationBlock(values=self.x32[:, :cfg.hidden_dim].clone(),
+                                generated_step=cfg.num_steps)
+        timeline = None
+        if gpu_seconds is not None or self._expert_events:
+            timeline = {"expert_ffn_ms": [a.elapsed_time(b) for a, b, _, _ in self._expert_events]}
+        return RunResult(
+            final=final, timeline=timeline, staleness_records=self.records,
+            strategy=self.strategy, policy=self.policy, seed=self.seed,
+            model_hash=model_hash(self.model),
+            x0_hash=hashlib.sha256(
+                np.ascontiguousarray(torch.as_tensor(self.x0.values).detach().cpu().numpy()
+                                     ).tobytes()).hexdigest(),
+            config=cfg, cluster=self.cluster, dispatch_bytes=dispatch_bytes,
+            combine_bytes=combine_bytes, peak_buffer_bytes=self.peak_buffer_bytes,
+            active_pairs=sum(per_step_active), total_pairs=sum(per_step_total),
+            per_step_active_pairs=per_step_active, per_step_total_pairs=per_step_total,
+            step_inputs=self.step_inputs if self.record_inputs else None,
+            step_routes=self.step_routes if self.record_routes else None,
+            gpu_seconds=gpu_seconds)
+
+    def run(self) -> RunResult:
+        self.launch()
+        return self.finish()
+
+
+def run_sampling(model: ToyModel, x0: ActivationBlock, strategy: Strategy,
+                 policies: PolicyConfig, cluster: ClusterConfig, seed: int, *,
+                 record_inputs: bool = False, record_routes: bool = False) -> RunResult:
+    """Execute a full sampling run on the GPU (schedules.py:493-501)."""
+    runner = DeviceRunner(model, x0, strategy, policies, cluster, seed,
+                          record_inputs=record_inputs, record_routes=record_routes)
+    return runner.run()

@@ -1,0 +1,236 @@
+"""GPU parity of the product path against the reference's golden vectors and
+the CPU oracle. Tolerances (stated, SURVEY.md §8c protocol):
+
+* routing ids / cond-comm masks / staleness records / pair counts: bit-exact
+  (ids: outside the fp32 tie band TAU = 1e-5 of adjacent top-(k+1) scores);
+* single-op activations through bf16 GEMMs: max |err| <= 2e-2 * max|ref|;
+* free-running final latents: rel-L2 of the accumulated update (final - x0)
+  <= 3e-2 and max |err| <= 3e-3 (small configs); config 1: max |err| <= 1e-3.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2411_16786_b200 as D  # noqa: E402
+from oracle import dice_oracle as O  # noqa: E402
+from tests.golden.make_golden_patterns import fresh_pattern  # noqa: E402
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TAU = 1e-5
+dev = "cuda"
+
+
+def load(name):
+    return np.load(os.path.join(G, name))
+
+
+def cfg_of(d):
+    return D.ModelConfig(**d)
+
+
+def policy_of(d):
+    return D.PolicyConfig(
+        sync_strategy=D.SyncStrategy(d["sync_strategy"]),
+        explicit_layers=None if d["explicit_layers"] is None else frozenset(d["explicit_layers"]),
+        cond_strategy=D.CondStrategy(d["cond_strategy"]), refresh_interval=d["refresh_interval"],
+        cond_seed=d["cond_seed"], warmup=d["warmup"],
+        period=math.inf if d["period"] is None else d["period"],
+        strict_refresh=d["strict_refresh"])
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / (np.abs(b).max() + 1e-30))
+
+
+# ----------------------------------------------------------- functional API
+def test_functional_ops_vs_reference_golden():
+    cfg = cfg_of(json.load(open(os.path.join(G, "tiny_model.json"))))
+    z = load("tiny_model.npz")
+    model = D.init_model(cfg, seed=7)
+    tok = torch.tensor(z["tokens"], dtype=torch.float32, device=dev)
+    blk = D.ActivationBlock(tok, 0)
+    for l in range(2):
+        r = D.gate(model, l, blk)
+        assert np.array_equal(r.expert_ids.cpu().numpy(), z[f"l{l}_ids"])
+        assert rel(r.gates.cpu(), z[f"l{l}_gates"]) < 1e-5
+        assert rel(r.scores.cpu(), z[f"l{l}_scores"]) < 1e-5
+        assert rel(D.local_block(model, l, blk).values.cpu(), z[f"l{l}_local"]) < 2e-2
+        assert rel(D.shared_forward(model, l, blk).cpu(), z[f"l{l}_shared"]) < 2e-2
+        assert rel(D.expert_forward(model, l, 2, tok).cpu(), z[f"l{l}_e2"]) < 2e-2
+        rows = D.routed_rows(model, l, tok, r)
+        assert rel(rows.cpu(), z[f"l{l}_rows"]) < 2e-2
+        act = torch.tensor(z[f"l{l}_act"], device=dev)
+        rows_a = D.routed_rows(model, l, tok, r, act)
+        assert rel(rows_a.cpu(), z[f"l{l}_rows_act"]) < 2e-2
+        ref_route = D.RouteDecision(torch.tensor(z[f"l{l}_ids"], device=dev),
+                                    torch.tensor(z[f"l{l}_gates"], dtype=torch.float32, device=dev),
+                                    torch.tensor(z[f"l{l}_scores"], device=dev))
+        comb = D.combine_outputs(ref_route, torch.tensor(z[f"l{l}_rows"], device=dev),
+                                 torch.tensor(z[f"l{l}_shared"], device=dev), ref_route)
+        assert rel(comb.cpu(), z[f"l{l}_combine"]) < 1e-6
+    x0 = D.sample_x0(cfg, 7)
+    assert rel(x0.values.cpu(), z["x0"]) < 1e-7
+
+
+def test_weights_bit_exact_vs_reference_stream():
+    """Device-generated weights = fp32/bf16 casts of the reference's fp64 weights."""
+    cfg = cfg_of(json.load(open(os.path.join(G, "tiny_model.json"))))
+    z = load("tiny_model.npz")
+    model = D.init_model(cfg, seed=7)
+    h, e = cfg.hidden_dim, cfg.expert_dim
+    bf = lambda a: torch.tensor(a.astype(np.float32)).to(torch.bfloat16).float().numpy()
+    for l in range(2):
+        lw = model.layers[l]
+        assert np.array_equal(lw.w_gate_t[:, :h].cpu().numpy(), z[f"l{l}_w_gate"].T.astype(np.float32))
+        assert np.array_equal(lw.w_mix_t[:h, :h].float().cpu().numpy(), bf(z[f"l{l}_w_mix"].T))
+        for j in range(cfg.num_experts):
+            assert np.array_equal(lw.w1_t[j * model.ep:j * model.ep + e, :h].float().cpu().numpy(),
+                                  bf(z[f"l{l}_e{j}_w1"].T))
+            assert np.array_equal(lw.w2_t[j * model.hp:j * model.hp + h, :e].float().cpu().numpy(),
+                                  bf(z[f"l{l}_e{j}_w2"].T))
+        for i in range(cfg.num_shared):
+            assert np.array_equal(lw.ws2_t[:h, i * model.ep:i * model.ep + e].float().cpu().numpy(),
+                                  bf(z[f"l{l}_s{i}_w2"].T))
+        # pads are zero
+        assert lw.w_mix_t[h:].abs().sum().item() == 0 and lw.w_mix_t[:, h:].abs().sum().item() == 0
+
+
+def test_gate_ties_and_topk_variants():
+    z = load("gate.npz")
+    cfg = D.ModelConfig(num_layers=1, num_experts=8, num_shared=0, top_k=2, hidden_dim=16,
+                        expert_dim=8, num_tokens=64, batch=1, num_steps=1)
+    model = D.init_model(cfg, seed=3)
+    u = torch.tensor(z["u"], dtype=torch.float32, device=dev)
+    r = D.gate(model, 0, D.ActivationBlock(u, 0))
+    ids = r.expert_ids.cpu().numpy()
+    assert ids[0].tolist() == [0, 1] and np.allclose(r.gates[0].cpu().numpy(), [0.5, 0.5])
+    sc = np.sort(z["scores"], axis=1)[:, ::-1]
+    clear = np.all(np.abs(np.diff(sc[:, :3], axis=1)) > TAU, axis=1)
+    assert np.array_equal(ids[clear], z["ids"][clear])
+    for k in (1, 3, 8):
+        mk = D.init_model(D.ModelConfig(**{**cfg.__dict__, "top_k": k}), seed=3)
+        rk = D.gate(mk, 0, D.ActivationBlock(u, 0))
+        sk = np.sort(z["scores"], axis=1)[:, ::-1]
+        gaps = np.abs(np.diff(sk[:, :min(k + 1, 8)], axis=1))
+        ok = np.all(gaps > TAU, axis=1) if gaps.size else np.ones(64, bool)
+        ok[0] = True
+        assert np.array_equal(rk.expert_ids.cpu().numpy()[ok], z[f"ids_k{k}"][ok])
+        assert rel(rk.gates.cpu().numpy()[ok], z[f"gates_k{k}"][ok]) < 1e-5
+
+
+def test_gate_teacher_forced_config1():
+    """Routing ids bit-exact outside the tie band, teacher-forced on the
+    reference's own per-layer MoE inputs at BASELINE config 1 geometry."""
+    meta = json.load(open(os.path.join(G, "config1.json")))
+    z = load("config1.npz")
+    cfg = cfg_of(meta["config"])
+    model = D.init_model(cfg, seed=0)
+    total = excluded = 0
+    for name in ("sync",):
+        u_slice = z[name + "_u_slice"]     # [2 steps, L, 32, h]
+        ids_ref = z[name + "_ids"]         # [2 steps, L, R, k]
+        for si in range(2):
+            for l in range(cfg.num_layers):
+                u = u_slice[si, l]
+                r = D.gate(model, l, D.ActivationBlock(torch.tensor(u, dtype=torch.float32, device=dev), 0))
+                ref = O.route_tokens(u, O.gate_weight(O.Geometry(**meta["config"]), 0, l), cfg.top_k)
+                assert np.array_equal(ref.ids, ids_ref[si, l, :32].astype(np.int64))
+                sc = np.sort(ref.scores, axis=1)[:, ::-1]
+                clear = np.all(np.diff(sc[:, :cfg.top_k + 1], axis=1) < -TAU, axis=1)
+                got = r.expert_ids.cpu().numpy()
+                assert np.array_equal(got[clear], ref.ids[clear])
+                total += len(clear)
+                excluded += int((~clear).sum())
+    assert excluded <= 0.05 * total, (excluded, total)
+
+
+def test_cache_decide_assemble_sequences():
+    z = load("cache.npz")
+    meta = json.load(open(os.path.join(G, "cache.json")))
+    for m in meta:
+        p = f"c{m['case']}_"
+        pol = policy_of(m["policy"])
+        n, k, h, L = m["n"], m["k"], m["h"], m["layers"]
+        cache = D.TokenCache(L, n, k, h, device=dev)
+        i = 0
+        for step in range(m["steps"]):
+            for layer in range(L):
+                ids = torch.tensor(z[p + "ids"][i].astype(np.int64), device=dev)
+                gates = torch.tensor(z[p + "gates"][i], dtype=torch.float32, device=dev)
+                route = D.RouteDecision(ids, gates, torch.zeros(n, 6, device=dev))
+                a, w = cache.decide(layer, step, route, pol, bool(z[p + "force"][i]))
+                assert np.array_equal(a.cpu().numpy(), z[p + "active"][i]), (m["case"], step, layer)
+                assert np.array_equal(w.cpu().numpy(), z[p + "write"][i])
+                fresh = fresh_pattern(step, layer, k, n, h) * z[p + "active"][i].T[:, :, None]
+                rows, g = cache.assemble(layer, torch.tensor(fresh, dtype=torch.float32, device=dev),
+                                         route, a, w)
+                want = torch.tensor(z[p + "rows"][i]).to(torch.bfloat16).float().numpy()
+                assert np.array_equal(rows.cpu().numpy(), want)
+                assert np.array_equal(g.cpu().numpy(), z[p + "outg"][i].astype(np.float32))
+                i += 1
+
+
+RUNS = json.load(open(os.path.join(G, "runs.json")))
+
+
+@pytest.mark.parametrize("idx", range(len(RUNS)))
+def test_engine_runs_vs_reference(idx):
+    m = RUNS[idx]
+    z = load("runs.npz")
+    cfg = cfg_of(m["config"])
+    model = D.init_model(cfg, seed=m["seed"])
+    x0 = D.sample_x0(cfg, m["seed"])
+    res = D.run_sampling(model, x0, D.Strategy(m["strategy"]), policy_of(m["policy"]),
+                         D.ClusterConfig(num_devices=m["devices"]), m["seed"])
+    fin = res.final.values.cpu().numpy().astype(np.float64)
+    ref = z[f"r{idx}_final"]
+    x0n = x0.values.cpu().numpy().astype(np.float64)
+    # free-running: bf16 GEMM noise enters only through eta * h; compare the
+    # accumulated update (final - x0) in relative L2, plus an absolute cap
+    drift_err = np.linalg.norm((fin - x0n) - (ref - x0n)) / np.linalg.norm(ref - x0n)
+    assert drift_err < 3e-2, drift_err
+    assert np.abs(fin - ref).max() < 3e-3
+    st = np.array([(r.layer, r.used_step, r.generated_step) for r in res.staleness_records])
+    assert np.array_equal(st, z[f"r{idx}_staleness"])
+    assert res.peak_buffer_bytes == m["peak_buffer_bytes"]
+    assert (res.active_pairs, res.total_pairs) == (m["active_pairs"], m["total_pairs"])
+    assert res.per_step_active_pairs == z[f"r{idx}_per_step_active"].tolist()
+    assert res.dispatch_bytes == m["dispatch_bytes"]
+    assert res.combine_bytes == m["combine_bytes"]
+
+
+def test_config1_latents_and_staleness_quality():
+    """BASELINE config 1 (S/2-8E2A geometry, R=1024, 10 steps, D=2): final
+    latents vs the reference within 1e-3 abs; staleness MSE per DICE mode vs
+    the GPU's own synchronous path, reported next to the reference's."""
+    meta = json.load(open(os.path.join(G, "config1.json")))
+    z = load("config1.npz")
+    cfg = cfg_of(meta["config"])
+    model = D.init_model(cfg, seed=0)
+    x0 = D.sample_x0(cfg, 0)
+    cl = D.ClusterConfig(num_devices=2)
+    runs = {"sync": (D.Strategy.SYNCHRONOUS, D.NEUTRAL),
+            "interweaved": (D.Strategy.INTERWEAVED, D.NEUTRAL),
+            "dice": (D.Strategy.INTERWEAVED, D.dice_policy())}
+    finals = {}
+    for name, (st, pol) in runs.items():
+        res = D.run_sampling(model, x0, st, pol, cl, 0)
+        finals[name] = res.final.values.cpu().numpy().astype(np.float64)
+        err = np.abs(finals[name] - z[name + "_final"]).max()
+        assert err < 1e-3, (name, err)
+        assert {str(k): v for k, v in res.staleness_histogram().items()} == meta[name]["histogram"]
+        assert res.active_pairs == meta[name]["active_pairs"]
+    for name in ("interweaved", "dice"):
+        d = finals[name] - finals["sync"]
+        mse = float(np.mean(d * d))
+        ref = meta[name]["mse_vs_sync"]
+        print(f"{name}: GPU latent MSE vs GPU sync {mse:.3e}; reference {ref:.3e}")
+        assert 0.25 * ref < mse < 4 * ref

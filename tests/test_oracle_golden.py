@@ -164,3 +164,9 @@ def test_divergence_reports_step():
                    expert_dim=16, num_tokens=4, batch=2, num_steps=8, step_size=1e150)
     with np.errstate(all="ignore"), pytest.raises((O.DivergedAt, O.NonFinite)):
         O.run_schedule(g, O.init_params(g, 7), O.initial_latent(g, 7), O.SYNC, O.Policy(), 2, 7)
+
+
+def test_gate_weight_matches_full_init():
+    g, z = tiny()
+    for l in range(2):
+        assert np.array_equal(O.gate_weight(g, 7, l), z[f"l{l}_w_gate"])
