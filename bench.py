@@ -1,0 +1,320 @@
+"""Benchmark of the B200-native DICE sampling path (BASELINE.json metric).
+
+Workload (BASELINE configs[2], restated at the SURVEY.md §8 XL preset):
+DiT-MoE-XL/2-8E2A toy geometry (L=28, E=8, S=2, k=2, h=1152, e=4608),
+256 px = 256 tokens/image, 32 images per GPU, 50 denoising steps of
+x <- x - eta*h, full DICE = interweaved + Deep selective sync + LowScore
+conditional communication (R=5) + warmup 6 / period 10. Synthetic latents
+and random-init weights from the reference's splitmix64 streams.
+
+One bench "step" = one full 50-step sampling run of the 32-image batch.
+value = images/s (whole job), device-timed with CUDA events; e2e = the same
+metric through the serving call (DeviceRunner.sample: x0 H2D from pinned host
+memory, run, final latent D2H) timed around the call.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DiT-MoE-XL/2 img/s (full-DICE 50-step sampling, 256px, 32 img/GPU)"
+IMAGES_PER_GPU = 32
+PRESET = "xl2-8e2a"
+WORKLOAD = ("DiT-MoE-XL/2-8E2A toy geometry (L=28,E=8,S=2,k=2,h=1152,e=4608), 256 tok/img, "
+            "32 img/GPU, 50-step full-DICE sampling (interweaved+Deep sync+LowScore R=5, W=6, P=10)")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops_sustained"], p["hbm_gbs"], "measured"
+    except Exception:
+        return 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- CPU oracle
+_CPU_PARAMS = []
+
+
+def cpu_sample(threads_note: str):
+    """Oracle (numpy fp64 restatement) timed on a bounded sample of the same
+    workload: one synchronous MoE-layer stage (mixing block, gate, routed
+    experts, shared experts, combine) of XL geometry at 8192 rows, 2 layers.
+    Weight generation is excluded (weights are resident on the GPU side too)."""
+    import numpy as np
+    from oracle import dice_oracle as O
+    g = O.Geometry(**O.PRESETS["xl2-8e2a"], batch=IMAGES_PER_GPU)
+    layers = 2
+    x = O.initial_latent(g, 0)
+    if not _CPU_PARAMS:
+        _CPU_PARAMS.extend(O.init_layer(g, 0, layer) for layer in range(layers))
+    t_compute = 0.0
+    h = x
+    for layer in range(layers):
+        p = _CPU_PARAMS[layer]
+        t0 = time.perf_counter()
+        u = O.mixing_block(p, h)
+        r = O.route_tokens(u, p.w_gate, g.top_k)
+        rows = O.expert_rows(p, u, r)
+        h = u + O.weighted_combine(rows, O.shared_sum(p, u), r.gates)
+        t_compute += time.perf_counter() - t0
+    per_layer = t_compute / layers
+    run_seconds = per_layer * g.num_layers * g.num_steps
+    return {
+        "value": IMAGES_PER_GPU / run_seconds, "unit": "img/s", "cores": os.cpu_count(),
+        "kind": "port",
+        "sample": (f"{layers} synchronous MoE-layer stages (local+gate+8 routed experts+2 shared+"
+                   f"combine) at XL geometry, 8192 rows, fp64 numpy/OpenBLAS ({threads_note}); "
+                   f"{per_layer:.2f} s/layer extrapolated x28 layers x50 steps"),
+        "seconds_per_layer": per_layer,
+    }
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cores = os.cpu_count()
+    vals = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(f"{cores} host threads")
+        if i >= args.warmup:
+            vals.append(s)
+    v = statistics.median([s["value"] for s in vals])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "img/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": IMAGES_PER_GPU / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "img/s", "cores": cores, "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": v, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2411_16786_b200 as D
+    from paper_2411_16786_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = D.preset(PRESET, batch=IMAGES_PER_GPU)
+    seed = 1000 + rank
+    model = D.init_model(cfg, seed=0)
+    x0 = D.sample_x0(cfg, seed)
+    policy = D.dice_policy()
+    # one process per GPU; each rank samples its own 32-image batch (replicas)
+    cluster = D.ClusterConfig(num_devices=1)
+    runner = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed,
+                            time_experts=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        runner.launch()
+    runner.finish()          # raises NumericalDivergenceError on non-finite
+    barrier()
+    runner._expert_events = []
+    l0 = _lib.launch_count[0]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            runner.launch()
+        e1.record()
+        barrier()
+    launches = _lib.launch_count[0] - l0
+    ms = e0.elapsed_time(e1)
+    expert_events = list(runner._expert_events)
+    res = runner.finish()
+    cnt = runner.counters.cpu().numpy()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * IMAGES_PER_GPU * args.steps / (ms / 1e3)
+
+    # roofline: grouped expert FFN (GEMM1 gelu + GEMM2), algorithmic FLOPs over
+    # the active (token, expert) pairs each launch processed
+    h, e = cfg.hidden_dim, cfg.expert_dim
+    pair_flops = 4.0 * h * e
+    flops = sum(pair_flops * cnt[gen, layer, 0] for _, _, gen, layer in expert_events)
+    t_exp = sum(a.elapsed_time(b) for a, b, _, _ in expert_events) * 1e-3
+    n_launch = len(expert_events)
+    achieved = flops / t_exp / 1e12
+    peak_tf, _, peak_kind = peaks()
+
+    # e2e through the serving call with host buffers
+    x0_host = x0.values.cpu().pin_memory()
+    runner.sample(x0_host)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        runner.sample(x0_host)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = world * IMAGES_PER_GPU * args.steps / e2e_s
+    final_dice = runner._final_host.clone().numpy().astype(np.float64)
+
+    # staleness quality: latent MSE of DICE / interweaved vs the synchronous path (same GPU numerics)
+    quality = {}
+    if not args.no_quality:
+        del runner
+        torch.cuda.empty_cache()
+        finals = {"dice": final_dice}
+        for name, st, pol in (("sync", D.Strategy.SYNCHRONOUS, D.NEUTRAL),
+                              ("interweaved", D.Strategy.INTERWEAVED, D.NEUTRAL)):
+            r = D.DeviceRunner(model, x0, st, pol, cluster, seed)
+            finals[name] = r.sample(x0_host).clone().numpy().astype(np.float64)
+            if name == "sync":
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record(); r.launch(); ev1.record(); torch.cuda.synchronize()
+                quality["sync_ms_per_run"] = ev0.elapsed_time(ev1)
+            del r
+            torch.cuda.empty_cache()
+        for name in ("dice", "interweaved"):
+            d = finals[name] - finals["sync"]
+            quality[f"{name}_latent_mse_vs_sync"] = float(np.mean(d * d))
+            quality[f"{name}_rel_l2_vs_sync"] = float(np.linalg.norm(d) / np.linalg.norm(finals["sync"]))
+        quality["speedup_dice_vs_sync"] = quality["sync_ms_per_run"] / ms_per_step
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_sample(f"{os.cpu_count()} host threads")
+    line = {
+        "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 GEMM operands / fp32 accum+residual",
+        "data": "synthetic (splitmix64 latents, random-init weights)",
+        "config": {"workload": WORKLOAD, "images_per_gpu": IMAGES_PER_GPU,
+                   "global_batch": IMAGES_PER_GPU * world, "tokens_per_image": cfg.num_tokens,
+                   "denoise_steps": cfg.num_steps, "eta": cfg.step_size,
+                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu (all 8 experts)",
+                   "l2": "inputs larger than L2: 6.0 GB of bf16 weights streamed per denoising step"},
+        "moe_layer_us": ms_per_step * 1e3 / (cfg.num_steps * cfg.num_layers),
+        "exposed_a2a_us": 0.0,
+        "roofline": {"bound": "tensor", "kernel": "grouped expert FFN (tcgen05 GEMM1+GELU, GEMM2)",
+                     "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tf, "traffic": None,
+                     "peak_kind": f"{peak_kind} bf16 sustained",
+                     "launches": n_launch, "flops_per_pair": pair_flops,
+                     "share_of_step": t_exp / (ms / 1e3)},
+        "e2e": {"value": e2e, "unit": "img/s",
+                "h2d_bytes_per_step": int(x0_host.numel() * 4),
+                "d2h_bytes_per_step": int(x0_host.numel() * 4)},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "quality": quality,
+        "pairs": {"active": res.active_pairs, "total": res.total_pairs},
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-quality", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -180,6 +180,17 @@ def route_tokens(u: np.ndarray, w_gate: np.ndarray, k: int) -> Route:
     return Route(ids.astype(np.int64), picked / picked.sum(axis=1, keepdims=True), scores)
 
 
+def forced_route(u: np.ndarray, w_gate: np.ndarray, ids: np.ndarray) -> Route:
+    """Teacher-forced routing: the given expert ids with gates renormalised
+    from this oracle's own softmax scores (model.py:216-222)."""
+    logits = u @ w_gate
+    ex = np.exp(logits - logits.max(axis=1, keepdims=True))
+    scores = ex / ex.sum(axis=1, keepdims=True)
+    ids = np.asarray(ids, dtype=np.int64)
+    picked = np.take_along_axis(scores, ids, axis=1)
+    return Route(ids, picked / picked.sum(axis=1, keepdims=True), scores)
+
+
 def mlp(x: np.ndarray, w1: np.ndarray, w2: np.ndarray) -> np.ndarray:
     """gelu(x W1) W2 (model.py:226-232)."""
     return gelu(x @ w1) @ w2
@@ -394,7 +405,7 @@ class DivergedAt(Exception):
 
 def run_schedule(g: Geometry, params: list, x0: np.ndarray, strategy: str,
                  policy: Policy, devices: int, seed: int, *, record=False,
-                 layer_limit=None, step_limit=None) -> OracleResult:
+                 layer_limit=None, step_limit=None, forced_ids=None) -> OracleResult:
     """Restatement of ScheduleRunner (schedules.py:142-490).
 
     Per step, per layer: mixing block, gate, then a synchronous, displaced or
@@ -403,7 +414,9 @@ def run_schedule(g: Geometry, params: list, x0: np.ndarray, strategy: str,
     keeps one pending dispatch and one combine slot per layer
     (schedules.py:372-402); the displaced stage keeps a dispatch and a combine
     slot per layer (347-370).  ``layer_limit``/``step_limit`` bound the work
-    for CPU timing samples only.
+    for CPU timing samples only. ``forced_ids[step][layer]`` teacher-forces the
+    routing decisions (e.g. to the ids a device run produced) so schedule
+    accounting and latents can be compared without route-flip amplification.
     """
     if policy.cond_strategy == COND_RANDOM and policy.cond_seed is None:   # schedules.py:158-159
         policy = Policy(**{**policy.__dict__, "cond_seed": seed})
@@ -447,7 +460,10 @@ def run_schedule(g: Geometry, params: list, x0: np.ndarray, strategy: str,
         for layer in range(L):
             p = params[layer]
             u = mixing_block(p, hcur)
-            route = route_tokens(u, p.w_gate, k)
+            if forced_ids is None:
+                route = route_tokens(u, p.w_gate, k)
+            else:
+                route = forced_route(u, p.w_gate, forced_ids[step][layer])
             if strategy == SYNC or sync_step(step, policy.warmup, policy.period) \
                     or layer in sync_set:
                 is_sync = True

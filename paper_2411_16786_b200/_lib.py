@@ -84,7 +84,13 @@ def check(rc: int, what: str) -> None:
     raise exc(f"{what}: rejected by the CUDA library (code {rc})")
 
 
+# kernels each entry point launches (for the bench's gpu_launches count)
+KERNELS_PER_CALL = {"dice_route_permute": 2, "dice_grouped_ffn": 2}
+launch_count = [0]
+
+
 def call(name: str, *args):
     rc = getattr(load(), name)(*args)
     check(rc, name)
+    launch_count[0] += KERNELS_PER_CALL.get(name, 1)
     return rc

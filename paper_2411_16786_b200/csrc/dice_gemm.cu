@@ -16,6 +16,7 @@
 #include "dice_gemm.h"
 #include "dice_ptx.cuh"
 
+#include <climits>
 #include <mutex>
 #include <unordered_map>
 
@@ -28,13 +29,16 @@ constexpr int kThreads = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w1
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 192 ? 5 : 6);
+  static constexpr int kStages = BN == 256 ? 4 : (BN == 192 ? 4 : 6);
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // two accumulator buffers; allocation is a power of two >= 32 columns
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/;
+  // per epilogue warp: a 32x32 fp32 transpose tile (XOR-swizzled, conflict free)
+  static constexpr int kEpiBytes = 8 * 32 * 32 * 4;
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 1024 /*barriers*/;
 };
 
 struct __align__(8) GemmShared {
@@ -53,52 +57,28 @@ __device__ __forceinline__ int find_group(const int* off, int groups, int m_tile
   return g;
 }
 
+// Epilogue on 4 consecutive columns per lane: 8 lanes cover the 32 columns of
+// one output row, a warp covers 4 rows per pass, so residual loads and f32 /
+// bf16 stores are coalesced 128-byte / 64-byte row segments.
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, int row, int col, uint32_t (&r)[32]) {
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+__device__ __forceinline__ void epilogue_vec4(const GemmArgs& a, int64_t row, int col, float4 v) {
   if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    v.x = gelu_erf(v.x); v.y = gelu_erf(v.y); v.z = gelu_erf(v.z); v.w = gelu_erf(v.w);
   }
   if constexpr (EPI == EPI_GELU_RESID) {
-    const float4* res = reinterpret_cast<const float4*>(a.residual + (int64_t)row * a.ld_res + col);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 t = res[q];
-      v[4 * q + 0] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
-    }
+    const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
+    v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
   }
   if constexpr (EPI == EPI_CONSUME) {
-    const float4* res = reinterpret_cast<const float4*>(a.residual + (int64_t)row * a.ld_res + col);
-    const float4* add = reinterpret_cast<const float4*>(a.addend + (int64_t)row * a.ld_add + col);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 t = res[q], s = add[q];
-      v[4 * q + 0] = t.x + (v[4 * q + 0] + s.x);
-      v[4 * q + 1] = t.y + (v[4 * q + 1] + s.y);
-      v[4 * q + 2] = t.z + (v[4 * q + 2] + s.z);
-      v[4 * q + 3] = t.w + (v[4 * q + 3] + s.w);
-    }
+    const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
+    const float4 q = *reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col);
+    v.x = r.x + (v.x + q.x); v.y = r.y + (v.y + q.y); v.z = r.z + (v.z + q.z); v.w = r.w + (v.w + q.w);
   }
-  if (a.out_f32 != nullptr) {
-    float4* dst = reinterpret_cast<float4*>(a.out_f32 + (int64_t)row * a.ld_f32 + col);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  }
+  if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = v;
   if (a.out_bf16 != nullptr) {
-    uint4* dst = reinterpret_cast<uint4*>(a.out_bf16 + (int64_t)row * a.ld_bf16 + col);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t w[4];
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * q + 2 * p], v[8 * q + 2 * p + 1]);
-        w[p] = *reinterpret_cast<uint32_t*>(&b2);
-      }
-      dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
   }
 }
 
@@ -111,7 +91,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + C::kStages * C::kABytes;
-  GemmShared* sh = reinterpret_cast<GemmShared*>(smem + C::kStages * C::kStageBytes);
+  float* sm_epi = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
+  GemmShared* sh = reinterpret_cast<GemmShared*>(smem + C::kStages * C::kStageBytes + C::kEpiBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -196,6 +177,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     // --------------------------------------------------------------- epilogue
     const int sub = warp & 3;            // TMEM lane quadrant this warp may access
     const int half = (warp - 4) >> 2;    // which half of the BN columns
+    float* stage = sm_epi + (warp - 4) * 1024;
+    const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int m_tile = tile % m_tiles;
@@ -204,16 +187,32 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&sh->tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_tile * BM + sub * 32 + lane;
-      const bool row_ok = args.group_tile_offsets != nullptr || row < args.M_valid;
+      const int row0 = m_tile * BM + sub * 32;
 #pragma unroll 1
       for (int c = 0; c < BN / 2; c += 32) {
         const int col_in_tile = half * (BN / 2) + c;
-        const int col = n_blk * BN + col_in_tile;
+        const int col0 = n_blk * BN + col_in_tile;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN + col_in_tile, r);
         tmem_ld_wait();
-        if (row_ok && col < args.N) epilogue_chunk<EPI>(args, row, col, r);
+        if (col0 >= args.N) continue;  // warp-uniform
+        // transpose through shared memory (16-byte chunks XOR-swizzled by row):
+        // thread = row on the way in, 8 lanes per row x 4 columns on the way out
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stage + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        __syncwarp();
+        const int q = lane & 7;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + (lane >> 3);
+          const int row = row0 + rr;
+          const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
+          if (row < row_limit) epilogue_vec4<EPI>(args, row, col0 + 4 * q, v);
+        }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();

@@ -75,85 +75,119 @@ __global__ void splitmix_bits_kernel(uint64_t seed, uint64_t start, int64_t coun
 // reduced with butterfly shuffles; softmax; stable top-k by (score desc, id asc)
 // (model.py:215-222).
 template <int EMAX>
-__global__ void gate_topk_kernel(const float* __restrict__ u, const float* __restrict__ wt,
-                                 int64_t n, int hp, int E, int k, int32_t* __restrict__ ids,
-                                 float* __restrict__ gates, float* __restrict__ scores,
-                                 int32_t* status, int step, int layer) {
+__device__ __forceinline__ void gate_finish(float (&acc)[EMAX], int E, int k, int64_t t, int lane,
+                                            int32_t* __restrict__ ids, float* __restrict__ gates,
+                                            float* __restrict__ scores) {
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    if (e < E) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    }
+  }
+  // softmax over the E logits (model.py:216-218)
+  float mx = acc[0];
+#pragma unroll
+  for (int e = 1; e < EMAX; ++e) if (e < E) mx = fmaxf(mx, acc[e]);
+  float sum = 0.f;
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) if (e < E) { acc[e] = expf(acc[e] - mx); sum += acc[e]; }
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) if (e < E) acc[e] = acc[e] / sum;
+  if (scores != nullptr) {
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) if (e < E && (e & 31) == lane) scores[t * E + e] = acc[e];
+  }
+  if (lane == 0) {
+    // stable top-k on scores: strictly greater wins, so ties keep the lower id
+    uint64_t taken = 0;
+    int pick[EMAX];
+    float pv[EMAX];
+    float psum = 0.f;
+    for (int j = 0; j < k; ++j) {
+      int best = -1;
+      float bv = 0.f;
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e) {
+        if (e < E && !((taken >> e) & 1ull) && (best < 0 || acc[e] > bv)) { best = e; bv = acc[e]; }
+      }
+      taken |= 1ull << best;
+      pick[j] = best;
+      pv[j] = bv;
+      psum += bv;
+    }
+    for (int j = 0; j < k; ++j) {
+      ids[t * k + j] = pick[j];
+      gates[t * k + j] = pv[j] / psum;
+    }
+  }
+}
+
+// One warp per pair of token rows (W_gate^T reads from shared memory are
+// shared by both rows). fp32 dot products reduced with butterfly shuffles,
+// softmax, stable top-k by (score desc, id asc) (model.py:215-222).
+template <int EMAX>
+__global__ void __launch_bounds__(512) gate_topk_kernel(
+    const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int E, int k,
+    int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
+    int32_t* status, int step, int layer) {
   extern __shared__ float sw[];  // [E, hp]
-  for (int i = threadIdx.x; i < E * hp; i += blockDim.x) sw[i] = wt[i];
+  {
+    const float4* src = reinterpret_cast<const float4*>(wt);
+    float4* dst = reinterpret_cast<float4*>(sw);
+    for (int i = threadIdx.x; i < E * hp / 4; i += blockDim.x) dst[i] = src[i];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
-  for (int64_t t = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5); t < n;
-       t += (int64_t)gridDim.x * warps) {
-    float acc[EMAX];
+  const int64_t pairs = (n + 1) / 2;
+  for (int64_t q = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5); q < pairs;
+       q += (int64_t)gridDim.x * warps) {
+    const int64_t t0 = 2 * q, t1 = 2 * q + 1;
+    const bool has1 = t1 < n;
+    float a0[EMAX], a1[EMAX];
 #pragma unroll
-    for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
+    for (int e = 0; e < EMAX; ++e) { a0[e] = 0.f; a1[e] = 0.f; }
     bool finite = true;
-    const float* row = u + t * hp;
-    for (int c = lane * 4; c < hp; c += 128) {
-      const float4 x = *reinterpret_cast<const float4*>(row + c);
-      finite &= isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w);
+    const float* r0 = u + t0 * hp;
+    const float* r1 = u + (has1 ? t1 : t0) * hp;
+    constexpr int CH = 4;  // 128-column strips per batch: 2*CH 16-byte loads in flight per lane
+    for (int base = 0; base < hp; base += 128 * CH) {
+      float4 xs[CH], ys[CH];
 #pragma unroll
-      for (int e = 0; e < EMAX; ++e) {
-        if (e < E) {
-          const float4 w = *reinterpret_cast<const float4*>(sw + e * hp + c);
-          acc[e] = fmaf(x.x, w.x, acc[e]);
-          acc[e] = fmaf(x.y, w.y, acc[e]);
-          acc[e] = fmaf(x.z, w.z, acc[e]);
-          acc[e] = fmaf(x.w, w.w, acc[e]);
+      for (int j = 0; j < CH; ++j) {
+        const int c = base + 128 * j + lane * 4;
+        if (c < hp) {
+          xs[j] = *reinterpret_cast<const float4*>(r0 + c);
+          ys[j] = *reinterpret_cast<const float4*>(r1 + c);
+        } else {
+          xs[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          ys[j] = xs[j];
         }
       }
-    }
 #pragma unroll
-    for (int e = 0; e < EMAX; ++e) {
-      if (e < E) {
+      for (int j = 0; j < CH; ++j) {
+        const int c = base + 128 * j + lane * 4;
+        if (c >= hp) break;
+        const float4 x = xs[j], y = ys[j];
+        finite &= isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w);
+        finite &= isfinite(y.x) && isfinite(y.y) && isfinite(y.z) && isfinite(y.w);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+        for (int e = 0; e < EMAX; ++e) {
+          if (e < E) {
+            const float4 w = *reinterpret_cast<const float4*>(sw + e * hp + c);
+            a0[e] = fmaf(x.x, w.x, a0[e]); a0[e] = fmaf(x.y, w.y, a0[e]);
+            a0[e] = fmaf(x.z, w.z, a0[e]); a0[e] = fmaf(x.w, w.w, a0[e]);
+            a1[e] = fmaf(y.x, w.x, a1[e]); a1[e] = fmaf(y.y, w.y, a1[e]);
+            a1[e] = fmaf(y.z, w.z, a1[e]); a1[e] = fmaf(y.w, w.w, a1[e]);
+          }
+        }
       }
     }
     finite = __all_sync(0xffffffffu, finite);
     if (!finite && lane == 0) record_nonfinite(status, step, layer);
-    // softmax over the E logits (model.py:216-218)
-    float mx = acc[0];
-#pragma unroll
-    for (int e = 1; e < EMAX; ++e) if (e < E) mx = fmaxf(mx, acc[e]);
-    float sum = 0.f;
-#pragma unroll
-    for (int e = 0; e < EMAX; ++e) if (e < E) { acc[e] = expf(acc[e] - mx); sum += acc[e]; }
-#pragma unroll
-    for (int e = 0; e < EMAX; ++e) if (e < E) acc[e] = acc[e] / sum;
-    if (scores != nullptr) {
-      for (int e = lane; e < E; e += 32) {
-        float v = 0.f;
-#pragma unroll
-        for (int q = 0; q < EMAX; ++q) if (q == e) v = acc[q];
-        scores[t * E + e] = v;
-      }
-    }
-    if (lane == 0) {
-      uint64_t taken = 0;
-      int pick[EMAX];
-      float psum = 0.f;
-      for (int j = 0; j < k; ++j) {
-        int best = -1;
-        float bv = 0.f;
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          if (e < E && !((taken >> e) & 1ull) && (best < 0 || acc[e] > bv)) { best = e; bv = acc[e]; }
-        }
-        taken |= 1ull << best;
-        pick[j] = best;
-        psum += bv;
-        ids[t * k + j] = best;
-      }
-      for (int j = 0; j < k; ++j) {
-        float v = 0.f;
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) if (e == pick[j]) v = acc[e];
-        gates[t * k + j] = v / psum;
-      }
-    }
+    gate_finish<EMAX>(a0, E, k, t0, lane, ids, gates, scores);
+    if (has1) gate_finish<EMAX>(a1, E, k, t1, lane, ids, gates, scores);
   }
 }
 
@@ -310,11 +344,8 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
 
 __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
-    const uint16_t* __restrict__ u16, int hp, uint16_t* __restrict__ x_perm, int32_t* pos,
-    const int32_t* __restrict__ scratch) {
+    int32_t* pos, const int32_t* __restrict__ scratch) {
   __shared__ int wcnt[32][64];
-  __shared__ int rows_of[kPermBlock];
-  __shared__ int src_of[kPermBlock];
   const int64_t P = n * k;
   const int64_t p = (int64_t)blockIdx.x * kPermBlock + threadIdx.x;
   int e = 0, s = 0;
@@ -323,23 +354,30 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
   const bool in_range = p < P;
   if (in_range) valid = pair_of(p, n, k, ids, active, e, t, s);
   const int r = block_rank(valid, e, E, wcnt);
-  int dst = -1;
-  if (valid) {
-    dst = scratch[1 + e] + scratch[2 + E + (int64_t)blockIdx.x * E + e] + r;
-  }
-  if (in_range) pos[t * k + s] = dst;
-  rows_of[threadIdx.x] = dst;
-  src_of[threadIdx.x] = (int)t;
-  __syncthreads();
-  // gather: each warp copies rows of the block's pairs, 16 B per lane per step
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (in_range)
+    pos[t * k + s] = valid ? scratch[1 + e] + scratch[2 + E + (int64_t)blockIdx.x * E + e] + r : -1;
+}
+
+// Row gather x_perm[pos[t, s]] = u16[t]: one warp per (token, slot) pair,
+// 16-byte vector copies, grid over all pairs.
+__global__ void __launch_bounds__(256) permute_gather_kernel(
+    const int32_t* __restrict__ pos, int64_t pairs, const uint16_t* __restrict__ u16, int k,
+    int hp, uint16_t* __restrict__ x_perm) {
+  const int lane = threadIdx.x & 31;
   const int vec = hp / 8;
-  for (int i = warp; i < kPermBlock; i += kPermBlock / 32) {
-    const int d = rows_of[i];
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < pairs;
+       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int d = pos[q];
     if (d < 0) continue;
-    const uint4* src = reinterpret_cast<const uint4*>(u16 + (int64_t)src_of[i] * hp);
+    const int64_t t = q / k;
+    const uint4* src = reinterpret_cast<const uint4*>(u16 + t * hp);
     uint4* out = reinterpret_cast<uint4*>(x_perm + (int64_t)d * hp);
-    for (int c = lane; c < vec; c += 32) out[c] = src[c];
+    uint4 v[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) if (lane + 32 * j < vec) v[j] = src[lane + 32 * j];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) if (lane + 32 * j < vec) out[lane + 32 * j] = v[j];
+    for (int c = lane + 160; c < vec; c += 32) out[c] = src[c];
   }
 }
 
@@ -349,55 +387,77 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
 // row; inactive pairs read the cached row and gate (policies.py:197-202);
 // write pairs persist row / gate / id (policies.py:203-207). write implies
 // active, so no thread reads a cache entry another thread writes.
-__global__ void cache_assemble_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos,
-                                      const uint8_t* __restrict__ active,
-                                      const uint8_t* __restrict__ write,
-                                      const float* __restrict__ gates, const int32_t* __restrict__ ids,
-                                      int64_t n, int k, int hp, uint16_t* cache_rows,
-                                      float* cache_gates, int32_t* cache_ids, float* routed,
-                                      float* rows_out, float* gates_out) {
+__global__ void __launch_bounds__(256) cache_assemble_kernel(
+    const uint16_t* __restrict__ y, const int32_t* __restrict__ pos,
+    const uint8_t* __restrict__ active, const uint8_t* __restrict__ write,
+    const float* __restrict__ gates, const int32_t* __restrict__ ids, int64_t n, int k, int hp,
+    uint16_t* cache_rows, float* cache_gates, int32_t* cache_ids, float* routed, float* rows_out,
+    float* gates_out) {
+  constexpr int KMAX = 8;
+  const int lane = threadIdx.x & 31;
   const int vec = hp / 8;
-  const int64_t total = n * vec;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / vec;
-    const int c = (int)(i - t * vec) * 8;
-    float acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    for (int s = 0; s < k; ++s) {
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    // per-slot metadata, loaded once per warp
+    const uint16_t* src[KMAX];
+    float g[KMAX];
+    bool wr[KMAX];
+    for (int s = 0; s < k && s < KMAX; ++s) {
       const int64_t ps = t * k + s;
       const bool act = active == nullptr || active[ps] != 0;
-      uint4 raw;
-      float g;
+      wr[s] = act && write != nullptr && write[ps] != 0;
       if (act) {
-        raw = *reinterpret_cast<const uint4*>(y + (int64_t)pos[ps] * hp + c);
-        g = gates[ps];
-        if (write != nullptr && write[ps]) {
-          *reinterpret_cast<uint4*>(cache_rows + ((int64_t)s * n + t) * hp + c) = raw;
-          if (c == 0) { cache_gates[ps] = g; cache_ids[ps] = ids[ps]; }
-        }
+        src[s] = y + (int64_t)pos[ps] * hp;
+        g[s] = gates[ps];
       } else if (cache_rows != nullptr) {
-        raw = *reinterpret_cast<const uint4*>(cache_rows + ((int64_t)s * n + t) * hp + c);
-        g = cache_gates[ps];
+        src[s] = cache_rows + ((int64_t)s * n + t) * hp;
+        g[s] = cache_gates[ps];
       } else {  // no cache: inactive pairs stay zero (routed_rows, model.py:262)
-        raw = make_uint4(0, 0, 0, 0);
-        g = 0.f;
+        src[s] = nullptr;
+        g[s] = 0.f;
       }
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw);
-      float v[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) { v[j] = bf16_bits_to_f32(h[j]); acc[j] = fmaf(g, v[j], acc[j]); }
-      if (rows_out != nullptr) {
-        float4* ro = reinterpret_cast<float4*>(rows_out + ((int64_t)s * n + t) * hp + c);
-        ro[0] = make_float4(v[0], v[1], v[2], v[3]);
-        ro[1] = make_float4(v[4], v[5], v[6], v[7]);
+      if (lane == 0) {
+        if (wr[s]) { cache_gates[ps] = g[s]; cache_ids[ps] = ids[ps]; }
+        if (gates_out != nullptr) gates_out[ps] = g[s];
       }
-      if (gates_out != nullptr && c == 0) gates_out[ps] = g;
     }
-    float4* o = reinterpret_cast<float4*>(routed + t * hp + c);
-    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    constexpr int CH = 3;  // 8-column chunks per lane per batch (k*CH loads in flight)
+    for (int base = 0; base < vec; base += 32 * CH) {
+      uint4 raw[KMAX][CH];
+      for (int s = 0; s < k && s < KMAX; ++s) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int c8 = base + 32 * j + lane;
+          raw[s][j] = (src[s] != nullptr && c8 < vec)
+                          ? *reinterpret_cast<const uint4*>(src[s] + c8 * 8)
+                          : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c8 = base + 32 * j + lane;
+        if (c8 >= vec) break;
+        const int c = c8 * 8;
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+        for (int s = 0; s < k && s < KMAX; ++s) {
+          if (wr[s]) *reinterpret_cast<uint4*>(cache_rows + ((int64_t)s * n + t) * hp + c) = raw[s][j];
+          const uint16_t* hv = reinterpret_cast<const uint16_t*>(&raw[s][j]);
+          float v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) { v[q] = bf16_bits_to_f32(hv[q]); acc[q] = fmaf(g[s], v[q], acc[q]); }
+          if (rows_out != nullptr) {
+            float4* ro = reinterpret_cast<float4*>(rows_out + ((int64_t)s * n + t) * hp + c);
+            ro[0] = make_float4(v[0], v[1], v[2], v[3]);
+            ro[1] = make_float4(v[4], v[5], v[6], v[7]);
+          }
+        }
+        float4* o = reinterpret_cast<float4*>(routed + t * hp + c);
+        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
+    }
   }
 }
 
@@ -507,8 +567,9 @@ int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int
   if (E < 1 || E > 64 || k < 1 || k > E || hp % 64 != 0) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
   const size_t smem = (size_t)E * hp * sizeof(float);
-  const int threads = 256;
-  const int grid = grid_for(n, threads / 32);
+  const int threads = 512;
+  int64_t want = ((n + 1) / 2 + 15) / 16;
+  const int grid = (int)(want < 4 * 148 ? (want < 1 ? 1 : want) : 4 * 148);
   cudaStream_t s = (cudaStream_t)stream;
 #define DICE_GATE(EM)                                                                          \
   {                                                                                            \
@@ -568,8 +629,8 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
   permute_count_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, tile_offsets,
                                                      reinterpret_cast<long long*>(counters), devices,
                                                      row0, rows_total, scratch);
-  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, u16, hp, x_perm, pos,
-                                                       scratch);
+  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, pos, scratch);
+  permute_gather_kernel<<<grid_for(P * 32, 256), 256, 0, s>>>(pos, P, u16, k, hp, x_perm);
   return launch_ok();
 }
 
@@ -598,9 +659,9 @@ int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* ac
                         const uint8_t* write, const float* gates, const int32_t* ids, int64_t n, int k,
                         int hp, uint16_t* cache_rows, float* cache_gates, int32_t* cache_ids,
                         float* routed, float* rows_out, float* gates_out, void* stream) {
-  if (hp % 64 != 0 || k < 1) return DICE_ERR_CONTRACT;
+  if (hp % 64 != 0 || k < 1 || k > 8) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
-  cache_assemble_kernel<<<grid_for(n * (hp / 8), 256), 256, 0, (cudaStream_t)stream>>>(
+  cache_assemble_kernel<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(
       y, pos, active, write, gates, ids, n, k, hp, cache_rows, cache_gates, cache_ids, routed,
       rows_out, gates_out);
   return launch_ok();

@@ -172,16 +172,19 @@ class DeviceRunner:
         self._expert_events = []
 
     # ------------------------------------------------------------ helpers
-    def _reset_state(self):
+    def _reset_state(self, x0_device=None):
         cfg = self.cfg
         ops.status_reset(self.status)
         self.counters.zero_()
-        x0 = torch.as_tensor(self.x0.values).to(device=self.dev, dtype=torch.float32).contiguous()
+        x0 = x0_device
+        if x0 is None:
+            x0 = torch.as_tensor(self.x0.values).to(device=self.dev, dtype=torch.float32).contiguous()
         ops.pack_rows(x0, self.hp, self.x32, self.x16)
         if self.cache is not None:
-            c = self.cache
-            c.rows.zero_(); c.gates.zero_(); c.expert_ids.fill_(-1)
-            c.last_refresh.fill_(-(10 ** 9)); c.reduced_mask.zero_(); c.has_subset.zero_()
+            # an unprimed token is due (policies.py:171), and every cache entry is
+            # written at that refresh before it is read, so clearing the primed
+            # flags resets the cache
+            self.cache.has_subset.zero_()
         L = cfg.num_layers
         self.slot_gen = [None] * L          # generating step of each combine slot
         self.dispatch_slot = [None] * L     # displaced only
@@ -334,11 +337,26 @@ class DeviceRunner:
         if self.record_routes:
             self.step_routes.append(routes_here)
 
-    def launch(self):
-        """Enqueue the whole run (no host sync)."""
-        self._reset_state()
+    def launch(self, x0_device=None):
+        """Enqueue the whole run (no host sync). ``x0_device`` (f32 [R, h] on
+        the device) replaces the constructor's x0 for repeated sampling."""
+        self._reset_state(x0_device)
         for step in range(self.cfg.num_steps):
             self._run_step(step)
+
+    def sample(self, x0_host: torch.Tensor) -> torch.Tensor:
+        """Serving entry: x0 from (pinned) host memory -> final latent in host
+        memory. H2D, the full schedule and the D2H read are stream-ordered."""
+        if not hasattr(self, "_x0_stage"):
+            self._x0_stage = torch.empty(self.n, self.cfg.hidden_dim, dtype=torch.float32,
+                                         device=self.dev)
+            self._final_host = torch.empty(self.n, self.cfg.hidden_dim, dtype=torch.float32,
+                                           pin_memory=True)
+        self._x0_stage.copy_(x0_host, non_blocking=True)
+        self.launch(self._x0_stage)
+        self._final_host.copy_(self.x32[:, :self.cfg.hidden_dim], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self._final_host
 
     def finish(self, gpu_seconds=None) -> RunResult:
         """One device->host read of status + counters; build the RunResult."""

@@ -6,7 +6,7 @@ sys.path.insert(0, ".")
 from paper_2411_16786_b200 import ops
 
 dev = "cuda"
-flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+flush = torch.ones(64 * 2 ** 20, dtype=torch.float32, device=dev)  # 256 MB, read to evict L2
 
 
 def bench(M, N, K, epi, reps=20, label=""):
@@ -21,7 +21,7 @@ def bench(M, N, K, epi, reps=20, label=""):
         run()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        flush.sum()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(); run(); e1.record()
         torch.cuda.synchronize()
@@ -34,7 +34,7 @@ def bench(M, N, K, epi, reps=20, label=""):
         A @ B.T
     tt = []
     for _ in range(reps):
-        flush.zero_()
+        flush.sum()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(); A @ B.T; e1.record()
         torch.cuda.synchronize()
