@@ -95,8 +95,8 @@ int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force,
 /* Token permute (block prefix-sum) for routed_rows' (slot, expert) grouping
  * (model.py:255-276) and the all-to-all byte plan (cluster.py:82-109).
  * Pairs (t, s) with active[t, s] (active NULL = all) are assigned rows of the
- * expert-sorted, 128-row-padded buffer: pos[t, s] = row or -1.
- * tile_offsets: int32 [E+1] m-tile prefix per expert (device-resident; feeds
+ * expert-sorted, 256-row-padded buffer: pos[t, s] = row or -1.
+ * tile_offsets: int32 [E+1] 256-row m-tile prefix per expert (device-resident; feeds
  * the grouped GEMM with no host sync). counters: int64 [2] accumulated
  * {active pairs, active pairs whose expert lives off the token's home device}
  * under placement expert_dev = e / (E/D), home = ((row0+t)*D)/R_total.

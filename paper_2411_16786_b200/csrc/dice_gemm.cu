@@ -5,7 +5,7 @@
 //
 // One kernel serves every dense contraction of the MoE layer:
 //   * grouped expert FFN (expert_forward, model.py:226-232): rows of A are the
-//     expert-sorted token rows padded per expert to 128-row tiles; B is the
+//     expert-sorted token rows padded per expert to 256-row tiles; B is the
 //     stacked per-expert weight [G*N, K]; a device-resident tile->expert prefix
 //     (group_tile_offsets) selects the B block per tile, so no host sync.
 //   * shared FFN (shared_forward, model.py:235-241) with the S shared experts
@@ -17,6 +17,7 @@
 #include "dice_ptx.cuh"
 
 #include <climits>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -59,26 +60,52 @@ __device__ __forceinline__ int find_group(const int* off, int groups, int m_tile
 
 // Epilogue on 4 consecutive columns per lane: 8 lanes cover the 32 columns of
 // one output row, a warp covers 4 rows per pass, so residual loads and f32 /
-// bf16 stores are coalesced 128-byte / 64-byte row segments.
+// bf16 stores are coalesced 128-byte / 64-byte row segments. All 8 passes'
+// global loads are issued before any math so their latencies overlap.
 template <int EPI>
-__device__ __forceinline__ void epilogue_vec4(const GemmArgs& a, int64_t row, int col, float4 v) {
-  if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
-    v.x = gelu_erf(v.x); v.y = gelu_erf(v.y); v.z = gelu_erf(v.z); v.w = gelu_erf(v.w);
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, const float* stage, int lane,
+                                               int row0, int row_limit, int col0) {
+  const int q = lane & 7;
+  const int col = col0 + 4 * q;
+  float4 v[8], r[8], ad[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    v[it] = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
   }
-  if constexpr (EPI == EPI_GELU_RESID) {
-    const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
-    v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
+  if constexpr (EPI == EPI_GELU_RESID || EPI == EPI_CONSUME) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int64_t row = row0 + it * 4 + (lane >> 3);
+      if (row < row_limit) {
+        r[it] = __ldg(reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col));
+        if constexpr (EPI == EPI_CONSUME)
+          ad[it] = __ldg(reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col));
+      }
+    }
   }
-  if constexpr (EPI == EPI_CONSUME) {
-    const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
-    const float4 q = *reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col);
-    v.x = r.x + (v.x + q.x); v.y = r.y + (v.y + q.y); v.z = r.z + (v.z + q.z); v.w = r.w + (v.w + q.w);
-  }
-  if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = v;
-  if (a.out_bf16 != nullptr) {
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-    *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
-        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int64_t row = row0 + it * 4 + (lane >> 3);
+    float4 x = v[it];
+    if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
+      x.x = gelu_erf(x.x); x.y = gelu_erf(x.y); x.z = gelu_erf(x.z); x.w = gelu_erf(x.w);
+    }
+    if constexpr (EPI == EPI_GELU_RESID) {
+      x.x += r[it].x; x.y += r[it].y; x.z += r[it].z; x.w += r[it].w;
+    }
+    if constexpr (EPI == EPI_CONSUME) {
+      x.x = r[it].x + (x.x + ad[it].x); x.y = r[it].y + (x.y + ad[it].y);
+      x.z = r[it].z + (x.z + ad[it].z); x.w = r[it].w + (x.w + ad[it].w);
+    }
+    if (row < row_limit) {
+      if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
+      if (a.out_bf16 != nullptr) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+        *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
+            make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      }
+    }
   }
 }
 
@@ -204,14 +231,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
               make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         __syncwarp();
-        const int q = lane & 7;
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int rr = it * 4 + (lane >> 3);
-          const int row = row0 + rr;
-          const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
-          if (row < row_limit) epilogue_vec4<EPI>(args, row, col0 + 4 * q, v);
-        }
+        epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
         __syncwarp();
       }
       tc_fence_before();
@@ -224,6 +244,161 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+// --------------------------------------------------------- CTA-pair kernel
+// cta_group::2: a cluster of two CTAs computes a 256 x BN tile. Each CTA
+// stages its own 128 rows of A and half (BN/2 rows) of B, so per-CTA operand
+// traffic per MMA FLOP is 2/3 of the single-CTA 128 x BN tile; the even CTA
+// issues the pair MMAs and both CTAs drain their 128 TMEM lanes.
+template <int BN>
+struct PairCfg {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = (BN / 2) * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kEpiBytes = 8 * 32 * 32 * 4;
+  static constexpr int kBudget = 232448 - kEpiBytes - 2048;
+  static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 2048;
+};
+
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const GemmArgs args) {
+  using C = PairCfg<BN>;
+  constexpr int kPairM = 2 * BM;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + C::kStages * C::kABytes;
+  float* sm_epi = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
+  GemmShared* sh = reinterpret_cast<GemmShared*>(smem + C::kStages * C::kStageBytes + C::kEpiBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) { mbar_init(&sh->full[s], 2); mbar_init(&sh->empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 16); }
+    fence_barrier_init();
+    if (args.group_tile_offsets != nullptr) {
+      for (int g = 0; g <= args.num_groups; ++g) sh->group_off[g] = args.group_tile_offsets[g];
+      sh->m_tiles = sh->group_off[args.num_groups];
+    } else {
+      sh->group_off[0] = 0;
+      sh->group_off[1] = args.num_m_tiles;
+      sh->m_tiles = args.num_m_tiles;
+    }
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 2) tmem_alloc_pair<C::kTmemCols>(&sh->tmem_base);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+
+  const uint32_t tmem_base = sh->tmem_base;
+  const int m_tiles = sh->m_tiles;  // 256-row tiles
+  const int groups = args.group_tile_offsets != nullptr ? args.num_groups : 1;
+  const int n_blocks = args.num_n_blocks;
+  const int k_blocks = args.num_k_blocks;
+  const int num_tiles = m_tiles * n_blocks;
+  const int pair = blockIdx.x >> 1;
+  const int num_pairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        const int m_tile = tile % m_tiles;
+        const int n_blk = tile / m_tiles;
+        const int g = find_group(sh->group_off, groups, m_tile);
+        const int a_row = m_tile * kPairM + rank * BM;
+        const int b_row = g * args.N + n_blk * BN + rank * (BN / 2);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&sh->empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0), C::kStageBytes);
+          tma_load_2d_pair(smA + stage * C::kABytes, &tmA, &sh->full[stage], kb * BK, a_row);
+          tma_load_2d_pair(smB + stage * C::kBBytes, &tmB, &sh->full[stage], kb * BK, b_row);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kPairM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&sh->full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smA + stage * C::kABytes);
+          const uint32_t b_base = smem_u32(smB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            umma_bf16_pair(d_tmem, umma_desc_sw128(a_base + k * UMMA_K * 2),
+                           umma_desc_sw128(b_base + k * UMMA_K * 2), idesc, (kb | k) != 0);
+          }
+          umma_commit_pair(&sh->empty[stage]);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&sh->tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int sub = warp & 3;
+    const int half = (warp - 4) >> 2;
+    float* stage = sm_epi + (warp - 4) * 1024;
+    const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
+    int local = 0;
+    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+      const int m_tile = tile % m_tiles;
+      const int n_blk = tile / m_tiles;
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&sh->tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row0 = m_tile * kPairM + rank * BM + sub * 32;
+#pragma unroll 1
+      for (int c = 0; c < BN / 2; c += 32) {
+        const int col_in_tile = half * (BN / 2) + c;
+        const int col0 = n_blk * BN + col_in_tile;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN + col_in_tile, r);
+        tmem_ld_wait();
+        if (col0 >= args.N) continue;  // warp-uniform
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stage + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        __syncwarp();
+        epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<C::kTmemCols>(tmem_base);
   }
 }
 
@@ -319,6 +494,37 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int 
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 
+template <int BN, int EPI>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
+                cudaStream_t stream) {
+  using C = PairCfg<BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmemBytes) != cudaSuccess)
+      return DICE_ERR_CUDA;
+    attr_done = true;
+  }
+  int grid = 2 * max_tiles < num_sms() ? 2 * max_tiles : num_sms();
+  grid &= ~1;
+  if (grid <= 0) return 0;
+  gemm_bf16_pair<BN, EPI><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, a);
+  return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
+}
+
+template <int BN>
+int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                  int max_tiles, cudaStream_t s) {
+  switch (epi) {
+    case EPI_STORE_BF16: return launch_pair<BN, EPI_STORE_BF16>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_BF16: return launch_pair<BN, EPI_GELU_BF16>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID>(ta, tb, a, max_tiles, s);
+    case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME>(ta, tb, a, max_tiles, s);
+    default: return DICE_ERR_CONTRACT;
+  }
+}
+
 template <int BN>
 int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                  int max_tiles, cudaStream_t s) {
@@ -334,14 +540,26 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const Ge
 
 }  // namespace
 
+bool use_pair_kernel() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("DICE_GEMM_PAIR");
+    mode = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
   if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
   const int bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
+  // grouped GEMMs always use 256-row tiles (the permute pads experts to 256 rows)
+  const bool pair = p.group_tile_offsets != nullptr || use_pair_kernel();
+  const int tile_m = pair ? 2 * BM : BM;
   CUtensorMap ta, tb;
   int rc = tensor_map(p.A, p.A_rows, p.K, BM, &ta);
   if (rc) return rc;
-  rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, bn, &tb);
+  rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, pair ? bn / 2 : bn, &tb);
   if (rc) return rc;
   GemmArgs a = p.epi;
   a.M_valid = p.M;
@@ -351,9 +569,14 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   a.num_k_blocks = (p.K + BK - 1) / BK;
   a.group_tile_offsets = p.group_tile_offsets;
   a.num_groups = p.num_groups;
-  a.num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + BM - 1) / BM;
+  a.num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + tile_m - 1) / tile_m;
   const int max_tiles = a.num_m_tiles * a.num_n_blocks;
   if (max_tiles == 0) return 0;
+  if (pair) {
+    if (bn == 256) return dispatch_pair<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
+    if (bn == 192) return dispatch_pair<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
+    return dispatch_pair<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
+  }
   if (bn == 256) return dispatch_epi<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
   if (bn == 192) return dispatch_epi<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
   return dispatch_epi<128>(p.epi_kind, ta, tb, a, max_tiles, stream);

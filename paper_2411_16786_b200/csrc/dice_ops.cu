@@ -237,8 +237,9 @@ __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, i
 // expert follow routed_rows' (slot, token-ascending) grouping (model.py:267-275).
 // Block b owns pairs [b*1024, (b+1)*1024). Pass 1 counts per (block, expert)
 // and the last block to finish turns the counts into per-block prefixes and
-// 128-row-padded expert bases; pass 2 recomputes in-block ranks and scatters.
+// 256-row-padded expert bases; pass 2 recomputes in-block ranks and scatters.
 constexpr int kPermBlock = 1024;
+constexpr int kRowTile = 256;  // expert groups padded to the CTA-pair GEMM's 256-row tile
 
 struct PermScratch {
   // scratch layout (int32): [0] done counter, [1..1+E] expert row base,
@@ -334,8 +335,8 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
     int tiles = 0;
     for (int ex = 0; ex < E; ++ex) {
       tile_offsets[ex] = tiles;
-      PermScratch::base(scratch)[ex] = tiles * 128;
-      tiles += (cnt[ex] + 127) / 128;
+      PermScratch::base(scratch)[ex] = tiles * kRowTile;
+      tiles += (cnt[ex] + kRowTile - 1) / kRowTile;
     }
     tile_offsets[E] = tiles;
     *PermScratch::done(scratch) = 0;
@@ -603,8 +604,8 @@ int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, 
 }
 
 int64_t dice_permute_max_rows(int64_t n, int k, int E) {
-  const int64_t tiles = (n * k + 127 * (int64_t)E + 127) / 128;
-  return (tiles < 1 ? 1 : tiles) * 128;
+  const int64_t tiles = (n * k + (kRowTile - 1) * (int64_t)E + kRowTile - 1) / kRowTile;
+  return (tiles < 1 ? 1 : tiles) * kRowTile;
 }
 
 int64_t dice_permute_scratch_ints(int64_t n, int k, int E) {
@@ -637,19 +638,19 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
 int dice_grouped_ffn(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
                      const uint16_t* w2_t, int E, int hp, int ep, const int32_t* tile_offsets,
                      uint16_t* hbuf, uint16_t* y, void* stream) {
-  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % 128 != 0)
+  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0)
     return DICE_ERR_CONTRACT;
   cudaStream_t s = (cudaStream_t)stream;
   GemmProblem p{};
   p.A = x_perm; p.A_rows = max_rows; p.B = w1_t; p.M = (int)max_rows; p.N = ep; p.K = hp;
-  p.num_groups = E; p.group_tile_offsets = tile_offsets; p.max_m_tiles = (int)(max_rows / 128);
+  p.num_groups = E; p.group_tile_offsets = tile_offsets; p.max_m_tiles = (int)(max_rows / kRowTile);
   p.epi_kind = EPI_GELU_BF16;
   p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(hbuf); p.epi.ld_bf16 = ep;
   int rc = gemm_bf16(p, s);
   if (rc) return rc;
   GemmProblem q{};
   q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
-  q.num_groups = E; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / 128);
+  q.num_groups = E; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / kRowTile);
   q.epi_kind = EPI_STORE_BF16;
   q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(y); q.epi.ld_bf16 = hp;
   return gemm_bf16(q, s);
