@@ -53,6 +53,13 @@ extern "C" {
 /* Library version / build identification (sm_100a). */
 int dice_version(void);
 
+/* CUDA events for stage timing that survive CUDA-graph capture (recorded as
+ * external event nodes while the stream is capturing). */
+int dice_event_create(void** event);
+int dice_event_destroy(void* event);
+int dice_event_record(void* event, void* stream);
+int dice_event_elapsed_ms(void* start, void* end, float* ms);
+
 /* status[0] = first step with a non-finite value (INT32_MAX if none),
  * status[1] = layer of the first non-finite gate input, status[2..3] reserved. */
 int dice_status_reset(int32_t* status, void* stream);
@@ -95,7 +102,9 @@ int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force,
 /* Token permute (block prefix-sum) for routed_rows' (slot, expert) grouping
  * (model.py:255-276) and the all-to-all byte plan (cluster.py:82-109).
  * Pairs (t, s) with active[t, s] (active NULL = all) are assigned rows of the
- * expert-sorted, 256-row-padded buffer: pos[t, s] = row or -1.
+ * expert-sorted, 256-row-padded buffer: pos[t, s] = row or -1. Within an
+ * expert, rows follow token-major pair order (deterministic; GEMM rows are
+ * independent so the reference's slot-major grouping changes no value).
  * tile_offsets: int32 [E+1] 256-row m-tile prefix per expert (device-resident; feeds
  * the grouped GEMM with no host sync). counters: int64 [2] accumulated
  * {active pairs, active pairs whose expert lives off the token's home device}
@@ -110,8 +119,7 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
 /* Upper bound of rows of the padded permuted buffer for n*k pairs over E experts. */
 int64_t dice_permute_max_rows(int64_t n, int k, int E);
 
-/* int32 words of scratch dice_route_permute needs; scratch[0] must be zero
- * when first used (the kernel leaves it zero). */
+/* int32 words of scratch dice_route_permute needs (per-block expert counts). */
 int64_t dice_permute_scratch_ints(int64_t n, int k, int E);
 
 /* Grouped expert FFN on the permuted rows (expert_forward, model.py:226-232):

@@ -23,6 +23,10 @@ P = c_void_p
 # name -> (restype, argtypes); mirrors include/dice_b200.h
 SIGNATURES = {
     "dice_version": (c_int, []),
+    "dice_event_create": (c_int, [ctypes.POINTER(c_void_p)]),
+    "dice_event_destroy": (c_int, [P]),
+    "dice_event_record": (c_int, [P, P]),
+    "dice_event_elapsed_ms": (c_int, [P, P, ctypes.POINTER(c_float)]),
     "dice_status_reset": (c_int, [P, P]),
     "dice_splitmix_fill": (c_int, [c_uint64, c_uint64, c_int64, c_int64, c_double, c_int, c_int,
                                    P, c_int64, P]),
@@ -85,7 +89,8 @@ def check(rc: int, what: str) -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches count)
-KERNELS_PER_CALL = {"dice_route_permute": 2, "dice_grouped_ffn": 2}
+KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_grouped_ffn": 2, "dice_event_create": 0,
+                    "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0}
 launch_count = [0]
 
 

@@ -156,8 +156,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_tile = tile % m_tiles;
-        const int n_blk = tile / m_tiles;
+        const int n_blk = tile % n_blocks;   // N-fastest: resident tiles share A rows
+        const int m_tile = tile / n_blocks;
         const int g = find_group(sh->group_off, groups, m_tile);
         const int a_row = m_tile * BM;
         const int b_row = g * args.N + n_blk * BN;
@@ -208,8 +208,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int m_tile = tile % m_tiles;
-      const int n_blk = tile / m_tiles;
+      const int n_blk = tile % n_blocks;
+      const int m_tile = tile / n_blocks;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&sh->tfull[acc], acc_phase);
@@ -314,8 +314,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < num_tiles; tile += num_pairs) {
-        const int m_tile = tile % m_tiles;
-        const int n_blk = tile / m_tiles;
+        const int n_blk = tile % n_blocks;   // N-fastest: resident tiles share A rows
+        const int m_tile = tile / n_blocks;
         const int g = find_group(sh->group_off, groups, m_tile);
         const int a_row = m_tile * kPairM + rank * BM;
         const int b_row = g * args.N + n_blk * BN + rank * (BN / 2);
@@ -365,8 +365,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
     int local = 0;
     for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
-      const int m_tile = tile % m_tiles;
-      const int n_blk = tile / m_tiles;
+      const int n_blk = tile % n_blocks;
+      const int m_tile = tile / n_blocks;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&sh->tfull[acc], acc_phase);

@@ -191,6 +191,132 @@ __global__ void __launch_bounds__(512) gate_topk_kernel(
   }
 }
 
+// Fast gate for E in {8, 16}: two token rows per warp; the 2E per-lane
+// partial dot products are reduced with a transpose-reduce (each butterfly
+// level exchanges half of the remaining values), leaving lane L with the full
+// logit of (row L>>4, expert ...). Softmax and the stable top-k ranking
+// (score desc, id asc; model.py:216-222) are then done lane-parallel within
+// each row's 16-lane group.
+template <int N>
+__device__ __forceinline__ void tr_level(float (&a)[32], int lane, int off) {
+  const bool upper = (lane & off) != 0;
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j) {
+    const float send = upper ? a[j] : a[j + N / 2];
+    const float keep = upper ? a[j + N / 2] : a[j];
+    a[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+  }
+}
+
+template <int E>
+__global__ void __launch_bounds__(512) gate_topk_fast_kernel(
+    const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
+    int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
+    int32_t* status, int step, int layer) {
+  static_assert(E == 8 || E == 16, "fast gate handles E = 8 or 16");
+  constexpr int V = 2 * E;
+  constexpr int DUP = E == 8 ? 2 : 1;   // lanes holding the same (row, expert)
+  extern __shared__ float sw[];         // [E, hp]
+  {
+    const float4* src = reinterpret_cast<const float4*>(wt);
+    float4* dst = reinterpret_cast<float4*>(sw);
+    for (int i = threadIdx.x; i < E * hp / 4; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int64_t pairs = (n + 1) / 2;
+  for (int64_t q = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5); q < pairs;
+       q += (int64_t)gridDim.x * warps) {
+    const int64_t t0 = 2 * q;
+    const bool has1 = t0 + 1 < n;
+    const float* r0 = u + t0 * hp;
+    const float* r1 = u + (has1 ? t0 + 1 : t0) * hp;
+    float a[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = 0.f;
+    constexpr int CH = 4;
+    for (int base = 0; base < hp; base += 128 * CH) {
+      float4 xs[CH], ys[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = base + 128 * j + lane * 4;
+        if (c < hp) {
+          xs[j] = __ldg(reinterpret_cast<const float4*>(r0 + c));
+          ys[j] = __ldg(reinterpret_cast<const float4*>(r1 + c));
+        } else {
+          xs[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          ys[j] = xs[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = base + 128 * j + lane * 4;
+        if (c >= hp) break;
+        const float4 x = xs[j], y = ys[j];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float4 w = *reinterpret_cast<const float4*>(sw + e * hp + c);
+          a[e] = fmaf(x.x, w.x, a[e]); a[e] = fmaf(x.y, w.y, a[e]);
+          a[e] = fmaf(x.z, w.z, a[e]); a[e] = fmaf(x.w, w.w, a[e]);
+          a[E + e] = fmaf(y.x, w.x, a[E + e]); a[E + e] = fmaf(y.y, w.y, a[E + e]);
+          a[E + e] = fmaf(y.z, w.z, a[E + e]); a[E + e] = fmaf(y.w, w.w, a[E + e]);
+        }
+      }
+    }
+    // transpose-reduce: V values -> 1 value per lane
+    if constexpr (V == 32) {
+      tr_level<32>(a, lane, 16); tr_level<16>(a, lane, 8); tr_level<8>(a, lane, 4);
+      tr_level<4>(a, lane, 2); tr_level<2>(a, lane, 1);
+    } else {
+      tr_level<16>(a, lane, 16); tr_level<8>(a, lane, 8); tr_level<4>(a, lane, 4);
+      tr_level<2>(a, lane, 2);
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+    }
+    const float logit = a[0];
+    const int row = lane >> 4;                      // 0 or 1
+    const int e_me = (lane & 15) / DUP;             // expert held by this lane
+    const int64_t t = t0 + row;
+    const bool row_ok = row == 0 || has1;
+    // non-finite MoE input shows up as a non-finite logit (model.py:212-213)
+    const bool bad = !isfinite(logit) && row_ok;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) record_nonfinite(status, step, layer);
+    // softmax within the row group (offsets 1..8 cover the 16 lanes of a row)
+    float mx = logit;
+#pragma unroll
+    for (int off = DUP; off < 16; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const float ex = expf(logit - mx);
+    float sum = ex;
+#pragma unroll
+    for (int off = DUP; off < 16; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    const float sc = ex / sum;
+    // rank = #experts with a higher score, or an equal score and a lower id
+    const int rowbase = row * 16;
+    int rank = 0;
+#pragma unroll
+    for (int qe = 0; qe < E; ++qe) {
+      const float sq = __shfl_sync(0xffffffffu, sc, rowbase + qe * DUP);
+      rank += (sq > sc) || (sq == sc && qe < e_me);
+    }
+    const bool primary = (lane % DUP) == 0;
+    if (scores != nullptr && primary && row_ok) scores[t * E + e_me] = sc;
+    const unsigned rowmask = row == 0 ? 0x0000ffffu : 0xffff0000u;
+    float psum = 0.f, my_s = 0.f;
+    int my_e = 0;
+    for (int j = 0; j < k; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, primary && rank == j) & rowmask;
+      const int src = __ffs(m) - 1;
+      const float sj = __shfl_sync(0xffffffffu, sc, src);
+      psum += sj;
+      if ((lane & 15) == j) { my_s = sj; my_e = (src & 15) / DUP; }
+    }
+    if ((lane & 15) < k && row_ok) {
+      ids[t * k + (lane & 15)] = my_e;
+      gates[t * k + (lane & 15)] = my_s / psum;
+    }
+  }
+}
+
 // ------------------------------------------------------------ cond decide
 // Per token (policies.py:159-186): due = force | !primed | (step - last) >= R;
 // due tokens redraw the reduced-slot subset (policies.py:118-139) and reset the
@@ -233,33 +359,26 @@ __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, i
 }
 
 // ------------------------------------------------------------- permute
-// Pairs are visited in slot-major order p = s*n + t, so positions within an
-// expert follow routed_rows' (slot, token-ascending) grouping (model.py:267-275).
-// Block b owns pairs [b*1024, (b+1)*1024). Pass 1 counts per (block, expert)
-// and the last block to finish turns the counts into per-block prefixes and
-// 256-row-padded expert bases; pass 2 recomputes in-block ranks and scatters.
+// Pairs are visited in token-major order p = t*k + s; within an expert the
+// rows are ordered by p, a deterministic order (the GEMM rows are independent,
+// so the grouping order of routed_rows, model.py:267-275, does not change any
+// value). Block b owns pairs [b*1024, (b+1)*1024): the count kernel writes the
+// per-(block, expert) counts; the scatter kernel derives its block prefix and
+// the 256-row-padded expert bases from all blocks' counts (no grid-wide sync)
+// and assigns positions from warp-level match ranks.
 constexpr int kPermBlock = 1024;
 constexpr int kRowTile = 256;  // expert groups padded to the CTA-pair GEMM's 256-row tile
 
-struct PermScratch {
-  // scratch layout (int32): [0] done counter, [1..1+E] expert row base,
-  // [2+E .. 2+E+nb*E) per-block prefix, followed by nothing.
-  __device__ static int* done(int32_t* s) { return s; }
-  __device__ static int* base(int32_t* s) { return s + 1; }
-  __device__ static int* blk(int32_t* s, int E, int b) { return s + 2 + E + (int64_t)b * E; }
-};
-
-__device__ __forceinline__ bool pair_of(int64_t p, int64_t n, int k, const int32_t* ids,
+__device__ __forceinline__ bool pair_of(int64_t p, int k, const int32_t* ids,
                                         const uint8_t* active, int& e, int64_t& t, int& s) {
-  s = (int)(p / n);
-  t = p - (int64_t)s * n;
-  e = ids[t * k + s];
-  return active == nullptr || active[t * k + s] != 0;
+  t = p / k;
+  s = (int)(p - t * k);
+  e = ids[p];
+  return active == nullptr || active[p] != 0;
 }
 
 // Rank of this thread's pair among earlier pairs of the same expert in its
-// block; fills wcnt[warp][e] with per-warp counts turned into exclusive
-// prefixes over warps. Returns rank within the block.
+// block (wcnt: per-warp counts turned into exclusive prefixes over warps).
 __device__ __forceinline__ int block_rank(bool valid, int e, int E, int (*wcnt)[64]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
@@ -279,11 +398,9 @@ __device__ __forceinline__ int block_rank(bool valid, int e, int E, int (*wcnt)[
 
 __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
-    int32_t* tile_offsets, long long* counters, int devices, int64_t row0, int64_t rows_total,
-    int32_t* scratch) {
+    long long* counters, int devices, int64_t row0, int64_t rows_total, int32_t* block_counts) {
   __shared__ int cnt[64];
   __shared__ unsigned long long red[2];
-  __shared__ bool is_last;
   if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 2) red[threadIdx.x] = 0;
   __syncthreads();
@@ -292,7 +409,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
   int e = 0, s = 0;
   int64_t t = 0;
   bool valid = false;
-  if (p < P) valid = pair_of(p, n, k, ids, active, e, t, s);
+  if (p < P) valid = pair_of(p, k, ids, active, e, t, s);
   const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : -1);
   const int lane = threadIdx.x & 31;
   if (valid && __popc(peers & ((1u << lane) - 1)) == 0) atomicAdd(&cnt[e], __popc(peers));
@@ -305,58 +422,52 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
   }
   const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
   const unsigned nr = __popc(__ballot_sync(0xffffffffu, remote));
-  if (lane == 0) { atomicAdd(&red[0], (unsigned long long)nv); atomicAdd(&red[1], (unsigned long long)nr); }
+  if (lane == 0 && nv) atomicAdd(&red[0], (unsigned long long)nv);
+  if (lane == 0 && nr) atomicAdd(&red[1], (unsigned long long)nr);
   __syncthreads();
-  if (threadIdx.x < E) PermScratch::blk(scratch, E, blockIdx.x)[threadIdx.x] = cnt[threadIdx.x];
+  if (threadIdx.x < E) block_counts[(int64_t)blockIdx.x * E + threadIdx.x] = cnt[threadIdx.x];
   if (threadIdx.x == 0 && counters != nullptr) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&counters[0]), red[0]);
     atomicAdd(reinterpret_cast<unsigned long long*>(&counters[1]), red[1]);
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(PermScratch::done(scratch), 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  // last block: per-expert exclusive prefix over blocks, padded bases, tile offsets
-  if (threadIdx.x < E) {
-    const int ex = threadIdx.x;
-    int acc = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      volatile int* q = PermScratch::blk(scratch, E, b);
-      const int c = q[ex];
-      q[ex] = acc;
-      acc += c;
-    }
-    cnt[ex] = acc;  // total pairs of expert ex
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tiles = 0;
-    for (int ex = 0; ex < E; ++ex) {
-      tile_offsets[ex] = tiles;
-      PermScratch::base(scratch)[ex] = tiles * kRowTile;
-      tiles += (cnt[ex] + kRowTile - 1) / kRowTile;
-    }
-    tile_offsets[E] = tiles;
-    *PermScratch::done(scratch) = 0;
   }
 }
 
 __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
-    int32_t* pos, const int32_t* __restrict__ scratch) {
+    int32_t* pos, const int32_t* __restrict__ block_counts, int32_t* tile_offsets) {
   __shared__ int wcnt[32][64];
+  __shared__ int base[64];
+  const int nb = gridDim.x;
+  if (threadIdx.x < E) {
+    int before = 0, total = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int c = block_counts[(int64_t)b * E + threadIdx.x];
+      if (b < (int)blockIdx.x) before += c;
+      total += c;
+    }
+    wcnt[0][threadIdx.x] = total;
+    base[threadIdx.x] = before;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tiles = 0;
+    for (int ex = 0; ex < E; ++ex) {
+      if (blockIdx.x == 0) tile_offsets[ex] = tiles;
+      base[ex] += tiles * kRowTile;
+      tiles += (wcnt[0][ex] + kRowTile - 1) / kRowTile;
+    }
+    if (blockIdx.x == 0) tile_offsets[E] = tiles;
+  }
+  __syncthreads();
   const int64_t P = n * k;
   const int64_t p = (int64_t)blockIdx.x * kPermBlock + threadIdx.x;
   int e = 0, s = 0;
   int64_t t = 0;
   bool valid = false;
   const bool in_range = p < P;
-  if (in_range) valid = pair_of(p, n, k, ids, active, e, t, s);
+  if (in_range) valid = pair_of(p, k, ids, active, e, t, s);
   const int r = block_rank(valid, e, E, wcnt);
-  if (in_range)
-    pos[t * k + s] = valid ? scratch[1 + e] + scratch[2 + E + (int64_t)blockIdx.x * E + e] + r : -1;
+  if (in_range) pos[p] = valid ? base[e] + r : -1;
 }
 
 // Row gather x_perm[pos[t, s]] = u16[t]: one warp per (token, slot) pair,
@@ -541,6 +652,32 @@ extern "C" {
 
 int dice_version(void) { return 100; }
 
+int dice_event_create(void** event) {
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return DICE_ERR_CUDA;
+  *event = (void*)e;
+  return DICE_OK;
+}
+
+int dice_event_destroy(void* event) {
+  return cudaEventDestroy((cudaEvent_t)event) == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+}
+
+// Records as an event node when the stream is being captured into a CUDA
+// graph (cudaEventRecordExternal), so graph replays keep per-kernel timing.
+int dice_event_record(void* event, void* stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing((cudaStream_t)stream, &st);
+  const unsigned flags = st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0;
+  return cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, flags) == cudaSuccess
+             ? DICE_OK : DICE_ERR_CUDA;
+}
+
+int dice_event_elapsed_ms(void* start, void* end, float* ms) {
+  return cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end) == cudaSuccess
+             ? DICE_OK : DICE_ERR_CUDA;
+}
+
 int dice_status_reset(int32_t* status, void* stream) {
   status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status);
   return launch_ok();
@@ -584,10 +721,24 @@ int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int
                                                      scores, status, step, layer);             \
   }
   if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
-  if (E <= 8) DICE_GATE(8)
+#define DICE_GATE_FAST(EE)                                                                     \
+  {                                                                                            \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(gate_topk_fast_kernel<EE>,                                          \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);           \
+      attr = true;                                                                             \
+    }                                                                                          \
+    gate_topk_fast_kernel<EE><<<grid, threads, smem, s>>>(u, w_gate_t, n, hp, k, ids, gates,   \
+                                                          scores, status, step, layer);        \
+  }
+  if (E == 8 && k <= 8) DICE_GATE_FAST(8)
+  else if (E == 16 && k <= 16) DICE_GATE_FAST(16)
+  else if (E <= 8) DICE_GATE(8)
   else if (E <= 16) DICE_GATE(16)
   else DICE_GATE(64)
 #undef DICE_GATE
+#undef DICE_GATE_FAST
   return launch_ok();
 }
 
@@ -610,7 +761,7 @@ int64_t dice_permute_max_rows(int64_t n, int k, int E) {
 
 int64_t dice_permute_scratch_ints(int64_t n, int k, int E) {
   const int64_t blocks = (n * k + kPermBlock - 1) / kPermBlock;
-  return 2 + E + (blocks < 1 ? 1 : blocks) * E;
+  return (blocks < 1 ? 1 : blocks) * E;
 }
 
 int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
@@ -627,10 +778,11 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
     cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (E + 1), s);
     return launch_ok();
   }
-  permute_count_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, tile_offsets,
+  permute_count_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E,
                                                      reinterpret_cast<long long*>(counters), devices,
                                                      row0, rows_total, scratch);
-  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, pos, scratch);
+  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, pos, scratch,
+                                                       tile_offsets);
   permute_gather_kernel<<<grid_for(P * 32, 256), 256, 0, s>>>(pos, P, u16, k, hp, x_perm);
   return launch_ok();
 }

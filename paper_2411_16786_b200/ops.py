@@ -38,6 +38,31 @@ def _need(t, dtype, what):
         raise ContractError(f"{what}: expected a contiguous tensor")
 
 
+class DeviceEvent:
+    """CUDA event usable inside CUDA-graph capture (external event node)."""
+
+    def __init__(self):
+        import ctypes
+        h = ctypes.c_void_p()
+        _lib.call("dice_event_create", ctypes.byref(h))
+        self.handle = h
+
+    def record(self):
+        _lib.call("dice_event_record", self.handle, _stream())
+
+    def elapsed_ms(self, end: "DeviceEvent") -> float:
+        import ctypes
+        ms = ctypes.c_float()
+        _lib.call("dice_event_elapsed_ms", self.handle, end.handle, ctypes.byref(ms))
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            _lib.load().dice_event_destroy(self.handle)
+        except Exception:
+            pass
+
+
 def status_reset(status):
     _lib.call("dice_status_reset", _ptr(status), _stream())
 

@@ -170,6 +170,9 @@ class DeviceRunner:
         self.status = torch.empty(4, dtype=torch.int32, device=dev)
         self.sync_layers = select_sync_layers(policy.sync_strategy, L, policy.explicit_layers)
         self._expert_events = []
+        self._event_pool = []
+        self.graph = None
+        self.launches_per_run = 0
 
     # ------------------------------------------------------------ helpers
     def _reset_state(self, x0_device=None):
@@ -196,7 +199,7 @@ class DeviceRunner:
         self.dispatch_log = []
         self.combine_log = []
         self.step_inputs, self.step_routes = [], []
-        self._expert_events = []
+        self._expert_events = []  # (start, end, generated step, layer) of each expert-FFN launch
 
     def _track(self, kind, layer):
         self.occupied.add((kind, layer))
@@ -247,8 +250,10 @@ class DeviceRunner:
         combine slot (_process_dispatch, schedules.py:388-397)."""
         lw = self.model.layers[p.layer]
         if self.time_experts:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            i = len(self._expert_events)
+            if i >= len(self._event_pool):
+                self._event_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
+            e0, e1 = self._event_pool[i]
             e0.record()
         ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
         if self.time_experts:
@@ -339,17 +344,43 @@ class DeviceRunner:
 
     def launch(self, x0_device=None):
         """Enqueue the whole run (no host sync). ``x0_device`` (f32 [R, h] on
-        the device) replaces the constructor's x0 for repeated sampling."""
+        the device) replaces the constructor's x0 for repeated sampling. With a
+        captured graph this is one graph launch."""
+        if self.graph is not None:
+            if x0_device is not None and x0_device.data_ptr() != self._x0_graph.data_ptr():
+                self._x0_graph.copy_(x0_device)
+            self.graph.replay()
+            return
+        from . import _lib
+        c0 = _lib.launch_count[0]
         self._reset_state(x0_device)
         for step in range(self.cfg.num_steps):
             self._run_step(step)
+        self.launches_per_run = _lib.launch_count[0] - c0
+
+    def capture(self):
+        """Capture one whole sampling run into a CUDA graph. The schedule's
+        control flow is host-deterministic and every buffer is static, so the
+        graph replays the identical kernel sequence; x0 is read from a static
+        staging buffer (see sample())."""
+        self._x0_graph = torch.as_tensor(self.x0.values).to(
+            device=self.dev, dtype=torch.float32).contiguous().clone()
+        self.launch(self._x0_graph)          # warm: kernel attributes, tensor maps
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch(self._x0_graph)
+        torch.cuda.synchronize()
+        self.graph = g
+        return self
 
     def sample(self, x0_host: torch.Tensor) -> torch.Tensor:
         """Serving entry: x0 from (pinned) host memory -> final latent in host
         memory. H2D, the full schedule and the D2H read are stream-ordered."""
-        if not hasattr(self, "_x0_stage"):
-            self._x0_stage = torch.empty(self.n, self.cfg.hidden_dim, dtype=torch.float32,
-                                         device=self.dev)
+        if not hasattr(self, "_final_host"):
+            self._x0_stage = (self._x0_graph if self.graph is not None else
+                              torch.empty(self.n, self.cfg.hidden_dim, dtype=torch.float32,
+                                          device=self.dev))
             self._final_host = torch.empty(self.n, self.cfg.hidden_dim, dtype=torch.float32,
                                            pin_memory=True)
         self._x0_stage.copy_(x0_host, non_blocking=True)
@@ -375,7 +406,7 @@ class DeviceRunner:
                                 generated_step=cfg.num_steps)
         timeline = None
         if gpu_seconds is not None or self._expert_events:
-            timeline = {"expert_ffn_ms": [a.elapsed_time(b) for a, b, _, _ in self._expert_events]}
+            timeline = {"expert_ffn_ms": [a.elapsed_ms(b) for a, b, _, _ in self._expert_events]}
         return RunResult(
             final=final, timeline=timeline, staleness_records=self.records,
             strategy=self.strategy, policy=self.policy, seed=self.seed,
