@@ -26,18 +26,21 @@ namespace dice {
 constexpr int BM = 128;
 constexpr int BK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int UMMA_K = 16;
-constexpr int kThreads = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
+constexpr int kEpiWarps = 12;   // 3 per TMEM lane quadrant
+constexpr int kEpiGroups = kEpiWarps / 4;
+constexpr int kThreads = 128 + 32 * kEpiWarps;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4.. epilogue
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 192 ? 4 : 6);
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStagesFit = (232448 - kEpiWarps * 4096 - 2048) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   // two accumulator buffers; allocation is a power of two >= 32 columns
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   // per epilogue warp: a 32x32 fp32 transpose tile (XOR-swizzled, conflict free)
-  static constexpr int kEpiBytes = 8 * 32 * 32 * 4;
+  static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;
   static constexpr int kSmemBytes =
       kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 1024 /*barriers*/;
 };
@@ -67,43 +70,46 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, const float* s
                                                int row0, int row_limit, int col0) {
   const int q = lane & 7;
   const int col = col0 + 4 * q;
-  float4 v[8], r[8], ad[8];
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int rr = it * 4 + (lane >> 3);
-    v[it] = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
-  }
-  if constexpr (EPI == EPI_GELU_RESID || EPI == EPI_CONSUME) {
+  for (int half = 0; half < 2; ++half) {
+    float4 v[4], r[4], ad[4];
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int64_t row = row0 + it * 4 + (lane >> 3);
-      if (row < row_limit) {
-        r[it] = __ldg(reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col));
-        if constexpr (EPI == EPI_CONSUME)
-          ad[it] = __ldg(reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col));
+    for (int it = 0; it < 4; ++it) {
+      const int rr = (half * 4 + it) * 4 + (lane >> 3);
+      v[it] = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
+    }
+    if constexpr (EPI == EPI_GELU_RESID || EPI == EPI_CONSUME) {
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int64_t row = row0 + (half * 4 + it) * 4 + (lane >> 3);
+        if (row < row_limit) {
+          r[it] = __ldg(reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col));
+          if constexpr (EPI == EPI_CONSUME)
+            ad[it] = __ldg(reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col));
+        }
       }
     }
-  }
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int64_t row = row0 + it * 4 + (lane >> 3);
-    float4 x = v[it];
-    if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
-      x.x = gelu_erf(x.x); x.y = gelu_erf(x.y); x.z = gelu_erf(x.z); x.w = gelu_erf(x.w);
-    }
-    if constexpr (EPI == EPI_GELU_RESID) {
-      x.x += r[it].x; x.y += r[it].y; x.z += r[it].z; x.w += r[it].w;
-    }
-    if constexpr (EPI == EPI_CONSUME) {
-      x.x = r[it].x + (x.x + ad[it].x); x.y = r[it].y + (x.y + ad[it].y);
-      x.z = r[it].z + (x.z + ad[it].z); x.w = r[it].w + (x.w + ad[it].w);
-    }
-    if (row < row_limit) {
-      if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
-      if (a.out_bf16 != nullptr) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
-        *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
-            make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    for (int it = 0; it < 4; ++it) {
+      const int64_t row = row0 + (half * 4 + it) * 4 + (lane >> 3);
+      float4 x = v[it];
+      if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
+        x.x = gelu_erf(x.x); x.y = gelu_erf(x.y); x.z = gelu_erf(x.z); x.w = gelu_erf(x.w);
+      }
+      if constexpr (EPI == EPI_GELU_RESID) {
+        x.x += r[it].x; x.y += r[it].y; x.z += r[it].z; x.w += r[it].w;
+      }
+      if constexpr (EPI == EPI_CONSUME) {
+        x.x = r[it].x + (x.x + ad[it].x); x.y = r[it].y + (x.y + ad[it].y);
+        x.z = r[it].z + (x.z + ad[it].z); x.w = r[it].w + (x.w + ad[it].w);
+      }
+      if (row < row_limit) {
+        if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
+        if (a.out_bf16 != nullptr) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+          *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
+              make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+        }
       }
     }
   }
@@ -126,7 +132,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) { mbar_init(&sh->full[s], 1); mbar_init(&sh->empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 8); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], kEpiWarps); }
     fence_barrier_init();
     if (args.group_tile_offsets != nullptr) {
       for (int g = 0; g <= args.num_groups; ++g) sh->group_off[g] = args.group_tile_offsets[g];
@@ -203,7 +209,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   } else if (warp >= 4) {
     // --------------------------------------------------------------- epilogue
     const int sub = warp & 3;            // TMEM lane quadrant this warp may access
-    const int half = (warp - 4) >> 2;    // which half of the BN columns
+    const int grp = (warp - 4) >> 2;     // which 32-column chunks of the tile (round robin)
     float* stage = sm_epi + (warp - 4) * 1024;
     const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
     int local = 0;
@@ -216,8 +222,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       tc_fence_after();
       const int row0 = m_tile * BM + sub * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 2; c += 32) {
-        const int col_in_tile = half * (BN / 2) + c;
+      for (int ci = grp; ci < BN / 32; ci += kEpiGroups) {
+        const int col_in_tile = ci * 32;
         const int col0 = n_blk * BN + col_in_tile;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN + col_in_tile, r);
@@ -257,7 +263,7 @@ struct PairCfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = (BN / 2) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = 8 * 32 * 32 * 4;
+  static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;
   static constexpr int kBudget = 232448 - kEpiBytes - 2048;
   static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
@@ -283,7 +289,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) { mbar_init(&sh->full[s], 2); mbar_init(&sh->empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 16); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 2 * kEpiWarps); }
     fence_barrier_init();
     if (args.group_tile_offsets != nullptr) {
       for (int g = 0; g <= args.num_groups; ++g) sh->group_off[g] = args.group_tile_offsets[g];
@@ -358,7 +364,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
   } else if (warp >= 4) {
     const int sub = warp & 3;
-    const int half = (warp - 4) >> 2;
+    const int grp = (warp - 4) >> 2;
     float* stage = sm_epi + (warp - 4) * 1024;
     const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), 0);
@@ -373,8 +379,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc_fence_after();
       const int row0 = m_tile * kPairM + rank * BM + sub * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 2; c += 32) {
-        const int col_in_tile = half * (BN / 2) + c;
+      for (int ci = grp; ci < BN / 32; ci += kEpiGroups) {
+        const int col_in_tile = ci * 32;
         const int col0 = n_blk * BN + col_in_tile;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN + col_in_tile, r);
@@ -552,7 +558,11 @@ bool use_pair_kernel() {
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
   if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
-  const int bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
+  int bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
+  if (const char* e = getenv("DICE_GEMM_BN_NARROW")) {
+    // experiment hook: use 128-wide tiles for N not divisible by 256 (wave quantisation)
+    if (e[0] == '1' && p.N % 256 != 0) bn = 128;
+  }
   // grouped GEMMs always use 256-row tiles (the permute pads experts to 256 rows)
   const bool pair = p.group_tile_offsets != nullptr || use_pair_kernel();
   const int tile_m = pair ? 2 * BM : BM;
