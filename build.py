@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_2411_16786_b200")
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "_dice_b200.so")
-SOURCES = ["dice_gemm.cu", "dice_ops.cu"]
+SOURCES = ["dice_gemm.cu", "dice_ops.cu", "dice_ep.cu"]
 HEADERS = ["dice_gemm.h", "dice_ptx.cuh", os.path.join("..", "..", "include", "dice_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

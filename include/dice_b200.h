@@ -168,6 +168,55 @@ int dice_denoise(float* x, uint16_t* x16, const float* y, float eta, int64_t n, 
 int dice_pack_rows(const float* in, int64_t n, int cols, int64_t ld_in, int hp, float* out32,
                    uint16_t* out16, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Expert parallelism over peer memory (one process per GPU, NVLink/NVSwitch).
+ * Replaces the simulated dispatch / combine all-to-alls (schedules.py:326,
+ * 332, 376, 393; cluster.py:93-109) with P2P stores into IPC-shared windows.
+ * ------------------------------------------------------------------------ */
+
+/* cudaMalloc + zero fill (windows must be whole allocations to be IPC-shared). */
+int dice_device_alloc(int64_t bytes, void** ptr);
+int dice_device_free(void* ptr);
+
+/* CUDA IPC: 64-byte handle of a dice_device_alloc allocation; open / close a
+ * peer's handle (not the caller's own). */
+int dice_ipc_get_handle(const void* dev_ptr, uint8_t* handle64);
+int dice_ipc_open(const uint8_t* handle64, void** dev_ptr);
+int dice_ipc_close(void* dev_ptr);
+
+/* Batched stream memory operations on 32-bit flags (addrs: host array of
+ * device addresses, local or peer-mapped). wait: the stream stalls until every
+ * flag == value. write: each write is ordered after (and fenced against) prior
+ * work on the stream. Both are captured by CUDA graphs. */
+int dice_stream_wait_eq(const uint64_t* addrs, int count, uint32_t value, void* stream);
+int dice_stream_write(const uint64_t* addrs, int count, uint32_t value, void* stream);
+
+/* Dispatch all-to-all send of one layer: groups this rank's active pairs by
+ * destination rank (expert e lives on rank e/(E/D)), accumulates
+ * {active pairs, remote pairs} in counters, and stores each pair's bf16 row
+ * and int2 (local expert, pair index) into the destination's window region for
+ * source `me`, plus the per-destination row count. rx_*: host arrays of D
+ * device pointers to those regions. pos_dest int32 [n*k], dest_offsets int32
+ * [D+1], scratch >= dice_permute_scratch_ints(n, k, D). */
+int dice_ep_dispatch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E, int D,
+                     int me, const uint16_t* u16, int hp, int32_t* pos_dest, int32_t* dest_offsets,
+                     int64_t* counters, int64_t row0, int64_t rows_total, int32_t* scratch,
+                     const uint64_t* rx_rows, const uint64_t* rx_meta, const uint64_t* rx_count,
+                     void* stream);
+
+/* Expert side of one layer: groups the D*cap window rows by local expert,
+ * runs the grouped expert FFN (expert_forward, model.py:226-232) and stores
+ * every output row into its home rank's combine window at the home pair
+ * index (cx: host array of D device pointers). */
+int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
+                   int64_t cap, int El, int hp, int ep, const uint16_t* w1_t, const uint16_t* w2_t,
+                   int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
+                   uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
+                   const uint64_t* cx, void* stream);
+
+/* out[i] = i for i < count (identity pair positions for the combine window). */
+int dice_iota(int32_t* out, int64_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,19 @@ SIGNATURES = {
     "dice_combine": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P]),
     "dice_denoise": (c_int, [P, P, P, c_float, c_int64, c_int, P, c_int, P]),
     "dice_pack_rows": (c_int, [P, c_int64, c_int, c_int64, c_int, P, P, P]),
+    "dice_device_alloc": (c_int, [c_int64, ctypes.POINTER(c_void_p)]),
+    "dice_device_free": (c_int, [P]),
+    "dice_ipc_get_handle": (c_int, [P, ctypes.c_char_p]),
+    "dice_ipc_open": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_void_p)]),
+    "dice_ipc_close": (c_int, [P]),
+    "dice_stream_wait_eq": (c_int, [ctypes.POINTER(c_uint64), c_int, ctypes.c_uint32, P]),
+    "dice_stream_write": (c_int, [ctypes.POINTER(c_uint64), c_int, ctypes.c_uint32, P]),
+    "dice_ep_dispatch": (c_int, [P, P, c_int64, c_int, c_int, c_int, c_int, P, c_int, P, P, P,
+                                 c_int64, c_int64, P, ctypes.POINTER(c_uint64),
+                                 ctypes.POINTER(c_uint64), ctypes.POINTER(c_uint64), P]),
+    "dice_ep_expert": (c_int, [P, P, P, c_int, c_int64, c_int, c_int, c_int, P, P, P, P, P, P, P,
+                               c_int64, P, P, ctypes.POINTER(c_uint64), P]),
+    "dice_iota": (c_int, [P, c_int64, P]),
 }
 
 _lock = threading.Lock()
@@ -90,7 +103,10 @@ def check(rc: int, what: str) -> None:
 
 # kernels each entry point launches (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_grouped_ffn": 2, "dice_event_create": 0,
-                    "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0}
+                    "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
+                    "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
+                    "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,
+                    "dice_stream_write": 0, "dice_ep_dispatch": 3, "dice_ep_expert": 7}
 launch_count = [0]
 
 

@@ -1,0 +1,249 @@
+// Expert-parallel token exchange over peer memory (NVLink / NVSwitch).
+//
+// One process per GPU. Every rank exports its receive windows with CUDA IPC;
+// peers map them and the send kernels store token rows straight into the
+// owner's window (the permute writes the all-to-all), so there is no staging
+// copy and no host synchronisation. Completion is signalled with constant
+// valued ready/free flags driven by batched stream memory operations
+// (cuStreamBatchMemOp wait/write), which CUDA graphs capture, so a whole
+// sampling run replays as one graph on every rank.
+//
+// Reference semantics: the dispatch all-to-all moves the active (token, slot)
+// pairs to the rank owning the expert (schedules.py:326, cluster.py:93-109);
+// the combine all-to-all returns the expert rows to the token's home rank
+// (schedules.py:332, 393); expert e lives on rank e / (E/D) and token t on
+// rank (t*D)/R (cluster.py:61-72).
+#include <cstring>
+#include <mutex>
+
+#include "dice_gemm.h"
+#include "dice_ptx.cuh"
+
+namespace dice {
+
+constexpr int kMaxRanks = 16;
+
+struct PeerPtrs {
+  void* p[kMaxRanks];
+};
+
+// Sender: warp per active pair; rows go to the destination rank's window at
+// the pair's compact index within (me -> dest), metadata (local expert, pair).
+__global__ void __launch_bounds__(256) ep_send_kernel(
+    const int32_t* __restrict__ ids, const int32_t* __restrict__ pos_dest,
+    const int32_t* __restrict__ dest_offsets, int64_t pairs, int k, int El,
+    const uint16_t* __restrict__ u16, int hp, PeerPtrs rx_rows, PeerPtrs rx_meta, PeerPtrs rx_count,
+    int D) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x < D) {
+    const int d = threadIdx.x;
+    *reinterpret_cast<int32_t*>(rx_count.p[d]) = dest_offsets[d + 1] - dest_offsets[d];
+  }
+  const int vec = hp / 8;
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < pairs;
+       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int pd = pos_dest[q];
+    if (pd < 0) continue;
+    const int e = ids[q];
+    const int d = e / El;
+    const int idx = pd - dest_offsets[d];
+    const uint4* src = reinterpret_cast<const uint4*>(u16 + (q / k) * hp);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(rx_rows.p[d]) + (int64_t)idx * hp);
+    for (int c = lane; c < vec; c += 32) dst[c] = src[c];
+    if (lane == 0)
+      static_cast<int2*>(rx_meta.p[d])[idx] = make_int2(e - d * El, (int)q);
+  }
+}
+
+// Receiver: expert key of every received row (-1 beyond each source's count).
+__global__ void ep_rx_ids_kernel(const int2* __restrict__ meta, const int32_t* __restrict__ counts,
+                                 int D, int64_t cap, int32_t* ids_rx) {
+  const int64_t total = (int64_t)D * cap;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int src = (int)(g / cap);
+    const int64_t j = g - (int64_t)src * cap;
+    ids_rx[g] = j < counts[src] ? meta[g].x : -1;
+  }
+}
+
+// Owner -> home: expert output row of received row g goes back to its source
+// rank's combine window at the source's pair index.
+__global__ void __launch_bounds__(256) ep_combine_send_kernel(
+    const int32_t* __restrict__ pos_rx, const int2* __restrict__ meta, int64_t total, int64_t cap,
+    const uint16_t* __restrict__ y, int hp, PeerPtrs cx) {
+  const int lane = threadIdx.x & 31;
+  const int vec = hp / 8;
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < total;
+       g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int pr = pos_rx[g];
+    if (pr < 0) continue;
+    const int src = (int)(g / cap);
+    const int pair = meta[g].y;
+    const uint4* s = reinterpret_cast<const uint4*>(y + (int64_t)pr * hp);
+    uint4* d = reinterpret_cast<uint4*>(static_cast<uint16_t*>(cx.p[src]) + (int64_t)pair * hp);
+    for (int c = lane; c < vec; c += 32) d[c] = s[c];
+  }
+}
+
+__global__ void iota_pairs_kernel(int32_t* out, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+namespace {
+
+typedef CUresult (*BatchMemOpFn)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+
+BatchMemOpFn batch_memop() {
+  static BatchMemOpFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<BatchMemOpFn>(p);
+  });
+  return fn;
+}
+
+PeerPtrs table(const uint64_t* ptrs, int D, int64_t offset_bytes) {
+  PeerPtrs t;
+  memset(&t, 0, sizeof(t));
+  for (int d = 0; d < D; ++d)
+    t.p[d] = reinterpret_cast<void*>(ptrs[d] + (uint64_t)offset_bytes);
+  return t;
+}
+
+int grid_warps(int64_t warps) {
+  int64_t g = (warps * 32 + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return g < 1 ? 1 : (int)g;
+}
+
+}  // namespace
+}  // namespace dice
+
+using namespace dice;
+
+extern "C" {
+
+int dice_device_alloc(int64_t bytes, void** ptr) {
+  if (bytes <= 0) return DICE_ERR_CONTRACT;
+  if (cudaMalloc(ptr, (size_t)bytes) != cudaSuccess) return DICE_ERR_CUDA;
+  return cudaMemset(*ptr, 0, (size_t)bytes) == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+}
+
+int dice_device_free(void* ptr) { return cudaFree(ptr) == cudaSuccess ? DICE_OK : DICE_ERR_CUDA; }
+
+int dice_ipc_get_handle(const void* dev_ptr, uint8_t* handle64) {
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)) != cudaSuccess) return DICE_ERR_CUDA;
+  memcpy(handle64, &h, sizeof(h));
+  return DICE_OK;
+}
+
+int dice_ipc_open(const uint8_t* handle64, void** dev_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess
+             ? DICE_OK : DICE_ERR_CUDA;
+}
+
+int dice_ipc_close(void* dev_ptr) {
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+}
+
+// Stream-ordered waits until every 32-bit flag at addrs[i] equals `value`
+// (one batched memop; the stream stalls on the device, no SM spins).
+int dice_stream_wait_eq(const uint64_t* addrs, int count, uint32_t value, void* stream) {
+  BatchMemOpFn fn = batch_memop();
+  if (fn == nullptr || count < 0 || count > 64) return DICE_ERR_CUDA;
+  if (count == 0) return DICE_OK;
+  CUstreamBatchMemOpParams ops[64];
+  memset(ops, 0, sizeof(ops));
+  for (int i = 0; i < count; ++i) {
+    ops[i].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+    ops[i].waitValue.address = (CUdeviceptr)addrs[i];
+    ops[i].waitValue.value = value;
+    ops[i].waitValue.flags = CU_STREAM_WAIT_VALUE_EQ;
+  }
+  return fn((CUstream)stream, (unsigned)count, ops, 0) == CUDA_SUCCESS ? DICE_OK : DICE_ERR_CUDA;
+}
+
+// Stream-ordered 32-bit writes (each preceded by a fence over prior stream work).
+int dice_stream_write(const uint64_t* addrs, int count, uint32_t value, void* stream) {
+  BatchMemOpFn fn = batch_memop();
+  if (fn == nullptr || count < 0 || count > 64) return DICE_ERR_CUDA;
+  if (count == 0) return DICE_OK;
+  CUstreamBatchMemOpParams ops[64];
+  memset(ops, 0, sizeof(ops));
+  for (int i = 0; i < count; ++i) {
+    ops[i].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    ops[i].writeValue.address = (CUdeviceptr)addrs[i];
+    ops[i].writeValue.value = value;
+    ops[i].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+  }
+  return fn((CUstream)stream, (unsigned)count, ops, 0) == CUDA_SUCCESS ? DICE_OK : DICE_ERR_CUDA;
+}
+
+// Dispatch send for one layer (TokenCache.decide has produced `active`).
+// Groups this rank's active pairs by destination rank (compact, no padding),
+// counts bytes of remote pairs, and stores every row + (local expert, pair)
+// into the destination's window region reserved for this source rank.
+// rx_rows/rx_meta/rx_count: per-destination device pointers (peer-mapped) to
+// this layer's region for source `me`.
+int dice_ep_dispatch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E, int D,
+                     int me, const uint16_t* u16, int hp, int32_t* pos_dest, int32_t* dest_offsets,
+                     int64_t* counters, int64_t row0, int64_t rows_total, int32_t* scratch,
+                     const uint64_t* rx_rows, const uint64_t* rx_meta, const uint64_t* rx_count,
+                     void* stream) {
+  if (D < 1 || D > kMaxRanks || E % D != 0 || hp % 64 != 0 || me < 0 || me >= D)
+    return DICE_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int El = E / D;
+  int rc = permute_launch(ids, active, n, k, D, El, 1, E, nullptr, hp, nullptr, pos_dest,
+                          dest_offsets, counters, D, row0, rows_total, scratch, s);
+  if (rc) return rc;
+  ep_send_kernel<<<grid_warps(n * k), 256, 0, s>>>(ids, pos_dest, dest_offsets, n * k, k, El, u16, hp,
+                                                   table(rx_rows, D, 0), table(rx_meta, D, 0),
+                                                   table(rx_count, D, 0), D);
+  return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+}
+
+// Receive side of one layer: group the rows every source rank stored in this
+// rank's window by local expert (256-row padded tiles), run the grouped
+// expert FFN, and store each output row into its home rank's combine window
+// at the home's pair index. rx_rows [D*cap, hp], rx_meta [D*cap] (int2),
+// rx_count [D] are this rank's window for the layer; cx: per-source pointer to
+// the layer's combine window base [n_src*k, hp].
+int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
+                   int64_t cap, int El, int hp, int ep, const uint16_t* w1_t, const uint16_t* w2_t,
+                   int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
+                   uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
+                   const uint64_t* cx, void* stream) {
+  if (D < 1 || D > kMaxRanks || hp % 64 != 0 || ep % 64 != 0 || El < 1) return DICE_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t total = (int64_t)D * cap;
+  ep_rx_ids_kernel<<<(int)((total + 255) / 256 < 2368 ? (total + 255) / 256 : 2368), 256, 0, s>>>(
+      static_cast<const int2*>(rx_meta), rx_count, D, cap, ids_rx);
+  int rc = permute_launch(ids_rx, nullptr, total, 1, El, 1, 256, El, rx_rows, hp, x_perm, pos_rx,
+                          tile_offsets, nullptr, 1, 0, total, scratch, s);
+  if (rc) return rc;
+  rc = dice_grouped_ffn(x_perm, max_rows, w1_t, w2_t, El, hp, ep, tile_offsets, hbuf, y, stream);
+  if (rc) return rc;
+  ep_combine_send_kernel<<<grid_warps(total), 256, 0, s>>>(
+      pos_rx, static_cast<const int2*>(rx_meta), total, cap, y, hp, table(cx, D, 0));
+  return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+}
+
+int dice_iota(int32_t* out, int64_t count, void* stream) {
+  if (count <= 0) return DICE_OK;
+  iota_pairs_kernel<<<(int)((count + 255) / 256 < 2368 ? (count + 255) / 256 : 2368), 256, 0,
+                      (cudaStream_t)stream>>>(out, count);
+  return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -51,4 +51,12 @@ struct GemmProblem {
 
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream);
 
+// Count + scatter (+ optional row gather) of (token, slot) pairs grouped by
+// key = ids[p] / key_div, groups padded to row_tile rows (dice_ops.cu).
+int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int groups,
+                   int key_div, int row_tile, int experts_total, const uint16_t* rows, int hp,
+                   uint16_t* x_perm, int32_t* pos, int32_t* tile_offsets, int64_t* counters,
+                   int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
+                   cudaStream_t stream);
+
 }  // namespace dice

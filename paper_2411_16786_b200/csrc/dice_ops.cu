@@ -368,13 +368,17 @@ __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, i
 // and assigns positions from warp-level match ranks.
 constexpr int kPermBlock = 1024;
 constexpr int kRowTile = 256;  // expert groups padded to the CTA-pair GEMM's 256-row tile
+// (the EP send plan groups by destination rank with key_div = E/D and row_tile = 1)
 
 __device__ __forceinline__ bool pair_of(int64_t p, int k, const int32_t* ids,
-                                        const uint8_t* active, int& e, int64_t& t, int& s) {
+                                        const uint8_t* active, int key_div, int& e, int64_t& t,
+                                        int& s) {
   t = p / k;
   s = (int)(p - t * k);
   e = ids[p];
-  return active == nullptr || active[p] != 0;
+  const bool ok = e >= 0 && (active == nullptr || active[p] != 0);
+  if (key_div > 1) e /= key_div;
+  return ok;
 }
 
 // Rank of this thread's pair among earlier pairs of the same expert in its
@@ -398,7 +402,8 @@ __device__ __forceinline__ int block_rank(bool valid, int e, int E, int (*wcnt)[
 
 __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
-    long long* counters, int devices, int64_t row0, int64_t rows_total, int32_t* block_counts) {
+    long long* counters, int devices, int64_t row0, int64_t rows_total, int32_t* block_counts,
+    int key_div, int experts_total) {
   __shared__ int cnt[64];
   __shared__ unsigned long long red[2];
   if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
@@ -409,7 +414,8 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
   int e = 0, s = 0;
   int64_t t = 0;
   bool valid = false;
-  if (p < P) valid = pair_of(p, k, ids, active, e, t, s);
+  int e_raw = -1;
+  if (p < P) { valid = pair_of(p, k, ids, active, key_div, e, t, s); e_raw = ids[p]; }
   const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : -1);
   const int lane = threadIdx.x & 31;
   if (valid && __popc(peers & ((1u << lane) - 1)) == 0) atomicAdd(&cnt[e], __popc(peers));
@@ -417,7 +423,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
   bool remote = false;
   if (valid && devices > 1) {
     const int home = (int)(((row0 + t) * devices) / rows_total);
-    const int edev = e / (E / devices);
+    const int edev = e_raw / (experts_total / devices);
     remote = home != edev;
   }
   const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
@@ -434,7 +440,8 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
 
 __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
-    int32_t* pos, const int32_t* __restrict__ block_counts, int32_t* tile_offsets) {
+    int32_t* pos, const int32_t* __restrict__ block_counts, int32_t* tile_offsets, int key_div,
+    int row_tile) {
   __shared__ int wcnt[32][64];
   __shared__ int base[64];
   const int nb = gridDim.x;
@@ -453,8 +460,8 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     int tiles = 0;
     for (int ex = 0; ex < E; ++ex) {
       if (blockIdx.x == 0) tile_offsets[ex] = tiles;
-      base[ex] += tiles * kRowTile;
-      tiles += (wcnt[0][ex] + kRowTile - 1) / kRowTile;
+      base[ex] += tiles * row_tile;
+      tiles += (wcnt[0][ex] + row_tile - 1) / row_tile;
     }
     if (blockIdx.x == 0) tile_offsets[E] = tiles;
   }
@@ -465,7 +472,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
   int64_t t = 0;
   bool valid = false;
   const bool in_range = p < P;
-  if (in_range) valid = pair_of(p, k, ids, active, e, t, s);
+  if (in_range) valid = pair_of(p, k, ids, active, key_div, e, t, s);
   const int r = block_rank(valid, e, E, wcnt);
   if (in_range) pos[p] = valid ? base[e] + r : -1;
 }
@@ -635,6 +642,12 @@ __global__ void pack_rows_kernel(const float* __restrict__ in, int64_t n, int co
   }
 }
 
+int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int groups,
+                   int key_div, int row_tile, int experts_total, const uint16_t* rows, int hp,
+                   uint16_t* x_perm, int32_t* pos, int32_t* tile_offsets, int64_t* counters,
+                   int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
+                   cudaStream_t s);
+
 static int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;
@@ -643,6 +656,28 @@ static int grid_for(int64_t work, int threads) {
 }
 
 static inline int launch_ok() { return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA; }
+
+int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int groups,
+                   int key_div, int row_tile, int experts_total, const uint16_t* rows, int hp,
+                   uint16_t* x_perm, int32_t* pos, int32_t* tile_offsets, int64_t* counters,
+                   int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
+                   cudaStream_t s) {
+  const int64_t P = n * k;
+  const int blocks = (int)((P + kPermBlock - 1) / kPermBlock);
+  if (blocks == 0) {
+    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (groups + 1), s);
+    return launch_ok();
+  }
+  permute_count_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, groups,
+                                                     reinterpret_cast<long long*>(counters), devices,
+                                                     row0, rows_total, scratch, key_div,
+                                                     experts_total);
+  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, groups, pos, scratch,
+                                                       tile_offsets, key_div, row_tile);
+  if (x_perm != nullptr)
+    permute_gather_kernel<<<grid_for(P * 32, 256), 256, 0, s>>>(pos, P, rows, k, hp, x_perm);
+  return launch_ok();
+}
 
 }  // namespace dice
 
@@ -771,20 +806,9 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
   if (E < 1 || E > 64 || k < 1 || hp % 64 != 0 || devices < 1 || E % devices != 0)
     return DICE_ERR_CONTRACT;
   if (max_rows < dice_permute_max_rows(n, k, E)) return DICE_ERR_CONTRACT;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int64_t P = n * k;
-  const int blocks = (int)((P + kPermBlock - 1) / kPermBlock);
-  if (blocks == 0) {
-    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (E + 1), s);
-    return launch_ok();
-  }
-  permute_count_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E,
-                                                     reinterpret_cast<long long*>(counters), devices,
-                                                     row0, rows_total, scratch);
-  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, E, pos, scratch,
-                                                       tile_offsets);
-  permute_gather_kernel<<<grid_for(P * 32, 256), 256, 0, s>>>(pos, P, u16, k, hp, x_perm);
-  return launch_ok();
+  return dice::permute_launch(ids, active, n, k, E, 1, kRowTile, E, u16, hp, x_perm, pos,
+                              tile_offsets, counters, devices, row0, rows_total, scratch,
+                              (cudaStream_t)stream);
 }
 
 int dice_grouped_ffn(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,

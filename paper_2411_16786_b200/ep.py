@@ -1,0 +1,501 @@
+"""Expert-parallel DICE sampling across GPUs (one process per GPU).
+
+Placement follows the reference (cluster.py:61-72): routed expert e lives on
+rank e // (E/D); token row t is homed on rank (t*D)//R. W_mix, W_gate and the
+shared experts are replicated (row-wise data parallel work).
+
+Exchange: every rank cudaMallocs one window allocation, exports it with CUDA
+IPC and maps every peer's (handles travel through torch.distributed object
+collectives; that is the only use of the process group on the data path's
+setup). The dispatch kernel stores each active pair's bf16 row straight into
+the expert rank's window; the expert rank's combine kernel stores each
+output row straight into the home rank's combine window. Completion uses
+constant-valued flags (ready / free per layer and peer) driven by batched
+stream memory operations, so the schedule keeps host-deterministic control
+flow and a whole run captures into one CUDA graph per rank.
+
+Schedule (schedules.py:372-402, PAPER §4.1): dispatch(l) is sent in stage l and
+expert-processed in stage l+1 (or at a flush); its combine is assembled at the
+start of stage l of the next step, right before decide(l) so the TokenCache
+sees the reference's decide/assemble order (policies.py:159-208), and consumed
+with one-step staleness. Selective-sync / warmup / periodic stages run the
+blocking dispatch -> experts -> combine -> assemble sequence.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import hashlib
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .cluster import ClusterConfig, shard_rows
+from .errors import ConfigurationError, ContractError, NumericalDivergenceError
+from .model import ActivationBlock, RouteDecision, ToyModel, model_hash, mix64, _X0_STREAM_TAG
+from .policies import CondStrategy, PolicyConfig, TokenCache, is_sync_step, select_sync_layers
+from .schedules import INT32_MAX, RunResult, StalenessRecord, Strategy
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (for torch.as_tensor)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+_TYPESTR = {torch.float32: "<f4", torch.bfloat16: "<V2", torch.int32: "<i4", torch.uint8: "|u1",
+            torch.int64: "<i8"}
+
+
+class Window:
+    """One cudaMalloc'd allocation: receive windows, combine window and flags."""
+
+    def __init__(self, L, D, cap, ncap, hp, device):
+        self.L, self.D, self.cap, self.ncap, self.hp = L, D, cap, ncap, hp
+        off = 0
+
+        def take(nbytes):
+            nonlocal off
+            start = off
+            off += (nbytes + 255) // 256 * 256
+            return start
+
+        self.o_rx_rows = take(L * D * cap * hp * 2)
+        self.o_rx_meta = take(L * D * cap * 8)
+        self.o_rx_count = take(L * D * 4)
+        self.o_cx_rows = take(L * ncap * hp * 2)
+        self.o_rx_ready = take(L * D * 4)
+        self.o_cx_ready = take(L * D * 4)
+        self.o_rx_free = take(L * D * 4)
+        self.o_cx_free = take(L * D * 4)
+        self.nbytes = off
+        h = ctypes.c_void_p()
+        torch.cuda.set_device(device)
+        _lib.call("dice_device_alloc", self.nbytes, ctypes.byref(h))
+        self.ptr = int(h.value)
+        # free flags start at 1 (regions free), ready flags at 0
+        for o in (self.o_rx_free, self.o_cx_free):
+            self.view(o, (L * D,), torch.int32).fill_(1)
+        torch.cuda.synchronize()
+
+    def view(self, offset, shape, dtype):
+        if dtype is torch.bfloat16:
+            t = torch.as_tensor(_CudaArray(self.ptr + offset, shape, "<i2"), device="cuda")
+            return t.view(torch.bfloat16)
+        return torch.as_tensor(_CudaArray(self.ptr + offset, shape, _TYPESTR[dtype]), device="cuda")
+
+    def handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _lib.call("dice_ipc_get_handle", ctypes.c_void_p(self.ptr), buf)
+        return buf.raw
+
+    def free(self):
+        if self.ptr:
+            _lib.load().dice_device_free(ctypes.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+def _u64_array(values):
+    arr = (ctypes.c_uint64 * max(1, len(values)))(*[int(v) for v in values])
+    return arr
+
+
+class EPGroup:
+    """Rank-local view of the D windows (own + IPC-mapped peers)."""
+
+    def __init__(self, window: Window, rank: int, world: int, pg=None):
+        import torch.distributed as dist
+        self.win, self.rank, self.world = window, rank, world
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, window.handle(), group=pg)
+        self.base = []
+        self._opened = []
+        for r in range(world):
+            if r == rank:
+                self.base.append(window.ptr)
+            else:
+                h = ctypes.c_void_p()
+                _lib.call("dice_ipc_open", ctypes.c_char_p(handles[r]), ctypes.byref(h))
+                self.base.append(int(h.value))
+                self._opened.append(int(h.value))
+
+    def close(self):
+        for p in self._opened:
+            _lib.load().dice_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+
+    # addresses -----------------------------------------------------------
+    def rx_rows(self, owner, layer, src):
+        w = self.win
+        return self.base[owner] + w.o_rx_rows + ((layer * w.D + src) * w.cap) * w.hp * 2
+
+    def rx_meta(self, owner, layer, src):
+        w = self.win
+        return self.base[owner] + w.o_rx_meta + ((layer * w.D + src) * w.cap) * 8
+
+    def rx_count(self, owner, layer, src):
+        w = self.win
+        return self.base[owner] + w.o_rx_count + (layer * w.D + src) * 4
+
+    def cx_rows(self, owner, layer):
+        w = self.win
+        return self.base[owner] + w.o_cx_rows + layer * w.ncap * w.hp * 2
+
+    def flag(self, kind, owner, layer, peer):
+        w = self.win
+        o = {"rx_ready": w.o_rx_ready, "cx_ready": w.o_cx_ready, "rx_free": w.o_rx_free,
+             "cx_free": w.o_cx_free}[kind]
+        return self.base[owner] + o + (layer * w.D + peer) * 4
+
+    # stream memops ---------------------------------------------------------
+    def wait(self, addrs, value):
+        arr = _u64_array(addrs)
+        _lib.call("dice_stream_wait_eq", arr, len(addrs), value, ops._stream())
+
+    def write(self, addrs, value):
+        arr = _u64_array(addrs)
+        _lib.call("dice_stream_write", arr, len(addrs), value, ops._stream())
+
+
+class _EPPayload:
+    def __init__(self, n, k, device):
+        self.ids = torch.zeros(n, k, dtype=torch.int32, device=device)
+        self.gates = torch.zeros(n, k, dtype=torch.float32, device=device)
+        self.active = torch.ones(n, k, dtype=torch.uint8, device=device)
+        self.write = torch.zeros(n, k, dtype=torch.uint8, device=device)
+        self.layer = -1
+        self.gen = -1
+
+
+def sample_x0_shard(config, seed: int, rows: tuple, device="cuda") -> ActivationBlock:
+    """Rows [r0, r1) of sample_x0 (model.py:181-186): the tagged stream at offset r0*h."""
+    r0, r1 = rows
+    x = torch.empty(r1 - r0, config.hidden_dim, dtype=torch.float32, device=device)
+    ops.splitmix_fill(x, mix64(seed ^ _X0_STREAM_TAG), r0 * config.hidden_dim, r1 - r0,
+                      config.hidden_dim, 1.0)
+    return ActivationBlock(values=x, generated_step=0)
+
+
+class EPRunner:
+    """One rank of an expert-parallel sampling run (ScheduleRunner semantics,
+    schedules.py:142-490, for SYNCHRONOUS and INTERWEAVED)."""
+
+    def __init__(self, model: ToyModel, x0_shard: ActivationBlock, strategy: Strategy,
+                 policy: PolicyConfig, cluster: ClusterConfig, seed: int, *, rank: int,
+                 world: int, pg=None, time_waits: bool = False):
+        cfg = model.config
+        if strategy is Strategy.DISPLACED:
+            raise ConfigurationError("expert-parallel runs support synchronous and interweaved")
+        if cluster.num_devices != world:
+            raise ConfigurationError(f"cluster.num_devices={cluster.num_devices} != world={world}")
+        if cfg.num_experts % world:
+            raise ConfigurationError(f"num_experts={cfg.num_experts} not divisible by {world}")
+        if world > 16:
+            raise ConfigurationError("up to 16 ranks")
+        El = cfg.num_experts // world
+        if model.experts != (rank * El, (rank + 1) * El):
+            raise ContractError(f"rank {rank} must hold experts [{rank * El}, {(rank + 1) * El})")
+        self.r0, self.r1 = shard_rows(cfg.total_rows, world, rank)
+        n = self.r1 - self.r0
+        if tuple(x0_shard.values.shape) != (n, cfg.hidden_dim) or x0_shard.generated_step != 0:
+            raise ContractError(f"rank {rank} x0 shard must be [{n}, {cfg.hidden_dim}] at step 0")
+        if policy.cond_strategy is CondStrategy.RANDOM and policy.cond_seed is None:
+            policy = dataclasses.replace(policy, cond_seed=seed)
+        self.model, self.cfg, self.x0 = model, cfg, x0_shard
+        self.strategy, self.policy, self.cluster, self.seed = strategy, policy, cluster, seed
+        self.rank, self.world, self.pg, self.El = rank, world, pg, El
+        self.time_waits = time_waits
+        dev = model.device
+        self.dev = dev
+        k, E, S, hp, ep = cfg.top_k, cfg.num_experts, cfg.num_shared, model.hp, model.ep
+        self.n, self.k, self.E, self.S, self.hp, self.ep = n, k, E, S, hp, ep
+        n_max = max(shard_rows(cfg.total_rows, world, r)[1] - shard_rows(cfg.total_rows, world, r)[0]
+                    for r in range(world))
+        self.cap = n_max * k
+        L = cfg.num_layers
+        self.win = Window(L, world, self.cap, self.cap, hp, torch.cuda.current_device())
+        self.grp = EPGroup(self.win, rank, world, pg)
+        f32, bf = torch.float32, torch.bfloat16
+        self.x32 = torch.zeros(n, hp, dtype=f32, device=dev)
+        self.x16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        self.h32 = torch.zeros(n, hp, dtype=f32, device=dev)
+        self.h16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        self.u32 = torch.zeros(n, hp, dtype=f32, device=dev)
+        self.u16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        total = world * self.cap
+        self.max_rows = ops.permute_max_rows(total, 1, El)
+        self.hbuf = torch.empty(self.max_rows, ep, dtype=bf, device=dev)
+        self.y = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
+        self.x_perm = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
+        self.ids_rx = torch.empty(total, dtype=torch.int32, device=dev)
+        self.pos_rx = torch.empty(total, dtype=torch.int32, device=dev)
+        self.tiles = torch.empty(El + 1, dtype=torch.int32, device=dev)
+        self.pos_dest = torch.empty(n, k, dtype=torch.int32, device=dev)
+        self.dest_off = torch.empty(world + 1, dtype=torch.int32, device=dev)
+        self.pair_pos = torch.empty(n, k, dtype=torch.int32, device=dev)
+        _lib.call("dice_iota", self.pair_pos.data_ptr(), n * k, ops._stream())
+        sc = max(ops.permute_scratch_ints(n, k, world), ops.permute_scratch_ints(total, 1, El))
+        self.scratch = torch.zeros(sc, dtype=torch.int32, device=dev)
+        self.hsh = torch.empty(n, max(S, 1) * ep, dtype=bf, device=dev)
+        nslots = 1 if strategy is Strategy.SYNCHRONOUS else L
+        self.slots = torch.zeros(nslots, n, hp, dtype=f32, device=dev)
+        self.payloads = [_EPPayload(n, k, dev) for _ in range(L)]
+        self.cache = TokenCache(L, n, k, cfg.hidden_dim, device=dev) \
+            if policy.cond_strategy is not CondStrategy.OFF else None
+        self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
+        self.status = torch.empty(4, dtype=torch.int32, device=dev)
+        self.sync_layers = select_sync_layers(policy.sync_strategy, L, policy.explicit_layers)
+        self.graph = None
+        self._wait_events = []
+        self._event_pool = []
+        self.launches_per_run = 0
+
+    # --------------------------------------------------------------- helpers
+    def _slot(self, layer):
+        return self.slots[0] if self.strategy is Strategy.SYNCHRONOUS else self.slots[layer]
+
+    def _peers(self):
+        return range(self.world)
+
+    def _timed_wait(self, addrs, value):
+        if self.time_waits:
+            i = len(self._wait_events)
+            if i >= len(self._event_pool):
+                self._event_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
+            a, b = self._event_pool[i]
+            a.record()
+        self.grp.wait(addrs, value)
+        if self.time_waits:
+            b.record()
+            self._wait_events.append((a, b))
+
+    def _reset_state(self, x0_device=None):
+        cfg = self.cfg
+        ops.status_reset(self.status)
+        self.counters.zero_()
+        x0 = x0_device
+        if x0 is None:
+            x0 = torch.as_tensor(self.x0.values).to(device=self.dev, dtype=torch.float32).contiguous()
+        ops.pack_rows(x0, self.hp, self.x32, self.x16)
+        if self.cache is not None:
+            self.cache.has_subset.zero_()
+        L = cfg.num_layers
+        self.slot_gen = [None] * L
+        self.deferred = [None] * L    # payload whose combine is assembled at next stage l
+        self.pending = None
+        self.occupied = set()
+        self.peak_buffer_bytes = 0
+        self.records, self.dispatch_log, self.combine_log = [], [], []
+        self._wait_events = []
+
+    def _track(self, layer):
+        self.occupied.add(("c", layer))
+        slot_bytes = self.cfg.total_rows * self.cfg.hidden_dim * self.cluster.bytes_per_element
+        self.peak_buffer_bytes = max(self.peak_buffer_bytes, len(self.occupied) * slot_bytes)
+
+    def _stage_is_sync(self, step, layer):
+        if self.strategy is Strategy.SYNCHRONOUS:
+            return True
+        if is_sync_step(step, self.policy.warmup, self.policy.period):
+            return True
+        if layer in self.sync_layers:
+            return True
+        return self.slot_gen[layer] is None
+
+    # ------------------------------------------------------------- exchange
+    def _send(self, step, layer, p: _EPPayload, force):
+        """decide + dispatch all-to-all send of layer `layer`."""
+        g, me, D = self.grp, self.rank, self.world
+        if self.cache is not None:
+            self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write)
+            act = p.active
+        else:
+            act = None
+        # my regions in every destination window must have been consumed
+        self._timed_wait([g.flag("rx_free", me, layer, d) for d in self._peers()], 1)
+        g.write([g.flag("rx_free", me, layer, d) for d in self._peers()], 0)
+        rx_rows = _u64_array([g.rx_rows(d, layer, me) for d in self._peers()])
+        rx_meta = _u64_array([g.rx_meta(d, layer, me) for d in self._peers()])
+        rx_cnt = _u64_array([g.rx_count(d, layer, me) for d in self._peers()])
+        _lib.call("dice_ep_dispatch", p.ids.data_ptr(), None if act is None else act.data_ptr(),
+                  self.n, self.k, self.E, D, me, self.u16.data_ptr(), self.hp,
+                  self.pos_dest.data_ptr(), self.dest_off.data_ptr(),
+                  self.counters[step, layer].data_ptr(), self.r0, self.cfg.total_rows,
+                  self.scratch.data_ptr(), rx_rows, rx_meta, rx_cnt, ops._stream())
+        g.write([g.flag("rx_ready", d, layer, me) for d in self._peers()], 1)
+        p.layer, p.gen = layer, step
+        self.dispatch_log.append((step, layer))
+
+    def _expert(self, p: _EPPayload):
+        """Expert side of dispatch(p.layer): wait for every source, grouped FFN,
+        combine rows straight back to their home ranks."""
+        g, me, layer = self.grp, self.rank, p.layer
+        self._timed_wait([g.flag("rx_ready", me, layer, s) for s in self._peers()], 1)
+        g.write([g.flag("rx_ready", me, layer, s) for s in self._peers()], 0)
+        self._timed_wait([g.flag("cx_free", me, layer, h) for h in self._peers()], 1)
+        g.write([g.flag("cx_free", me, layer, h) for h in self._peers()], 0)
+        lw = self.model.layers[layer]
+        win = self.win
+        cx = _u64_array([g.cx_rows(h, layer) for h in self._peers()])
+        _lib.call("dice_ep_expert", g.rx_rows(me, layer, 0), g.rx_meta(me, layer, 0),
+                  g.rx_count(me, layer, 0), self.world, self.cap, self.El, self.hp, self.ep,
+                  lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.ids_rx.data_ptr(),
+                  self.pos_rx.data_ptr(), self.tiles.data_ptr(), self.scratch.data_ptr(),
+                  self.x_perm.data_ptr(), self.max_rows, self.hbuf.data_ptr(), self.y.data_ptr(),
+                  cx, ops._stream())
+        g.write([g.flag("rx_free", s, layer, me) for s in self._peers()], 1)
+        g.write([g.flag("cx_ready", h, layer, me) for h in self._peers()], 1)
+        self.deferred[layer] = p
+        self.slot_gen[layer] = p.gen          # the combine is in flight (_store_combine)
+        self.combine_log.append((p.gen, layer))
+
+    def _assemble(self, layer):
+        """Combine arrival at the home rank: stale-cache merge into slot[layer]."""
+        p = self.deferred[layer]
+        if p is None:
+            return
+        g, me = self.grp, self.rank
+        self._timed_wait([g.flag("cx_ready", me, layer, r) for r in self._peers()], 1)
+        g.write([g.flag("cx_ready", me, layer, r) for r in self._peers()], 0)
+        cxv = self.win.view(self.win.o_cx_rows + layer * self.cap * self.hp * 2,
+                            (self.cap, self.hp), torch.bfloat16)
+        c = self.cache
+        ops.cache_assemble(cxv, self.pair_pos, None if c is None else p.active,
+                           None if c is None else p.write, p.gates, p.ids, self._slot(layer),
+                           None if c is None else c.rows[layer],
+                           None if c is None else c.gates[layer],
+                           None if c is None else c.expert_ids[layer])
+        g.write([g.flag("cx_free", r, layer, me) for r in self._peers()], 1)
+        self.deferred[layer] = None
+
+    def _flush_pending(self):
+        prev, self.pending = self.pending, None
+        if prev is not None:
+            self._expert(prev)
+            self._track(prev.layer)
+
+    def _consume(self, layer, step, gen):
+        lw = self.model.layers[layer]
+        slot = self._slot(layer)
+        if self.S > 0:
+            ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
+            ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
+                     residual=self.u32, addend=slot)
+        else:
+            ops.combine(slot, slot, slot.new_empty(self.n, 0), self.h32, residual=self.u32,
+                        out_bf16=self.h16)
+        self.records.append(StalenessRecord(layer=layer, used_step=step, generated_step=gen))
+
+    def _run_step(self, step):
+        cfg = self.cfg
+        for layer in range(cfg.num_layers):
+            lw = self.model.layers[layer]
+            hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
+            ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32, out_bf16=self.u16,
+                     residual=hin32)
+            sync = self._stage_is_sync(step, layer)
+            if sync:
+                self._flush_pending()
+            self._assemble(layer)            # previous step's combine, before decide(layer)
+            p = self.payloads[layer]
+            ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, None, self.status,
+                          step, layer)
+            if sync:
+                self._send(step, layer, p, force=True)
+                self._expert(p)
+                self._assemble(layer)
+                if self.strategy is Strategy.INTERWEAVED:
+                    self._track(layer)
+                self._consume(layer, step, step)
+            else:
+                gen = self.slot_gen[layer]
+                self._send(step, layer, p, force=False)
+                prev, self.pending = self.pending, p
+                if prev is not None:
+                    self._expert(prev)
+                    self._track(prev.layer)
+                self._consume(layer, step, gen)
+        self._flush_pending()
+        ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
+
+    def _drain(self):
+        """Assemble every outstanding combine so all flags return to their
+        initial state (the run stays replayable)."""
+        for layer in range(self.cfg.num_layers):
+            self._assemble(layer)
+
+    # ------------------------------------------------------------- run API
+    def launch(self, x0_device=None):
+        if self.graph is not None:
+            if x0_device is not None and x0_device.data_ptr() != self._x0_graph.data_ptr():
+                self._x0_graph.copy_(x0_device)
+            self.graph.replay()
+            return
+        c0 = _lib.launch_count[0]
+        self._reset_state(x0_device)
+        for step in range(self.cfg.num_steps):
+            self._run_step(step)
+        self._drain()
+        self.launches_per_run = _lib.launch_count[0] - c0
+
+    def capture(self):
+        self._x0_graph = torch.as_tensor(self.x0.values).to(
+            device=self.dev, dtype=torch.float32).contiguous().clone()
+        self.launch(self._x0_graph)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch(self._x0_graph)
+        torch.cuda.synchronize()
+        self.graph = g
+        return self
+
+    def finish(self, reduce=True) -> RunResult:
+        """Status + counters; bytes / pairs summed over ranks (torch.distributed)."""
+        import torch.distributed as dist
+        cfg = self.cfg
+        status = self.status.cpu().tolist()
+        bad = torch.tensor([status[0]], dtype=torch.int64)
+        cnt = self.counters.cpu()
+        if reduce and self.world > 1:
+            dist.all_reduce(bad, op=dist.ReduceOp.MIN, group=self.pg)
+            dist.all_reduce(cnt, group=self.pg)
+        if int(bad.item()) != INT32_MAX:
+            raise NumericalDivergenceError(f"non-finite values at step {int(bad.item())}",
+                                           step=int(bad.item()))
+        cnt = cnt.numpy()
+        row_bytes = cfg.hidden_dim * self.cluster.bytes_per_element
+        dispatch_bytes = int(sum(cnt[s, l, 1] for s, l in self.dispatch_log)) * row_bytes
+        combine_bytes = int(sum(cnt[s, l, 1] for s, l in self.combine_log)) * row_bytes
+        per_step_active = [int(v) for v in cnt[:, :, 0].sum(axis=1)]
+        per_step_total = [cfg.num_layers * cfg.total_rows * self.k] * cfg.num_steps
+        timeline = None
+        if self._wait_events:
+            timeline = {"exposed_comm_seconds":
+                        sum(a.elapsed_ms(b) for a, b in self._wait_events) * 1e-3}
+        return RunResult(
+            final=ActivationBlock(values=self.x32[:, :cfg.hidden_dim].clone(),
+                                  generated_step=cfg.num_steps),
+            timeline=timeline, staleness_records=self.records, strategy=self.strategy,
+            policy=self.policy, seed=self.seed, model_hash=model_hash(self.model),
+            x0_hash=hashlib.sha256(np.ascontiguousarray(
+                torch.as_tensor(self.x0.values).cpu().numpy()).tobytes()).hexdigest(),
+            config=cfg, cluster=self.cluster, dispatch_bytes=dispatch_bytes,
+            combine_bytes=combine_bytes, peak_buffer_bytes=self.peak_buffer_bytes,
+            active_pairs=sum(per_step_active), total_pairs=sum(per_step_total),
+            per_step_active_pairs=per_step_active, per_step_total_pairs=per_step_total)
+
+    def run(self) -> RunResult:
+        self.launch()
+        return self.finish()
+
+    def close(self):
+        torch.cuda.synchronize()
+        self.graph = None
+        self.grp.close()
+        self.win.free()
