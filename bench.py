@@ -169,22 +169,47 @@ def run_gpu(args):
     from paper_2411_16786_b200 import _lib
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # DICE_BENCH_SAME_DEVICE=1: every rank on cuda:0 (functional test of the EP
+    # path on a one-GPU box; gloo for the host-side collectives)
+    same_device = os.environ.get("DICE_BENCH_SAME_DEVICE") == "1"
+    torch.cuda.set_device(0 if same_device else local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = D.preset(PRESET, batch=IMAGES_PER_GPU)
-    seed = 1000 + rank
-    model = D.init_model(cfg, seed=0)
-    x0 = D.sample_x0(cfg, seed)
+        if same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if same_device else "cuda"
+
+    def allreduce(x, op):
+        t = torch.tensor(x, device=coll_dev)
+        dist.all_reduce(t, op=op)
+        return t.cpu()
     policy = D.dice_policy()
-    # one process per GPU; each rank samples its own 32-image batch (replicas)
-    cluster = D.ClusterConfig(num_devices=1)
-    runner = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed,
-                            time_experts=True)
+    seed = 1000
+    if world == 1:
+        cfg = D.preset(PRESET, batch=IMAGES_PER_GPU)
+        model = D.init_model(cfg, seed=0)
+        x0 = D.sample_x0(cfg, seed)
+        cluster = D.ClusterConfig(num_devices=1)
+        runner = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed,
+                                time_experts=True)
+    else:
+        # expert parallelism: 32 images per GPU (weak scaling), experts e // (E/N) per
+        # rank, token rows (t*N)//R per rank, exchange over peer memory
+        from paper_2411_16786_b200.ep import EPRunner, sample_x0_shard
+        from paper_2411_16786_b200.cluster import shard_rows
+        cfg = D.preset(PRESET, batch=IMAGES_PER_GPU * world)
+        El = cfg.num_experts // world
+        model = D.init_model(cfg, seed=0, experts=(rank * El, (rank + 1) * El))
+        x0 = sample_x0_shard(cfg, seed, shard_rows(cfg.total_rows, world, rank))
+        cluster = D.ClusterConfig(num_devices=world)
+        runner = EPRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed, rank=rank,
+                          world=world, time_waits=True, time_experts=True)
     if not args.eager:
         runner.capture()       # the whole 50-step run as one CUDA graph
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -206,10 +231,13 @@ def run_gpu(args):
     expert_events = list(runner._expert_events)
     res = runner.finish()
     cnt = runner.counters.cpu().numpy()
+    exposed_ms = 0.0
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        exposed_ms = res.timeline["exposed_comm_seconds"] * 1e3 if res.timeline else 0.0
+        exposed_ms = float(allreduce([exposed_ms], dist.ReduceOp.MAX).item())
+        cnt = allreduce(cnt, dist.ReduceOp.SUM).numpy()
+    if world > 1:
+        ms = float(allreduce([ms], dist.ReduceOp.MAX).item())
     ms_per_step = ms / args.steps
     value = world * IMAGES_PER_GPU * args.steps / (ms / 1e3)
 
@@ -217,7 +245,9 @@ def run_gpu(args):
     # the active (token, expert) pairs each launch processed
     h, e = cfg.hidden_dim, cfg.expert_dim
     pair_flops = 4.0 * h * e
-    flops = sum(pair_flops * cnt[gen, layer, 0] for _, _, gen, layer in expert_events)
+    # pairs each launch processed; under EP the active pairs of (step, layer) are
+    # summed over ranks and spread evenly over the N expert ranks
+    flops = sum(pair_flops * cnt[gen, layer, 0] / world for _, _, gen, layer in expert_events)
     # the event pairs sit inside the captured graph: they hold the last timed replay
     t_exp = sum(a.elapsed_ms(b) for a, b, _, _ in expert_events) * 1e-3
     n_launch = len(expert_events)
@@ -225,7 +255,7 @@ def run_gpu(args):
     peak_tf, _, peak_kind = peaks()
 
     # e2e through the serving call with host buffers
-    x0_host = x0.values.cpu().pin_memory()
+    x0_host = torch.as_tensor(x0.values).cpu().pin_memory()
     runner.sample(x0_host)
     barrier()
     t0 = time.perf_counter()
@@ -234,15 +264,13 @@ def run_gpu(args):
     barrier()
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = float(allreduce([e2e_s], dist.ReduceOp.MAX).item())
     e2e = world * IMAGES_PER_GPU * args.steps / e2e_s
     final_dice = runner._final_host.clone().numpy().astype(np.float64)
 
     # staleness quality: latent MSE of DICE / interweaved vs the synchronous path (same GPU numerics)
     quality = {}
-    if not args.no_quality:
+    if not args.no_quality and world == 1:
         del runner
         torch.cuda.empty_cache()
         finals = {"dice": final_dice}
@@ -279,10 +307,11 @@ def run_gpu(args):
         "config": {"workload": WORKLOAD, "images_per_gpu": IMAGES_PER_GPU,
                    "global_batch": IMAGES_PER_GPU * world, "tokens_per_image": cfg.num_tokens,
                    "denoise_steps": cfg.num_steps, "eta": cfg.step_size,
-                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu (all 8 experts)",
+                   "parallelism": (f"ep{world} (experts e//(E/{world}) per GPU, peer-memory "
+                                   "all-to-all)") if world > 1 else "single-gpu (all 8 experts)",
                    "l2": "inputs larger than L2: 6.0 GB of bf16 weights streamed per denoising step"},
         "moe_layer_us": ms_per_step * 1e3 / (cfg.num_steps * cfg.num_layers),
-        "exposed_a2a_us": 0.0,
+        "exposed_a2a_us": exposed_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
         "roofline": {"bound": "tensor", "kernel": "grouped expert FFN (tcgen05 GEMM1+GELU, GEMM2)",
                      "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": None,

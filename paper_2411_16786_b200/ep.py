@@ -187,7 +187,7 @@ class EPRunner:
 
     def __init__(self, model: ToyModel, x0_shard: ActivationBlock, strategy: Strategy,
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *, rank: int,
-                 world: int, pg=None, time_waits: bool = False):
+                 world: int, pg=None, time_waits: bool = False, time_experts: bool = False):
         cfg = model.config
         if strategy is Strategy.DISPLACED:
             raise ConfigurationError("expert-parallel runs support synchronous and interweaved")
@@ -210,6 +210,7 @@ class EPRunner:
         self.strategy, self.policy, self.cluster, self.seed = strategy, policy, cluster, seed
         self.rank, self.world, self.pg, self.El = rank, world, pg, El
         self.time_waits = time_waits
+        self.time_experts = time_experts
         dev = model.device
         self.dev = dev
         k, E, S, hp, ep = cfg.top_k, cfg.num_experts, cfg.num_shared, model.hp, model.ep
@@ -253,6 +254,8 @@ class EPRunner:
         self.graph = None
         self._wait_events = []
         self._event_pool = []
+        self._expert_events = []
+        self._expert_pool = []
         self.launches_per_run = 0
 
     # --------------------------------------------------------------- helpers
@@ -292,6 +295,7 @@ class EPRunner:
         self.peak_buffer_bytes = 0
         self.records, self.dispatch_log, self.combine_log = [], [], []
         self._wait_events = []
+        self._expert_events = []
 
     def _track(self, layer):
         self.occupied.add(("c", layer))
@@ -342,12 +346,21 @@ class EPRunner:
         lw = self.model.layers[layer]
         win = self.win
         cx = _u64_array([g.cx_rows(h, layer) for h in self._peers()])
+        if self.time_experts:
+            i = len(self._expert_events)
+            if i >= len(self._expert_pool):
+                self._expert_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
+            e0, e1 = self._expert_pool[i]
+            e0.record()
         _lib.call("dice_ep_expert", g.rx_rows(me, layer, 0), g.rx_meta(me, layer, 0),
                   g.rx_count(me, layer, 0), self.world, self.cap, self.El, self.hp, self.ep,
                   lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.ids_rx.data_ptr(),
                   self.pos_rx.data_ptr(), self.tiles.data_ptr(), self.scratch.data_ptr(),
                   self.x_perm.data_ptr(), self.max_rows, self.hbuf.data_ptr(), self.y.data_ptr(),
                   cx, ops._stream())
+        if self.time_experts:
+            e1.record()
+            self._expert_events.append((e0, e1, p.gen, layer))
         g.write([g.flag("rx_free", s, layer, me) for s in self._peers()], 1)
         g.write([g.flag("cx_ready", h, layer, me) for h in self._peers()], 1)
         self.deferred[layer] = p
@@ -443,6 +456,21 @@ class EPRunner:
         self._drain()
         self.launches_per_run = _lib.launch_count[0] - c0
 
+    def sample(self, x0_host: torch.Tensor) -> torch.Tensor:
+        """Serving entry for this rank's shard: x0 rows from (pinned) host memory
+        -> final latent rows in host memory."""
+        if not hasattr(self, "_final_host"):
+            self._x0_stage = (self._x0_graph if self.graph is not None else
+                              torch.empty(self.n, self.cfg.hidden_dim, dtype=torch.float32,
+                                          device=self.dev))
+            self._final_host = torch.empty(self.n, self.cfg.hidden_dim, dtype=torch.float32,
+                                           pin_memory=True)
+        self._x0_stage.copy_(x0_host, non_blocking=True)
+        self.launch(self._x0_stage)
+        self._final_host.copy_(self.x32[:, :self.cfg.hidden_dim], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self._final_host
+
     def capture(self):
         self._x0_graph = torch.as_tensor(self.x0.values).to(
             device=self.dev, dtype=torch.float32).contiguous().clone()
@@ -460,11 +488,13 @@ class EPRunner:
         import torch.distributed as dist
         cfg = self.cfg
         status = self.status.cpu().tolist()
-        bad = torch.tensor([status[0]], dtype=torch.int64)
-        cnt = self.counters.cpu()
+        cdev = "cuda" if self.world > 1 and dist.get_backend(self.pg) == "nccl" else "cpu"
+        bad = torch.tensor([status[0]], dtype=torch.int64, device=cdev)
+        cnt = self.counters.to(cdev).clone()
         if reduce and self.world > 1:
             dist.all_reduce(bad, op=dist.ReduceOp.MIN, group=self.pg)
             dist.all_reduce(cnt, group=self.pg)
+        bad, cnt = bad.cpu(), cnt.cpu()
         if int(bad.item()) != INT32_MAX:
             raise NumericalDivergenceError(f"non-finite values at step {int(bad.item())}",
                                            step=int(bad.item()))
