@@ -55,6 +55,17 @@ class Window:
     """One cudaMalloc'd allocation: receive windows, combine window and flags."""
 
     def __init__(self, L, D, cap, ncap, hp, device):
+        self._layout(L, D, cap, ncap, hp)
+        h = ctypes.c_void_p()
+        torch.cuda.set_device(device)
+        _lib.call("dice_device_alloc", self.nbytes, ctypes.byref(h))
+        self.ptr = int(h.value)
+        # free flags start at 1 (regions free), ready flags at 0
+        for o in (self.o_rx_free, self.o_cx_free):
+            self.view(o, (L * D,), torch.int32).fill_(1)
+        torch.cuda.synchronize()
+
+    def _layout(self, L, D, cap, ncap, hp):
         self.L, self.D, self.cap, self.ncap, self.hp = L, D, cap, ncap, hp
         off = 0
 
@@ -73,14 +84,6 @@ class Window:
         self.o_rx_free = take(L * D * 4)
         self.o_cx_free = take(L * D * 4)
         self.nbytes = off
-        h = ctypes.c_void_p()
-        torch.cuda.set_device(device)
-        _lib.call("dice_device_alloc", self.nbytes, ctypes.byref(h))
-        self.ptr = int(h.value)
-        # free flags start at 1 (regions free), ready flags at 0
-        for o in (self.o_rx_free, self.o_cx_free):
-            self.view(o, (L * D,), torch.int32).fill_(1)
-        torch.cuda.synchronize()
 
     def view(self, offset, shape, dtype):
         if dtype is torch.bfloat16:
@@ -153,13 +156,24 @@ class EPGroup:
         return self.base[owner] + o + (layer * w.D + peer) * 4
 
     # stream memops ---------------------------------------------------------
+    trace = None   # optional list: the protocol simulation test records every op
+
     def wait(self, addrs, value):
+        if self.trace is not None:
+            self.trace.append(("wait", [int(a) for a in addrs], value))
         arr = _u64_array(addrs)
         _lib.call("dice_stream_wait_eq", arr, len(addrs), value, ops._stream())
 
     def write(self, addrs, value):
+        if self.trace is not None:
+            self.trace.append(("write", [int(a) for a in addrs], value))
         arr = _u64_array(addrs)
         _lib.call("dice_stream_write", arr, len(addrs), value, ops._stream())
+
+    def data(self, kind, regions):
+        """Record a data access of a kernel (test tracing only)."""
+        if self.trace is not None:
+            self.trace.append((kind, regions))
 
 
 class _EPPayload:
@@ -219,7 +233,8 @@ class EPRunner:
                     for r in range(world))
         self.cap = n_max * k
         L = cfg.num_layers
-        self.win = Window(L, world, self.cap, self.cap, hp, torch.cuda.current_device())
+        self.win = Window(L, world, self.cap, self.cap, hp,
+                          torch.cuda.current_device() if str(dev).startswith("cuda") else None)
         self.grp = EPGroup(self.win, rank, world, pg)
         f32, bf = torch.float32, torch.bfloat16
         self.x32 = torch.zeros(n, hp, dtype=f32, device=dev)
@@ -331,6 +346,7 @@ class EPRunner:
                   self.pos_dest.data_ptr(), self.dest_off.data_ptr(),
                   self.counters[step, layer].data_ptr(), self.r0, self.cfg.total_rows,
                   self.scratch.data_ptr(), rx_rows, rx_meta, rx_cnt, ops._stream())
+        g.data("write", [("rx", d, layer, me) for d in self._peers()])
         g.write([g.flag("rx_ready", d, layer, me) for d in self._peers()], 1)
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
@@ -361,6 +377,8 @@ class EPRunner:
         if self.time_experts:
             e1.record()
             self._expert_events.append((e0, e1, p.gen, layer))
+        g.data("read", [("rx", me, layer, s) for s in self._peers()])
+        g.data("write", [("cx", h, layer, me) for h in self._peers()])
         g.write([g.flag("rx_free", s, layer, me) for s in self._peers()], 1)
         g.write([g.flag("cx_ready", h, layer, me) for h in self._peers()], 1)
         self.deferred[layer] = p
@@ -383,6 +401,7 @@ class EPRunner:
                            None if c is None else c.rows[layer],
                            None if c is None else c.gates[layer],
                            None if c is None else c.expert_ids[layer])
+        g.data("read", [("cx", me, layer, r) for r in self._peers()])
         g.write([g.flag("cx_free", r, layer, me) for r in self._peers()], 1)
         self.deferred[layer] = None
 

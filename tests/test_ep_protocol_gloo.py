@@ -1,0 +1,128 @@
+"""CPU, world_size 2 and 4 over gloo: the expert-parallel exchange protocol
+(EPRunner host control flow, IPC-handle rendezvous through torch.distributed,
+ready/free flag handshakes) is simulated under many random interleavings of
+the ranks' stream operations. Checks: no deadlock, every window region is
+written exactly once before it is read and read before it is rewritten (no
+data race), every flag returns to its initial value (graph-replay safe), and
+all ranks follow the reference staleness law."""
+import json
+import os
+import pickle
+import random
+import socket
+import subprocess
+import sys
+import tempfile
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FAKE_BASE = 1 << 40
+
+CFG = dict(num_layers=3, num_experts=8, num_shared=1, top_k=2, hidden_dim=8, expert_dim=16,
+           num_tokens=4, batch=2, num_steps=7, step_size=1e-3)
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def collect(world, strategy, policy, runs=1):
+    port = free_port()
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "logs.pkl")
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "ep_protocol_worker.py"),
+                                   json.dumps(dict(rank=r, world=world, port=port, cfg=CFG,
+                                                   strategy=strategy, policy=policy, out=out,
+                                                   runs=runs))])
+                 for r in range(world)]
+        for p in procs:
+            p.wait(timeout=180)
+            assert p.returncode == 0
+        with open(out, "rb") as f:
+            return pickle.load(f)
+
+
+def initial_flags(logs):
+    flags = {}
+    for lg in logs:
+        lay, b = lg["layout"], FAKE_BASE * (lg["rank"] + 1)
+        n = lay["L"] * lay["D"]
+        for key, init in (("o_rx_ready", 0), ("o_cx_ready", 0), ("o_rx_free", 1), ("o_cx_free", 1)):
+            for i in range(n):
+                flags[b + lay[key] + 4 * i] = init
+    return flags
+
+
+def simulate(logs, seed):
+    rng = random.Random(seed)
+    flags = initial_flags(logs)
+    init = dict(flags)
+    full = set()            # window regions holding unread data
+    pcs = [0] * len(logs)
+    traces = [lg["trace"] for lg in logs]
+    steps = 0
+    while True:
+        ready = []
+        for r, tr in enumerate(traces):
+            if pcs[r] >= len(tr):
+                continue
+            op = tr[pcs[r]]
+            if op[0] == "wait" and not all(flags[a] == op[2] for a in op[1]):
+                continue
+            ready.append(r)
+        if not ready:
+            break
+        r = rng.choice(ready)
+        op = traces[r][pcs[r]]
+        if op[0] == "write":                      # flag write (stream memop)
+            for a in op[1]:
+                assert a in flags, hex(a)
+                flags[a] = op[2]
+        elif op[0] == "kwrite":                   # kernel stores into window regions
+            for reg in map(tuple, op[1]):
+                assert reg not in full, f"rank {r} overwrites unread {reg}"
+                full.add(reg)
+        elif op[0] == "read":                     # kernel reads window regions
+            for reg in map(tuple, op[1]):
+                assert reg in full, f"rank {r} reads {reg} before it was written"
+                full.discard(reg)
+        pcs[r] += 1
+        steps += 1
+    done = all(pcs[r] >= len(t) for r, t in enumerate(traces))
+    assert done, f"deadlock: pcs={pcs}"
+    assert not full, f"unread regions at the end: {sorted(full)[:4]}"
+    assert flags == init, "flags not restored"
+    return steps
+
+
+@pytest.mark.parametrize("world,strategy,policy", [(2, "synchronous", "neutral"),
+                                                   (2, "interweaved", "dice"),
+                                                   (4, "interweaved", "neutral"),
+                                                   (4, "interweaved", "deep")])
+def test_exchange_protocol_random_interleavings(world, strategy, policy):
+    logs = collect(world, strategy, policy, runs=2)
+    # the trace records kernel writes as ("write", [regions]) only when the
+    # items are region tuples; split them from flag writes (ints)
+    for lg in logs:
+        fixed = []
+        for op in lg["trace"]:
+            if op[0] == "write" and op[1] and not isinstance(op[1][0], int):
+                fixed.append(("kwrite", op[1]))
+            else:
+                fixed.append(op)
+        lg["trace"] = fixed
+    recs = [lg["records"] for lg in logs]
+    assert all(r == recs[0] for r in recs), "ranks disagree on the schedule"
+    for seed in range(40):
+        simulate(logs, seed)
+
+
+def test_handles_exchanged_over_gloo():
+    logs = collect(2, "synchronous", "neutral")
+    for lg in logs:
+        assert lg["base"] == [FAKE_BASE * (r + 1) for r in range(2)]
