@@ -108,6 +108,7 @@ class _Payload:
         self.x_perm = torch.empty(max_rows, hp, dtype=torch.bfloat16, device=device)
         self.layer = -1
         self.gen = -1
+        self.done = None     # side-stream event: expert FFN + merge of this payload finished
 
 
 class DeviceRunner:
@@ -117,7 +118,7 @@ class DeviceRunner:
     def __init__(self, model: ToyModel, x0: ActivationBlock, strategy: Strategy,
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *,
                  record_inputs: bool = False, record_routes: bool = False,
-                 time_experts: bool = False):
+                 time_experts: bool = False, overlap: bool = True):
         cfg = model.config
         if not isinstance(strategy, Strategy):
             raise ContractError(f"strategy must be a Strategy, got {strategy!r}")
@@ -158,7 +159,7 @@ class DeviceRunner:
         if strategy is Strategy.SYNCHRONOUS:
             self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev)]
         elif strategy is Strategy.INTERWEAVED:
-            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(2)]
+            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(3)]
         else:
             self.payloads = [[_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(2)]
                              for _ in range(L)]
@@ -173,6 +174,12 @@ class DeviceRunner:
         self._event_pool = []
         self.graph = None
         self.launches_per_run = 0
+        # interweaved: the pending dispatch's expert FFN + cache merge run on a side
+        # stream, concurrently with the next stage's shared FFN / consume on the
+        # main stream (the intra-GPU analogue of the interweaved overlap window)
+        self.side = None
+        if overlap and strategy is Strategy.INTERWEAVED and str(dev).startswith("cuda"):
+            self.side = torch.cuda.Stream(device=dev)
 
     # ------------------------------------------------------------ helpers
     def _reset_state(self, x0_device=None):
@@ -192,6 +199,10 @@ class DeviceRunner:
         self.slot_gen = [None] * L          # generating step of each combine slot
         self.dispatch_slot = [None] * L     # displaced only
         self.pending = None                 # interweaved only
+        self.slot_event = [None] * L        # side-stream event guarding slot[l] / cache[l]
+        self.side_tail = None
+        for p in (self.payloads if self.strategy is Strategy.INTERWEAVED else []):
+            p.done = None
         self.occupied = set()
         self.peak_buffer_bytes = 0
         self.ring = 0
@@ -223,7 +234,10 @@ class DeviceRunner:
             return self.payloads[0]
         if self.strategy is Strategy.INTERWEAVED:
             p = self.payloads[self.ring]
-            self.ring ^= 1
+            self.ring = (self.ring + 1) % len(self.payloads)
+            if p.done is not None:       # the side stream may still read this buffer
+                torch.cuda.current_stream().wait_event(p.done)
+                p.done = None
             return p
         pair = self.payloads[layer]
         return pair[1] if self.dispatch_slot[layer] is pair[0] else pair[0]
@@ -245,9 +259,32 @@ class DeviceRunner:
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 
-    def _process(self, p: _Payload):
+    def _process(self, p: _Payload, side: bool = False):
         """Expert FFN on a dispatched payload + stale-cache merge into its
-        combine slot (_process_dispatch, schedules.py:388-397)."""
+        combine slot (_process_dispatch, schedules.py:388-397). With side=True
+        the work is enqueued on the side stream after the payload's dispatch."""
+        if side and self.side is not None:
+            ready = torch.cuda.Event()
+            ready.record()
+            self.side.wait_event(ready)
+            with torch.cuda.stream(self.side):
+                self._process_body(p)
+                done = torch.cuda.Event()
+                done.record()
+            p.done = done
+            self.slot_event[p.layer] = done
+            self.side_tail = done
+            return
+        self._join_side()
+        self._process_body(p)
+
+    def _join_side(self):
+        """Main stream waits for all side-stream work (shared expert scratch)."""
+        if self.side_tail is not None:
+            torch.cuda.current_stream().wait_event(self.side_tail)
+            self.side_tail = None
+
+    def _process_body(self, p: _Payload):
         lw = self.model.layers[p.layer]
         if self.time_experts:
             i = len(self._expert_events)
@@ -268,10 +305,10 @@ class DeviceRunner:
         self.slot_gen[p.layer] = p.gen
         self.combine_log.append((p.gen, p.layer))
 
-    def _flush_pending(self):
+    def _flush_pending(self, side=False):
         prev, self.pending = self.pending, None
         if prev is not None:
-            self._process(prev)
+            self._process(prev, side=side)
             self._track("c", prev.layer)
 
     def _consume(self, layer, step, gen):
@@ -299,6 +336,10 @@ class DeviceRunner:
             sync = self._stage_is_sync(step, layer)
             if sync and self.strategy is Strategy.INTERWEAVED:
                 self._flush_pending()
+            if self.slot_event[layer] is not None:
+                # slot[layer] / cache[layer] are written on the side stream
+                torch.cuda.current_stream().wait_event(self.slot_event[layer])
+                self.slot_event[layer] = None
             p = self._next_payload(layer)
             ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores, self.status,
                           step, layer)
@@ -332,10 +373,10 @@ class DeviceRunner:
                 self._dispatch(step, layer, p, force=False)
                 prev, self.pending = self.pending, p
                 if prev is not None:
-                    self._process(prev)
+                    self._process(prev, side=True)
                     self._track("c", prev.layer)
                 self._consume(layer, step, self.slot_gen[layer])
-        self._flush_pending()
+        self._flush_pending(side=self.strategy is Strategy.INTERWEAVED)
         ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
         if self.record_inputs:
             self.step_inputs.append(inputs_here)
@@ -356,6 +397,7 @@ class DeviceRunner:
         self._reset_state(x0_device)
         for step in range(self.cfg.num_steps):
             self._run_step(step)
+        self._join_side()
         self.launches_per_run = _lib.launch_count[0] - c0
 
     def capture(self):

@@ -50,5 +50,6 @@ if __name__ == "__main__":
     bench(8192, 9216, 1152, 1, label="shared GEMM1 (gelu)")
     bench(8192, 1152, 9216, 4, label="shared GEMM2 (consume)")
     bench(16384, 4608, 1152, 1, label="expert GEMM1 (dense eq.)")
+    bench(16384, 4608, 1152, 0, label="expert GEMM1 no-GELU")
     bench(16384, 1152, 4608, 0, label="expert GEMM2 (dense eq.)")
     bench(8192, 8192, 8192, 0, label="square 8192")
