@@ -94,7 +94,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, const float* s
       const int64_t row = row0 + (half * 4 + it) * 4 + (lane >> 3);
       float4 x = v[it];
       if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
-        x.x = gelu_erf(x.x); x.y = gelu_erf(x.y); x.z = gelu_erf(x.z); x.w = gelu_erf(x.w);
+        const float2 lo = gelu_erf2(make_float2(x.x, x.y));
+        const float2 hi = gelu_erf2(make_float2(x.z, x.w));
+        x = make_float4(lo.x, lo.y, hi.x, hi.y);
       }
       if constexpr (EPI == EPI_GELU_RESID) {
         x.x += r[it].x; x.y += r[it].y; x.z += r[it].z; x.w += r[it].w;

@@ -127,6 +127,34 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 // the GELU at the magnitudes that matter and far below the bf16 output
 // rounding) with MUFU rcp/ex2 - about a third of the instructions of erff, which
 // matters because the GEMM1 epilogue is instruction-bound.
+// Two GELUs at once on the packed fp32x2 pipe (FFMA2 / FMUL2, sm_100): the
+// same A&S 7.1.26 arithmetic as gelu_erf with half the FP instructions.
+__device__ __forceinline__ float2 gelu_erf2(float2 x) {
+  const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
+  const float2 d = __ffma2_rn(ax, make_float2(0.3275911f * 0.70710678118654752440f,
+                                              0.3275911f * 0.70710678118654752440f),
+                              make_float2(1.0f, 1.0f));
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(d.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(d.y));
+  float2 p = __ffma2_rn(make_float2(1.061405429f, 1.061405429f), t,
+                        make_float2(-1.453152027f, -1.453152027f));
+  p = __ffma2_rn(p, t, make_float2(1.421413741f, 1.421413741f));
+  p = __ffma2_rn(p, t, make_float2(-0.284496736f, -0.284496736f));
+  p = __ffma2_rn(p, t, make_float2(0.254829592f, 0.254829592f));
+  p = __fmul2_rn(p, t);
+  // exp(-x^2/2) = ex2(x^2 * (-log2(e)/2))
+  const float2 q = __fmul2_rn(__fmul2_rn(x, x), make_float2(-0.72134752044448170368f,
+                                                           -0.72134752044448170368f));
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(q.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(q.y));
+  const float2 ea = __ffma2_rn(make_float2(-p.x, -p.y), e, make_float2(1.0f, 1.0f));
+  const float2 er = make_float2(copysignf(ea.x, x.x), copysignf(ea.y, x.y));
+  const float2 hx = __fmul2_rn(x, make_float2(0.5f, 0.5f));
+  return __ffma2_rn(hx, er, hx);
+}
+
 __device__ __forceinline__ float gelu_erf(float x) {
   const float z = fabsf(x) * 0.70710678118654752440f;
   float t;
