@@ -233,8 +233,9 @@ __global__ void __launch_bounds__(512) gate_topk_fast_kernel(
     const float* r0 = u + t0 * hp;
     const float* r1 = u + (has1 ? t0 + 1 : t0) * hp;
     float a[32];
+    float2 acc[E];   // (row 0, row 1) partial logits per expert, packed FFMA2
 #pragma unroll
-    for (int i = 0; i < 32; ++i) a[i] = 0.f;
+    for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
     constexpr int CH = 4;
     for (int base = 0; base < hp; base += 128 * CH) {
       float4 xs[CH], ys[CH];
@@ -254,16 +255,22 @@ __global__ void __launch_bounds__(512) gate_topk_fast_kernel(
         const int c = base + 128 * j + lane * 4;
         if (c >= hp) break;
         const float4 x = xs[j], y = ys[j];
+        const float2 p0 = make_float2(x.x, y.x), p1 = make_float2(x.y, y.y);
+        const float2 p2 = make_float2(x.z, y.z), p3 = make_float2(x.w, y.w);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const float4 w = *reinterpret_cast<const float4*>(sw + e * hp + c);
-          a[e] = fmaf(x.x, w.x, a[e]); a[e] = fmaf(x.y, w.y, a[e]);
-          a[e] = fmaf(x.z, w.z, a[e]); a[e] = fmaf(x.w, w.w, a[e]);
-          a[E + e] = fmaf(y.x, w.x, a[E + e]); a[E + e] = fmaf(y.y, w.y, a[E + e]);
-          a[E + e] = fmaf(y.z, w.z, a[E + e]); a[E + e] = fmaf(y.w, w.w, a[E + e]);
+          acc[e] = __ffma2_rn(p0, make_float2(w.x, w.x), acc[e]);
+          acc[e] = __ffma2_rn(p1, make_float2(w.y, w.y), acc[e]);
+          acc[e] = __ffma2_rn(p2, make_float2(w.z, w.z), acc[e]);
+          acc[e] = __ffma2_rn(p3, make_float2(w.w, w.w), acc[e]);
         }
       }
     }
+#pragma unroll
+    for (int e = 0; e < E; ++e) { a[e] = acc[e].x; a[E + e] = acc[e].y; }
+#pragma unroll
+    for (int i = 2 * E; i < 32; ++i) a[i] = 0.f;
     // transpose-reduce: V values -> 1 value per lane
     if constexpr (V == 32) {
       tr_level<32>(a, lane, 16); tr_level<16>(a, lane, 8); tr_level<8>(a, lane, 4);
@@ -506,13 +513,13 @@ __global__ void __launch_bounds__(256) permute_gather_kernel(
 // row; inactive pairs read the cached row and gate (policies.py:197-202);
 // write pairs persist row / gate / id (policies.py:203-207). write implies
 // active, so no thread reads a cache entry another thread writes.
+template <int KMAX>
 __global__ void __launch_bounds__(256) cache_assemble_kernel(
     const uint16_t* __restrict__ y, const int32_t* __restrict__ pos,
     const uint8_t* __restrict__ active, const uint8_t* __restrict__ write,
     const float* __restrict__ gates, const int32_t* __restrict__ ids, int64_t n, int k, int hp,
     uint16_t* cache_rows, float* cache_gates, int32_t* cache_ids, float* routed, float* rows_out,
     float* gates_out) {
-  constexpr int KMAX = 8;
   const int lane = threadIdx.x & 31;
   const int vec = hp / 8;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
@@ -742,7 +749,7 @@ int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int
   const size_t smem = (size_t)E * hp * sizeof(float);
   const int threads = 512;
   int64_t want = ((n + 1) / 2 + 15) / 16;
-  const int grid = (int)(want < 4 * 148 ? (want < 1 ? 1 : want) : 4 * 148);
+  const int grid = (int)(want < 2 * 148 ? (want < 1 ? 1 : want) : 2 * 148);
   cudaStream_t s = (cudaStream_t)stream;
 #define DICE_GATE(EM)                                                                          \
   {                                                                                            \
@@ -838,9 +845,18 @@ int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* ac
                         float* routed, float* rows_out, float* gates_out, void* stream) {
   if (hp % 64 != 0 || k < 1 || k > 8) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
-  cache_assemble_kernel<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      y, pos, active, write, gates, ids, n, k, hp, cache_rows, cache_gates, cache_ids, routed,
-      rows_out, gates_out);
+  // register footprint scales with the slot count: instantiate the small k's
+  const int grid = grid_for(n * 32, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+#define DICE_ASM(KK)                                                                           \
+  cache_assemble_kernel<KK><<<grid, 256, 0, st>>>(y, pos, active, write, gates, ids, n, k, hp, \
+                                                  cache_rows, cache_gates, cache_ids, routed,  \
+                                                  rows_out, gates_out)
+  if (k == 1) DICE_ASM(1);
+  else if (k == 2) DICE_ASM(2);
+  else if (k <= 4) DICE_ASM(4);
+  else DICE_ASM(8);
+#undef DICE_ASM
   return launch_ok();
 }
 
