@@ -253,6 +253,12 @@ def run_gpu(args):
     n_launch = len(expert_events)
     achieved = flops / t_exp / 1e12
     peak_tf, _, peak_kind = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_roofline_traffic.json")) as f:
+            traffic = json.load(f)["traffic_bytes_per_launch_pair"]
+    except Exception:
+        pass
 
     # e2e through the serving call with host buffers
     x0_host = torch.as_tensor(x0.values).cpu().pin_memory()
@@ -314,7 +320,8 @@ def run_gpu(args):
         "exposed_a2a_us": exposed_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
         "roofline": {"bound": "tensor", "kernel": "grouped expert FFN (tcgen05 GEMM1+GELU, GEMM2)",
                      "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tf, "traffic": None,
+                     "frac": achieved / peak_tf, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per grouped-FFN launch pair (ncu --set full)",
                      "peak_kind": f"{peak_kind} bf16 sustained",
                      "launches": n_launch, "flops_per_pair": pair_flops,
                      "share_of_step": t_exp / (ms_per_step / 1e3)},
