@@ -192,7 +192,7 @@ def run_gpu(args):
         x0 = D.sample_x0(cfg, seed)
         cluster = D.ClusterConfig(num_devices=1)
         runner = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed,
-                                time_experts=True)
+                                time_experts=True, overlap=args.overlap)
     else:
         # expert parallelism: 32 images per GPU (weak scaling), experts e // (E/N) per
         # rank, token rows (t*N)//R per rank, exchange over peer memory
@@ -350,6 +350,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-quality", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch kernels from Python, no CUDA graph")
+    ap.add_argument("--overlap", action="store_true",
+                    help="run the pending expert FFN on a side stream (intra-GPU interweaving)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

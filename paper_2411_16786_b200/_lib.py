@@ -102,11 +102,11 @@ def check(rc: int, what: str) -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches count)
-KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_grouped_ffn": 2, "dice_event_create": 0,
+KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_grouped_ffn": 4, "dice_gemm": 2, "dice_event_create": 0,
                     "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,
-                    "dice_stream_write": 0, "dice_ep_dispatch": 3, "dice_ep_expert": 7}
+                    "dice_stream_write": 0, "dice_ep_dispatch": 3, "dice_ep_expert": 9}
 launch_count = [0]
 
 

@@ -255,6 +255,136 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   }
 }
 
+// --------------------------------------------------------------- stream-K
+// Persistent pairs first run whole waves of tiles (data parallel), then split
+// the k-loops of the R < P remainder tiles evenly over all P pairs. A
+// remainder tile is covered by consecutive segments (pair q, tile j); each
+// segment stores its fp32 partial to workspace slot q + j, and a fixup kernel
+// sums the slots of each tile in pair order (deterministic) and applies the
+// epilogue. No CTA ever waits on another, so no co-residency assumption.
+struct SkPlan {
+  int T, KB, P, DP, R;
+  long long I;
+  bool on;
+  __device__ __forceinline__ void init(int T_, int KB_, int P_, bool allow) {
+    T = T_; KB = KB_; P = P_;
+    R = T % P;
+    // only where the partial last wave costs more than the partial sums
+    on = allow && R > 0 && T >= P && T < 8 * P && (long long)R * KB >= 2LL * P;
+    DP = on ? T - R : T;
+    I = on ? (long long)R * KB : 0;
+  }
+  __device__ __forceinline__ long long begin(int q) const { return (long long)q * I / P; }
+  __device__ __forceinline__ int pair_of(long long x) const {
+    int q = (int)(x * P / I);
+    while (q + 1 < P && begin(q + 1) <= x) ++q;
+    while (q > 0 && begin(q) > x) --q;
+    return q;
+  }
+  // number of work items of pair p
+  __device__ __forceinline__ int items(int p) const {
+    int n = p < DP ? (DP - 1 - p) / P + 1 : 0;
+    if (on) {
+      const long long b = begin(p), e = begin(p + 1);
+      if (e > b) n += (int)((e - 1) / KB - b / KB + 1);
+    }
+    return n;
+  }
+  // item i of pair p: tile, k-range [k0, k1), workspace slot (-1 = whole tile)
+  __device__ __forceinline__ void item(int p, int i, int& tile, int& k0, int& k1, int& slot) const {
+    const int ndp = p < DP ? (DP - 1 - p) / P + 1 : 0;
+    if (i < ndp) { tile = p + i * P; k0 = 0; k1 = KB; slot = -1; return; }
+    const long long b = begin(p), e = begin(p + 1);
+    const int jl = (int)(b / KB) + (i - ndp);
+    const long long s0 = (long long)jl * KB > b ? (long long)jl * KB : b;
+    const long long s1 = (long long)(jl + 1) * KB < e ? (long long)(jl + 1) * KB : e;
+    tile = DP + jl;
+    k0 = (int)(s0 - (long long)jl * KB);
+    k1 = (int)(s1 - (long long)jl * KB);
+    slot = p + jl;
+  }
+};
+
+constexpr int kSkMaxSlots = 160;   // >= pairs + remainder tiles (<= 74 + 73)
+
+// fp32 partial of this CTA's 128 rows x 32 columns into the tile's workspace slot
+__device__ __forceinline__ void epilogue_partial(const float* stage, int lane, float* ws_tile,
+                                                 int bn, int row_in_tile0, int col_in_tile) {
+  const int q = lane & 7;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
+    *reinterpret_cast<float4*>(ws_tile + (int64_t)(row_in_tile0 + rr) * bn + col_in_tile + 4 * q) = v;
+  }
+}
+
+// Sum each remainder tile's partial slots in pair order and apply the epilogue.
+// One block per (remainder tile, 16-row band); the tile's slot range is
+// computed once per block.
+template <int EPI>
+__global__ void __launch_bounds__(256) stream_k_fixup_kernel(const GemmArgs a, const float* ws,
+                                                             int bn, int pairs) {
+  __shared__ int info[4];   // m_tiles, q0, q1, on
+  if (threadIdx.x == 0)
+    info[0] = a.group_tile_offsets != nullptr ? a.group_tile_offsets[a.num_groups] : a.num_m_tiles;
+  __syncthreads();
+  SkPlan plan;
+  plan.init(info[0] * a.num_n_blocks, a.num_k_blocks, pairs, true);
+  if (!plan.on) return;
+  const int row_limit = a.group_tile_offsets != nullptr ? INT_MAX : a.M_valid;
+  const int c4n = bn / 4;
+  constexpr int kBand = 16;
+  const int bands = plan.R * (256 / kBand);
+  for (int b = blockIdx.x; b < bands; b += gridDim.x) {
+    const int jl = b / (256 / kBand);
+    const int row_base = (b - jl * (256 / kBand)) * kBand;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      info[1] = plan.pair_of((long long)jl * plan.KB);
+      info[2] = plan.pair_of((long long)(jl + 1) * plan.KB - 1);
+    }
+    __syncthreads();
+    const int q0 = info[1], q1 = info[2];
+    const int tile = plan.DP + jl;
+    const int n_blk = tile % a.num_n_blocks, m_tile = tile / a.num_n_blocks;
+    for (int e = threadIdx.x; e < kBand * c4n; e += blockDim.x) {
+      const int rr = e / c4n;
+      const int c4 = e - rr * c4n;
+      const int row_in = row_base + rr;
+      const int col = n_blk * bn + 4 * c4;
+      const int64_t row = (int64_t)m_tile * 256 + row_in;
+      if (col >= a.N || row >= row_limit) continue;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = q0; q <= q1; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(
+            ws + ((int64_t)(q + jl) * 256 + row_in) * bn + 4 * c4);
+        x.x += v.x; x.y += v.y; x.z += v.z; x.w += v.w;
+      }
+      if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
+        const float2 lo = gelu_erf2(make_float2(x.x, x.y));
+        const float2 hi = gelu_erf2(make_float2(x.z, x.w));
+        x = make_float4(lo.x, lo.y, hi.x, hi.y);
+      }
+      if constexpr (EPI == EPI_GELU_RESID) {
+        const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
+        x.x += r.x; x.y += r.y; x.z += r.z; x.w += r.w;
+      }
+      if constexpr (EPI == EPI_CONSUME) {
+        const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
+        const float4 q = *reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col);
+        x.x = r.x + (x.x + q.x); x.y = r.y + (x.y + q.y); x.z = r.z + (x.z + q.z); x.w = r.w + (x.w + q.w);
+      }
+      if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
+      if (a.out_bf16 != nullptr) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+        *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
+            make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      }
+    }
+  }
+}
+
 // --------------------------------------------------------- CTA-pair kernel
 // cta_group::2: a cluster of two CTAs computes a 256 x BN tile. Each CTA
 // stages its own 128 rows of A and half (BN/2 rows) of B, so per-CTA operand
@@ -316,18 +446,23 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int num_tiles = m_tiles * n_blocks;
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
+  SkPlan plan;
+  plan.init(num_tiles, k_blocks, num_pairs, args.sk_workspace != nullptr);
+  const int n_items = plan.items(pair);
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+      for (int it = 0; it < n_items; ++it) {
+        int tile, k0, k1, slot;
+        plan.item(pair, it, tile, k0, k1, slot);
         const int n_blk = tile % n_blocks;   // N-fastest: resident tiles share A rows
         const int m_tile = tile / n_blocks;
         const int g = find_group(sh->group_off, groups, m_tile);
         const int a_row = m_tile * kPairM + rank * BM;
         const int b_row = g * args.N + n_blk * BN + rank * (BN / 2);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0), C::kStageBytes);
           tma_load_2d_pair(smA + stage * C::kABytes, &tmA, &sh->full[stage], kb * BK, a_row);
@@ -341,14 +476,15 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       constexpr uint32_t idesc = idesc_bf16_f32(kPairM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
-      for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+      for (int local = 0; local < n_items; ++local) {
+        int tile, k0, k1, slot;
+        plan.item(pair, local, tile, k0, k1, slot);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::kABytes);
@@ -356,7 +492,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             umma_bf16_pair(d_tmem, umma_desc_sw128(a_base + k * UMMA_K * 2),
-                           umma_desc_sw128(b_base + k * UMMA_K * 2), idesc, (kb | k) != 0);
+                           umma_desc_sw128(b_base + k * UMMA_K * 2), idesc,
+                           (kb != k0 || k != 0) ? 1u : 0u);
           }
           umma_commit_pair(&sh->empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -371,8 +508,9 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
-    int local = 0;
-    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+    for (int local = 0; local < n_items; ++local) {
+      int tile, k0, k1, slot;
+      plan.item(pair, local, tile, k0, k1, slot);
       const int n_blk = tile % n_blocks;
       const int m_tile = tile / n_blocks;
       const int acc = local & 1;
@@ -380,6 +518,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_wait(&sh->tfull[acc], acc_phase);
       tc_fence_after();
       const int row0 = m_tile * kPairM + rank * BM + sub * 32;
+      float* ws_tile = slot >= 0 ? args.sk_workspace + (int64_t)slot * kPairM * BN : nullptr;
 #pragma unroll 1
       for (int ci = grp; ci < BN / 32; ci += kEpiGroups) {
         const int col_in_tile = ci * 32;
@@ -394,7 +533,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         __syncwarp();
-        epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
+        if (ws_tile != nullptr)
+          epilogue_partial(stage, lane, ws_tile, BN, rank * BM + sub * 32, col_in_tile);
+        else
+          epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
         __syncwarp();
       }
       tc_fence_before();
@@ -502,6 +644,35 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int 
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 
+// One stream-K partial-sum workspace per stream (concurrent GEMMs on different
+// streams must not share it). Allocated on first use, before any graph capture.
+std::mutex g_ws_mu;
+std::unordered_map<cudaStream_t, float*> g_ws;
+
+float* stream_k_workspace(cudaStream_t stream) {
+  static int mode = -1;
+  if (mode < 0) {
+    // measured slower on the MoE shapes (partial sums + fixup cost more than the
+    // last-wave tail), so opt-in only: DICE_GEMM_STREAMK=1
+    const char* e = getenv("DICE_GEMM_STREAMK");
+    mode = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  if (mode == 0) return nullptr;
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto it = g_ws.find(stream);
+  if (it != g_ws.end()) return it->second;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &st);
+  if (st != cudaStreamCaptureStatusNone) return nullptr;   // never allocate while capturing
+  float* p = nullptr;
+  if (cudaMalloc(&p, sizeof(float) * (size_t)kSkMaxSlots * 256 * 256) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  g_ws[stream] = p;
+  return p;
+}
+
 template <int BN, int EPI>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream) {
@@ -516,7 +687,11 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   int grid = 2 * max_tiles < num_sms() ? 2 * max_tiles : num_sms();
   grid &= ~1;
   if (grid <= 0) return 0;
-  gemm_bf16_pair<BN, EPI><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, a);
+  GemmArgs aa = a;
+  aa.sk_workspace = stream_k_workspace(stream);
+  gemm_bf16_pair<BN, EPI><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, aa);
+  if (aa.sk_workspace != nullptr)
+    stream_k_fixup_kernel<EPI><<<num_sms() * 2, 256, 0, stream>>>(aa, aa.sk_workspace, BN, grid / 2);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 

@@ -35,6 +35,7 @@ struct GemmArgs {
   int64_t ld_res;
   const float* addend;
   int64_t ld_add;
+  float* sk_workspace;   // stream-K partials (pair kernel); null disables stream-K
 };
 
 struct GemmProblem {

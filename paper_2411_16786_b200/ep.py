@@ -491,12 +491,20 @@ class EPRunner:
         return self._final_host
 
     def capture(self):
+        """Capture one whole sampling run into a CUDA graph. The schedule's
+        control flow is host-deterministic and every buffer is static, so the
+        graph replays the identical kernel sequence; x0 is read from a static
+        staging buffer (see sample()). The warm-up run uses the capture stream
+        so per-stream library state (stream-K workspace) exists before capture."""
         self._x0_graph = torch.as_tensor(self.x0.values).to(
             device=self.dev, dtype=torch.float32).contiguous().clone()
-        self.launch(self._x0_graph)
+        self._cap_stream = torch.cuda.Stream(device=self.dev)
+        self._cap_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self._cap_stream):
+            self.launch(self._x0_graph)          # warm: kernel attributes, tensor maps
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g, stream=self._cap_stream):
             self.launch(self._x0_graph)
         torch.cuda.synchronize()
         self.graph = g

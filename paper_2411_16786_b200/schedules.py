@@ -118,7 +118,7 @@ class DeviceRunner:
     def __init__(self, model: ToyModel, x0: ActivationBlock, strategy: Strategy,
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *,
                  record_inputs: bool = False, record_routes: bool = False,
-                 time_experts: bool = False, overlap: bool = True):
+                 time_experts: bool = False, overlap: bool = False):
         cfg = model.config
         if not isinstance(strategy, Strategy):
             raise ContractError(f"strategy must be a Strategy, got {strategy!r}")
@@ -404,13 +404,17 @@ class DeviceRunner:
         """Capture one whole sampling run into a CUDA graph. The schedule's
         control flow is host-deterministic and every buffer is static, so the
         graph replays the identical kernel sequence; x0 is read from a static
-        staging buffer (see sample())."""
+        staging buffer (see sample()). The warm-up run uses the capture stream
+        so per-stream library state (stream-K workspace) exists before capture."""
         self._x0_graph = torch.as_tensor(self.x0.values).to(
             device=self.dev, dtype=torch.float32).contiguous().clone()
-        self.launch(self._x0_graph)          # warm: kernel attributes, tensor maps
+        self._cap_stream = torch.cuda.Stream(device=self.dev)
+        self._cap_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self._cap_stream):
+            self.launch(self._x0_graph)          # warm: kernel attributes, tensor maps
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g, stream=self._cap_stream):
             self.launch(self._x0_graph)
         torch.cuda.synchronize()
         self.graph = g

@@ -63,3 +63,39 @@ def test_splitmix_fill_bit_exact_f64():
     assert np.array_equal(o32.cpu().numpy(), ref.astype(np.float32))
     bits = ops.splitmix_bits(seed, start, 100).cpu().numpy().view(np.uint64)
     assert np.array_equal(bits, O.stream_bits(seed, start, 100))
+
+
+def test_stream_k_path_matches_data_parallel():
+    """The opt-in stream-K schedule (DICE_GEMM_STREAMK=1, read once per process)
+    must give the same GEMM results; run in a subprocess with the variable set."""
+    import subprocess, sys, os
+    code = r"""
+import torch, numpy as np, sys
+sys.path.insert(0, '.')
+from paper_2411_16786_b200 import ops
+g = torch.Generator(device='cuda').manual_seed(0)
+for (M, N, K, epi) in [(8192, 1152, 1152, 3), (2048, 1152, 4608, 0), (4096, 1152, 2304, 4)]:
+    A = torch.randn(M, K, device='cuda', generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device='cuda', generator=g) / K ** 0.5).to(torch.bfloat16)
+    res = torch.randn(M, N, device='cuda', generator=g)
+    add = torch.randn(M, N, device='cuda', generator=g)
+    o32 = torch.empty(M, N, device='cuda')
+    kw = dict(out_f32=o32)
+    acc = A.float() @ B.float().T
+    if epi == 3:
+        ref = 0.5 * acc * (1 + torch.erf(acc / 2 ** 0.5)) + res; kw['residual'] = res
+    elif epi == 4:
+        ref = res + (acc + add); kw.update(residual=res, addend=add)
+    else:
+        ref = acc; epi = 2
+    ops.gemm(epi, A, B, **kw)
+    torch.cuda.synchronize()
+    err = ((o32 - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-4, (M, N, K, err)
+print('ok')
+"""
+    env = dict(os.environ, DICE_GEMM_STREAMK="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -264,3 +264,22 @@ def test_config1_latents_and_staleness_quality():
         ref = meta[name]["mse_vs_sync"]
         print(f"{name}: GPU latent MSE vs GPU sync {mse:.3e}; reference {ref:.3e}")
         assert 0.25 * ref < mse < 4 * ref
+
+
+def test_side_stream_overlap_is_bit_identical():
+    """Interweaved with the pending expert FFN on a side stream reproduces the
+    single-stream run exactly (only the enqueue order across streams changes)."""
+    cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=128,
+                        expert_dim=256, num_tokens=64, batch=4, num_steps=8, step_size=1e-3)
+    model = D.init_model(cfg, seed=11)
+    x0 = D.sample_x0(cfg, 11)
+    pol = D.dice_policy(refresh_interval=2, warmup=2, period=3)
+    outs = []
+    for overlap in (False, True):
+        r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, pol, D.ClusterConfig(num_devices=2),
+                           11, overlap=overlap)
+        r.capture()
+        r.launch()
+        res = r.finish()
+        outs.append((res.final.values.cpu().numpy(), res.active_pairs, res.dispatch_bytes))
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1:] == outs[1][1:]

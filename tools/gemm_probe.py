@@ -53,3 +53,5 @@ if __name__ == "__main__":
     bench(16384, 4608, 1152, 0, label="expert GEMM1 no-GELU")
     bench(16384, 1152, 4608, 0, label="expert GEMM2 (dense eq.)")
     bench(8192, 8192, 8192, 0, label="square 8192")
+    bench(9472, 1152, 9216, 4, label="GEMM2 consume, full waves")
+    bench(18944, 1152, 4608, 0, label="GEMM2 expert, full waves")
