@@ -390,3 +390,43 @@ def denoise_update(x: ActivationBlock, y, eta: float, step: int) -> ActivationBl
     yv = torch.nn.functional.pad(torch.as_tensor(y, device=xv.device).to(torch.float32), (0, hp - h)).contiguous()
     ops.denoise(xv, None, yv, eta)
     return ActivationBlock(values=xv[:, :h], generated_step=step + 1)
+
+
+@dataclass
+class StepSimilarity:
+    """model.py:308-313."""
+    per_layer_cosine: object
+    per_layer_agreement: object
+    mean_cosine: float
+    mean_agreement: float
+
+
+def _cosine(a: torch.Tensor, b: torch.Tensor) -> float:
+    a = a.reshape(-1).double()
+    b = b.reshape(-1).double()
+    na, nb = torch.linalg.vector_norm(a).item(), torch.linalg.vector_norm(b).item()
+    if na == 0.0 or nb == 0.0:
+        return 1.0 if na == nb else 0.0
+    return float(torch.dot(a, b).item() / (na * nb))
+
+
+def step_similarity(inputs: list, routes: list) -> StepSimilarity:
+    """Adjacent-step cosine of each layer's MoE input and top-1 routing
+    agreement (model.py:323-346). inputs[s][l]: [rows, h]; routes[s][l]: RouteDecision."""
+    steps = len(inputs)
+    if steps < 2:
+        raise ContractError("step_similarity needs at least two recorded steps")
+    layers = len(inputs[0])
+    cos = np.zeros(layers)
+    agree = np.zeros(layers)
+    for layer in range(layers):
+        c_vals, a_vals = [], []
+        for s in range(steps - 1):
+            c_vals.append(_cosine(torch.as_tensor(inputs[s][layer]), torch.as_tensor(inputs[s + 1][layer])))
+            t0 = torch.as_tensor(routes[s][layer].expert_ids)[:, 0]
+            t1 = torch.as_tensor(routes[s + 1][layer].expert_ids)[:, 0].to(t0.device)
+            a_vals.append(float((t0 == t1).double().mean().item()))
+        cos[layer] = np.mean(c_vals)
+        agree[layer] = np.mean(a_vals)
+    return StepSimilarity(per_layer_cosine=cos, per_layer_agreement=agree,
+                          mean_cosine=float(np.mean(cos)), mean_agreement=float(np.mean(agree)))

@@ -95,6 +95,29 @@ class RunResult:
         return dict(sorted(counts.items()))
 
 
+class GpuTimeline:
+    """Measured stage timeline in the reference's export schema
+    (cluster.py:132-138, 210-216): events {device, kind, start, end, label},
+    seconds from the start of the run, from CUDA events on the stream."""
+
+    def __init__(self, events, device=0):
+        self.events = events
+        self.device = device
+
+    def export(self) -> list:
+        return [dict(device=self.device, kind=k, start=a, end=b, label=l) for k, a, b, l in self.events]
+
+    def to_json(self) -> str:
+        import json
+        return json.dumps({"schema_version": 1, "events": self.export()}, separators=(",", ":"))
+
+    def makespan(self) -> float:
+        return max((b for _, _, b, _ in self.events), default=0.0)
+
+    def get(self, key, default=None):
+        return {"makespan_seconds": self.makespan()}.get(key, default)
+
+
 class _Payload:
     """Device buffers of one dispatch (DispatchPayload, schedules.py:48-57)."""
 
@@ -118,7 +141,7 @@ class DeviceRunner:
     def __init__(self, model: ToyModel, x0: ActivationBlock, strategy: Strategy,
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *,
                  record_inputs: bool = False, record_routes: bool = False,
-                 time_experts: bool = False, overlap: bool = False):
+                 time_experts: bool = False, overlap: bool = False, timeline: bool = False):
         cfg = model.config
         if not isinstance(strategy, Strategy):
             raise ContractError(f"strategy must be a Strategy, got {strategy!r}")
@@ -136,6 +159,7 @@ class DeviceRunner:
         self.strategy, self.policy, self.cluster, self.seed = strategy, policy, cluster, seed
         self.record_inputs, self.record_routes = record_inputs, record_routes
         self.time_experts = time_experts
+        self.want_timeline = timeline
         dev = model.device
         self.dev = dev
         n, k, E, S = cfg.total_rows, cfg.top_k, cfg.num_experts, cfg.num_shared
@@ -177,8 +201,9 @@ class DeviceRunner:
         # interweaved: the pending dispatch's expert FFN + cache merge run on a side
         # stream, concurrently with the next stage's shared FFN / consume on the
         # main stream (the intra-GPU analogue of the interweaved overlap window)
+        self._marks, self._mark_pool = [], []
         self.side = None
-        if overlap and strategy is Strategy.INTERWEAVED and str(dev).startswith("cuda"):
+        if overlap and strategy is Strategy.INTERWEAVED and str(dev).startswith("cuda") and not timeline:
             self.side = torch.cuda.Stream(device=dev)
 
     # ------------------------------------------------------------ helpers
@@ -211,6 +236,18 @@ class DeviceRunner:
         self.combine_log = []
         self.step_inputs, self.step_routes = [], []
         self._expert_events = []  # (start, end, generated step, layer) of each expert-FFN launch
+        self._marks = []
+
+    def _mark(self, label):
+        """Stage boundary for the measured timeline (graph-safe CUDA event)."""
+        if not self.want_timeline:
+            return
+        i = len(self._marks)
+        if i >= len(self._mark_pool):
+            self._mark_pool.append(ops.DeviceEvent())
+        ev = self._mark_pool[i]
+        ev.record()
+        self._marks.append((label, ev))
 
     def _track(self, kind, layer):
         self.occupied.add((kind, layer))
@@ -285,6 +322,7 @@ class DeviceRunner:
             self.side_tail = None
 
     def _process_body(self, p: _Payload):
+        self._mark(f"expert s{p.gen} L{p.layer}")
         lw = self.model.layers[p.layer]
         if self.time_experts:
             i = len(self._expert_events)
@@ -316,6 +354,7 @@ class DeviceRunner:
         (_consume, schedules.py:308-317; combine_outputs, model.py:279-298)."""
         lw = self.model.layers[layer]
         slot = self._slot(layer)
+        self._mark(f"shared+consume s{step} L{layer}")
         if self.S > 0:
             ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
             ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
@@ -331,8 +370,10 @@ class DeviceRunner:
         for layer in range(cfg.num_layers):
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
+            self._mark(f"local s{step} L{layer}")
             ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32, out_bf16=self.u16,
                      residual=hin32)
+            self._mark(f"gate+dispatch s{step} L{layer}")
             sync = self._stage_is_sync(step, layer)
             if sync and self.strategy is Strategy.INTERWEAVED:
                 self._flush_pending()
@@ -377,7 +418,9 @@ class DeviceRunner:
                     self._track("c", prev.layer)
                 self._consume(layer, step, self.slot_gen[layer])
         self._flush_pending(side=self.strategy is Strategy.INTERWEAVED)
+        self._mark(f"denoise s{step}")
         ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
+        self._mark(f"end s{step}")
         if self.record_inputs:
             self.step_inputs.append(inputs_here)
         if self.record_routes:
@@ -451,7 +494,15 @@ class DeviceRunner:
         final = ActivationBlock(values=self.x32[:, :cfg.hidden_dim].clone(),
                                 generated_step=cfg.num_steps)
         timeline = None
-        if gpu_seconds is not None or self._expert_events:
+        if self._marks:
+            t0 = self._marks[0][1]
+            times = [t0.elapsed_ms(ev) * 1e-3 for _, ev in self._marks]
+            events = [("compute", times[i], times[i + 1], self._marks[i][0])
+                      for i in range(len(self._marks) - 1)
+                      if not self._marks[i][0].startswith("end ")]
+            timeline = GpuTimeline(events, device=torch.cuda.current_device())
+            gpu_seconds = timeline.makespan() if gpu_seconds is None else gpu_seconds
+        elif self._expert_events:
             timeline = {"expert_ffn_ms": [a.elapsed_ms(b) for a, b, _, _ in self._expert_events]}
         return RunResult(
             final=final, timeline=timeline, staleness_records=self.records,

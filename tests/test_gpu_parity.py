@@ -283,3 +283,36 @@ def test_side_stream_overlap_is_bit_identical():
         res = r.finish()
         outs.append((res.final.values.cpu().numpy(), res.active_pairs, res.dispatch_bytes))
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1:] == outs[1][1:]
+
+
+def test_measured_timeline_export():
+    """f2: stage timeline from CUDA events in the reference export schema
+    (cluster.py:210-216): ordered, non-overlapping, covering every stage."""
+    cfg = D.ModelConfig(num_layers=3, num_experts=4, num_shared=1, top_k=2, hidden_dim=64,
+                        expert_dim=128, num_tokens=32, batch=2, num_steps=4, step_size=1e-3)
+    model = D.init_model(cfg, seed=2)
+    r = D.DeviceRunner(model, D.sample_x0(cfg, 2), D.Strategy.INTERWEAVED, D.NEUTRAL,
+                       D.ClusterConfig(num_devices=1), 2, timeline=True)
+    res = r.run()
+    doc = json.loads(res.timeline.to_json())
+    assert doc["schema_version"] == 1
+    ev = doc["events"]
+    assert {e["kind"] for e in ev} == {"compute"}
+    labels = [e["label"].split(" ")[0] for e in ev]
+    for kind in ("local", "gate+dispatch", "expert", "shared+consume", "denoise"):
+        assert kind in labels
+    for a, b in zip(ev, ev[1:]):
+        assert a["start"] <= a["end"] <= b["start"] + 1e-9
+    assert res.makespan_seconds > 0
+
+
+def test_step_similarity_precondition_xl_toy():
+    """f3 / acceptance criterion 9 (test_acceptance.py:282-293): the synchronous
+    xl-toy trajectory has adjacent-step MoE-input cosine >= 0.9 and top-1
+    routing agreement >= 0.8, computed from the GPU's own recorded inputs."""
+    cfg = D.preset("xl-toy")
+    model = D.init_model(cfg, seed=0)
+    res = D.run_sampling(model, D.sample_x0(cfg, 0), D.Strategy.SYNCHRONOUS, D.NEUTRAL,
+                         D.ClusterConfig(num_devices=4), 0, record_inputs=True, record_routes=True)
+    sim = D.step_similarity(res.step_inputs, res.step_routes)
+    assert sim.mean_cosine >= 0.9 and sim.mean_agreement >= 0.8, sim
