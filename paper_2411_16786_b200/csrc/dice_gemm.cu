@@ -45,9 +45,11 @@ struct GemmCfg {
       kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 1024 /*barriers*/;
 };
 
+constexpr int kMaxStages = 12;
+
 struct __align__(8) GemmShared {
-  uint64_t full[8];
-  uint64_t empty[8];
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
@@ -390,23 +392,51 @@ __global__ void __launch_bounds__(256) stream_k_fixup_kernel(const GemmArgs a, c
 // stages its own 128 rows of A and half (BN/2 rows) of B, so per-CTA operand
 // traffic per MMA FLOP is 2/3 of the single-CTA 128 x BN tile; the even CTA
 // issues the pair MMAs and both CTAs drain their 128 TMEM lanes.
-template <int BN>
+// NSUB > 1: a 256 x (NSUB*BN) tile of NSUB accumulators sharing each staged A
+// block (per-SM operand bytes per MMA cycle fall from 8192/BN + 32 to
+// 8192/(NSUB*BN) + 32), single-buffered in TMEM.
+template <int BN, bool DIRECT, int NSUB>
 struct PairCfg {
+  static constexpr int kTN = NSUB * BN;
+  static constexpr int kAccBufs = NSUB == 1 ? 2 : 1;
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = (BN / 2) * BK * 2;
+  static constexpr int kSubBBytes = (BN / 2) * BK * 2;
+  static constexpr int kBBytes = NSUB * kSubBBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;
+  // bf16-only epilogues store straight from registers (64 contiguous bytes of
+  // one row per lane, whole sectors), so their smem goes to the operand ring
+  static constexpr int kEpiBytes = DIRECT ? 0 : kEpiWarps * 32 * 32 * 4;
   static constexpr int kBudget = 232448 - kEpiBytes - 2048;
-  static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
-  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kStages = kBudget / kStageBytes > kMaxStages ? kMaxStages : kBudget / kStageBytes;
+  static constexpr int kTmemCols = kAccBufs * kTN <= 256 ? 256 : 512;
+  static_assert(kAccBufs * kTN <= 512, "TMEM holds 512 fp32 columns");
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 2048;
 };
 
-template <int BN, int EPI>
+// Direct bf16 epilogue: this lane owns one row and 32 consecutive columns.
+template <int EPI>
+__device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_t (&r)[32],
+                                                int64_t row, int col0) {
+  uint32_t w[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    float2 v = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+    if constexpr (EPI == EPI_GELU_BF16) v = gelu_erf2(v);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v.x, v.y);
+    w[j] = *reinterpret_cast<uint32_t*>(&b);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(a.out_bf16 + row * a.ld_bf16 + col0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+}
+
+template <int BN, int EPI, bool DIRECT, int NSUB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const GemmArgs args) {
-  using C = PairCfg<BN>;
+  using C = PairCfg<BN, DIRECT, NSUB>;
+  constexpr int TN = C::kTN;
+  const int kStages = args.stages;   // <= C::kStages (host-clamped)
   constexpr int kPairM = 2 * BM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -420,7 +450,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const uint32_t rank = cluster_ctarank();
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) { mbar_init(&sh->full[s], 2); mbar_init(&sh->empty[s], 1); }
+    for (int s = 0; s < kStages; ++s) { mbar_init(&sh->full[s], 2); mbar_init(&sh->empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 2 * kEpiWarps); }
     fence_barrier_init();
     if (args.group_tile_offsets != nullptr) {
@@ -461,13 +491,16 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int m_tile = tile / n_blocks;
         const int g = find_group(sh->group_off, groups, m_tile);
         const int a_row = m_tile * kPairM + rank * BM;
-        const int b_row = g * args.N + n_blk * BN + rank * (BN / 2);
+        const int b_row = g * args.N + n_blk * TN + rank * (BN / 2);
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0), C::kStageBytes);
           tma_load_2d_pair(smA + stage * C::kABytes, &tmA, &sh->full[stage], kb * BK, a_row);
-          tma_load_2d_pair(smB + stage * C::kBBytes, &tmB, &sh->full[stage], kb * BK, b_row);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+#pragma unroll
+          for (int sub = 0; sub < NSUB; ++sub)
+            tma_load_2d_pair(smB + stage * C::kBBytes + sub * C::kSubBBytes, &tmB, &sh->full[stage],
+                             kb * BK, b_row + sub * BN);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -479,11 +512,11 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int local = 0; local < n_items; ++local) {
         int tile, k0, k1, slot;
         plan.item(pair, local, tile, k0, k1, slot);
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
+        const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
         mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * TN;
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->full[stage], phase);
           tc_fence_after();
@@ -491,12 +524,15 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint32_t b_base = smem_u32(smB + stage * C::kBBytes);
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
-            umma_bf16_pair(d_tmem, umma_desc_sw128(a_base + k * UMMA_K * 2),
-                           umma_desc_sw128(b_base + k * UMMA_K * 2), idesc,
-                           (kb != k0 || k != 0) ? 1u : 0u);
+            const uint64_t ad = umma_desc_sw128(a_base + k * UMMA_K * 2);
+#pragma unroll
+            for (int sub = 0; sub < NSUB; ++sub)
+              umma_bf16_pair(d_tmem + sub * BN, ad,
+                             umma_desc_sw128(b_base + sub * C::kSubBBytes + k * UMMA_K * 2), idesc,
+                             (kb != k0 || k != 0) ? 1u : 0u);
           }
           umma_commit_pair(&sh->empty[stage]);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         umma_commit_pair(&sh->tfull[acc]);
       }
@@ -513,20 +549,25 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       plan.item(pair, local, tile, k0, k1, slot);
       const int n_blk = tile % n_blocks;
       const int m_tile = tile / n_blocks;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
+      const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
       mbar_wait(&sh->tfull[acc], acc_phase);
       tc_fence_after();
       const int row0 = m_tile * kPairM + rank * BM + sub * 32;
       float* ws_tile = slot >= 0 ? args.sk_workspace + (int64_t)slot * kPairM * BN : nullptr;
 #pragma unroll 1
-      for (int ci = grp; ci < BN / 32; ci += kEpiGroups) {
+      for (int ci = grp; ci < TN / 32; ci += kEpiGroups) {
         const int col_in_tile = ci * 32;
-        const int col0 = n_blk * BN + col_in_tile;
+        const int col0 = n_blk * TN + col_in_tile;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN + col_in_tile, r);
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * TN + col_in_tile, r);
         tmem_ld_wait();
         if (col0 >= args.N) continue;  // warp-uniform
+        if constexpr (DIRECT) {   // (the host never enables stream-K for DIRECT)
+          const int64_t row = row0 + lane;
+          if (row < row_limit) epilogue_direct<EPI>(args, r, row, col0);
+          continue;
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           *reinterpret_cast<float4*>(stage + lane * 32 + ((q ^ (lane & 7)) << 2)) =
@@ -673,13 +714,18 @@ float* stream_k_workspace(cudaStream_t stream) {
   return p;
 }
 
-template <int BN, int EPI>
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e != nullptr && e[0] != 0) ? atoi(e) : dflt;
+}
+
+template <int BN, int EPI, bool DIRECT, int NSUB = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream) {
-  using C = PairCfg<BN>;
+  using C = PairCfg<BN, DIRECT, NSUB>;
   static bool attr_done = false;
   if (!attr_done) {
-    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kSmemBytes) != cudaSuccess)
       return DICE_ERR_CUDA;
     attr_done = true;
@@ -688,22 +734,44 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   grid &= ~1;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
-  aa.sk_workspace = stream_k_workspace(stream);
-  gemm_bf16_pair<BN, EPI><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, aa);
+  aa.sk_workspace = (DIRECT || NSUB > 1) ? nullptr : stream_k_workspace(stream);
+  // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
+  static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
+  aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
+  gemm_bf16_pair<BN, EPI, DIRECT, NSUB><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, aa);
   if (aa.sk_workspace != nullptr)
     stream_k_fixup_kernel<EPI><<<num_sms() * 2, 256, 0, stream>>>(aa, aa.sk_workspace, BN, grid / 2);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 
+// 256 x 384 tiles (two 192-column accumulators) for N % 384 == 0
+int dispatch_wide(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                  int max_tiles, cudaStream_t s) {
+  switch (epi) {
+    case EPI_STORE_BF16: return launch_pair<192, EPI_STORE_BF16, true, 2>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_BF16: return launch_pair<192, EPI_GELU_BF16, true, 2>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_F32: return launch_pair<192, EPI_STORE_F32, false, 2>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID: return launch_pair<192, EPI_GELU_RESID, false, 2>(ta, tb, a, max_tiles, s);
+    case EPI_CONSUME: return launch_pair<192, EPI_CONSUME, false, 2>(ta, tb, a, max_tiles, s);
+    default: return DICE_ERR_CONTRACT;
+  }
+}
+
 template <int BN>
 int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                   int max_tiles, cudaStream_t s) {
+  // bf16-only epilogues default to direct register stores (DICE_GEMM_EPI_DIRECT=0: staged)
+  static const bool direct = env_int("DICE_GEMM_EPI_DIRECT", 1) != 0;
   switch (epi) {
-    case EPI_STORE_BF16: return launch_pair<BN, EPI_STORE_BF16>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_BF16: return launch_pair<BN, EPI_GELU_BF16>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID>(ta, tb, a, max_tiles, s);
-    case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_BF16:
+      return direct ? launch_pair<BN, EPI_STORE_BF16, true>(ta, tb, a, max_tiles, s)
+                    : launch_pair<BN, EPI_STORE_BF16, false>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_BF16:
+      return direct ? launch_pair<BN, EPI_GELU_BF16, true>(ta, tb, a, max_tiles, s)
+                    : launch_pair<BN, EPI_GELU_BF16, false>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false>(ta, tb, a, max_tiles, s);
+    case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false>(ta, tb, a, max_tiles, s);
     default: return DICE_ERR_CONTRACT;
   }
 }
@@ -736,12 +804,35 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
   if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
   int bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
+  if (const char* e = getenv("DICE_GEMM_BN")) {
+    // experiment hook: force the tile width (128 / 192 / 256)
+    const int f = atoi(e);
+    if (f == 128 || f == 192 || f == 256) bn = f;
+  }
   if (const char* e = getenv("DICE_GEMM_BN_NARROW")) {
     // experiment hook: use 128-wide tiles for N not divisible by 256 (wave quantisation)
     if (e[0] == '1' && p.N % 256 != 0) bn = 128;
   }
   // grouped GEMMs always use 256-row tiles (the permute pads experts to 256 rows)
   const bool pair = p.group_tile_offsets != nullptr || use_pair_kernel();
+  // N = 1152-class shapes: 256 x 384 tiles (DICE_GEMM_WIDE=0 disables)
+  // (measured, XL shapes: 16384x1152x4608 1148 -> 1348 TF/s). The single TMEM
+  // buffer exposes each tile's epilogue, so only for long-K bf16 epilogues, and
+  // only when the wave count does not lose what the wider tile gains.
+  static const int wide_mode = env_int("DICE_GEMM_WIDE", 1);
+  bool wide = false;
+  if (pair && bn == 192 && p.N % 384 == 0 && wide_mode != 0) {
+    const int64_t m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + 255) / 256;
+    const int pairs = num_sms() / 2;
+    auto wave_eff = [&](int64_t tiles) {
+      return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs);
+    };
+    const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16;
+    wide = wide_mode == 2 ||
+           (direct_epi && p.K >= 2048 &&
+            1.15 * wave_eff(m_tiles * (p.N / 384)) >= wave_eff(m_tiles * (p.N / 192)));
+  }
+  const int tile_n = wide ? 384 : bn;
   const int tile_m = pair ? 2 * BM : BM;
   CUtensorMap ta, tb;
   int rc = tensor_map(p.A, p.A_rows, p.K, BM, &ta);
@@ -752,13 +843,14 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   a.M_valid = p.M;
   a.N = p.N;
   a.K = p.K;
-  a.num_n_blocks = (p.N + bn - 1) / bn;
+  a.num_n_blocks = (p.N + tile_n - 1) / tile_n;
   a.num_k_blocks = (p.K + BK - 1) / BK;
   a.group_tile_offsets = p.group_tile_offsets;
   a.num_groups = p.num_groups;
   a.num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + tile_m - 1) / tile_m;
   const int max_tiles = a.num_m_tiles * a.num_n_blocks;
   if (max_tiles == 0) return 0;
+  if (wide) return dispatch_wide(p.epi_kind, ta, tb, a, max_tiles, stream);
   if (pair) {
     if (bn == 256) return dispatch_pair<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
     if (bn == 192) return dispatch_pair<192>(p.epi_kind, ta, tb, a, max_tiles, stream);

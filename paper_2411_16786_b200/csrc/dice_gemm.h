@@ -36,6 +36,7 @@ struct GemmArgs {
   const float* addend;
   int64_t ld_add;
   float* sk_workspace;   // stream-K partials (pair kernel); null disables stream-K
+  int stages;            // operand ring depth actually used (pair kernel; set by the host)
 };
 
 struct GemmProblem {

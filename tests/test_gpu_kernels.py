@@ -17,7 +17,8 @@ def gelu(x):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 128, 128), (1000, 192, 1152),
-                                   (64, 64, 64), (513, 1152, 640), (2048, 4608, 1152)])
+                                   (64, 64, 64), (513, 1152, 640), (2048, 4608, 1152),
+                                   (4096, 1152, 4608), (300, 768, 256), (777, 384, 128)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
 def test_dense_gemm_epilogues(M, N, K, epi):
     g = torch.Generator(device=dev).manual_seed(M * 7 + N + K + epi)

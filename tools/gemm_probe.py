@@ -9,6 +9,9 @@ dev = "cuda"
 flush = torch.ones(64 * 2 ** 20, dtype=torch.float32, device=dev)  # 256 MB, read to evict L2
 
 
+QUICK = "--quick" in __import__("sys").argv
+
+
 def bench(M, N, K, epi, reps=20, label=""):
     A = (torch.randn(M, K, device=dev) * 0.5).to(torch.bfloat16)
     B = (torch.randn(N, K, device=dev) * 0.05).to(torch.bfloat16)
@@ -29,6 +32,10 @@ def bench(M, N, K, epi, reps=20, label=""):
     ts.sort()
     t = ts[len(ts) // 2] * 1e-3
     tf = 2.0 * M * N * K / t / 1e12
+    if QUICK:
+        print(f"{label:28s} M={M:6d} N={N:5d} K={K:5d} epi={epi}: {t*1e6:8.1f} us {tf:7.1f} TF/s",
+              flush=True)
+        return
     # torch reference time
     for _ in range(3):
         A @ B.T
@@ -52,6 +59,14 @@ if __name__ == "__main__":
     bench(16384, 4608, 1152, 1, label="expert GEMM1 (dense eq.)")
     bench(16384, 4608, 1152, 0, label="expert GEMM1 no-GELU")
     bench(16384, 1152, 4608, 0, label="expert GEMM2 (dense eq.)")
+    if "--bn" in __import__("sys").argv:
+        bench(16384, 4608, 4608, 0, label="16k x 4608 x 4608")
+        bench(16384, 4608, 1152, 0, label="16k x 4608 x 1152")
+        bench(16384, 1152, 4608, 0, label="16k x 1152 x 4608")
+        bench(16384, 2304, 4608, 0, label="16k x 2304 x 4608")
+        raise SystemExit
+    if QUICK:
+        raise SystemExit
     bench(8192, 8192, 8192, 0, label="square 8192")
     bench(9472, 1152, 9216, 4, label="GEMM2 consume, full waves")
     bench(18944, 1152, 4608, 0, label="GEMM2 expert, full waves")
