@@ -87,6 +87,40 @@ int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int
                    int32_t* ids, float* gates, float* scores, int32_t* status, int step,
                    int layer, void* stream);
 
+/* local_block with the gate fused into its GEMM epilogue (model.py:244-252 then
+ * model.py:209-223): the GELU_RESID GEMM (u = gelu(A B^T) + residual -> out_f32,
+ * out_bf16) also dots each finished u row with w_gate (f32 [N, E], row c =
+ * hidden column c, E = 8 or 16) and stores partial logits f32 [P, M, E],
+ * P = dice_gate_parts(M, N, K, E), one slot per (column tile, epilogue warp
+ * group). The router never re-reads u from HBM. */
+int dice_gemm_local_gate(const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
+                         float* out_f32, int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16,
+                         const float* residual, int64_t ld_res, const float* w_gate, int E,
+                         float* parts, void* stream);
+int dice_gate_parts(int64_t M, int N, int K, int E);
+
+/* Router finish over those partials: logits = sum of the P slots in slot order,
+ * softmax, stable top-k, renormalised gates (same outputs and non-finite rule as
+ * dice_gate_topk). decide != 0 also runs the conditional-communication decision
+ * (dice_cond_decide's arguments and semantics) on the fresh ids in the same
+ * kernel. */
+int dice_gate_finish(const float* parts, int P, int64_t n, int E, int k, int32_t* ids,
+                     float* gates, float* scores, int32_t* status, int step, int layer,
+                     int decide, int force, int refresh_interval, int strategy, int strict,
+                     uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
+                     uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
+                     uint8_t* write, void* stream);
+
+/* dice_gate_topk followed, in the same kernel, by the conditional-communication
+ * decision of each token on its fresh ids (dice_cond_decide's arguments and
+ * semantics; the engine's gate + TokenCache.decide in one launch). */
+int dice_gate_topk_decide(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                          int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                          int layer, int force, int refresh_interval, int strategy, int strict,
+                          uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
+                          uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
+                          uint8_t* write, void* stream);
+
 /* Conditional-communication decision for one layer (TokenCache.decide,
  * policies.py:159-186 with reduced_slots 118-139, random_keep_slots 107-115).
  * State (this layer): last_refresh int32 [n] (init -1e9), primed uint8 [n],

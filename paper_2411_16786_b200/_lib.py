@@ -32,6 +32,14 @@ SIGNATURES = {
                                    P, c_int64, P]),
     "dice_splitmix_bits": (c_int, [c_uint64, c_uint64, c_int64, P, P]),
     "dice_gate_topk": (c_int, [P, P, c_int64, c_int, c_int, c_int, P, P, P, P, c_int, c_int, P]),
+    "dice_gate_topk_decide": (c_int, [P, P, c_int64, c_int, c_int, c_int, P, P, P, P, c_int, c_int,
+                                      c_int, c_int, c_int, c_int, c_uint64, P, P, P, P, P, P, P]),
+    "dice_gemm_local_gate": (c_int, [P, c_int64, P, c_int, c_int, P, c_int64, P, c_int64, P,
+                                     c_int64, P, c_int, P, P]),
+    "dice_gate_parts": (c_int, [c_int64, c_int, c_int, c_int]),
+    "dice_gate_finish": (c_int, [P, c_int, c_int64, c_int, c_int, P, P, P, P, c_int, c_int,
+                                 c_int, c_int, c_int, c_int, c_int, c_uint64, P, P, P, P, P, P,
+                                 P]),
     "dice_cond_decide": (c_int, [P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int, c_uint64,
                                  P, P, P, P, P, P, P]),
     "dice_route_permute": (c_int, [P, P, c_int64, c_int, c_int, P, c_int, P, c_int64, P, P, P,

@@ -67,8 +67,8 @@ __device__ __forceinline__ int find_group(const int* off, int groups, int m_tile
 // one output row, a warp covers 4 rows per pass, so residual loads and f32 /
 // bf16 stores are coalesced 128-byte / 64-byte row segments. All 8 passes'
 // global loads are issued before any math so their latencies overlap.
-template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, const float* stage, int lane,
+template <int EPI, bool WRITE_BACK = false>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, float* stage, int lane,
                                                int row0, int row_limit, int col0) {
   const int q = lane & 7;
   const int col = col0 + 4 * q;
@@ -106,6 +106,11 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, const float* s
       if constexpr (EPI == EPI_CONSUME) {
         x.x = r[it].x + (x.x + ad[it].x); x.y = r[it].y + (x.y + ad[it].y);
         x.z = r[it].z + (x.z + ad[it].z); x.w = r[it].w + (x.w + ad[it].w);
+      }
+      if constexpr (WRITE_BACK) {
+        // the finished values replace the accumulators in the transpose tile
+        const int rr = (half * 4 + it) * 4 + (lane >> 3);
+        *reinterpret_cast<float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2)) = x;
       }
       if (row < row_limit) {
         if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
@@ -254,6 +259,31 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+// Router logits of the finished u rows (gate, model.py:209-223, fused into the
+// local_block GEMM): the lane owning row `lane` of the transpose tile dots its
+// 32 finished values with W_gate[col0 .. col0+32, :] (warp-uniform broadcast
+// loads) into GE partial logits, accumulated over this warp's chunks of the tile.
+template <int GE>
+__device__ __forceinline__ void gate_accumulate(const GemmArgs& a, const float* stage, int lane,
+                                                int col0, float2 (&g)[GE / 2]) {
+  const float4* w = reinterpret_cast<const float4*>(a.gate_w + (int64_t)col0 * GE);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 xv = *reinterpret_cast<const float4*>(stage + lane * 32 + ((q ^ (lane & 7)) << 2));
+    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 xx = make_float2(xs[j], xs[j]);
+#pragma unroll
+      for (int e4 = 0; e4 < GE / 4; ++e4) {
+        const float4 wv = __ldg(w + (4 * q + j) * (GE / 4) + e4);
+        g[2 * e4] = __ffma2_rn(xx, make_float2(wv.x, wv.y), g[2 * e4]);
+        g[2 * e4 + 1] = __ffma2_rn(xx, make_float2(wv.z, wv.w), g[2 * e4 + 1]);
+      }
+    }
   }
 }
 
@@ -555,6 +585,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc_fence_after();
       const int row0 = m_tile * kPairM + rank * BM + sub * 32;
       float* ws_tile = slot >= 0 ? args.sk_workspace + (int64_t)slot * kPairM * BN : nullptr;
+      constexpr int GE = EpiTraits<EPI>::gate_e;
+      float2 gacc[GE > 0 ? GE / 2 : 1];
+#pragma unroll
+      for (int e = 0; e < (GE > 0 ? GE / 2 : 1); ++e) gacc[e] = make_float2(0.f, 0.f);
 #pragma unroll 1
       for (int ci = grp; ci < TN / 32; ci += kEpiGroups) {
         const int col_in_tile = ci * 32;
@@ -574,11 +608,26 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         __syncwarp();
-        if (ws_tile != nullptr)
+        if constexpr (GE > 0) {     // (the host never enables stream-K for GATE)
+          epilogue_chunk<EpiTraits<EPI>::base, true>(args, stage, lane, row0, row_limit, col0);
+          __syncwarp();
+          gate_accumulate<GE>(args, stage, lane, col0, gacc);
+        } else if (ws_tile != nullptr) {
           epilogue_partial(stage, lane, ws_tile, BN, rank * BM + sub * 32, col_in_tile);
-        else
+        } else {
           epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
+        }
         __syncwarp();
+      }
+      if constexpr (GE > 0) {
+        const int64_t row = row0 + lane;
+        if (row < row_limit) {
+          float4* dst = reinterpret_cast<float4*>(
+              args.gate_part + ((int64_t)(n_blk * kEpiGroups + grp) * args.M_valid + row) * GE);
+#pragma unroll
+          for (int e4 = 0; e4 < GE / 4; ++e4)
+            dst[e4] = make_float4(gacc[2 * e4].x, gacc[2 * e4].y, gacc[2 * e4 + 1].x, gacc[2 * e4 + 1].y);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -734,7 +783,8 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   grid &= ~1;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
-  aa.sk_workspace = (DIRECT || NSUB > 1) ? nullptr : stream_k_workspace(stream);
+  aa.sk_workspace = (DIRECT || NSUB > 1 || EpiTraits<EPI>::gate_e > 0) ? nullptr
+                                                                       : stream_k_workspace(stream);
   // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
   static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
   aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
@@ -772,6 +822,9 @@ int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
     case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false>(ta, tb, a, max_tiles, s);
     case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false>(ta, tb, a, max_tiles, s);
     case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID_GATE8: return launch_pair<BN, EPI_GELU_RESID_GATE8, false>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID_GATE16:
+      return launch_pair<BN, EPI_GELU_RESID_GATE16, false>(ta, tb, a, max_tiles, s);
     default: return DICE_ERR_CONTRACT;
   }
 }
@@ -800,39 +853,61 @@ bool use_pair_kernel() {
   return mode == 1;
 }
 
-int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
-  if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
-  if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
-  int bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
+struct TileChoice {
+  int bn;        // MMA N per accumulator
+  int tile_n;    // output columns per tile (bn, or 384 for the wide tiles)
+  bool pair;     // CTA-pair kernel (256-row tiles)
+  bool wide;
+};
+
+TileChoice choose_tile(const GemmProblem& p) {
+  TileChoice c{};
+  c.bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
   if (const char* e = getenv("DICE_GEMM_BN")) {
     // experiment hook: force the tile width (128 / 192 / 256)
     const int f = atoi(e);
-    if (f == 128 || f == 192 || f == 256) bn = f;
+    if (f == 128 || f == 192 || f == 256) c.bn = f;
   }
   if (const char* e = getenv("DICE_GEMM_BN_NARROW")) {
     // experiment hook: use 128-wide tiles for N not divisible by 256 (wave quantisation)
-    if (e[0] == '1' && p.N % 256 != 0) bn = 128;
+    if (e[0] == '1' && p.N % 256 != 0) c.bn = 128;
   }
-  // grouped GEMMs always use 256-row tiles (the permute pads experts to 256 rows)
-  const bool pair = p.group_tile_offsets != nullptr || use_pair_kernel();
+  const bool gate = p.epi_kind == EPI_GELU_RESID_GATE8 || p.epi_kind == EPI_GELU_RESID_GATE16;
+  // grouped GEMMs always use 256-row tiles (the permute pads experts to 256 rows);
+  // the gate-fused epilogue exists only in the pair kernel
+  c.pair = p.group_tile_offsets != nullptr || gate || use_pair_kernel();
   // N = 1152-class shapes: 256 x 384 tiles (DICE_GEMM_WIDE=0 disables)
   // (measured, XL shapes: 16384x1152x4608 1148 -> 1348 TF/s). The single TMEM
   // buffer exposes each tile's epilogue, so only for long-K bf16 epilogues, and
   // only when the wave count does not lose what the wider tile gains.
   static const int wide_mode = env_int("DICE_GEMM_WIDE", 1);
-  bool wide = false;
-  if (pair && bn == 192 && p.N % 384 == 0 && wide_mode != 0) {
+  c.wide = false;
+  if (c.pair && c.bn == 192 && p.N % 384 == 0 && wide_mode != 0 && !gate) {
     const int64_t m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + 255) / 256;
     const int pairs = num_sms() / 2;
     auto wave_eff = [&](int64_t tiles) {
       return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs);
     };
     const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16;
-    wide = wide_mode == 2 ||
-           (direct_epi && p.K >= 2048 &&
-            1.15 * wave_eff(m_tiles * (p.N / 384)) >= wave_eff(m_tiles * (p.N / 192)));
+    c.wide = wide_mode == 2 ||
+             (direct_epi && p.K >= 2048 &&
+              1.15 * wave_eff(m_tiles * (p.N / 384)) >= wave_eff(m_tiles * (p.N / 192)));
   }
-  const int tile_n = wide ? 384 : bn;
+  c.tile_n = c.wide ? 384 : c.bn;
+  return c;
+}
+
+int gemm_gate_parts(const GemmProblem& p) {
+  const TileChoice c = choose_tile(p);
+  return ((p.N + c.tile_n - 1) / c.tile_n) * kEpiGroups;
+}
+
+int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
+  if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
+  if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
+  const TileChoice tc = choose_tile(p);
+  const int bn = tc.bn, tile_n = tc.tile_n;
+  const bool pair = tc.pair, wide = tc.wide;
   const int tile_m = pair ? 2 * BM : BM;
   CUtensorMap ta, tb;
   int rc = tensor_map(p.A, p.A_rows, p.K, BM, &ta);

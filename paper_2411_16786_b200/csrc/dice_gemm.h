@@ -16,6 +16,26 @@ enum EpiKind : int {
   EPI_STORE_F32 = 2,   // out_f32 = acc (and out_bf16 if set)
   EPI_GELU_RESID = 3,  // v = gelu(acc) + residual -> out_f32, out_bf16   (local_block)
   EPI_CONSUME = 4,     // v = residual + (acc + addend) -> out_f32, out_bf16 (consume)
+  // GELU_RESID whose epilogue also emits partial router logits of the finished
+  // u rows (gate fused into local_block's GEMM, E = 8 / 16 experts)
+  EPI_GELU_RESID_GATE8 = 5,
+  EPI_GELU_RESID_GATE16 = 6,
+};
+
+template <int EPI>
+struct EpiTraits {
+  static constexpr int base = EPI;
+  static constexpr int gate_e = 0;
+};
+template <>
+struct EpiTraits<EPI_GELU_RESID_GATE8> {
+  static constexpr int base = EPI_GELU_RESID;
+  static constexpr int gate_e = 8;
+};
+template <>
+struct EpiTraits<EPI_GELU_RESID_GATE16> {
+  static constexpr int base = EPI_GELU_RESID;
+  static constexpr int gate_e = 16;
 };
 
 struct GemmArgs {
@@ -37,6 +57,8 @@ struct GemmArgs {
   int64_t ld_add;
   float* sk_workspace;   // stream-K partials (pair kernel); null disables stream-K
   int stages;            // operand ring depth actually used (pair kernel; set by the host)
+  const float* gate_w;   // GATE epilogues: W_gate f32 [N, E] (row c = hidden column c)
+  float* gate_part;      // GATE epilogues: partial logits f32 [P, M, E], P = gemm_gate_parts()
 };
 
 struct GemmProblem {
@@ -52,6 +74,8 @@ struct GemmProblem {
 };
 
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream);
+// number of partial-logit slots a GATE epilogue writes for this problem
+int gemm_gate_parts(const GemmProblem& p);
 
 // Count + scatter (+ optional row gather) of (token, slot) pairs grouped by
 // key = ids[p] / key_div, groups padded to row_tile rows (dice_ops.cu).

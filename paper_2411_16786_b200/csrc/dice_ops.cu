@@ -2,6 +2,7 @@
 // points declared in include/dice_b200.h. The dense contractions live in
 // dice_gemm.cu (tcgen05 / TMEM / TMA).
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "dice_gemm.h"
@@ -208,21 +209,87 @@ __device__ __forceinline__ void tr_level(float (&a)[32], int lane, int off) {
   }
 }
 
-template <int E>
-__global__ void __launch_bounds__(512) gate_topk_fast_kernel(
+// ------------------------------------------------------------ cond decide
+// Per token (policies.py:159-186): due = force | !primed | (step - last) >= R;
+// due tokens redraw the reduced-slot subset (policies.py:118-139) and reset the
+// cadence; active = !reduced | due; write = reduced & due; strict adds pairs
+// whose expert moved since the cached refresh.
+struct DecideArgs {
+  int on, step, force, R, strategy, strict;
+  uint64_t key;
+  int32_t* last;
+  uint8_t* primed;
+  uint8_t* reduced;
+  const int32_t* cached_ids;
+  uint8_t* active;
+  uint8_t* write;
+};
+
+// TokenCache.decide for token t (policies.py:159-186): cadence, mask redraw,
+// active / write masks (strict: also refresh reduced pairs whose expert changed)
+__device__ __forceinline__ void decide_token(int64_t t, int k, const int32_t* ids,
+                                             const DecideArgs& d) {
+  const int step = d.step, strategy = d.strategy;
+  int32_t* last = d.last;
+  uint8_t* primed = d.primed;
+  uint8_t* reduced = d.reduced;
+  uint8_t* active = d.active;
+  uint8_t* write = d.write;
+  {
+    if (strategy == DICE_COND_OFF) {
+      for (int s = 0; s < k; ++s) { active[t * k + s] = 1; write[t * k + s] = 0; }
+      return;
+    }
+    const int force = d.force, R = d.R, strict = d.strict;
+    const uint64_t key = d.key;
+    const int32_t* cached_ids = d.cached_ids;
+    const bool due = force || !primed[t] || (step - last[t]) >= R;
+    if (due) {
+      int keep = -1;
+      if (strategy == DICE_COND_RANDOM) keep = (int)(splitmix_at(key, (uint64_t)t + 1) % (uint64_t)k);
+      for (int s = 0; s < k; ++s) {
+        bool red;
+        if (strategy == DICE_COND_LOW_SCORE) red = s >= 1;
+        else if (strategy == DICE_COND_HIGH_SCORE) red = s == 0;
+        else red = s != keep;
+        reduced[t * k + s] = red;
+      }
+      last[t] = step;
+      primed[t] = 1;
+    }
+    for (int s = 0; s < k; ++s) {
+      const bool red = reduced[t * k + s] != 0;
+      bool a = !red || due;
+      bool w = red && due;
+      if (strict && red && !due && ids[t * k + s] != cached_ids[t * k + s]) { a = true; w = true; }
+      active[t * k + s] = a;
+      write[t * k + s] = w;
+    }
+  }
+}
+
+__global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, int k,
+                                   const DecideArgs d) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    decide_token(t, k, ids, d);
+}
+
+// Warp per row pair, no shared-memory prologue: W_gate is read through L1
+// (37 KB per SM, coalesced 512-byte lines per expert), every lane issues all of
+// its 16-byte row loads before any math (u was just written by the local_block
+// GEMM and is L2-resident), and 2 x 16 lanes finish the rows' softmax / top-k.
+// d.on: the token's conditional-communication state is prefetched alongside
+// the row loads and its decision (decide_token's semantics) is taken by the k
+// slot lanes right after the top-k, so the decision adds no memory round trip.
+template <int E, int CH, int MINB>
+__global__ void __launch_bounds__(256, MINB) gate_topk_fast_kernel(
     const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
     int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
-    int32_t* status, int step, int layer) {
+    int32_t* status, int step, int layer, const DecideArgs d) {
   static_assert(E == 8 || E == 16, "fast gate handles E = 8 or 16");
   constexpr int V = 2 * E;
   constexpr int DUP = E == 8 ? 2 : 1;   // lanes holding the same (row, expert)
-  extern __shared__ float sw[];         // [E, hp]
-  {
-    const float4* src = reinterpret_cast<const float4*>(wt);
-    float4* dst = reinterpret_cast<float4*>(sw);
-    for (int i = threadIdx.x; i < E * hp / 4; i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
   const int64_t pairs = (n + 1) / 2;
@@ -230,13 +297,26 @@ __global__ void __launch_bounds__(512) gate_topk_fast_kernel(
        q += (int64_t)gridDim.x * warps) {
     const int64_t t0 = 2 * q;
     const bool has1 = t0 + 1 < n;
+    const int row = lane >> 4;                      // 0 or 1
+    const int64_t t = t0 + row;
+    const bool row_ok = row == 0 || has1;
+    const int slot = lane & 15;
+    // decision state prefetch (independent of the gate)
+    int32_t d_last = 0, d_cid = -1;
+    uint8_t d_primed = 1, d_red = 0;
+    const bool d_lane = d.on && d.strategy != DICE_COND_OFF && row_ok && slot < k;
+    if (d_lane) {
+      d_last = d.last[t];
+      d_primed = d.primed[t];
+      d_red = d.reduced[t * k + slot];
+      if (d.strict) d_cid = d.cached_ids[t * k + slot];
+    }
     const float* r0 = u + t0 * hp;
     const float* r1 = u + (has1 ? t0 + 1 : t0) * hp;
     float a[32];
     float2 acc[E];   // (row 0, row 1) partial logits per expert, packed FFMA2
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
-    constexpr int CH = 4;
     for (int base = 0; base < hp; base += 128 * CH) {
       float4 xs[CH], ys[CH];
 #pragma unroll
@@ -259,7 +339,7 @@ __global__ void __launch_bounds__(512) gate_topk_fast_kernel(
         const float2 p2 = make_float2(x.z, y.z), p3 = make_float2(x.w, y.w);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const float4 w = *reinterpret_cast<const float4*>(sw + e * hp + c);
+          const float4 w = __ldg(reinterpret_cast<const float4*>(wt + (int64_t)e * hp + c));
           acc[e] = __ffma2_rn(p0, make_float2(w.x, w.x), acc[e]);
           acc[e] = __ffma2_rn(p1, make_float2(w.y, w.y), acc[e]);
           acc[e] = __ffma2_rn(p2, make_float2(w.z, w.z), acc[e]);
@@ -281,10 +361,7 @@ __global__ void __launch_bounds__(512) gate_topk_fast_kernel(
       a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
     }
     const float logit = a[0];
-    const int row = lane >> 4;                      // 0 or 1
     const int e_me = (lane & 15) / DUP;             // expert held by this lane
-    const int64_t t = t0 + row;
-    const bool row_ok = row == 0 || has1;
     // non-finite MoE input shows up as a non-finite logit (model.py:212-213)
     const bool bad = !isfinite(logit) && row_ok;
     if (__any_sync(0xffffffffu, bad) && lane == 0) record_nonfinite(status, step, layer);
@@ -315,53 +392,98 @@ __global__ void __launch_bounds__(512) gate_topk_fast_kernel(
       const int src = __ffs(m) - 1;
       const float sj = __shfl_sync(0xffffffffu, sc, src);
       psum += sj;
-      if ((lane & 15) == j) { my_s = sj; my_e = (src & 15) / DUP; }
+      if (slot == j) { my_s = sj; my_e = (src & 15) / DUP; }
     }
-    if ((lane & 15) < k && row_ok) {
-      ids[t * k + (lane & 15)] = my_e;
-      gates[t * k + (lane & 15)] = my_s / psum;
+    if (slot < k && row_ok) {
+      ids[t * k + slot] = my_e;
+      gates[t * k + slot] = my_s / psum;
+    }
+    if (d.on && slot < k && row_ok) {
+      // TokenCache.decide for (t, slot) (policies.py:159-186; decide_token)
+      if (d.strategy == DICE_COND_OFF) {
+        d.active[t * k + slot] = 1;
+        d.write[t * k + slot] = 0;
+      } else {
+        const bool due = d.force || !d_primed || (step - d_last) >= d.R;
+        bool red = d_red != 0;
+        if (due) {
+          if (d.strategy == DICE_COND_LOW_SCORE) red = slot >= 1;
+          else if (d.strategy == DICE_COND_HIGH_SCORE) red = slot == 0;
+          else red = slot != (int)(splitmix_at(d.key, (uint64_t)t + 1) % (uint64_t)k);
+          d.reduced[t * k + slot] = red;
+          if (slot == 0) { d.last[t] = step; d.primed[t] = 1; }
+        }
+        bool act = !red || due;
+        bool wr = red && due;
+        if (d.strict && red && !due && my_e != d_cid) { act = true; wr = true; }
+        d.active[t * k + slot] = act;
+        d.write[t * k + slot] = wr;
+      }
     }
   }
 }
 
-// ------------------------------------------------------------ cond decide
-// Per token (policies.py:159-186): due = force | !primed | (step - last) >= R;
-// due tokens redraw the reduced-slot subset (policies.py:118-139) and reset the
-// cadence; active = !reduced | due; write = reduced & due; strict adds pairs
-// whose expert moved since the cached refresh.
-__global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, int k, int step,
-                                   int force, int R, int strategy, int strict, uint64_t key,
-                                   int32_t* last, uint8_t* primed, uint8_t* reduced,
-                                   const int32_t* __restrict__ cached_ids, uint8_t* active,
-                                   uint8_t* write) {
+// Gate finish over the partial logits the local_block GEMM epilogue emitted
+// (EPI_GELU_RESID_GATE*): logit = sum of the P slot partials in slot order,
+// softmax over E, stable top-k (ties -> lower id), gates renormalised over the
+// k picked in pick order (model.py:209-223); non-finite logits record
+// (step, layer) (model.py:212-213). One thread per token; optionally the
+// conditional-communication decision for the token follows in the same thread.
+template <int E>
+__global__ void __launch_bounds__(64) gate_parts_kernel(
+    const float* __restrict__ parts, int P, int64_t n, int k, int32_t* __restrict__ ids,
+    float* __restrict__ gates, float* __restrict__ scores, int32_t* status, int step, int layer,
+    const DecideArgs d) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
-    if (strategy == DICE_COND_OFF) {
-      for (int s = 0; s < k; ++s) { active[t * k + s] = 1; write[t * k + s] = 0; }
-      continue;
-    }
-    const bool due = force || !primed[t] || (step - last[t]) >= R;
-    if (due) {
-      int keep = -1;
-      if (strategy == DICE_COND_RANDOM) keep = (int)(splitmix_at(key, (uint64_t)t + 1) % (uint64_t)k);
-      for (int s = 0; s < k; ++s) {
-        bool red;
-        if (strategy == DICE_COND_LOW_SCORE) red = s >= 1;
-        else if (strategy == DICE_COND_HIGH_SCORE) red = s == 0;
-        else red = s != keep;
-        reduced[t * k + s] = red;
+    float l[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) l[e] = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float4* src = reinterpret_cast<const float4*>(parts + ((int64_t)p * n + t) * E);
+#pragma unroll
+      for (int e4 = 0; e4 < E / 4; ++e4) {
+        const float4 v = __ldg(src + e4);
+        l[4 * e4] += v.x; l[4 * e4 + 1] += v.y; l[4 * e4 + 2] += v.z; l[4 * e4 + 3] += v.w;
       }
-      last[t] = step;
-      primed[t] = 1;
     }
-    for (int s = 0; s < k; ++s) {
-      const bool red = reduced[t * k + s] != 0;
-      bool a = !red || due;
-      bool w = red && due;
-      if (strict && red && !due && ids[t * k + s] != cached_ids[t * k + s]) { a = true; w = true; }
-      active[t * k + s] = a;
-      write[t * k + s] = w;
+    bool finite = true;
+    float mx = l[0];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { finite = finite && isfinite(l[e]); mx = fmaxf(mx, l[e]); }
+    if (!finite) record_nonfinite(status, step, layer);
+    float sc[E], sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) { sc[e] = expf(l[e] - mx); sum += sc[e]; }
+#pragma unroll
+    for (int e = 0; e < E; ++e) sc[e] = sc[e] / sum;
+    if (scores != nullptr) {
+      float4* dst = reinterpret_cast<float4*>(scores + t * E);
+#pragma unroll
+      for (int e4 = 0; e4 < E / 4; ++e4)
+        dst[e4] = make_float4(sc[4 * e4], sc[4 * e4 + 1], sc[4 * e4 + 2], sc[4 * e4 + 3]);
     }
+    uint32_t taken = 0;
+    float psum = 0.f, pick_s[E];
+    int pick_e[E];
+    for (int j = 0; j < k; ++j) {
+      int best = -1;
+      float bs = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const bool free_e = ((taken >> e) & 1u) == 0;
+        if (free_e && (best < 0 || sc[e] > bs)) { best = e; bs = sc[e]; }
+      }
+      taken |= 1u << best;
+      pick_e[j] = best;
+      pick_s[j] = bs;
+      psum += bs;
+    }
+    for (int j = 0; j < k; ++j) {
+      ids[t * k + j] = pick_e[j];
+      gates[t * k + j] = pick_s[j] / psum;
+    }
+    if (d.on) decide_token(t, k, ids, d);
   }
 }
 
@@ -741,16 +863,43 @@ int dice_splitmix_bits(uint64_t seed, uint64_t start, int64_t count, uint64_t* o
   return launch_ok();
 }
 
-int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
-                   int32_t* ids, float* gates, float* scores, int32_t* status, int step, int layer,
-                   void* stream) {
+namespace {
+int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                     int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                     int layer, const DecideArgs& d, cudaStream_t s) {
   if (E < 1 || E > 64 || k < 1 || k > E || hp % 64 != 0) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
   const size_t smem = (size_t)E * hp * sizeof(float);
   const int threads = 512;
   int64_t want = ((n + 1) / 2 + 15) / 16;
+  if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
+  if ((E == 8 && k <= 8) || (E == 16 && k <= 16)) {
+    const int64_t gw = ((n + 1) / 2 + 7) / 8;     // 8 warps per block, a row pair each
+    const int grid = (int)(gw < 1 ? 1 : gw);
+    const int ch = hp / 128 <= 9 ? 9 : 4;   // 16-byte loads in flight per lane and row
+    static const int minb = [] {
+      const char* e = getenv("DICE_GATE_MINB");   // experiment hook (1 / 2 / 3)
+      return e != nullptr ? atoi(e) : 2;
+    }();
+#define DICE_GATE_FAST(EE, CC, MB)                                                             \
+    gate_topk_fast_kernel<EE, CC, MB><<<grid, 256, 0, s>>>(u, w_gate_t, n, hp, k, ids, gates,  \
+                                                           scores, status, step, layer, d)
+#define DICE_GATE_FAST_MB(EE, CC)                                                              \
+    {                                                                                          \
+      if (minb == 1) DICE_GATE_FAST(EE, CC, 1);                                                \
+      else if (minb == 3) DICE_GATE_FAST(EE, CC, 3);                                           \
+      else DICE_GATE_FAST(EE, CC, 2);                                                          \
+    }
+    if (E == 8) {
+      if (ch == 9) DICE_GATE_FAST_MB(8, 9) else DICE_GATE_FAST_MB(8, 4)
+    } else {
+      if (ch == 9) DICE_GATE_FAST_MB(16, 9) else DICE_GATE_FAST_MB(16, 4)
+    }
+#undef DICE_GATE_FAST_MB
+#undef DICE_GATE_FAST
+    return launch_ok();
+  }
   const int grid = (int)(want < 2 * 148 ? (want < 1 ? 1 : want) : 2 * 148);
-  cudaStream_t s = (cudaStream_t)stream;
 #define DICE_GATE(EM)                                                                          \
   {                                                                                            \
     static bool attr = false;                                                                  \
@@ -762,26 +911,36 @@ int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int
     gate_topk_kernel<EM><<<grid, threads, smem, s>>>(u, w_gate_t, n, hp, E, k, ids, gates,     \
                                                      scores, status, step, layer);             \
   }
-  if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
-#define DICE_GATE_FAST(EE)                                                                     \
-  {                                                                                            \
-    static bool attr = false;                                                                  \
-    if (!attr) {                                                                               \
-      cudaFuncSetAttribute(gate_topk_fast_kernel<EE>,                                          \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);           \
-      attr = true;                                                                             \
-    }                                                                                          \
-    gate_topk_fast_kernel<EE><<<grid, threads, smem, s>>>(u, w_gate_t, n, hp, k, ids, gates,   \
-                                                          scores, status, step, layer);        \
-  }
-  if (E == 8 && k <= 8) DICE_GATE_FAST(8)
-  else if (E == 16 && k <= 16) DICE_GATE_FAST(16)
-  else if (E <= 8) DICE_GATE(8)
+  if (E <= 8) DICE_GATE(8)
   else if (E <= 16) DICE_GATE(16)
   else DICE_GATE(64)
 #undef DICE_GATE
-#undef DICE_GATE_FAST
+  if (d.on) {
+    cond_decide_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, n, k, d);
+  }
   return launch_ok();
+}
+}  // namespace
+
+int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                   int32_t* ids, float* gates, float* scores, int32_t* status, int step, int layer,
+                   void* stream) {
+  const DecideArgs d{0, 0, 0, 1, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  return gate_topk_launch(u, w_gate_t, n, hp, E, k, ids, gates, scores, status, step, layer, d,
+                          (cudaStream_t)stream);
+}
+
+int dice_gate_topk_decide(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                          int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                          int layer, int force, int refresh_interval, int strategy, int strict,
+                          uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
+                          uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
+                          uint8_t* write, void* stream) {
+  if (refresh_interval < 1 || strategy < 0 || strategy > 3) return DICE_ERR_CONFIG;
+  const DecideArgs d{1, step, force, refresh_interval, strategy, strict, random_key,
+                     last_refresh, primed, reduced, cached_ids, active, write};
+  return gate_topk_launch(u, w_gate_t, n, hp, E, k, ids, gates, scores, status, step, layer, d,
+                          (cudaStream_t)stream);
 }
 
 int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, int refresh_interval,
@@ -790,9 +949,59 @@ int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, 
                      uint8_t* write, void* stream) {
   if (k < 1 || refresh_interval < 1 || strategy < 0 || strategy > 3) return DICE_ERR_CONFIG;
   if (n == 0) return DICE_OK;
-  cond_decide_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
-      ids, n, k, step, force, refresh_interval, strategy, strict, random_key, last_refresh, primed,
-      reduced, cached_ids, active, write);
+  const DecideArgs d{1, step, force, refresh_interval, strategy, strict, random_key, last_refresh,
+                     primed, reduced, cached_ids, active, write};
+  cond_decide_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(ids, n, k, d);
+  return launch_ok();
+}
+
+int dice_gemm_local_gate(const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
+                         float* out_f32, int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16,
+                         const float* residual, int64_t ld_res, const float* w_gate, int E,
+                         float* parts, void* stream) {
+  if (M < 0 || M > INT_MAX || (E != 8 && E != 16) || residual == nullptr || w_gate == nullptr ||
+      parts == nullptr)
+    return DICE_ERR_CONTRACT;
+  if (M == 0) return DICE_OK;
+  GemmProblem p{};
+  p.A = A; p.A_rows = M; p.B = B; p.M = (int)M; p.N = N; p.K = K;
+  p.num_groups = 1; p.group_tile_offsets = nullptr; p.max_m_tiles = 0;
+  p.epi_kind = E == 8 ? EPI_GELU_RESID_GATE8 : EPI_GELU_RESID_GATE16;
+  p.epi.out_f32 = out_f32; p.epi.ld_f32 = ld_f32;
+  p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out_bf16); p.epi.ld_bf16 = ld_bf16;
+  p.epi.residual = residual; p.epi.ld_res = ld_res;
+  p.epi.gate_w = w_gate;
+  p.epi.gate_part = parts;
+  return gemm_bf16(p, (cudaStream_t)stream);
+}
+
+int dice_gate_parts(int64_t M, int N, int K, int E) {
+  if (E != 8 && E != 16) return -DICE_ERR_CONTRACT;
+  GemmProblem p{};
+  p.M = (int)M; p.N = N; p.K = K; p.num_groups = 1;
+  p.epi_kind = E == 8 ? EPI_GELU_RESID_GATE8 : EPI_GELU_RESID_GATE16;
+  return gemm_gate_parts(p);
+}
+
+int dice_gate_finish(const float* parts, int P, int64_t n, int E, int k, int32_t* ids,
+                     float* gates, float* scores, int32_t* status, int step, int layer,
+                     int decide, int force, int refresh_interval, int strategy, int strict,
+                     uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
+                     uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
+                     uint8_t* write, void* stream) {
+  if ((E != 8 && E != 16) || k < 1 || k > E || P < 1) return DICE_ERR_CONTRACT;
+  if (decide && (refresh_interval < 1 || strategy < 0 || strategy > 3)) return DICE_ERR_CONFIG;
+  if (n == 0) return DICE_OK;
+  const DecideArgs d{decide ? 1 : 0, step, force, refresh_interval, strategy, strict, random_key,
+                     last_refresh, primed, reduced, cached_ids, active, write};
+  // one token per thread, small blocks so every SM gets some
+  const int grid = grid_for(n, 64);
+  if (E == 8)
+    gate_parts_kernel<8><<<grid, 64, 0, (cudaStream_t)stream>>>(parts, P, n, k, ids, gates, scores,
+                                                                status, step, layer, d);
+  else
+    gate_parts_kernel<16><<<grid, 64, 0, (cudaStream_t)stream>>>(parts, P, n, k, ids, gates,
+                                                                 scores, status, step, layer, d);
   return launch_ok();
 }
 

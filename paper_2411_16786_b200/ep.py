@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import hashlib
+import os
 
 import numpy as np
 import torch
@@ -243,6 +244,12 @@ class EPRunner:
         self.h16 = torch.zeros(n, hp, dtype=bf, device=dev)
         self.u32 = torch.zeros(n, hp, dtype=f32, device=dev)
         self.u16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        # router fused into the local_block GEMM epilogue (see DeviceRunner)
+        E_all = cfg.num_experts
+        self.fused_gate = E_all in (8, 16) and os.environ.get("DICE_FUSED_GATE", "0") == "1"
+        if self.fused_gate:
+            self.gparts = torch.empty(ops.gate_parts(n, hp, hp, E_all), n, E_all, dtype=f32,
+                                      device=dev)
         total = world * self.cap
         self.max_rows = ops.permute_max_rows(total, 1, El)
         self.hbuf = torch.empty(self.max_rows, ep, dtype=bf, device=dev)
@@ -428,15 +435,22 @@ class EPRunner:
         for layer in range(cfg.num_layers):
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
-            ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32, out_bf16=self.u16,
-                     residual=hin32)
+            if self.fused_gate:
+                ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
+                                    self.gparts)
+            else:
+                ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
+                         out_bf16=self.u16, residual=hin32)
             sync = self._stage_is_sync(step, layer)
             if sync:
                 self._flush_pending()
             self._assemble(layer)            # previous step's combine, before decide(layer)
             p = self.payloads[layer]
-            ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, None, self.status,
-                          step, layer)
+            if self.fused_gate:
+                ops.gate_finish(self.gparts, p.ids, p.gates, None, self.status, step, layer)
+            else:
+                ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, None, self.status,
+                              step, layer)
             if sync:
                 self._send(step, layer, p, force=True)
                 self._expert(p)

@@ -80,12 +80,65 @@ def splitmix_bits(seed, start, count, device="cuda"):
     return out
 
 
-def gate_topk(u32, w_gate_t, k, ids, gates, scores=None, status=None, step=0, layer=0):
+def gate_topk(u32, w_gate_t, k, ids, gates, scores=None, status=None, step=0, layer=0,
+              decide=None):
+    """Fused gate (softmax + stable top-k); ``decide`` = TokenCache.decide_args(...)
+    also runs the conditional-communication decision in the same kernel."""
     n, hp = u32.shape
     E = w_gate_t.shape[0]
     _need(u32, torch.float32, "gate u")
-    _lib.call("dice_gate_topk", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids), _ptr(gates),
-              _ptr(scores), _ptr(status), step, layer, _stream())
+    if decide is None:
+        _lib.call("dice_gate_topk", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids),
+                  _ptr(gates), _ptr(scores), _ptr(status), step, layer, _stream())
+        return
+    (force, R, strat, strict, key, last, primed, reduced, cached, active, write) = decide
+    _lib.call("dice_gate_topk_decide", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids),
+              _ptr(gates), _ptr(scores), _ptr(status), step, layer, int(force), R, strat,
+              int(strict), key & 0xFFFFFFFFFFFFFFFF, _ptr(last), _ptr(primed), _ptr(reduced),
+              _ptr(cached), _ptr(active), _ptr(write), _stream())
+
+
+def gate_parts(M, N, K, E):
+    """Partial-logit slots the gate-fused local GEMM writes (dice_gate_parts)."""
+    P = int(_lib.load().dice_gate_parts(M, N, K, E))
+    if P < 1:
+        raise ContractError(f"gate-fused GEMM: unsupported E={E}")
+    return P
+
+
+def gemm_local_gate(A, B, w_gate_c, out_f32, out_bf16, residual, parts):
+    """local_block GEMM (u = gelu(A @ B^T) + residual) with the router's partial
+    logits of the finished u rows fused into the epilogue: parts [P, M, E]."""
+    _need(A, torch.bfloat16, "gemm A")
+    _need(B, torch.bfloat16, "gemm B")
+    _need(w_gate_c, torch.float32, "w_gate")
+    _need(parts, torch.float32, "gate parts")
+    M, K = A.shape
+    N = B.shape[0]
+    E = w_gate_c.shape[1]
+    if B.shape[1] != K or w_gate_c.shape[0] != N or parts.shape[1:] != (M, E):
+        raise ContractError(f"gemm_local_gate: A {tuple(A.shape)} B {tuple(B.shape)} "
+                            f"w_gate {tuple(w_gate_c.shape)} parts {tuple(parts.shape)}")
+    _lib.call("dice_gemm_local_gate", _ptr(A), M, _ptr(B), N, K, _ptr(out_f32), out_f32.shape[-1],
+              _ptr(out_bf16), out_bf16.shape[-1], _ptr(residual), residual.shape[-1],
+              _ptr(w_gate_c), E, _ptr(parts), _stream())
+
+
+def gate_finish(parts, ids, gates, scores=None, status=None, step=0, layer=0, decide=None):
+    """Router finish over the fused partial logits (softmax, stable top-k,
+    renormalised gates); ``decide`` = TokenCache.decide_args(...) also runs the
+    conditional-communication decision in the same kernel."""
+    P, n, E = parts.shape
+    k = ids.shape[1]
+    if decide is None:
+        d = (0, 0, 1, 0, 0, 0, None, None, None, None, None, None)
+    else:
+        d = (1,) + tuple(decide)
+    (on, force, R, strat, strict, key, last, primed, reduced, cached, active, write) = d
+    _lib.call("dice_gate_finish", _ptr(parts), P, n, E, k, _ptr(ids), _ptr(gates), _ptr(scores),
+              _ptr(status), step, layer, on, int(force), R, strat, int(strict),
+              key & 0xFFFFFFFFFFFFFFFF, _ptr(last), _ptr(primed), _ptr(reduced), _ptr(cached),
+              _ptr(active), _ptr(write), _stream())
 
 
 def cond_decide(ids, step, force, refresh_interval, strategy, strict, random_key, last, primed,

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import dataclasses
 import hashlib
+import os
 from collections import Counter
 from dataclasses import dataclass
 from enum import Enum
@@ -191,6 +192,13 @@ class DeviceRunner:
         if policy.cond_strategy is not CondStrategy.OFF:
             self.cache = TokenCache(L, n, k, cfg.hidden_dim, device=dev)
         self.scratch = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+        # DICE_FUSED_GATE=1: router partial logits fused into the local_block GEMM
+        # epilogue (measured slower at the XL shape: the local GEMM's epilogue is
+        # its critical path); default: standalone persistent gate kernel. Either
+        # way the conditional-communication decision runs inside the gate launch.
+        self.fused_gate = E in (8, 16) and os.environ.get("DICE_FUSED_GATE", "0") == "1"
+        if self.fused_gate:
+            self.gparts = torch.empty(ops.gate_parts(n, hp, hp, E), n, E, dtype=f32, device=dev)
         self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
         self.status = torch.empty(4, dtype=torch.int32, device=dev)
         self.sync_layers = select_sync_layers(policy.sync_strategy, L, policy.explicit_layers)
@@ -283,10 +291,11 @@ class DeviceRunner:
         return self.slots[0] if self.strategy is Strategy.SYNCHRONOUS else self.slots[layer]
 
     # -------------------------------------------------------------- stages
-    def _dispatch(self, step, layer, p: _Payload, force: bool):
+    def _dispatch(self, step, layer, p: _Payload, force: bool, decided: bool = False):
         """decide (policies.py:159-186) + permute/pack of the token rows that travel."""
         if self.cache is not None:
-            self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write)
+            if not decided:
+                self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write)
             act = p.active
         else:
             act = None
@@ -371,8 +380,12 @@ class DeviceRunner:
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
             self._mark(f"local s{step} L{layer}")
-            ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32, out_bf16=self.u16,
-                     residual=hin32)
+            if self.fused_gate:
+                ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
+                                    self.gparts)
+            else:
+                ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
+                         out_bf16=self.u16, residual=hin32)
             self._mark(f"gate+dispatch s{step} L{layer}")
             sync = self._stage_is_sync(step, layer)
             if sync and self.strategy is Strategy.INTERWEAVED:
@@ -382,15 +395,23 @@ class DeviceRunner:
                 torch.cuda.current_stream().wait_event(self.slot_event[layer])
                 self.slot_event[layer] = None
             p = self._next_payload(layer)
-            ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores, self.status,
-                          step, layer)
+            dec = None
+            if self.cache is not None:
+                dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write)
+            if self.fused_gate:
+                ops.gate_finish(self.gparts, p.ids, p.gates, self.scores, self.status, step, layer,
+                                decide=dec)
+            else:
+                ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
+                              self.status, step, layer, decide=dec)
+            decided = dec is not None
             if self.record_inputs:
                 inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu())
             if self.record_routes:
                 routes_here.append(RouteDecision(p.ids.long().cpu(), p.gates.cpu(),
                                                  self.scores.cpu()))
             if sync:
-                self._dispatch(step, layer, p, force=True)
+                self._dispatch(step, layer, p, force=True, decided=decided)
                 self._process(p)
                 if self.strategy is Strategy.DISPLACED:
                     self.dispatch_slot[layer] = p
@@ -400,7 +421,7 @@ class DeviceRunner:
                     self._track("c", layer)
                 self._consume(layer, step, step)
             elif self.strategy is Strategy.DISPLACED:
-                self._dispatch(step, layer, p, force=False)
+                self._dispatch(step, layer, p, force=False, decided=decided)
                 old = self.dispatch_slot[layer]
                 self.dispatch_slot[layer] = p
                 self._track("d", layer)
@@ -411,7 +432,7 @@ class DeviceRunner:
                 self._process(old)
                 self._track("c", layer)
             else:
-                self._dispatch(step, layer, p, force=False)
+                self._dispatch(step, layer, p, force=False, decided=decided)
                 prev, self.pending = self.pending, p
                 if prev is not None:
                     self._process(prev, side=True)

@@ -100,3 +100,121 @@ print('ok')
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("M,E,k", [(8192, 8, 2), (1000, 8, 2), (777, 16, 2), (256, 8, 3), (130, 16, 5)])
+def test_local_gemm_fused_gate(M, E, k):
+    """local_block GEMM with the router's partial logits fused into its epilogue
+    + the finish kernel vs the unfused GELU_RESID GEMM + dice_gate_topk: u
+    bit-identical, ids identical outside the tie band, gates/scores within fp32
+    reassociation (the logit sum order differs), decide masks identical."""
+    hp = 1152
+    g = torch.Generator(device=dev).manual_seed(M + E + k)
+    x32 = torch.randn(M, hp, device=dev, generator=g)
+    x16 = x32.to(torch.bfloat16)
+    W = (torch.randn(hp, hp, device=dev, generator=g) / np.sqrt(hp)).to(torch.bfloat16)
+    wg_t = (torch.rand(E, hp, device=dev, generator=g) * 2 - 1) / np.sqrt(hp)
+    wg_c = wg_t.t().contiguous()
+    u32a = torch.empty(M, hp, device=dev); u16a = torch.empty(M, hp, device=dev, dtype=torch.bfloat16)
+    u32b = torch.empty_like(u32a); u16b = torch.empty_like(u16a)
+    ops.gemm(ops.EPI_GELU_RESID, x16, W, out_f32=u32a, out_bf16=u16a, residual=x32)
+    P = ops.gate_parts(M, hp, hp, E)
+    parts = torch.empty(P, M, E, device=dev)
+    ops.gemm_local_gate(x16, W, wg_c, u32b, u16b, x32, parts)
+    assert torch.equal(u32a, u32b) and torch.equal(u16a, u16b)
+    ids_a = torch.empty(M, k, dtype=torch.int32, device=dev); gates_a = torch.empty(M, k, device=dev)
+    sc_a = torch.empty(M, E, device=dev)
+    ids_b = torch.empty_like(ids_a); gates_b = torch.empty_like(gates_a); sc_b = torch.empty_like(sc_a)
+    st = torch.empty(4, dtype=torch.int32, device=dev)
+    ops.status_reset(st)
+    ops.gate_topk(u32a, wg_t, k, ids_a, gates_a, sc_a, st, 0, 0)
+    # logits in fp64 from the same u, for the tie band
+    logits = u32a.double() @ wg_c.double()
+    sc = torch.softmax(logits, dim=1)
+    top = torch.sort(sc, dim=1, descending=True).values
+    gap = (top[:, :k] - top[:, 1:k + 1]).abs().min(dim=1).values
+    clear = gap > 1e-5
+    # fused finish, with the cond decision fused (LowScore, R=2, step 0: all due)
+    n = M
+    last = torch.full((n,), -10 ** 9, dtype=torch.int32, device=dev)
+    primed = torch.zeros(n, dtype=torch.uint8, device=dev)
+    red = torch.zeros(n, k, dtype=torch.uint8, device=dev)
+    cids = torch.full((n, k), -1, dtype=torch.int32, device=dev)
+    act_b = torch.empty(n, k, dtype=torch.uint8, device=dev); wr_b = torch.empty_like(act_b)
+    dec = (False, 2, ops.COND_CODES["low_score"], False, 0, last, primed, red, cids, act_b, wr_b)
+    ops.gate_finish(parts, ids_b, gates_b, sc_b, st, 0, 0, decide=dec)
+    torch.cuda.synchronize()
+    assert int(st[0].item()) == 2 ** 31 - 1
+    assert torch.equal(ids_a[clear], ids_b[clear])
+    assert (gates_a - gates_b).abs().max().item() < 1e-5
+    assert (sc_a - sc_b).abs().max().item() < 1e-5
+    # same decision as the standalone kernel on the fused ids
+    last2 = torch.full((n,), -10 ** 9, dtype=torch.int32, device=dev)
+    primed2 = torch.zeros(n, dtype=torch.uint8, device=dev)
+    red2 = torch.zeros(n, k, dtype=torch.uint8, device=dev)
+    act_a = torch.empty_like(act_b); wr_a = torch.empty_like(wr_b)
+    ops.cond_decide(ids_b, 0, False, 2, "low_score", False, 0, last2, primed2, red2, cids, act_a, wr_a)
+    torch.cuda.synchronize()
+    for a_, b_ in ((act_a, act_b), (wr_a, wr_b), (last2, last), (primed2, primed), (red2, red)):
+        assert torch.equal(a_, b_)
+
+
+def test_fused_gate_nonfinite_flag():
+    M, hp, E = 300, 1152, 8
+    x32 = torch.zeros(M, hp, device=dev)
+    x32[123, 7] = float("inf")
+    W = torch.zeros(hp, hp, device=dev, dtype=torch.bfloat16)
+    wg_c = torch.ones(hp, E, device=dev) * 1e-3
+    u32 = torch.empty(M, hp, device=dev); u16 = torch.empty(M, hp, device=dev, dtype=torch.bfloat16)
+    parts = torch.empty(ops.gate_parts(M, hp, hp, E), M, E, device=dev)
+    ops.gemm_local_gate(x32.to(torch.bfloat16), W, wg_c, u32, u16, x32, parts)
+    ids = torch.empty(M, 2, dtype=torch.int32, device=dev); gates = torch.empty(M, 2, device=dev)
+    st = torch.empty(4, dtype=torch.int32, device=dev)
+    ops.status_reset(st)
+    ops.gate_finish(parts, ids, gates, None, st, 5, 3)
+    torch.cuda.synchronize()
+    assert st[:2].tolist() == [5, 3]
+
+
+@pytest.mark.parametrize("n,E,k,hp,strategy,strict", [(8192, 8, 2, 1152, "low_score", False),
+                                                      (999, 16, 2, 640, "random", True),
+                                                      (300, 8, 3, 128, "high_score", False),
+                                                      (77, 4, 2, 64, "low_score", True)])
+def test_gate_topk_with_fused_decide(n, E, k, hp, strategy, strict):
+    """dice_gate_topk_decide == dice_gate_topk then dice_cond_decide (same
+    kernel for the gate, so ids/gates are bit-identical), over a few steps of
+    evolving cache state."""
+    g = torch.Generator(device=dev).manual_seed(n + E)
+    wg = (torch.rand(E, hp, device=dev, generator=g) * 2 - 1) / np.sqrt(hp)
+    st = {}
+    for name in ("a", "b"):
+        st[name] = dict(last=torch.full((n,), -10 ** 9, dtype=torch.int32, device=dev),
+                        primed=torch.zeros(n, dtype=torch.uint8, device=dev),
+                        red=torch.zeros(n, k, dtype=torch.uint8, device=dev),
+                        cids=torch.randint(0, E, (n, k), dtype=torch.int32, device=dev, generator=g))
+    st["b"]["cids"] = st["a"]["cids"].clone()
+    status = torch.empty(4, dtype=torch.int32, device=dev)
+    ops.status_reset(status)
+    for step in range(5):
+        u = torch.randn(n, hp, device=dev, generator=g)
+        out = {}
+        for name in ("a", "b"):
+            s_ = st[name]
+            ids = torch.empty(n, k, dtype=torch.int32, device=dev)
+            gates = torch.empty(n, k, device=dev)
+            act = torch.empty(n, k, dtype=torch.uint8, device=dev)
+            wr = torch.empty_like(act)
+            force = step == 3
+            if name == "a":
+                ops.gate_topk(u, wg, k, ids, gates, None, status, step, 0)
+                ops.cond_decide(ids, step, force, 2, strategy, strict, 0x1234 + step, s_["last"],
+                                s_["primed"], s_["red"], s_["cids"], act, wr)
+            else:
+                dec = (force, 2, ops.COND_CODES[strategy], strict, 0x1234 + step, s_["last"],
+                       s_["primed"], s_["red"], s_["cids"], act, wr)
+                ops.gate_topk(u, wg, k, ids, gates, None, status, step, 0, decide=dec)
+            out[name] = (ids, gates, act, wr)
+        for x, y in zip(out["a"], out["b"]):
+            assert torch.equal(x, y)
+        for key in ("last", "primed", "red"):
+            assert torch.equal(st["a"][key], st["b"][key])

@@ -316,3 +316,29 @@ def test_step_similarity_precondition_xl_toy():
                          D.ClusterConfig(num_devices=4), 0, record_inputs=True, record_routes=True)
     sim = D.step_similarity(res.step_inputs, res.step_routes)
     assert sim.mean_cosine >= 0.9 and sim.mean_agreement >= 0.8, sim
+
+
+def test_fused_gate_engine_matches_unfused(monkeypatch):
+    """The engine with the router fused into the local GEMM epilogue (+ decide
+    fused into the finish kernel) reproduces the unfused engine: identical
+    staleness / pair counts and latents within fp32 logit-reassociation noise."""
+    cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=128,
+                        expert_dim=256, num_tokens=64, batch=4, num_steps=8, step_size=1e-3)
+    model = D.init_model(cfg, seed=5)
+    x0 = D.sample_x0(cfg, 5)
+    pol = D.dice_policy(refresh_interval=2, warmup=2, period=3)
+    out = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("DICE_FUSED_GATE", fused)
+        r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, pol, D.ClusterConfig(num_devices=2), 5)
+        assert r.fused_gate == (fused == "1")
+        res = r.run()
+        out[fused] = res
+    a, b = out["1"], out["0"]
+    assert [(s.layer, s.used_step, s.generated_step) for s in a.staleness_records] == \
+        [(s.layer, s.used_step, s.generated_step) for s in b.staleness_records]
+    assert (a.active_pairs, a.total_pairs) == (b.active_pairs, b.total_pairs)
+    fa, fb = a.final.values.cpu().double(), b.final.values.cpu().double()
+    x0d = torch.as_tensor(x0.values).double().cpu()
+    rel = (torch.linalg.norm((fa - x0d) - (fb - x0d)) / torch.linalg.norm(fb - x0d)).item()
+    assert rel < 1e-3, rel
