@@ -298,6 +298,10 @@ struct SkPlan {
   int T, KB, P, DP, R;
   long long I;
   bool on;
+  int S = 1;   // chained split-K factor (> 1 replaces stream-K)
+  __device__ __forceinline__ void init_chain(int T_, int KB_, int P_, int S_) {
+    T = T_; KB = KB_; P = P_; S = S_; on = false; DP = T; R = 0; I = 0;
+  }
   __device__ __forceinline__ void init(int T_, int KB_, int P_, bool allow) {
     T = T_; KB = KB_; P = P_;
     R = T % P;
@@ -315,6 +319,7 @@ struct SkPlan {
   }
   // number of work items of pair p
   __device__ __forceinline__ int items(int p) const {
+    if (S > 1) return p < T * S ? (T * S - 1 - p) / P + 1 : 0;
     int n = p < DP ? (DP - 1 - p) / P + 1 : 0;
     if (on) {
       const long long b = begin(p), e = begin(p + 1);
@@ -323,7 +328,19 @@ struct SkPlan {
     return n;
   }
   // item i of pair p: tile, k-range [k0, k1), workspace slot (-1 = whole tile)
+  // (chain items: slot = -2 - split)
   __device__ __forceinline__ void item(int p, int i, int& tile, int& k0, int& k1, int& slot) const {
+    if (S > 1) {
+      // split-major order: item (t, s) follows (t, s-1) by T items (more than a
+      // wave when T >= P), so the partial it adds is usually already written
+      const int idx = p + i * P;
+      const int s = idx / T;
+      tile = idx - s * T;
+      k0 = s * KB / S;
+      k1 = (s + 1) * KB / S;
+      slot = -2 - s;
+      return;
+    }
     const int ndp = p < DP ? (DP - 1 - p) / P + 1 : 0;
     if (i < ndp) { tile = p + i * P; k0 = 0; k1 = KB; slot = -1; return; }
     const long long b = begin(p), e = begin(p + 1);
@@ -349,6 +366,45 @@ __device__ __forceinline__ void epilogue_partial(const float* stage, int lane, f
     const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
     *reinterpret_cast<float4*>(ws_tile + (int64_t)(row_in_tile0 + rr) * bn + col_in_tile + 4 * q) = v;
   }
+}
+
+// Chained split-K helpers. Partial layout: f32 [tile][256 rows][ld] (this
+// CTA's rows at rank*128). stage += partial of the previous split (L2 reads:
+// the partial was written by another SM during this launch).
+__device__ __forceinline__ void chain_add_prev(float* stage, int lane, const float* ws, int ld,
+                                               int row_in_tile0, int col_in_tile) {
+  const int q = lane & 7;
+  float4 pv[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    pv[it] = __ldcg(reinterpret_cast<const float4*>(ws + (int64_t)(row_in_tile0 + rr) * ld +
+                                                    col_in_tile + 4 * q));
+  }
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    float4* sp = reinterpret_cast<float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
+    const float4 a = *sp;   // prev + acc: the fixed summation order of the chain
+    *sp = make_float4(pv[it].x + a.x, pv[it].y + a.y, pv[it].z + a.z, pv[it].w + a.w);
+  }
+}
+
+__device__ __forceinline__ void chain_store(const float* stage, int lane, float* ws, int ld,
+                                            int row_in_tile0, int col_in_tile) {
+  const int q = lane & 7;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
+    __stcg(reinterpret_cast<float4*>(ws + (int64_t)(row_in_tile0 + rr) * ld + col_in_tile + 4 * q), v);
+  }
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Sum each remainder tile's partial slots in pair order and apply the epilogue.
@@ -507,7 +563,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
   SkPlan plan;
-  plan.init(num_tiles, k_blocks, num_pairs, args.sk_workspace != nullptr);
+  if (args.ksplit > 1)
+    plan.init_chain(num_tiles, k_blocks, num_pairs, args.ksplit);
+  else
+    plan.init(num_tiles, k_blocks, num_pairs, args.sk_workspace != nullptr);
   const int n_items = plan.items(pair);
 
   if (warp == 0) {
@@ -585,6 +644,16 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc_fence_after();
       const int row0 = m_tile * kPairM + rank * BM + sub * 32;
       float* ws_tile = slot >= 0 ? args.sk_workspace + (int64_t)slot * kPairM * BN : nullptr;
+      // chained split-K item: split index, partial buffer, wait for split - 1
+      const int csplit = slot <= -2 ? -2 - slot : -1;
+      float* cws = csplit >= 0 ? args.chain_ws + (int64_t)tile * kPairM * TN : nullptr;
+      if (!DIRECT && csplit > 0) {
+        if (lane == 0) {
+          const unsigned want = (unsigned)(2 * kEpiWarps * csplit);
+          while (ld_acquire_u32(args.chain_flags + 2 * tile) < want) __nanosleep(64);
+        }
+        __syncwarp();
+      }
       constexpr int GE = EpiTraits<EPI>::gate_e;
       float2 gacc[GE > 0 ? GE / 2 : 1];
 #pragma unroll
@@ -614,10 +683,33 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           gate_accumulate<GE>(args, stage, lane, col0, gacc);
         } else if (ws_tile != nullptr) {
           epilogue_partial(stage, lane, ws_tile, BN, rank * BM + sub * 32, col_in_tile);
+        } else if (csplit >= 0) {
+          if (csplit > 0) {
+            chain_add_prev(stage, lane, cws, TN, rank * BM + sub * 32, col_in_tile);
+            __syncwarp();
+          }
+          if (csplit < args.ksplit - 1)
+            chain_store(stage, lane, cws, TN, rank * BM + sub * 32, col_in_tile);
+          else
+            epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
         } else {
           epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
         }
         __syncwarp();
+      }
+      if (!DIRECT && csplit >= 0) {
+        if (csplit < args.ksplit - 1) {
+          __threadfence();           // partial visible before the arrival
+          __syncwarp();
+          if (lane == 0) atomicAdd(args.chain_flags + 2 * tile, 1u);
+        } else {
+          __syncwarp();
+          // the last of the final item's warps returns the tile's counters to 0
+          if (lane == 0 && atomicAdd(args.chain_flags + 2 * tile + 1, 1u) == 2u * kEpiWarps - 1) {
+            args.chain_flags[2 * tile] = 0;
+            args.chain_flags[2 * tile + 1] = 0;
+          }
+        }
       }
       if constexpr (GE > 0) {
         const int64_t row = row0 + lane;
@@ -768,6 +860,44 @@ int env_int(const char* name, int dflt) {
   return (e != nullptr && e[0] != 0) ? atoi(e) : dflt;
 }
 
+// Chained split-K partials + counters, one set per stream, grown only outside
+// graph capture (the warm-up run before capture sizes it).
+struct ChainWs {
+  float* ws = nullptr;
+  unsigned* flags = nullptr;
+  size_t ws_bytes = 0;
+  int tiles = 0;
+};
+std::mutex g_chain_mu;
+std::unordered_map<cudaStream_t, ChainWs> g_chain;
+
+int chain_workspace(cudaStream_t stream, int tiles, int tile_n, float** ws, unsigned** flags) {
+  std::lock_guard<std::mutex> lk(g_chain_mu);
+  ChainWs& c = g_chain[stream];
+  const size_t need = (size_t)tiles * 256 * tile_n * sizeof(float);
+  if (c.ws_bytes < need || c.tiles < tiles) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &st);
+    if (st != cudaStreamCaptureStatusNone) return DICE_ERR_CONTRACT;   // size it before capture
+    cudaStreamSynchronize(stream);
+    if (c.ws) cudaFree(c.ws);
+    if (c.flags) cudaFree(c.flags);
+    c.ws = nullptr; c.flags = nullptr;
+    if (cudaMalloc(&c.ws, need) != cudaSuccess || cudaMalloc(&c.flags, sizeof(unsigned) * 2 * tiles) != cudaSuccess ||
+        cudaMemset(c.flags, 0, sizeof(unsigned) * 2 * tiles) != cudaSuccess) {
+      cudaGetLastError();
+      c.ws_bytes = 0; c.tiles = 0;
+      return DICE_ERR_CUDA;
+    }
+    cudaDeviceSynchronize();
+    c.ws_bytes = need;
+    c.tiles = tiles;
+  }
+  *ws = c.ws;
+  *flags = c.flags;
+  return 0;
+}
+
 template <int BN, int EPI, bool DIRECT, int NSUB = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream) {
@@ -779,12 +909,20 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
       return DICE_ERR_CUDA;
     attr_done = true;
   }
-  int grid = 2 * max_tiles < num_sms() ? 2 * max_tiles : num_sms();
+  const int items = max_tiles * (a.ksplit > 1 ? a.ksplit : 1);
+  int grid = 2 * items < num_sms() ? 2 * items : num_sms();
   grid &= ~1;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
   aa.sk_workspace = (DIRECT || NSUB > 1 || EpiTraits<EPI>::gate_e > 0) ? nullptr
                                                                        : stream_k_workspace(stream);
+  if (aa.ksplit > 1) {
+    if (DIRECT) return DICE_ERR_CONTRACT;
+    const int rc = chain_workspace(stream, max_tiles, NSUB * BN, &aa.chain_ws, &aa.chain_flags);
+    if (rc) return rc;
+  } else {
+    aa.ksplit = 1;
+  }
   // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
   static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
   aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
@@ -858,6 +996,7 @@ struct TileChoice {
   int tile_n;    // output columns per tile (bn, or 384 for the wide tiles)
   bool pair;     // CTA-pair kernel (256-row tiles)
   bool wide;
+  int ksplit;    // chained split-K factor (wide staged epilogues), 1 = off
 };
 
 TileChoice choose_tile(const GemmProblem& p) {
@@ -882,6 +1021,7 @@ TileChoice choose_tile(const GemmProblem& p) {
   // only when the wave count does not lose what the wider tile gains.
   static const int wide_mode = env_int("DICE_GEMM_WIDE", 1);
   c.wide = false;
+  c.ksplit = 1;
   if (c.pair && c.bn == 192 && p.N % 384 == 0 && wide_mode != 0 && !gate) {
     const int64_t m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + 255) / 256;
     const int pairs = num_sms() / 2;
@@ -889,9 +1029,27 @@ TileChoice choose_tile(const GemmProblem& p) {
       return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs);
     };
     const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16;
+    const double narrow = wave_eff(m_tiles * (p.N / 192));
     c.wide = wide_mode == 2 ||
-             (direct_epi && p.K >= 2048 &&
-              1.15 * wave_eff(m_tiles * (p.N / 384)) >= wave_eff(m_tiles * (p.N / 192)));
+             (direct_epi && p.K >= 2048 && 1.15 * wave_eff(m_tiles * (p.N / 384)) >= narrow);
+    // long-K dense staged epilogues (the shared-FFN GEMM2 + consume): wide tiles
+    // with a chained split-K factor that fills the last wave. Opt-in
+    // (DICE_GEMM_CHAIN=1; 2 forces it): measured slower at the XL consume shape
+    // (172 vs 162 us) because the single TMEM buffer of a 384-wide tile exposes
+    // the heavy f32 consume epilogue of every item.
+    static const int chain_mode = env_int("DICE_GEMM_CHAIN", 0);
+    const bool staged = p.epi_kind == EPI_CONSUME || p.epi_kind == EPI_STORE_F32;
+    if (!c.wide && chain_mode != 0 && staged && p.group_tile_offsets == nullptr && p.K >= 4096) {
+      const int64_t T = m_tiles * (p.N / 384);
+      const int KB = (p.K + BK - 1) / BK;
+      double best = 1.15 * wave_eff(T) - 0.0;
+      int best_s = 1;
+      for (int S = 2; S <= 4 && KB / S >= 16; ++S) {
+        const double e = 1.15 * wave_eff(T * S) - 0.03 * (S - 1);
+        if (e > best) { best = e; best_s = S; }
+      }
+      if (chain_mode == 2 || best > narrow) { c.wide = true; c.ksplit = best_s; }
+    }
   }
   c.tile_n = c.wide ? 384 : c.bn;
   return c;
@@ -908,6 +1066,7 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   const TileChoice tc = choose_tile(p);
   const int bn = tc.bn, tile_n = tc.tile_n;
   const bool pair = tc.pair, wide = tc.wide;
+
   const int tile_m = pair ? 2 * BM : BM;
   CUtensorMap ta, tb;
   int rc = tensor_map(p.A, p.A_rows, p.K, BM, &ta);
@@ -923,6 +1082,7 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   a.group_tile_offsets = p.group_tile_offsets;
   a.num_groups = p.num_groups;
   a.num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + tile_m - 1) / tile_m;
+  a.ksplit = tc.ksplit;
   const int max_tiles = a.num_m_tiles * a.num_n_blocks;
   if (max_tiles == 0) return 0;
   if (wide) return dispatch_wide(p.epi_kind, ta, tb, a, max_tiles, stream);
