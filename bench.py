@@ -161,6 +161,74 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------- GPU arm
+def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
+    """Per-op device time of one graph replay of the bench run, with graph-safe
+    CUDA events around every library op, and each op's achieved rate against
+    its roofline: HBM-bound ops in GB/s of algorithmic bytes over the measured
+    HBM copy bandwidth, GEMMs in TFLOP/s over the sustained bf16 peak.
+    Algorithmic bytes / FLOPs per call (R rows, h hidden, e expert width, k slots,
+    E experts, S shared, P active pairs of that (step, layer) from the device
+    counters):
+      gate_decide     4Rh (u) + 4Eh (W_gate) + 8Rk (ids, gates) + 5R + 3Rk (cache state)
+      permute         4hP (row gather read + write, bf16) + 9Rk (ids, masks, positions)
+      cache_assemble  2hP (fresh rows) + 2h(Rk - P) (cached rows) + 4Rh (combine slot) + 10Rk
+                      (cache-row writes of refreshed pairs not counted: a lower bound)
+      denoise         14Rh
+      local_gemm      2Rh^2;  shared_gemm1 / shared_gemm2_consume 2RhSe each;  grouped_ffn 4heP
+    """
+    import torch
+    r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed, time_ops=True,
+                       overlap=args.overlap)
+    if not args.eager:
+        r.capture()
+    r.launch()
+    r.launch()
+    torch.cuda.synchronize()
+    times = r.op_times()
+    cnt = r.counters.cpu().numpy()
+    del r
+    torch.cuda.empty_cache()
+    R, h, e, k, E, S = (cfg.total_rows, cfg.hidden_dim, cfg.expert_dim, cfg.top_k,
+                        cfg.num_experts, cfg.num_shared)
+    peak_tf, hbm, _ = peaks()
+    agg = {}
+    for name, ms, step, layer in times:
+        P = float(cnt[step, layer, 0]) if layer >= 0 else 0.0
+        if name == "gate_decide":
+            work, kind = 4 * R * h + 4 * E * h + 8 * R * k + 5 * R + 3 * R * k, "hbm"
+        elif name == "permute":
+            work, kind = 4 * h * P + 9 * R * k, "hbm"
+        elif name == "cache_assemble":
+            work, kind = 2 * h * P + 2 * h * (R * k - P) + 4 * R * h + 10 * R * k, "hbm"
+        elif name == "denoise":
+            work, kind = 14 * R * h, "hbm"
+        elif name == "local_gemm":
+            work, kind = 2.0 * R * h * h, "tensor"
+        elif name in ("shared_gemm1", "shared_gemm2_consume"):
+            work, kind = 2.0 * R * h * S * e, "tensor"
+        elif name == "grouped_ffn":
+            work, kind = 4.0 * h * e * P, "tensor"
+        else:
+            continue
+        a = agg.setdefault(name, [0.0, 0, 0.0, kind])
+        a[0] += ms
+        a[1] += 1
+        a[2] += work
+    total_ms = sum(v[0] for v in agg.values())
+    out = {}
+    for name, (ms, calls, work, kind) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        rate = work / (ms * 1e-3)
+        if kind == "hbm":
+            achieved, unit, peak = rate / 1e9, "GB/s", hbm
+        else:
+            achieved, unit, peak = rate / 1e12, "TFLOP/s", peak_tf
+        out[name] = {"us_per_call": ms * 1e3 / calls, "calls": calls, "share": ms / total_ms,
+                     "bound": kind, "achieved": achieved, "unit": unit, "peak": peak,
+                     "frac": achieved / peak}
+    return out
+
+
+
 def run_gpu(args):
     import numpy as np
     import torch
@@ -274,6 +342,12 @@ def run_gpu(args):
     e2e = world * IMAGES_PER_GPU * args.steps / e2e_s
     final_dice = runner._final_host.clone().numpy().astype(np.float64)
 
+    # per-op device time inside the real step (separate timed replay: the events
+    # cost a few % of the step, so the headline value above is taken without them)
+    breakdown = None
+    if world == 1 and not args.no_breakdown:
+        breakdown = op_breakdown(D, model, x0, policy, cluster, seed, cfg, args)
+
     # staleness quality: latent MSE of DICE / interweaved vs the synchronous path (same GPU numerics)
     quality = {}
     if not args.no_quality and world == 1:
@@ -331,6 +405,7 @@ def run_gpu(args):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "quality": quality,
+        "breakdown": breakdown,
         "pairs": {"active": res.active_pairs, "total": res.total_pairs},
     }
     if cpu is not None:
@@ -349,6 +424,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-quality", action="store_true")
+    ap.add_argument("--no-breakdown", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch kernels from Python, no CUDA graph")
     ap.add_argument("--overlap", action="store_true",
                     help="run the pending expert FFN on a side stream (intra-GPU interweaving)")

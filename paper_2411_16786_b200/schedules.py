@@ -142,7 +142,8 @@ class DeviceRunner:
     def __init__(self, model: ToyModel, x0: ActivationBlock, strategy: Strategy,
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *,
                  record_inputs: bool = False, record_routes: bool = False,
-                 time_experts: bool = False, overlap: bool = False, timeline: bool = False):
+                 time_experts: bool = False, overlap: bool = False, timeline: bool = False,
+                 time_ops: bool = False):
         cfg = model.config
         if not isinstance(strategy, Strategy):
             raise ContractError(f"strategy must be a Strategy, got {strategy!r}")
@@ -160,6 +161,10 @@ class DeviceRunner:
         self.strategy, self.policy, self.cluster, self.seed = strategy, policy, cluster, seed
         self.record_inputs, self.record_routes = record_inputs, record_routes
         self.time_experts = time_experts
+        # time_ops: graph-safe CUDA events around every library op of the run
+        # (per-op device time inside the real step; costs a few % of the step)
+        self.time_ops = time_ops
+        self._op_events, self._op_pool = [], []
         self.want_timeline = timeline
         dev = model.device
         self.dev = dev
@@ -245,6 +250,7 @@ class DeviceRunner:
         self.step_inputs, self.step_routes = [], []
         self._expert_events = []  # (start, end, generated step, layer) of each expert-FFN launch
         self._marks = []
+        self._op_events = []      # (op, start, end, step, layer) when time_ops
 
     def _mark(self, label):
         """Stage boundary for the measured timeline (graph-safe CUDA event)."""
@@ -256,6 +262,30 @@ class DeviceRunner:
         ev = self._mark_pool[i]
         ev.record()
         self._marks.append((label, ev))
+
+    def _op(self, name, step, layer):
+        """Context bracketing one library op with graph-safe events (time_ops)."""
+        runner = self
+
+        class _Ctx:
+            def __enter__(self_):
+                if not runner.time_ops:
+                    return
+                i = len(runner._op_events)
+                if i >= len(runner._op_pool):
+                    runner._op_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
+                self_.ev = runner._op_pool[i]
+                self_.ev[0].record()
+
+            def __exit__(self_, *a):
+                if runner.time_ops:
+                    self_.ev[1].record()
+                    runner._op_events.append((name, self_.ev[0], self_.ev[1], step, layer))
+        return _Ctx()
+
+    def op_times(self):
+        """[(op, ms, step, layer)] of the last run / replay (time_ops)."""
+        return [(n, a.elapsed_ms(b), s, l) for n, a, b, s, l in self._op_events]
 
     def _track(self, kind, layer):
         self.occupied.add((kind, layer))
@@ -299,9 +329,10 @@ class DeviceRunner:
             act = p.active
         else:
             act = None
-        ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
-                          self.counters[step, layer], self.scratch, self.E,
-                          devices=self.cluster.num_devices, row0=0, rows_total=self.n)
+        with self._op("permute", step, layer):
+            ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
+                              self.counters[step, layer], self.scratch, self.E,
+                              devices=self.cluster.num_devices, row0=0, rows_total=self.n)
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 
@@ -339,16 +370,18 @@ class DeviceRunner:
                 self._event_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
             e0, e1 = self._event_pool[i]
             e0.record()
-        ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
+        with self._op("grouped_ffn", p.gen, p.layer):
+            ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
         if self.time_experts:
             e1.record()
             self._expert_events.append((e0, e1, p.gen, p.layer))
         c = self.cache
-        ops.cache_assemble(self.y, p.pos, None if c is None else p.active,
-                           None if c is None else p.write, p.gates, p.ids, self._slot(p.layer),
-                           None if c is None else c.rows[p.layer],
-                           None if c is None else c.gates[p.layer],
-                           None if c is None else c.expert_ids[p.layer])
+        with self._op("cache_assemble", p.gen, p.layer):
+            ops.cache_assemble(self.y, p.pos, None if c is None else p.active,
+                               None if c is None else p.write, p.gates, p.ids, self._slot(p.layer),
+                               None if c is None else c.rows[p.layer],
+                               None if c is None else c.gates[p.layer],
+                               None if c is None else c.expert_ids[p.layer])
         self.slot_gen[p.layer] = p.gen
         self.combine_log.append((p.gen, p.layer))
 
@@ -365,9 +398,11 @@ class DeviceRunner:
         slot = self._slot(layer)
         self._mark(f"shared+consume s{step} L{layer}")
         if self.S > 0:
-            ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
-            ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
-                     residual=self.u32, addend=slot)
+            with self._op("shared_gemm1", step, layer):
+                ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
+            with self._op("shared_gemm2_consume", step, layer):
+                ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
+                         residual=self.u32, addend=slot)
         else:
             empty = slot.new_empty(self.n, 0)
             ops.combine(slot, slot, empty, self.h32, residual=self.u32, out_bf16=self.h16)
@@ -380,12 +415,13 @@ class DeviceRunner:
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
             self._mark(f"local s{step} L{layer}")
-            if self.fused_gate:
-                ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
-                                    self.gparts)
-            else:
-                ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
-                         out_bf16=self.u16, residual=hin32)
+            with self._op("local_gemm", step, layer):
+                if self.fused_gate:
+                    ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
+                                        self.gparts)
+                else:
+                    ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
+                             out_bf16=self.u16, residual=hin32)
             self._mark(f"gate+dispatch s{step} L{layer}")
             sync = self._stage_is_sync(step, layer)
             if sync and self.strategy is Strategy.INTERWEAVED:
@@ -398,12 +434,13 @@ class DeviceRunner:
             dec = None
             if self.cache is not None:
                 dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write)
-            if self.fused_gate:
-                ops.gate_finish(self.gparts, p.ids, p.gates, self.scores, self.status, step, layer,
-                                decide=dec)
-            else:
-                ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
-                              self.status, step, layer, decide=dec)
+            with self._op("gate_decide", step, layer):
+                if self.fused_gate:
+                    ops.gate_finish(self.gparts, p.ids, p.gates, self.scores, self.status, step,
+                                    layer, decide=dec)
+                else:
+                    ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
+                                  self.status, step, layer, decide=dec)
             decided = dec is not None
             if self.record_inputs:
                 inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu())
@@ -440,7 +477,8 @@ class DeviceRunner:
                 self._consume(layer, step, self.slot_gen[layer])
         self._flush_pending(side=self.strategy is Strategy.INTERWEAVED)
         self._mark(f"denoise s{step}")
-        ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
+        with self._op("denoise", step, -1):
+            ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
         self._mark(f"end s{step}")
         if self.record_inputs:
             self.step_inputs.append(inputs_here)

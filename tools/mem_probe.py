@@ -7,7 +7,8 @@ sys.path.insert(0, ".")
 from paper_2411_16786_b200 import ops
 
 dev = "cuda"
-n, k, E, h = 8192, 2, 8, 1152
+n = int(sys.argv[sys.argv.index("--rows") + 1]) if "--rows" in sys.argv else 8192
+k, E, h = 2, 8, 1152
 hp = h
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if __import__("os").path.exists("MEASURED_PEAKS.json") else 6650.0
 flush = torch.ones(64 * 2 ** 20, dtype=torch.float32, device=dev)  # 256 MB, read to evict L2

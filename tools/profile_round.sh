@@ -1,0 +1,21 @@
+#!/bin/bash
+# Round profile capture (run under gpurun, 1 GPU): launch list of the bench
+# workload's steps 6-7 (the recipe's cold-cache pass) + one ncu --set full
+# launch of each top kernel of an async step (7). CSV exports only (small).
+OUT=gpurun_out/${1:-prof}
+mkdir -p $OUT
+ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+    --log-file $OUT/launches_steps6-7.csv python tools/profile_step.py > $OUT/launch.log 2>&1
+python tools/summarize_launches.py $OUT/launches_steps6-7.csv > $OUT/launch_summary.txt
+i=0
+for k in "256, .int.1, .bool.1" "192, .int.4, .bool.0" "192, .int.0, .bool.1, .int.2" "192, .int.3" \
+         "gate_topk_fast" "cache_assemble" "permute_gather"; do
+  i=$((i+1))
+  timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
+      --kernel-name-base demangled -k "regex:$k" -s 1 -c 1 -o $OUT/k$i python tools/profile_kernels.py \
+      > $OUT/k$i.log 2>&1
+  ncu -i $OUT/k$i.ncu-rep --page raw --csv > $OUT/k${i}_raw.csv 2>/dev/null
+  ncu -i $OUT/k$i.ncu-rep --page details --csv > $OUT/k${i}_details.csv 2>/dev/null
+  rm -f $OUT/k$i.ncu-rep
+done
+du -sh $OUT
