@@ -110,7 +110,11 @@ def check(rc: int, what: str) -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches count)
-KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_grouped_ffn": 4, "dice_gemm": 2, "dice_event_create": 0,
+# (stream-K, opt-in, adds a fixup kernel per GEMM; the single-launch permute is the default)
+_SK = 1 if os.environ.get("DICE_GEMM_STREAMK") == "1" else 0
+KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSED") == "1" else 3,
+                    "dice_grouped_ffn": 2 * (1 + _SK), "dice_gemm": 1 + _SK,
+                    "dice_gemm_local_gate": 1, "dice_gate_parts": 0, "dice_event_create": 0,
                     "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,

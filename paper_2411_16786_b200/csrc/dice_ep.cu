@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(256) ep_send_kernel(
     const int32_t* __restrict__ dest_offsets, int64_t pairs, int k, int El,
     const uint16_t* __restrict__ u16, int hp, PeerPtrs rx_rows, PeerPtrs rx_meta, PeerPtrs rx_count,
     int D) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x < D) {
     const int d = threadIdx.x;
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(256) ep_send_kernel(
 // Receiver: expert key of every received row (-1 beyond each source's count).
 __global__ void ep_rx_ids_kernel(const int2* __restrict__ meta, const int32_t* __restrict__ counts,
                                  int D, int64_t cap, int32_t* ids_rx) {
+  pdl_enter();
   const int64_t total = (int64_t)D * cap;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -72,6 +74,7 @@ __global__ void ep_rx_ids_kernel(const int2* __restrict__ meta, const int32_t* _
 __global__ void __launch_bounds__(256) ep_combine_send_kernel(
     const int32_t* __restrict__ pos_rx, const int2* __restrict__ meta, int64_t total, int64_t cap,
     const uint16_t* __restrict__ y, int hp, PeerPtrs cx) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int vec = hp / 8;
   for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < total;
@@ -87,6 +90,7 @@ __global__ void __launch_bounds__(256) ep_combine_send_kernel(
 }
 
 __global__ void iota_pairs_kernel(int32_t* out, int64_t count) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)i;

@@ -128,6 +128,7 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const GemmArgs args) {
+  pdl_enter();
   using C = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -413,6 +414,7 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 template <int EPI>
 __global__ void __launch_bounds__(256) stream_k_fixup_kernel(const GemmArgs a, const float* ws,
                                                              int bn, int pairs) {
+  pdl_enter();
   __shared__ int info[4];   // m_tiles, q0, q1, on
   if (threadIdx.x == 0)
     info[0] = a.group_tile_offsets != nullptr ? a.group_tile_offsets[a.num_groups] : a.num_m_tiles;
@@ -520,6 +522,7 @@ template <int BN, int EPI, bool DIRECT, int NSUB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const GemmArgs args) {
+  pdl_enter();
   using C = PairCfg<BN, DIRECT, NSUB>;
   constexpr int TN = C::kTN;
   const int kStages = args.stages;   // <= C::kStages (host-clamped)
@@ -822,7 +825,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int 
   }
   int grid = max_tiles < num_sms() ? max_tiles : num_sms();
   if (grid <= 0) return 0;
-  gemm_bf16_tcgen05<BN, EPI><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, a);
+  launch_pdl(gemm_bf16_tcgen05<BN, EPI>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ta, tb, a);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 
@@ -910,7 +913,9 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
     attr_done = true;
   }
   const int items = max_tiles * (a.ksplit > 1 ? a.ksplit : 1);
-  int grid = 2 * items < num_sms() ? 2 * items : num_sms();
+  static const int cta_cap = env_int("DICE_GEMM_MAX_CTAS", 1 << 30);   // experiment hook
+  const int sms = num_sms() < cta_cap ? num_sms() : cta_cap;
+  int grid = 2 * items < sms ? 2 * items : sms;
   grid &= ~1;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
@@ -926,9 +931,9 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
   static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
   aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
-  gemm_bf16_pair<BN, EPI, DIRECT, NSUB><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, aa);
+  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ta, tb, aa);
   if (aa.sk_workspace != nullptr)
-    stream_k_fixup_kernel<EPI><<<num_sms() * 2, 256, 0, stream>>>(aa, aa.sk_workspace, BN, grid / 2);
+    launch_pdl(stream_k_fixup_kernel<EPI>, dim3(num_sms() * 2), dim3(256), 0, stream, aa, aa.sk_workspace, BN, grid / 2);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 

@@ -33,6 +33,7 @@ __device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
 
 // ------------------------------------------------------------------ status
 __global__ void status_reset_kernel(int32_t* s) {
+  pdl_enter();
   s[0] = INT_MAX;
   s[1] = -1;
   s[2] = 0;
@@ -46,6 +47,7 @@ __global__ void status_reset_kernel(int32_t* s) {
 __global__ void splitmix_fill_kernel(uint64_t seed, uint64_t start, int64_t rows, int64_t cols,
                                      double a, int transpose, int out_dtype, void* out,
                                      int64_t ld) {
+  pdl_enter();
   const int64_t total = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -66,6 +68,7 @@ __global__ void splitmix_fill_kernel(uint64_t seed, uint64_t start, int64_t rows
 }
 
 __global__ void splitmix_bits_kernel(uint64_t seed, uint64_t start, int64_t count, uint64_t* out) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = splitmix_at(seed, start + (uint64_t)i + 1);
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(512) gate_topk_kernel(
     const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int E, int k,
     int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
     int32_t* status, int step, int layer) {
+  pdl_enter();
   extern __shared__ float sw[];  // [E, hp]
   {
     const float4* src = reinterpret_cast<const float4*>(wt);
@@ -270,6 +274,7 @@ __device__ __forceinline__ void decide_token(int64_t t, int k, const int32_t* id
 
 __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, int k,
                                    const DecideArgs d) {
+  pdl_enter();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x)
     decide_token(t, k, ids, d);
@@ -287,6 +292,7 @@ __global__ void __launch_bounds__(256, MINB) gate_topk_fast_kernel(
     const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
     int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
     int32_t* status, int step, int layer, const DecideArgs d) {
+  pdl_enter();
   static_assert(E == 8 || E == 16, "fast gate handles E = 8 or 16");
   constexpr int V = 2 * E;
   constexpr int DUP = E == 8 ? 2 : 1;   // lanes holding the same (row, expert)
@@ -434,6 +440,7 @@ __global__ void __launch_bounds__(64) gate_parts_kernel(
     const float* __restrict__ parts, int P, int64_t n, int k, int32_t* __restrict__ ids,
     float* __restrict__ gates, float* __restrict__ scores, int32_t* status, int step, int layer,
     const DecideArgs d) {
+  pdl_enter();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     float l[E];
@@ -533,6 +540,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
     long long* counters, int devices, int64_t row0, int64_t rows_total, int32_t* block_counts,
     int key_div, int experts_total) {
+  pdl_enter();
   __shared__ int cnt[64];
   __shared__ unsigned long long red[2];
   if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
@@ -571,6 +579,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
     int32_t* pos, const int32_t* __restrict__ block_counts, int32_t* tile_offsets, int key_div,
     int row_tile) {
+  pdl_enter();
   __shared__ int wcnt[32][64];
   __shared__ int base[64];
   const int nb = gridDim.x;
@@ -606,11 +615,157 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
   if (in_range) pos[p] = valid ? base[e] + r : -1;
 }
 
+// ------------------------------------------------- single-launch permute
+// The engine's route_permute as ONE persistent launch (grid <= #SMs, every
+// block co-resident): count per (block, expert) -> grid barrier -> 256-row
+// padded expert bases + positions in pair order (the same deterministic order
+// as the three-kernel path) -> grid barrier -> row gather by all warps.
+constexpr int kFusedPermMaxBlocks = 160;
+constexpr int kFusedPermThreads = 1024;
+
+// Sense-free generation barrier; state {arrivals, generation} persists across
+// launches (and CUDA-graph replays): arrivals return to 0 at every barrier.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned gen;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      unsigned g;
+      do {
+        __nanosleep(32);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      } while (g == gen);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFusedPermThreads, 1) route_permute_fused_kernel(
+    const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
+    const uint16_t* __restrict__ u16, int hp, uint16_t* __restrict__ x_perm, int32_t* pos,
+    int32_t* tile_offsets, long long* counters, int devices, int64_t row0, int64_t rows_total,
+    int32_t* block_counts, unsigned* bar) {
+  pdl_enter();
+  __shared__ int cnt[64];
+  __shared__ int base[64];
+  __shared__ int wcnt[32][64];
+  __shared__ int stride_tot[64];
+  __shared__ unsigned long long red[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t P = n * k;
+  const int64_t chunk = (P + gridDim.x - 1) / gridDim.x;
+  const int64_t p0 = (int64_t)blockIdx.x * chunk;
+  const int64_t p1 = p0 + chunk < P ? p0 + chunk : P;
+  if (tid < 64) cnt[tid] = 0;
+  if (tid < 2) red[tid] = 0;
+  __syncthreads();
+  // phase 1: per-(block, expert) counts and the byte-plan counters (cluster.py:75-90)
+  for (int64_t q0 = p0; q0 < p1; q0 += blockDim.x) {
+    const int64_t p = q0 + tid;
+    int e = 0, s = 0;
+    int64_t t = 0;
+    const bool valid = p < p1 && pair_of(p, k, ids, active, 1, e, t, s);
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : -1);
+    if (valid && __popc(peers & ((1u << lane) - 1)) == 0) atomicAdd(&cnt[e], __popc(peers));
+    bool remote = false;
+    if (valid && devices > 1) {
+      const int home = (int)(((row0 + t) * devices) / rows_total);
+      remote = home != e / (E / devices);
+    }
+    const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
+    const unsigned nr = __popc(__ballot_sync(0xffffffffu, remote));
+    if (lane == 0 && nv) atomicAdd(&red[0], (unsigned long long)nv);
+    if (lane == 0 && nr) atomicAdd(&red[1], (unsigned long long)nr);
+  }
+  __syncthreads();
+  if (tid < E) block_counts[(int64_t)blockIdx.x * E + tid] = cnt[tid];
+  if (tid == 0 && counters != nullptr) {
+    if (red[0]) atomicAdd(reinterpret_cast<unsigned long long*>(&counters[0]), red[0]);
+    if (red[1]) atomicAdd(reinterpret_cast<unsigned long long*>(&counters[1]), red[1]);
+  }
+  grid_barrier(bar);
+  // phase 2: expert bases (groups padded to 256-row GEMM tiles), positions.
+  // All blocks' counts are staged in smem with one coalesced pass (wcnt as
+  // scratch: gridDim.x * E <= 32 * 64 ints), then summed per expert.
+  int* all_counts = &wcnt[0][0];
+  for (int i = tid; i < (int)gridDim.x * E; i += blockDim.x) all_counts[i] = __ldcg(block_counts + i);
+  __syncthreads();
+  if (tid < E) {
+    int before = 0, total = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      const int c = all_counts[b * E + tid];
+      if (b < (int)blockIdx.x) before += c;
+      total += c;
+    }
+    cnt[tid] = total;
+    base[tid] = before;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int tiles = 0;
+    for (int ex = 0; ex < E; ++ex) {
+      if (blockIdx.x == 0) tile_offsets[ex] = tiles;
+      base[ex] += tiles * kRowTile;
+      tiles += (cnt[ex] + kRowTile - 1) / kRowTile;
+    }
+    if (blockIdx.x == 0) tile_offsets[E] = tiles;
+  }
+  __syncthreads();
+  for (int64_t q0 = p0; q0 < p1; q0 += blockDim.x) {
+    const int64_t p = q0 + tid;
+    int e = 0, s = 0;
+    int64_t t = 0;
+    const bool in_range = p < p1;
+    const bool valid = in_range && pair_of(p, k, ids, active, 1, e, t, s);
+    // rank in pair order within this stride: warp match ranks + per-warp prefixes
+    for (int i = tid; i < 32 * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
+    __syncthreads();
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : -1);
+    const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
+    if (valid && rank_in_warp == 0) wcnt[warp][e] = __popc(peers);
+    __syncthreads();
+    if (tid < E) {
+      int acc = 0;
+      for (int w = 0; w < 32; ++w) { const int c = wcnt[w][tid]; wcnt[w][tid] = acc; acc += c; }
+      stride_tot[tid] = acc;
+    }
+    __syncthreads();
+    if (in_range) pos[p] = valid ? base[e] + wcnt[warp][e] + rank_in_warp : -1;
+    __syncthreads();
+    if (tid < E) base[tid] += stride_tot[tid];   // running bases for the next stride
+    __syncthreads();
+  }
+  grid_barrier(bar);
+  // phase 3: row gather by every warp of the grid, one pair per warp iteration
+  const int vec = hp / 8;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; q < P; q += warps_total) {
+    const int d = __ldcg(pos + q);
+    if (d < 0) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(u16 + (q / k) * hp);
+    uint4* out = reinterpret_cast<uint4*>(x_perm + (int64_t)d * hp);
+    uint4 v[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) if (lane + 32 * j < vec) v[j] = src[lane + 32 * j];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) if (lane + 32 * j < vec) out[lane + 32 * j] = v[j];
+    for (int c = lane + 160; c < vec; c += 32) out[c] = src[c];
+  }
+}
+
 // Row gather x_perm[pos[t, s]] = u16[t]: one warp per (token, slot) pair,
 // 16-byte vector copies, grid over all pairs.
 __global__ void __launch_bounds__(256) permute_gather_kernel(
     const int32_t* __restrict__ pos, int64_t pairs, const uint16_t* __restrict__ u16, int k,
     int hp, uint16_t* __restrict__ x_perm) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int vec = hp / 8;
   for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < pairs;
@@ -642,6 +797,7 @@ __global__ void __launch_bounds__(256) cache_assemble_kernel(
     const float* __restrict__ gates, const int32_t* __restrict__ ids, int64_t n, int k, int hp,
     uint16_t* cache_rows, float* cache_gates, int32_t* cache_ids, float* routed, float* rows_out,
     float* gates_out) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int vec = hp / 8;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
@@ -713,6 +869,7 @@ __global__ void __launch_bounds__(256) cache_assemble_kernel(
 __global__ void combine_kernel(const float* __restrict__ base, const float* __restrict__ rows,
                                const float* __restrict__ gates, const float* __restrict__ residual,
                                int64_t n, int k, int hp, float* out, __nv_bfloat16* out16) {
+  pdl_enter();
   const int vec = hp / 4;
   const int64_t total = n * vec;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -741,6 +898,7 @@ __global__ void combine_kernel(const float* __restrict__ base, const float* __re
 // ---------------------------------------------------------------- denoise
 __global__ void denoise_kernel(float* x, __nv_bfloat16* x16, const float* __restrict__ y, float eta,
                                int64_t count4, int32_t* status, int step) {
+  pdl_enter();
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -760,6 +918,7 @@ __global__ void denoise_kernel(float* x, __nv_bfloat16* x16, const float* __rest
 
 __global__ void pack_rows_kernel(const float* __restrict__ in, int64_t n, int cols, int64_t ld_in,
                                  int hp, float* out32, __nv_bfloat16* out16) {
+  pdl_enter();
   const int64_t total = n * hp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -797,14 +956,14 @@ int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, 
     cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (groups + 1), s);
     return launch_ok();
   }
-  permute_count_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, groups,
+  launch_pdl(permute_count_kernel, dim3(blocks), dim3(kPermBlock), 0, s, ids, active, n, k, groups,
                                                      reinterpret_cast<long long*>(counters), devices,
                                                      row0, rows_total, scratch, key_div,
                                                      experts_total);
-  permute_scatter_kernel<<<blocks, kPermBlock, 0, s>>>(ids, active, n, k, groups, pos, scratch,
+  launch_pdl(permute_scatter_kernel, dim3(blocks), dim3(kPermBlock), 0, s, ids, active, n, k, groups, pos, scratch,
                                                        tile_offsets, key_div, row_tile);
   if (x_perm != nullptr)
-    permute_gather_kernel<<<grid_for(P * 32, 256), 256, 0, s>>>(pos, P, rows, k, hp, x_perm);
+    launch_pdl(permute_gather_kernel, dim3(grid_for(P * 32, 256)), dim3(256), 0, s, pos, P, rows, k, hp, x_perm);
   return launch_ok();
 }
 
@@ -882,7 +1041,7 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
       return e != nullptr ? atoi(e) : 2;
     }();
 #define DICE_GATE_FAST(EE, CC, MB)                                                             \
-    gate_topk_fast_kernel<EE, CC, MB><<<grid, 256, 0, s>>>(u, w_gate_t, n, hp, k, ids, gates,  \
+    launch_pdl(gate_topk_fast_kernel<EE, CC, MB>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids, gates,  \
                                                            scores, status, step, layer, d)
 #define DICE_GATE_FAST_MB(EE, CC)                                                              \
     {                                                                                          \
@@ -908,7 +1067,7 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
                            200 * 1024);                                                        \
       attr = true;                                                                             \
     }                                                                                          \
-    gate_topk_kernel<EM><<<grid, threads, smem, s>>>(u, w_gate_t, n, hp, E, k, ids, gates,     \
+    launch_pdl(gate_topk_kernel<EM>, dim3(grid), dim3(threads), smem, s, u, w_gate_t, n, hp, E, k, ids, gates,     \
                                                      scores, status, step, layer);             \
   }
   if (E <= 8) DICE_GATE(8)
@@ -916,7 +1075,7 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
   else DICE_GATE(64)
 #undef DICE_GATE
   if (d.on) {
-    cond_decide_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, n, k, d);
+    launch_pdl(cond_decide_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, ids, n, k, d);
   }
   return launch_ok();
 }
@@ -951,7 +1110,7 @@ int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, 
   if (n == 0) return DICE_OK;
   const DecideArgs d{1, step, force, refresh_interval, strategy, strict, random_key, last_refresh,
                      primed, reduced, cached_ids, active, write};
-  cond_decide_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(ids, n, k, d);
+  launch_pdl(cond_decide_kernel, dim3(grid_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, ids, n, k, d);
   return launch_ok();
 }
 
@@ -997,10 +1156,10 @@ int dice_gate_finish(const float* parts, int P, int64_t n, int E, int k, int32_t
   // one token per thread, small blocks so every SM gets some
   const int grid = grid_for(n, 64);
   if (E == 8)
-    gate_parts_kernel<8><<<grid, 64, 0, (cudaStream_t)stream>>>(parts, P, n, k, ids, gates, scores,
+    launch_pdl(gate_parts_kernel<8>, dim3(grid), dim3(64), 0, (cudaStream_t)stream, parts, P, n, k, ids, gates, scores,
                                                                 status, step, layer, d);
   else
-    gate_parts_kernel<16><<<grid, 64, 0, (cudaStream_t)stream>>>(parts, P, n, k, ids, gates,
+    launch_pdl(gate_parts_kernel<16>, dim3(grid), dim3(64), 0, (cudaStream_t)stream, parts, P, n, k, ids, gates,
                                                                  scores, status, step, layer, d);
   return launch_ok();
 }
@@ -1011,8 +1170,12 @@ int64_t dice_permute_max_rows(int64_t n, int k, int E) {
 }
 
 int64_t dice_permute_scratch_ints(int64_t n, int k, int E) {
+  // three-kernel path: per-1024-pair block counts; single-launch path: per-block
+  // counts of up to kFusedPermMaxBlocks blocks; + 32 ints of grid-barrier state
   const int64_t blocks = (n * k + kPermBlock - 1) / kPermBlock;
-  return (blocks < 1 ? 1 : blocks) * E;
+  const int64_t a = (blocks < 1 ? 1 : blocks) * E;
+  const int64_t b = (int64_t)kFusedPermMaxBlocks * E;
+  return (a > b ? a : b) + 32;
 }
 
 int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
@@ -1022,6 +1185,27 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
   if (E < 1 || E > 64 || k < 1 || hp % 64 != 0 || devices < 1 || E % devices != 0)
     return DICE_ERR_CONTRACT;
   if (max_rows < dice_permute_max_rows(n, k, E)) return DICE_ERR_CONTRACT;
+  // DICE_PERMUTE_FUSED=1: the single-launch permute (measured slower inside the
+  // step than the three kernels: its two grid barriers serialise more than the
+  // launches they save); read per call
+  const char* fe = getenv("DICE_PERMUTE_FUSED");
+  const int mode = fe != nullptr ? atoi(fe) : 0;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t P = n * k;
+  if (mode != 0 && P > 0 && x_perm != nullptr) {
+    int grid = (int)(sms < kFusedPermMaxBlocks ? sms : kFusedPermMaxBlocks);
+    if (grid * E > 32 * 64) grid = (32 * 64) / E;   // all blocks' counts fit the smem stage
+    unsigned* bar = reinterpret_cast<unsigned*>(scratch + dice_permute_scratch_ints(n, k, E) - 32);
+    launch_pdl(route_permute_fused_kernel, dim3(grid), dim3(kFusedPermThreads), 0, (cudaStream_t)stream, 
+        ids, active, n, k, E, u16, hp, x_perm, pos, tile_offsets,
+        reinterpret_cast<long long*>(counters), devices, row0, rows_total, scratch, bar);
+    return launch_ok();
+  }
   return dice::permute_launch(ids, active, n, k, E, 1, kRowTile, E, u16, hp, x_perm, pos,
                               tile_offsets, counters, devices, row0, rows_total, scratch,
                               (cudaStream_t)stream);
@@ -1058,7 +1242,7 @@ int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* ac
   const int grid = grid_for(n * 32, 256);
   cudaStream_t st = (cudaStream_t)stream;
 #define DICE_ASM(KK)                                                                           \
-  cache_assemble_kernel<KK><<<grid, 256, 0, st>>>(y, pos, active, write, gates, ids, n, k, hp, \
+  launch_pdl(cache_assemble_kernel<KK>, dim3(grid), dim3(256), 0, st, y, pos, active, write, gates, ids, n, k, hp, \
                                                   cache_rows, cache_gates, cache_ids, routed,  \
                                                   rows_out, gates_out)
   if (k == 1) DICE_ASM(1);
@@ -1091,7 +1275,7 @@ int dice_combine(const float* base, const float* rows, const float* gates, const
                  int64_t n, int k, int hp, float* out, uint16_t* out_bf16, void* stream) {
   if (hp % 4 != 0) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
-  combine_kernel<<<grid_for(n * (hp / 4), 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(combine_kernel, dim3(grid_for(n * (hp / 4), 256)), dim3(256), 0, (cudaStream_t)stream, 
       base, rows, gates, residual, n, k, hp, out, reinterpret_cast<__nv_bfloat16*>(out_bf16));
   return launch_ok();
 }
@@ -1101,7 +1285,7 @@ int dice_denoise(float* x, uint16_t* x16, const float* y, float eta, int64_t n, 
   if (hp % 4 != 0) return DICE_ERR_CONTRACT;
   const int64_t c4 = n * hp / 4;
   if (c4 == 0) return DICE_OK;
-  denoise_kernel<<<grid_for(c4, 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(denoise_kernel, dim3(grid_for(c4, 256)), dim3(256), 0, (cudaStream_t)stream, 
       x, reinterpret_cast<__nv_bfloat16*>(x16), y, eta, c4, status, step);
   return launch_ok();
 }

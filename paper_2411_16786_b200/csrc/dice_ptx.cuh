@@ -6,7 +6,51 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace dice {
+
+// ------------------------------------------- programmatic dependent launch
+// Every kernel starts with pdl_enter(): griddepcontrol.wait blocks until the
+// stream predecessor grid has completed and its writes are visible (a no-op
+// for a normal launch), then launch_dependents lets the stream successor be
+// scheduled early, so kernel-boundary launch latency overlaps this kernel.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DICE_PDL");   // DICE_PDL=0: plain stream-ordered launches
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
+// Launch with the programmatic-stream-serialization attribute (captured into
+// CUDA graphs as programmatic edges). The kernel must call pdl_enter/pdl_wait
+// before touching memory its predecessor writes or reads.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

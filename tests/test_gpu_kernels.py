@@ -278,3 +278,51 @@ print('ok')
         r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,k,E,devices,masked", [(8192, 2, 8, 1, True), (8192, 2, 8, 4, False),
+                                                  (1000, 3, 16, 2, True), (37, 2, 8, 1, False),
+                                                  (32768, 2, 16, 8, True)])
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_route_permute_single_launch(n, k, E, devices, masked, fused, monkeypatch):
+    """The single-launch permute (count -> grid barrier -> positions -> grid
+    barrier -> gather) against a numpy restatement of the grouping: pairs of
+    an expert in pair order t*k+s, experts padded to 256-row tiles, inactive
+    pairs -1, byte-plan counters (cluster.py:75-90); repeated launches reuse
+    the barrier state. Both the three-kernel path and the single launch
+    (DICE_PERMUTE_FUSED=1, read per call) are checked."""
+    monkeypatch.setenv("DICE_PERMUTE_FUSED", fused)
+    hp = 128
+    g = torch.Generator(device=dev).manual_seed(n + k + E)
+    ids = torch.randint(0, E, (n, k), dtype=torch.int32, device=dev, generator=g)
+    active = (torch.rand(n, k, device=dev, generator=g) > 0.3).to(torch.uint8) if masked else None
+    u16 = torch.randn(n, hp, device=dev, generator=g).to(torch.bfloat16)
+    max_rows = ops.permute_max_rows(n, k, E)
+    scratch = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+    idn = ids.cpu().numpy().reshape(-1)
+    act = np.ones(n * k, bool) if active is None else active.cpu().numpy().reshape(-1).astype(bool)
+    pos_ref = np.full(n * k, -1, np.int64)
+    tiles, base = [0], 0
+    for e in range(E):
+        sel = np.nonzero((idn == e) & act)[0]
+        pos_ref[sel] = base + np.arange(len(sel))
+        nt = (len(sel) + 255) // 256
+        base += nt * 256
+        tiles.append(tiles[-1] + nt)
+    homes = (np.arange(n) * devices) // n
+    t_of = np.arange(n * k) // k
+    remote = act & (homes[t_of] != idn // (E // devices))
+    for rep in range(3):
+        x_perm = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
+        pos = torch.empty(n, k, dtype=torch.int32, device=dev)
+        tile_off = torch.empty(E + 1, dtype=torch.int32, device=dev)
+        counters = torch.zeros(2, dtype=torch.int64, device=dev)
+        ops.route_permute(ids, active, u16, x_perm, pos, tile_off, counters, scratch, E,
+                          devices=devices, row0=0, rows_total=n)
+        torch.cuda.synchronize()
+        assert np.array_equal(pos.cpu().numpy().reshape(-1), pos_ref)
+        assert tile_off.cpu().tolist() == tiles
+        assert counters.cpu().tolist() == [int(act.sum()), int(remote.sum())]
+        v = pos_ref >= 0
+        assert torch.equal(x_perm[torch.as_tensor(pos_ref[v], device=dev)],
+                           u16[torch.as_tensor(t_of[v], device=dev)])
