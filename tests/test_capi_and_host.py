@@ -45,7 +45,10 @@ def test_permute_sizing_helpers():
     lib = _lib.load()
     rows = lib.dice_permute_max_rows(8192, 2, 8)
     assert rows % 256 == 0 and rows >= 8192 * 2 + 8 * 255
-    assert lib.dice_permute_scratch_ints(8192, 2, 8) == 16 * 8
+    # per-block counts of the three-kernel path (16 blocks of 1024 pairs) or of the
+    # single-launch path (<= 160 blocks), whichever is larger, + 32 barrier ints
+    assert lib.dice_permute_scratch_ints(8192, 2, 8) == max(16 * 8, 160 * 8) + 32
+    assert lib.dice_permute_scratch_ints(1 << 20, 2, 8) == 2048 * 8 + 32
 
 
 def test_missing_library_fails_loudly(monkeypatch, tmp_path):
