@@ -522,7 +522,6 @@ template <int BN, int EPI, bool DIRECT, int NSUB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const GemmArgs args) {
-  pdl_enter();
   using C = PairCfg<BN, DIRECT, NSUB>;
   constexpr int TN = C::kTN;
   const int kStages = args.stages;   // <= C::kStages (host-clamped)
@@ -538,10 +537,17 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
 
+  // prologue before the programmatic-dependency wait: it touches no memory the
+  // stream predecessor writes, so under PDL it overlaps that kernel's tail
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&sh->full[s], 2); mbar_init(&sh->empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 2 * kEpiWarps); }
     fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 2) tmem_alloc_pair<C::kTmemCols>(&sh->tmem_base);
+  pdl_wait();
+  if (threadIdx.x == 0) {
     if (args.group_tile_offsets != nullptr) {
       for (int g = 0; g <= args.num_groups; ++g) sh->group_off[g] = args.group_tile_offsets[g];
       sh->m_tiles = sh->group_off[args.num_groups];
@@ -551,11 +557,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       sh->m_tiles = args.num_m_tiles;
     }
   }
-  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
-  if (warp == 2) tmem_alloc_pair<C::kTmemCols>(&sh->tmem_base);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  pdl_trigger();
 
   const uint32_t tmem_base = sh->tmem_base;
   const int m_tiles = sh->m_tiles;  // 256-row tiles

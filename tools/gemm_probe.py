@@ -59,6 +59,14 @@ if __name__ == "__main__":
     bench(16384, 4608, 1152, 1, label="expert GEMM1 (dense eq.)")
     bench(16384, 4608, 1152, 0, label="expert GEMM1 no-GELU")
     bench(16384, 1152, 4608, 0, label="expert GEMM2 (dense eq.)")
+    if "--local" in __import__("sys").argv:
+        for epi in (0, 2, 3):
+            bench(8192, 1152, 1152, epi, label=f"local shape epi={epi}")
+        for M in (2048, 4096, 16384, 32768):
+            bench(M, 1152, 1152, 0, label=f"M={M} epi=0")
+        bench(8192, 4608, 1152, 0, label="8192x4608x1152 epi=0")
+        bench(8192, 1152, 2304, 0, label="8192x1152x2304 epi=0")
+        raise SystemExit
     if "--bn" in __import__("sys").argv:
         bench(16384, 4608, 4608, 0, label="16k x 4608 x 4608")
         bench(16384, 4608, 1152, 0, label="16k x 4608 x 1152")
