@@ -175,6 +175,8 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
                       (cache-row writes of refreshed pairs not counted: a lower bound)
       denoise         14Rh
       local_gemm      2Rh^2;  shared_gemm1 / shared_gemm2_consume 2RhSe each;  grouped_ffn 4heP
+      (grouped_ffn+shared_gemm1: the expert FFN launches that also carry the stage's
+       shared GEMM1, 4heP + 2RhSe)
     """
     import torch
     r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed, time_ops=True,
@@ -208,6 +210,8 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
             work, kind = 2.0 * R * h * S * e, "tensor"
         elif name == "grouped_ffn":
             work, kind = 4.0 * h * e * P, "tensor"
+        elif name == "grouped_ffn+shared_gemm1":
+            work, kind = 4.0 * h * e * P + 2.0 * R * h * S * e, "tensor"
         else:
             continue
         a = agg.setdefault(name, [0.0, 0, 0.0, kind])
@@ -315,9 +319,14 @@ def run_gpu(args):
     pair_flops = 4.0 * h * e
     # pairs each launch processed; under EP the active pairs of (step, layer) are
     # summed over ranks and spread evenly over the N expert ranks
-    flops = sum(pair_flops * cnt[gen, layer, 0] / world for _, _, gen, layer in expert_events)
+    # (when the stage's shared-expert GEMM1 rides in the same launch, its
+    # 2*R*h*S*e FLOPs are counted too: the bracket then times both)
+    shared_flops = 2.0 * cfg.total_rows / world * h * cfg.num_shared * e
+    flops = sum(pair_flops * cnt[ev[2], ev[3], 0] / world
+                + (shared_flops if len(ev) > 4 and ev[4] else 0.0) for ev in expert_events)
+    merged_launches = sum(1 for ev in expert_events if len(ev) > 4 and ev[4])
     # the event pairs sit inside the captured graph: they hold the last timed replay
-    t_exp = sum(a.elapsed_ms(b) for a, b, _, _ in expert_events) * 1e-3
+    t_exp = sum(ev[0].elapsed_ms(ev[1]) for ev in expert_events) * 1e-3
     n_launch = len(expert_events)
     achieved = flops / t_exp / 1e12
     peak_tf, _, peak_kind = peaks()
@@ -392,12 +401,13 @@ def run_gpu(args):
                    "l2": "inputs larger than L2: 6.0 GB of bf16 weights streamed per denoising step"},
         "moe_layer_us": ms_per_step * 1e3 / (cfg.num_steps * cfg.num_layers),
         "exposed_a2a_us": exposed_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
-        "roofline": {"bound": "tensor", "kernel": "grouped expert FFN (tcgen05 GEMM1+GELU, GEMM2)",
+        "roofline": {"bound": "tensor", "kernel": "grouped expert FFN (tcgen05 GEMM1+GELU, GEMM2; the stage's shared-expert GEMM1 shares the GEMM1 launch)",
                      "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per grouped-FFN launch pair (ncu --set full)",
                      "peak_kind": f"{peak_kind} bf16 sustained",
                      "launches": n_launch, "flops_per_pair": pair_flops,
+                     "launches_with_shared_gemm1": merged_launches,
                      "share_of_step": t_exp / (ms_per_step / 1e3)},
         "e2e": {"value": e2e, "unit": "img/s",
                 "h2d_bytes_per_step": int(x0_host.numel() * 4),

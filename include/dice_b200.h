@@ -186,6 +186,18 @@ int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, i
               const float* residual, int64_t ld_res, const float* addend, int64_t ld_add,
               void* stream);
 
+/* The two halves of dice_grouped_ffn, the first merged with a dense GELU GEMM
+ * of the same K in ONE persistent launch: hbuf = gelu(x_perm W1_e) over the
+ * expert tiles AND out2 [M2, N2] = gelu(A2 B2^T) (the stage's shared-expert
+ * GEMM1, shared_forward model.py:235-241, A2 = u bf16 [M2, hp], B2 = ws1_t);
+ * then y = hbuf W2_e (expert_forward model.py:226-232). */
+int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
+                                 int E, int hp, int ep, const int32_t* tile_offsets,
+                                 uint16_t* hbuf, const uint16_t* A2, int64_t M2,
+                                 const uint16_t* B2, int N2, uint16_t* out2, void* stream);
+int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
+                      int ep, const int32_t* tile_offsets, uint16_t* y, void* stream);
+
 /* out[t] = base[t] + sum_s gates[t, s] * rows[s, t] (f32, combine_outputs
  * model.py:279-298 and the consume residual, schedules.py:317). rows f32
  * [k, n, hp]; base f32 [n, hp]; optional residual adds u first:

@@ -521,7 +521,11 @@ __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_
 template <int BN, int EPI, bool DIRECT, int NSUB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const GemmArgs args) {
+               const GemmArgs args, const __grid_constant__ CUtensorMap tmA2,
+               const __grid_constant__ CUtensorMap tmB2, const GemmArgs args2) {
+  // args2.num_m_tiles > 0: a second, dense problem with the same K and epilogue
+  // kind runs in the same persistent launch; its tiles follow the first's
+  // (one launch and one wave tail for two independent GEMMs)
   using C = PairCfg<BN, DIRECT, NSUB>;
   constexpr int TN = C::kTN;
   const int kStages = args.stages;   // <= C::kStages (host-clamped)
@@ -544,7 +548,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 2 * kEpiWarps); }
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB);
+    if (args2.num_m_tiles > 0) { tma_prefetch_desc(&tmA2); tma_prefetch_desc(&tmB2); }
+  }
   if (warp == 2) tmem_alloc_pair<C::kTmemCols>(&sh->tmem_base);
   pdl_wait();
   if (threadIdx.x == 0) {
@@ -567,7 +574,14 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int groups = args.group_tile_offsets != nullptr ? args.num_groups : 1;
   const int n_blocks = args.num_n_blocks;
   const int k_blocks = args.num_k_blocks;
-  const int num_tiles = m_tiles * n_blocks;
+  const int T1 = m_tiles * n_blocks;
+  const int n_blocks2 = args2.num_n_blocks;
+  const int num_tiles = T1 + (args2.num_m_tiles > 0 ? args2.num_m_tiles * n_blocks2 : 0);
+  // tile -> (problem, n block, m tile); N-fastest within each problem
+  auto locate = [&](int tile, int& prob, int& n_blk, int& m_tile) {
+    if (tile < T1) { prob = 0; n_blk = tile % n_blocks; m_tile = tile / n_blocks; }
+    else { prob = 1; const int t2 = tile - T1; n_blk = t2 % n_blocks2; m_tile = t2 / n_blocks2; }
+  };
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
   SkPlan plan;
@@ -584,18 +598,20 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int it = 0; it < n_items; ++it) {
         int tile, k0, k1, slot;
         plan.item(pair, it, tile, k0, k1, slot);
-        const int n_blk = tile % n_blocks;   // N-fastest: resident tiles share A rows
-        const int m_tile = tile / n_blocks;
-        const int g = find_group(sh->group_off, groups, m_tile);
+        int prob, n_blk, m_tile;   // N-fastest: resident tiles share A rows
+        locate(tile, prob, n_blk, m_tile);
+        const int g = prob == 0 ? find_group(sh->group_off, groups, m_tile) : 0;
         const int a_row = m_tile * kPairM + rank * BM;
-        const int b_row = g * args.N + n_blk * TN + rank * (BN / 2);
+        const int b_row = g * (prob == 0 ? args.N : args2.N) + n_blk * TN + rank * (BN / 2);
+        const CUtensorMap* mA = prob == 0 ? &tmA : &tmA2;
+        const CUtensorMap* mB = prob == 0 ? &tmB : &tmB2;
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0), C::kStageBytes);
-          tma_load_2d_pair(smA + stage * C::kABytes, &tmA, &sh->full[stage], kb * BK, a_row);
+          tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
 #pragma unroll
           for (int sub = 0; sub < NSUB; ++sub)
-            tma_load_2d_pair(smB + stage * C::kBBytes + sub * C::kSubBBytes, &tmB, &sh->full[stage],
+            tma_load_2d_pair(smB + stage * C::kBBytes + sub * C::kSubBBytes, mB, &sh->full[stage],
                              kb * BK, b_row + sub * BN);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -644,8 +660,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     for (int local = 0; local < n_items; ++local) {
       int tile, k0, k1, slot;
       plan.item(pair, local, tile, k0, k1, slot);
-      const int n_blk = tile % n_blocks;
-      const int m_tile = tile / n_blocks;
+      int prob, n_blk, m_tile;
+      locate(tile, prob, n_blk, m_tile);
+      const GemmArgs& ar = prob == 0 ? args : args2;
+      const int rl = prob == 0 ? row_limit : args2.M_valid;
       const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
       const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
       mbar_wait(&sh->tfull[acc], acc_phase);
@@ -673,10 +691,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * TN + col_in_tile, r);
         tmem_ld_wait();
-        if (col0 >= args.N) continue;  // warp-uniform
+        if (col0 >= ar.N) continue;  // warp-uniform
         if constexpr (DIRECT) {   // (the host never enables stream-K for DIRECT)
           const int64_t row = row0 + lane;
-          if (row < row_limit) epilogue_direct<EPI>(args, r, row, col0);
+          if (row < rl) epilogue_direct<EPI>(ar, r, row, col0);
           continue;
         }
 #pragma unroll
@@ -699,9 +717,9 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (csplit < args.ksplit - 1)
             chain_store(stage, lane, cws, TN, rank * BM + sub * 32, col_in_tile);
           else
-            epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
+            epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         } else {
-          epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
+          epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         }
         __syncwarp();
       }
@@ -908,7 +926,8 @@ int chain_workspace(cudaStream_t stream, int tiles, int tile_n, float** ws, unsi
 
 template <int BN, int EPI, bool DIRECT, int NSUB = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
-                cudaStream_t stream) {
+                cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
+                const CUtensorMap* tb2 = nullptr, const GemmArgs* a2 = nullptr) {
   using C = PairCfg<BN, DIRECT, NSUB>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -917,7 +936,8 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
       return DICE_ERR_CUDA;
     attr_done = true;
   }
-  const int items = max_tiles * (a.ksplit > 1 ? a.ksplit : 1);
+  const int items = max_tiles * (a.ksplit > 1 ? a.ksplit : 1) +
+                    (a2 != nullptr ? a2->num_m_tiles * a2->num_n_blocks : 0);
   static const int cta_cap = env_int("DICE_GEMM_MAX_CTAS", 1 << 30);   // experiment hook
   const int sms = num_sms() < cta_cap ? num_sms() : cta_cap;
   int grid = 2 * items < sms ? 2 * items : sms;
@@ -936,7 +956,14 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
   static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
   aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
-  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ta, tb, aa);
+  GemmArgs bb{};
+  if (a2 != nullptr) {
+    if (aa.ksplit > 1 || aa.sk_workspace != nullptr || EpiTraits<EPI>::gate_e > 0)
+      return DICE_ERR_CONTRACT;
+    bb = *a2;
+  }
+  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
+             ta, tb, aa, a2 != nullptr ? *ta2 : ta, a2 != nullptr ? *tb2 : tb, bb);
   if (aa.sk_workspace != nullptr)
     launch_pdl(stream_k_fixup_kernel<EPI>, dim3(num_sms() * 2), dim3(256), 0, stream, aa, aa.sk_workspace, BN, grid / 2);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
@@ -1070,29 +1097,39 @@ int gemm_gate_parts(const GemmProblem& p) {
   return ((p.N + c.tile_n - 1) / c.tile_n) * kEpiGroups;
 }
 
-int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
+namespace {
+// tensor maps + kernel arguments of one problem for its tile choice
+int prepare(const GemmProblem& p, const TileChoice& tc, CUtensorMap* ta, CUtensorMap* tb,
+            GemmArgs* a) {
   if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
   if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
-  const TileChoice tc = choose_tile(p);
-  const int bn = tc.bn, tile_n = tc.tile_n;
-  const bool pair = tc.pair, wide = tc.wide;
+  const int tile_m = tc.pair ? 2 * BM : BM;
+  int rc = tensor_map(p.A, p.A_rows, p.K, BM, ta);
+  if (rc) return rc;
+  rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, tc.pair ? tc.bn / 2 : tc.bn, tb);
+  if (rc) return rc;
+  *a = p.epi;
+  a->M_valid = p.M;
+  a->N = p.N;
+  a->K = p.K;
+  a->num_n_blocks = (p.N + tc.tile_n - 1) / tc.tile_n;
+  a->num_k_blocks = (p.K + BK - 1) / BK;
+  a->group_tile_offsets = p.group_tile_offsets;
+  a->num_groups = p.num_groups;
+  a->num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + tile_m - 1) / tile_m;
+  a->ksplit = tc.ksplit;
+  return 0;
+}
+}  // namespace
 
-  const int tile_m = pair ? 2 * BM : BM;
+int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
+  const TileChoice tc = choose_tile(p);
+  const int bn = tc.bn;
+  const bool pair = tc.pair, wide = tc.wide;
   CUtensorMap ta, tb;
-  int rc = tensor_map(p.A, p.A_rows, p.K, BM, &ta);
+  GemmArgs a;
+  int rc = prepare(p, tc, &ta, &tb, &a);
   if (rc) return rc;
-  rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, pair ? bn / 2 : bn, &tb);
-  if (rc) return rc;
-  GemmArgs a = p.epi;
-  a.M_valid = p.M;
-  a.N = p.N;
-  a.K = p.K;
-  a.num_n_blocks = (p.N + tile_n - 1) / tile_n;
-  a.num_k_blocks = (p.K + BK - 1) / BK;
-  a.group_tile_offsets = p.group_tile_offsets;
-  a.num_groups = p.num_groups;
-  a.num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + tile_m - 1) / tile_m;
-  a.ksplit = tc.ksplit;
   const int max_tiles = a.num_m_tiles * a.num_n_blocks;
   if (max_tiles == 0) return 0;
   if (wide) return dispatch_wide(p.epi_kind, ta, tb, a, max_tiles, stream);
@@ -1104,6 +1141,41 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   if (bn == 256) return dispatch_epi<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
   if (bn == 192) return dispatch_epi<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
   return dispatch_epi<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
+}
+
+// Two independent GEMMs with the same K and bf16-only epilogue kind in ONE
+// persistent launch (p1 may be grouped, p2 dense): the grouped expert GEMM1
+// and the shared-expert GEMM1 of a stage. Falls back to two launches when the
+// tile choices differ (or DICE_GEMM_DUAL=0).
+int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t stream) {
+  static const int dual_mode = env_int("DICE_GEMM_DUAL", 1);
+  const TileChoice c1 = choose_tile(p1), c2 = choose_tile(p2);
+  static const bool direct = env_int("DICE_GEMM_EPI_DIRECT", 1) != 0;
+  const bool ok = dual_mode != 0 && direct && p1.K == p2.K && p1.epi_kind == p2.epi_kind &&
+                  (p1.epi_kind == EPI_STORE_BF16 || p1.epi_kind == EPI_GELU_BF16) &&
+                  p2.group_tile_offsets == nullptr && c1.pair && c2.pair && !c1.wide &&
+                  !c2.wide && c1.bn == c2.bn && c1.ksplit == 1 && c2.ksplit == 1 &&
+                  (c1.bn == 256 || c1.bn == 192);
+  if (!ok) {
+    const int rc = gemm_bf16(p1, stream);
+    return rc ? rc : gemm_bf16(p2, stream);
+  }
+  CUtensorMap ta1, tb1, ta2, tb2;
+  GemmArgs a1, a2;
+  int rc = prepare(p1, c1, &ta1, &tb1, &a1);
+  if (rc) return rc;
+  rc = prepare(p2, c2, &ta2, &tb2, &a2);
+  if (rc) return rc;
+  const int t1 = a1.num_m_tiles * a1.num_n_blocks;
+  if (a2.num_m_tiles * a2.num_n_blocks == 0) return gemm_bf16(p1, stream);
+  if (c1.bn == 256) {
+    return p1.epi_kind == EPI_GELU_BF16
+               ? launch_pair<256, EPI_GELU_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2)
+               : launch_pair<256, EPI_STORE_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2);
+  }
+  return p1.epi_kind == EPI_GELU_BF16
+             ? launch_pair<192, EPI_GELU_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2)
+             : launch_pair<192, EPI_STORE_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2);
 }
 
 }  // namespace dice

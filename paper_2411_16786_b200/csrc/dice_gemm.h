@@ -80,6 +80,8 @@ struct GemmProblem {
 };
 
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream);
+// two independent problems (same K, bf16-only epilogue) in one persistent launch
+int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t stream);
 // number of partial-logit slots a GATE epilogue writes for this problem
 int gemm_gate_parts(const GemmProblem& p);
 

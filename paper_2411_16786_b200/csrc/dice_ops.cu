@@ -1211,6 +1211,39 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
                               (cudaStream_t)stream);
 }
 
+int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
+                                 int E, int hp, int ep, const int32_t* tile_offsets,
+                                 uint16_t* hbuf, const uint16_t* A2, int64_t M2,
+                                 const uint16_t* B2, int N2, uint16_t* out2, void* stream) {
+  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0 ||
+      M2 < 0 || M2 > INT_MAX || N2 % 64 != 0)
+    return DICE_ERR_CONTRACT;
+  GemmProblem p{};
+  p.A = x_perm; p.A_rows = max_rows; p.B = w1_t; p.M = (int)max_rows; p.N = ep; p.K = hp;
+  p.num_groups = E; p.group_tile_offsets = tile_offsets; p.max_m_tiles = (int)(max_rows / kRowTile);
+  p.epi_kind = EPI_GELU_BF16;
+  p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(hbuf); p.epi.ld_bf16 = ep;
+  GemmProblem q{};
+  q.A = A2; q.A_rows = M2; q.B = B2; q.M = (int)M2; q.N = N2; q.K = hp;
+  q.num_groups = 1; q.group_tile_offsets = nullptr; q.max_m_tiles = 0;
+  q.epi_kind = EPI_GELU_BF16;
+  q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out2); q.epi.ld_bf16 = N2;
+  if (M2 == 0) return gemm_bf16(p, (cudaStream_t)stream);
+  return gemm_bf16_dual(p, q, (cudaStream_t)stream);
+}
+
+int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
+                      int ep, const int32_t* tile_offsets, uint16_t* y, void* stream) {
+  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0)
+    return DICE_ERR_CONTRACT;
+  GemmProblem q{};
+  q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
+  q.num_groups = E; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / kRowTile);
+  q.epi_kind = EPI_STORE_BF16;
+  q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(y); q.epi.ld_bf16 = hp;
+  return gemm_bf16(q, (cudaStream_t)stream);
+}
+
 int dice_grouped_ffn(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
                      const uint16_t* w2_t, int E, int hp, int ep, const int32_t* tile_offsets,
                      uint16_t* hbuf, uint16_t* y, void* stream) {

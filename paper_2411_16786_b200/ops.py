@@ -173,6 +173,23 @@ def grouped_ffn(x_perm, w1_t, w2_t, E, tile_offsets, hbuf, y):
               _ptr(tile_offsets), _ptr(hbuf), _ptr(y), _stream())
 
 
+def expert_gemm1_with_shared(x_perm, w1_t, E, tile_offsets, hbuf, u16, ws1_t, hsh):
+    """Grouped expert GEMM1 (+GELU) and the shared experts' GEMM1 (+GELU) in
+    one persistent launch (dice_expert_gemm1_with_dense)."""
+    max_rows, hp = x_perm.shape
+    ep = hbuf.shape[1]
+    _lib.call("dice_expert_gemm1_with_dense", _ptr(x_perm), max_rows, _ptr(w1_t), E, hp, ep,
+              _ptr(tile_offsets), _ptr(hbuf), _ptr(u16), u16.shape[0], _ptr(ws1_t), ws1_t.shape[0],
+              _ptr(hsh), _stream())
+
+
+def expert_gemm2(hbuf, w2_t, E, tile_offsets, y):
+    max_rows, ep = hbuf.shape
+    hp = y.shape[1]
+    _lib.call("dice_expert_gemm2", _ptr(hbuf), max_rows, _ptr(w2_t), E, hp, ep, _ptr(tile_offsets),
+              _ptr(y), _stream())
+
+
 def cache_assemble(y, pos, active, write, gates, ids, routed, cache_rows=None, cache_gates=None,
                    cache_ids=None, rows_out=None, gates_out=None):
     n, k = pos.shape

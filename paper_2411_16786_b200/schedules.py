@@ -218,6 +218,11 @@ class DeviceRunner:
         self.side = None
         if overlap and strategy is Strategy.INTERWEAVED and str(dev).startswith("cuda") and not timeline:
             self.side = torch.cuda.Stream(device=dev)
+        # the processed dispatch's expert GEMM1 and the stage's shared-expert GEMM1
+        # are independent: one persistent launch for both (DICE_MERGE_GEMM1=0 off)
+        self.merge_gemm1 = (S > 0 and self.side is None
+                            and strategy in (Strategy.SYNCHRONOUS, Strategy.INTERWEAVED)
+                            and os.environ.get("DICE_MERGE_GEMM1", "1") != "0")
 
     # ------------------------------------------------------------ helpers
     def _reset_state(self, x0_device=None):
@@ -336,7 +341,7 @@ class DeviceRunner:
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 
-    def _process(self, p: _Payload, side: bool = False):
+    def _process(self, p: _Payload, side: bool = False, shared_layer=None):
         """Expert FFN on a dispatched payload + stale-cache merge into its
         combine slot (_process_dispatch, schedules.py:388-397). With side=True
         the work is enqueued on the side stream after the payload's dispatch."""
@@ -345,7 +350,7 @@ class DeviceRunner:
             ready.record()
             self.side.wait_event(ready)
             with torch.cuda.stream(self.side):
-                self._process_body(p)
+                self._process_body(p, shared_layer)
                 done = torch.cuda.Event()
                 done.record()
             p.done = done
@@ -353,7 +358,7 @@ class DeviceRunner:
             self.side_tail = done
             return
         self._join_side()
-        self._process_body(p)
+        self._process_body(p, shared_layer)
 
     def _join_side(self):
         """Main stream waits for all side-stream work (shared expert scratch)."""
@@ -361,7 +366,9 @@ class DeviceRunner:
             torch.cuda.current_stream().wait_event(self.side_tail)
             self.side_tail = None
 
-    def _process_body(self, p: _Payload):
+    def _process_body(self, p: _Payload, shared_layer=None):
+        """shared_layer: also run that layer's shared-expert GEMM1 (u16 -> hsh)
+        inside the expert GEMM1 launch."""
         self._mark(f"expert s{p.gen} L{p.layer}")
         lw = self.model.layers[p.layer]
         if self.time_experts:
@@ -370,11 +377,18 @@ class DeviceRunner:
                 self._event_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
             e0, e1 = self._event_pool[i]
             e0.record()
-        with self._op("grouped_ffn", p.gen, p.layer):
-            ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
+        if shared_layer is None:
+            with self._op("grouped_ffn", p.gen, p.layer):
+                ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
+        else:
+            with self._op("grouped_ffn+shared_gemm1", p.gen, p.layer):
+                ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
+                                             self.u16, self.model.layers[shared_layer].ws1_t,
+                                             self.hsh)
+                ops.expert_gemm2(self.hbuf, lw.w2_t, self.E, p.tiles, self.y)
         if self.time_experts:
             e1.record()
-            self._expert_events.append((e0, e1, p.gen, p.layer))
+            self._expert_events.append((e0, e1, p.gen, p.layer, shared_layer is not None))
         c = self.cache
         with self._op("cache_assemble", p.gen, p.layer):
             ops.cache_assemble(self.y, p.pos, None if c is None else p.active,
@@ -391,15 +405,16 @@ class DeviceRunner:
             self._process(prev, side=side)
             self._track("c", prev.layer)
 
-    def _consume(self, layer, step, gen):
+    def _consume(self, layer, step, gen, gemm1_done=False):
         """u + (shared + routed) fused into the shared-FFN GEMM2 epilogue
         (_consume, schedules.py:308-317; combine_outputs, model.py:279-298)."""
         lw = self.model.layers[layer]
         slot = self._slot(layer)
         self._mark(f"shared+consume s{step} L{layer}")
         if self.S > 0:
-            with self._op("shared_gemm1", step, layer):
-                ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
+            if not gemm1_done:
+                with self._op("shared_gemm1", step, layer):
+                    ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
             with self._op("shared_gemm2_consume", step, layer):
                 ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
                          residual=self.u32, addend=slot)
@@ -449,14 +464,14 @@ class DeviceRunner:
                                                  self.scores.cpu()))
             if sync:
                 self._dispatch(step, layer, p, force=True, decided=decided)
-                self._process(p)
+                self._process(p, shared_layer=layer if self.merge_gemm1 else None)
                 if self.strategy is Strategy.DISPLACED:
                     self.dispatch_slot[layer] = p
                     self._track("d", layer)
                     self._track("c", layer)
                 elif self.strategy is Strategy.INTERWEAVED:
                     self._track("c", layer)
-                self._consume(layer, step, step)
+                self._consume(layer, step, step, gemm1_done=self.merge_gemm1)
             elif self.strategy is Strategy.DISPLACED:
                 self._dispatch(step, layer, p, force=False, decided=decided)
                 old = self.dispatch_slot[layer]
@@ -471,10 +486,11 @@ class DeviceRunner:
             else:
                 self._dispatch(step, layer, p, force=False, decided=decided)
                 prev, self.pending = self.pending, p
+                merged = self.merge_gemm1 and prev is not None
                 if prev is not None:
-                    self._process(prev, side=True)
+                    self._process(prev, side=True, shared_layer=layer if merged else None)
                     self._track("c", prev.layer)
-                self._consume(layer, step, self.slot_gen[layer])
+                self._consume(layer, step, self.slot_gen[layer], gemm1_done=merged)
         self._flush_pending(side=self.strategy is Strategy.INTERWEAVED)
         self._mark(f"denoise s{step}")
         with self._op("denoise", step, -1):
@@ -562,7 +578,7 @@ class DeviceRunner:
             timeline = GpuTimeline(events, device=torch.cuda.current_device())
             gpu_seconds = timeline.makespan() if gpu_seconds is None else gpu_seconds
         elif self._expert_events:
-            timeline = {"expert_ffn_ms": [a.elapsed_ms(b) for a, b, _, _ in self._expert_events]}
+            timeline = {"expert_ffn_ms": [ev[0].elapsed_ms(ev[1]) for ev in self._expert_events]}
         return RunResult(
             final=final, timeline=timeline, staleness_records=self.records,
             strategy=self.strategy, policy=self.policy, seed=self.seed,

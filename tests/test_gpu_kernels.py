@@ -326,3 +326,34 @@ def test_route_permute_single_launch(n, k, E, devices, masked, fused, monkeypatc
         v = pos_ref >= 0
         assert torch.equal(x_perm[torch.as_tensor(pos_ref[v], device=dev)],
                            u16[torch.as_tensor(t_of[v], device=dev)])
+
+
+def test_expert_gemm1_with_shared_dual_launch():
+    """Grouped expert GEMM1 + the dense shared GEMM1 in one persistent launch:
+    bit-identical to the two separate launches (same tiles, same epilogue)."""
+    n, k, E, hp, ep, S = 3000, 2, 8, 1152, 512, 2
+    g = torch.Generator(device=dev).manual_seed(11)
+    ids = torch.randint(0, E, (n, k), dtype=torch.int32, device=dev, generator=g)
+    u16 = (torch.randn(n, hp, device=dev, generator=g) * 0.5).to(torch.bfloat16)
+    w1 = (torch.randn(E * ep, hp, device=dev, generator=g) / 34).to(torch.bfloat16)
+    w2 = (torch.randn(E * hp, ep, device=dev, generator=g) / 23).to(torch.bfloat16)
+    ws1 = (torch.randn(S * ep, hp, device=dev, generator=g) / 34).to(torch.bfloat16)
+    max_rows = ops.permute_max_rows(n, k, E)
+    x_perm = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
+    pos = torch.empty(n, k, dtype=torch.int32, device=dev)
+    tiles = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    scr = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+    ops.route_permute(ids, None, u16, x_perm, pos, tiles, cnt, scr, E)
+    h_a = torch.zeros(max_rows, ep, dtype=torch.bfloat16, device=dev)
+    y_a = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
+    hs_a = torch.zeros(n, S * ep, dtype=torch.bfloat16, device=dev)
+    ops.grouped_ffn(x_perm, w1, w2, E, tiles, h_a, y_a)
+    ops.gemm(ops.EPI_GELU_BF16, u16, ws1, out_bf16=hs_a)
+    h_b, y_b, hs_b = torch.zeros_like(h_a), torch.zeros_like(y_a), torch.zeros_like(hs_a)
+    ops.expert_gemm1_with_shared(x_perm, w1, E, tiles, h_b, u16, ws1, hs_b)
+    ops.expert_gemm2(h_b, w2, E, tiles, y_b)
+    torch.cuda.synchronize()
+    nt = int(tiles[-1].item()) * 256
+    assert torch.equal(h_a[:nt], h_b[:nt]) and torch.equal(y_a[:nt], y_b[:nt])
+    assert torch.equal(hs_a, hs_b)

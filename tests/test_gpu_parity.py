@@ -342,3 +342,21 @@ def test_fused_gate_engine_matches_unfused(monkeypatch):
     x0d = torch.as_tensor(x0.values).double().cpu()
     rel = (torch.linalg.norm((fa - x0d) - (fb - x0d)) / torch.linalg.norm(fb - x0d)).item()
     assert rel < 1e-3, rel
+
+
+@pytest.mark.parametrize("strategy", ["synchronous", "interweaved"])
+def test_merged_gemm1_engine_bit_identical(strategy, monkeypatch):
+    """The engine with the shared-expert GEMM1 riding in the expert GEMM1 launch
+    reproduces the unmerged engine bit for bit."""
+    cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=256,
+                        expert_dim=512, num_tokens=256, batch=4, num_steps=6, step_size=1e-3)
+    model = D.init_model(cfg, seed=7)
+    x0 = D.sample_x0(cfg, 7)
+    pol = D.dice_policy(refresh_interval=2, warmup=2, period=3)
+    finals = {}
+    for merge in ("1", "0"):
+        monkeypatch.setenv("DICE_MERGE_GEMM1", merge)
+        r = D.DeviceRunner(model, x0, D.Strategy(strategy), pol, D.ClusterConfig(num_devices=1), 7)
+        assert r.merge_gemm1 == (merge == "1")
+        finals[merge] = r.run().final.values.cpu()
+    assert torch.equal(finals["1"], finals["0"])
