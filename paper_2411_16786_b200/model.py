@@ -149,7 +149,7 @@ def init_model(config: ModelConfig, seed: int, device="cuda", experts=None) -> T
     (expert parallelism); stream offsets are unchanged.
     """
     h, e, E, S = config.hidden_dim, config.expert_dim, config.num_experts, config.num_shared
-    hp, ep = ops.pad64(h), ops.pad64(e)
+    hp, ep = ops.pad_hidden(h), ops.pad64(e)
     first, last = experts if experts is not None else (0, E)
     if not 0 <= first <= last <= E:
         raise ConfigurationError(f"expert block {experts} outside [0, {E}]")

@@ -19,6 +19,18 @@ def pad64(x: int) -> int:
     return (x + 63) // 64 * 64
 
 
+def pad_hidden(h: int) -> int:
+    """Padded hidden width of the device layouts: a multiple of 64, raised to a
+    multiple of 256 when that costs <= 10 % and the 64-multiple would leave the
+    N = hidden GEMMs on 128-wide tiles (e.g. the G preset, 1664 -> 1792). Pads
+    are zero in every weight and activation, so values are unchanged."""
+    hp = pad64(h)
+    if hp % 192 == 0 or hp % 256 == 0:
+        return hp
+    h256 = (h + 255) // 256 * 256
+    return h256 if h256 <= 1.1 * hp else hp
+
+
 def _ptr(t):
     return None if t is None else t.data_ptr()
 

@@ -43,6 +43,7 @@ def fake_call(name, *args):
 class FakeOps:
     EPI_STORE_BF16, EPI_GELU_BF16, EPI_STORE_F32, EPI_GELU_RESID, EPI_CONSUME = range(5)
     pad64 = staticmethod(ops.pad64)
+    pad_hidden = staticmethod(ops.pad_hidden)
 
     @staticmethod
     def _stream():
@@ -72,7 +73,7 @@ class FakeOps:
 
 
 def cpu_model(cfg, experts):
-    hp, ep_ = ops.pad64(cfg.hidden_dim), ops.pad64(cfg.expert_dim)
+    hp, ep_ = ops.pad_hidden(cfg.hidden_dim), ops.pad64(cfg.expert_dim)
     El = experts[1] - experts[0]
     S = cfg.num_shared
     bf = torch.bfloat16

@@ -160,7 +160,7 @@ class _FakeOps:
 
 
 def _cpu_model(cfg):
-    hp, ep = ops.pad64(cfg.hidden_dim), ops.pad64(cfg.expert_dim)
+    hp, ep = ops.pad_hidden(cfg.hidden_dim), ops.pad64(cfg.expert_dim)
     E, S = cfg.num_experts, cfg.num_shared
     bf = torch.bfloat16
     layers = [D.model.LayerWeights(torch.zeros(hp, hp, dtype=bf), torch.zeros(E, hp),
@@ -218,3 +218,9 @@ def test_runner_rejects_bad_inputs():
     with pytest.raises(D.ContractError):
         D.DeviceRunner(model, D.ActivationBlock(torch.zeros(4, 8), 0), "displaced",
                        D.NEUTRAL, D.ClusterConfig(num_devices=1), 0)
+
+
+def test_pad_hidden_rule():
+    # multiples of 192 / 256 keep the 64-padding; others go to 256 when <= 10 % more
+    assert [ops.pad_hidden(h) for h in (32, 128, 384, 1152, 1664, 2048, 1000, 4096)] == \
+        [64, 128, 384, 1152, 1792, 2048, 1024, 4096]
