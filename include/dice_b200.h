@@ -253,12 +253,15 @@ int dice_ep_dispatch(const int32_t* ids, const uint8_t* active, int64_t n, int k
 /* Expert side of one layer: groups the D*cap window rows by local expert,
  * runs the grouped expert FFN (expert_forward, model.py:226-232) and stores
  * every output row into its home rank's combine window at the home pair
- * index (cx: host array of D device pointers). */
+ * index (cx: host array of D device pointers). A2 != NULL: the rank's dense
+ * shared-expert GEMM1 out2 = gelu(A2 B2^T) [M2, N2] runs in the same GEMM1
+ * launch (dice_expert_gemm1_with_dense). */
 int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
                    int64_t cap, int El, int hp, int ep, const uint16_t* w1_t, const uint16_t* w2_t,
                    int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
                    uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
-                   const uint64_t* cx, void* stream);
+                   const uint64_t* cx, const uint16_t* A2, int64_t M2, const uint16_t* B2,
+                   int N2, uint16_t* out2, void* stream);
 
 /* out[i] = i for i < count (identity pair positions for the combine window). */
 int dice_iota(int32_t* out, int64_t count, void* stream);

@@ -227,7 +227,8 @@ int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* 
                    int64_t cap, int El, int hp, int ep, const uint16_t* w1_t, const uint16_t* w2_t,
                    int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
                    uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
-                   const uint64_t* cx, void* stream) {
+                   const uint64_t* cx, const uint16_t* A2, int64_t M2, const uint16_t* B2,
+                   int N2, uint16_t* out2, void* stream) {
   if (D < 1 || D > kMaxRanks || hp % 64 != 0 || ep % 64 != 0 || El < 1) return DICE_ERR_CONTRACT;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t total = (int64_t)D * cap;
@@ -236,7 +237,15 @@ int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* 
   int rc = permute_launch(ids_rx, nullptr, total, 1, El, 1, 256, El, rx_rows, hp, x_perm, pos_rx,
                           tile_offsets, nullptr, 1, 0, total, scratch, s);
   if (rc) return rc;
-  rc = dice_grouped_ffn(x_perm, max_rows, w1_t, w2_t, El, hp, ep, tile_offsets, hbuf, y, stream);
+  if (A2 != nullptr && M2 > 0) {
+    // this rank's shared-expert GEMM1 rides in the expert GEMM1 launch
+    rc = dice_expert_gemm1_with_dense(x_perm, max_rows, w1_t, El, hp, ep, tile_offsets, hbuf, A2,
+                                      M2, B2, N2, out2, stream);
+    if (rc) return rc;
+    rc = dice_expert_gemm2(hbuf, max_rows, w2_t, El, hp, ep, tile_offsets, y, stream);
+  } else {
+    rc = dice_grouped_ffn(x_perm, max_rows, w1_t, w2_t, El, hp, ep, tile_offsets, hbuf, y, stream);
+  }
   if (rc) return rc;
   ep_combine_send_kernel<<<grid_warps(total), 256, 0, s>>>(
       pos_rx, static_cast<const int2*>(rx_meta), total, cap, y, hp, table(cx, D, 0));

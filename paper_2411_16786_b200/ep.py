@@ -244,6 +244,8 @@ class EPRunner:
         self.h16 = torch.zeros(n, hp, dtype=bf, device=dev)
         self.u32 = torch.zeros(n, hp, dtype=f32, device=dev)
         self.u16 = torch.zeros(n, hp, dtype=bf, device=dev)
+        # the shared-expert GEMM1 rides in the expert GEMM1 launch (see DeviceRunner)
+        self.merge_gemm1 = cfg.num_shared > 0 and os.environ.get("DICE_MERGE_GEMM1", "1") != "0"
         # router fused into the local_block GEMM epilogue (see DeviceRunner)
         E_all = cfg.num_experts
         self.fused_gate = E_all in (8, 16) and os.environ.get("DICE_FUSED_GATE", "0") == "1"
@@ -334,11 +336,13 @@ class EPRunner:
         return self.slot_gen[layer] is None
 
     # ------------------------------------------------------------- exchange
-    def _send(self, step, layer, p: _EPPayload, force):
-        """decide + dispatch all-to-all send of layer `layer`."""
+    def _send(self, step, layer, p: _EPPayload, force, decided=False):
+        """decide (unless the gate launch already took it) + dispatch all-to-all
+        send of layer `layer`."""
         g, me, D = self.grp, self.rank, self.world
         if self.cache is not None:
-            self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write)
+            if not decided:
+                self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write)
             act = p.active
         else:
             act = None
@@ -358,9 +362,10 @@ class EPRunner:
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 
-    def _expert(self, p: _EPPayload):
+    def _expert(self, p: _EPPayload, shared_layer=None):
         """Expert side of dispatch(p.layer): wait for every source, grouped FFN,
-        combine rows straight back to their home ranks."""
+        combine rows straight back to their home ranks. shared_layer: that
+        layer's shared-expert GEMM1 (u16 -> hsh) rides in the expert GEMM1 launch."""
         g, me, layer = self.grp, self.rank, p.layer
         self._timed_wait([g.flag("rx_ready", me, layer, s) for s in self._peers()], 1)
         g.write([g.flag("rx_ready", me, layer, s) for s in self._peers()], 0)
@@ -380,10 +385,10 @@ class EPRunner:
                   lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.ids_rx.data_ptr(),
                   self.pos_rx.data_ptr(), self.tiles.data_ptr(), self.scratch.data_ptr(),
                   self.x_perm.data_ptr(), self.max_rows, self.hbuf.data_ptr(), self.y.data_ptr(),
-                  cx, ops._stream())
+                  cx, *self._shared_args(shared_layer), ops._stream())
         if self.time_experts:
             e1.record()
-            self._expert_events.append((e0, e1, p.gen, layer))
+            self._expert_events.append((e0, e1, p.gen, layer, shared_layer is not None))
         g.data("read", [("rx", me, layer, s) for s in self._peers()])
         g.data("write", [("cx", h, layer, me) for h in self._peers()])
         g.write([g.flag("rx_free", s, layer, me) for s in self._peers()], 1)
@@ -391,6 +396,12 @@ class EPRunner:
         self.deferred[layer] = p
         self.slot_gen[layer] = p.gen          # the combine is in flight (_store_combine)
         self.combine_log.append((p.gen, layer))
+
+    def _shared_args(self, shared_layer):
+        if shared_layer is None:
+            return (None, 0, None, 0, None)
+        ws1 = self.model.layers[shared_layer].ws1_t
+        return (self.u16.data_ptr(), self.n, ws1.data_ptr(), ws1.shape[0], self.hsh.data_ptr())
 
     def _assemble(self, layer):
         """Combine arrival at the home rank: stale-cache merge into slot[layer]."""
@@ -418,11 +429,12 @@ class EPRunner:
             self._expert(prev)
             self._track(prev.layer)
 
-    def _consume(self, layer, step, gen):
+    def _consume(self, layer, step, gen, gemm1_done=False):
         lw = self.model.layers[layer]
         slot = self._slot(layer)
         if self.S > 0:
-            ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
+            if not gemm1_done:
+                ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
             ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
                      residual=self.u32, addend=slot)
         else:
@@ -446,26 +458,33 @@ class EPRunner:
                 self._flush_pending()
             self._assemble(layer)            # previous step's combine, before decide(layer)
             p = self.payloads[layer]
+            # the conditional-communication decision rides in the gate launch
+            dec = None
+            if self.cache is not None:
+                dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write)
             if self.fused_gate:
-                ops.gate_finish(self.gparts, p.ids, p.gates, None, self.status, step, layer)
+                ops.gate_finish(self.gparts, p.ids, p.gates, None, self.status, step, layer,
+                                decide=dec)
             else:
                 ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, None, self.status,
-                              step, layer)
+                              step, layer, decide=dec)
+            decided = dec is not None
             if sync:
-                self._send(step, layer, p, force=True)
-                self._expert(p)
+                self._send(step, layer, p, force=True, decided=decided)
+                self._expert(p, shared_layer=layer if self.merge_gemm1 else None)
                 self._assemble(layer)
                 if self.strategy is Strategy.INTERWEAVED:
                     self._track(layer)
-                self._consume(layer, step, step)
+                self._consume(layer, step, step, gemm1_done=self.merge_gemm1)
             else:
                 gen = self.slot_gen[layer]
-                self._send(step, layer, p, force=False)
+                self._send(step, layer, p, force=False, decided=decided)
                 prev, self.pending = self.pending, p
+                merged = self.merge_gemm1 and prev is not None
                 if prev is not None:
-                    self._expert(prev)
+                    self._expert(prev, shared_layer=layer if merged else None)
                     self._track(prev.layer)
-                self._consume(layer, step, gen)
+                self._consume(layer, step, gen, gemm1_done=merged)
         self._flush_pending()
         ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
 

@@ -44,6 +44,7 @@ class FakeOps:
     EPI_STORE_BF16, EPI_GELU_BF16, EPI_STORE_F32, EPI_GELU_RESID, EPI_CONSUME = range(5)
     pad64 = staticmethod(ops.pad64)
     pad_hidden = staticmethod(ops.pad_hidden)
+    COND_CODES = ops.COND_CODES
 
     @staticmethod
     def _stream():

@@ -32,11 +32,11 @@ CFG = dict(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=128, e
            num_tokens=64, batch=3, num_steps=7, step_size=1e-3)
 
 
-@pytest.mark.parametrize("strategy,policy", [("synchronous", "neutral"),
-                                             ("interweaved", "neutral"),
-                                             ("interweaved", "dice")])
-def test_ep_two_ranks_matches_single_gpu(strategy, policy):
-    world = 2
+@pytest.mark.parametrize("strategy,policy,world", [("synchronous", "neutral", 2),
+                                                   ("interweaved", "neutral", 2),
+                                                   ("interweaved", "dice", 2),
+                                                   ("interweaved", "dice", 4)])
+def test_ep_two_ranks_matches_single_gpu(strategy, policy, world):
     same = torch.cuda.device_count() < world
     port = free_port()
     with tempfile.TemporaryDirectory() as td:
