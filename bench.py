@@ -48,7 +48,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, index=0):
         self.index = index
@@ -85,8 +85,19 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        def num(i):
+            out = []
+            for r in self.rows:
+                try:
+                    out.append(float(r[i]))
+                except (IndexError, ValueError):
+                    pass
+            return out
+        pw, pl = num(7), num(8)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "power_w": statistics.median(pw) if pw else None,
+                "power_limit_w": max(pl) if pl else None,
                 "samples": len(self.rows)}
 
 

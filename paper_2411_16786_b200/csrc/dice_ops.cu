@@ -280,6 +280,139 @@ __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, i
     decide_token(t, k, ids, d);
 }
 
+// E = 8: warp per FOUR rows. Each W_gate float4 (4 columns of one expert) now
+// feeds four rows (two FFMA2 row pairs), halving the L1 wavefronts per row, and
+// the 4 x 8 partial logits transpose-reduce to exactly one (row, expert) per
+// lane (lane = 8 row + e). Rows are loaded in CH-chunk batches.
+template <int CH>
+__global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
+    const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
+    int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
+    int32_t* status, int step, int layer, const DecideArgs d) {
+  pdl_enter();
+  constexpr int E = 8;
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int64_t quads = (n + 3) / 4;
+  for (int64_t q = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5); q < quads;
+       q += (int64_t)gridDim.x * warps) {
+    const int64_t t0 = 4 * q;
+    const int row = lane >> 3;             // 0..3
+    const int e_me = lane & 7;             // expert held by this lane after the reduce
+    const int64_t t = t0 + row;
+    const bool row_ok = t < n;
+    const int slot = e_me;
+    int32_t d_last = 0, d_cid = -1;
+    uint8_t d_primed = 1, d_red = 0;
+    const bool d_lane = d.on && d.strategy != DICE_COND_OFF && row_ok && slot < k;
+    if (d_lane) {
+      d_last = d.last[t];
+      d_primed = d.primed[t];
+      d_red = d.reduced[t * k + slot];
+      if (d.strict) d_cid = d.cached_ids[t * k + slot];
+    }
+    const float* rp[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rp[i] = u + (t0 + i < n ? t0 + i : t0) * hp;
+    float2 a01[E], a23[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { a01[e] = make_float2(0.f, 0.f); a23[e] = a01[e]; }
+    for (int base = 0; base < hp; base += 128 * CH) {
+      float4 x[4][CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = base + 128 * j + lane * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          x[i][j] = c < hp ? __ldg(reinterpret_cast<const float4*>(rp[i] + c))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = base + 128 * j + lane * 4;
+        if (c >= hp) break;
+        const float2 p0 = make_float2(x[0][j].x, x[1][j].x), p1 = make_float2(x[0][j].y, x[1][j].y);
+        const float2 p2 = make_float2(x[0][j].z, x[1][j].z), p3 = make_float2(x[0][j].w, x[1][j].w);
+        const float2 r0 = make_float2(x[2][j].x, x[3][j].x), r1 = make_float2(x[2][j].y, x[3][j].y);
+        const float2 r2 = make_float2(x[2][j].z, x[3][j].z), r3 = make_float2(x[2][j].w, x[3][j].w);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float4 w = __ldg(reinterpret_cast<const float4*>(wt + (int64_t)e * hp + c));
+          a01[e] = __ffma2_rn(p0, make_float2(w.x, w.x), a01[e]);
+          a23[e] = __ffma2_rn(r0, make_float2(w.x, w.x), a23[e]);
+          a01[e] = __ffma2_rn(p1, make_float2(w.y, w.y), a01[e]);
+          a23[e] = __ffma2_rn(r1, make_float2(w.y, w.y), a23[e]);
+          a01[e] = __ffma2_rn(p2, make_float2(w.z, w.z), a01[e]);
+          a23[e] = __ffma2_rn(r2, make_float2(w.z, w.z), a23[e]);
+          a01[e] = __ffma2_rn(p3, make_float2(w.w, w.w), a01[e]);
+          a23[e] = __ffma2_rn(r3, make_float2(w.w, w.w), a23[e]);
+        }
+      }
+    }
+    float a[32];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      a[e] = a01[e].x; a[8 + e] = a01[e].y; a[16 + e] = a23[e].x; a[24 + e] = a23[e].y;
+    }
+    tr_level<32>(a, lane, 16); tr_level<16>(a, lane, 8); tr_level<8>(a, lane, 4);
+    tr_level<4>(a, lane, 2); tr_level<2>(a, lane, 1);
+    const float logit = a[0];              // row (lane >> 3), expert (lane & 7)
+    const bool bad = !isfinite(logit) && row_ok;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) record_nonfinite(status, step, layer);
+    float mx = logit;
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const float ex = expf(logit - mx);
+    float sum = ex;
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    const float sc = ex / sum;
+    const int rowbase = row * 8;
+    int rank = 0;
+#pragma unroll
+    for (int qe = 0; qe < E; ++qe) {
+      const float sq = __shfl_sync(0xffffffffu, sc, rowbase + qe);
+      rank += (sq > sc) || (sq == sc && qe < e_me);
+    }
+    if (scores != nullptr && row_ok) scores[t * E + e_me] = sc;
+    const unsigned rowmask = 0xFFu << rowbase;
+    float psum = 0.f, my_s = 0.f;
+    int my_e = 0;
+    for (int j = 0; j < k; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, rank == j) & rowmask;
+      const int src = __ffs(m) - 1;
+      const float sj = __shfl_sync(0xffffffffu, sc, src);
+      psum += sj;
+      if (slot == j) { my_s = sj; my_e = src & 7; }
+    }
+    if (slot < k && row_ok) {
+      ids[t * k + slot] = my_e;
+      gates[t * k + slot] = my_s / psum;
+    }
+    if (d.on && slot < k && row_ok) {
+      if (d.strategy == DICE_COND_OFF) {
+        d.active[t * k + slot] = 1;
+        d.write[t * k + slot] = 0;
+      } else {
+        const bool due = d.force || !d_primed || (step - d_last) >= d.R;
+        bool red = d_red != 0;
+        if (due) {
+          if (d.strategy == DICE_COND_LOW_SCORE) red = slot >= 1;
+          else if (d.strategy == DICE_COND_HIGH_SCORE) red = slot == 0;
+          else red = slot != (int)(splitmix_at(d.key, (uint64_t)t + 1) % (uint64_t)k);
+          d.reduced[t * k + slot] = red;
+          if (slot == 0) { d.last[t] = step; d.primed[t] = 1; }
+        }
+        bool act = !red || due;
+        bool wr = red && due;
+        if (d.strict && red && !due && my_e != d_cid) { act = true; wr = true; }
+        d.active[t * k + slot] = act;
+        d.write[t * k + slot] = wr;
+      }
+    }
+  }
+}
+
 // Warp per row pair, no shared-memory prologue: W_gate is read through L1
 // (37 KB per SM, coalesced 512-byte lines per expert), every lane issues all of
 // its 16-byte row loads before any math (u was just written by the local_block
@@ -1032,6 +1165,22 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
   const int threads = 512;
   int64_t want = ((n + 1) / 2 + 15) / 16;
   if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
+  const char* g4 = getenv("DICE_GATE4");        // 0: the row-pair kernel for E = 8
+  if (E == 8 && k <= 8 && !(g4 != nullptr && g4[0] == '0')) {
+    const int64_t gw = ((n + 3) / 4 + 7) / 8;     // 8 warps per block, four rows each
+    const int grid = (int)(gw < 1 ? 1 : gw);
+    const int ch = g4 != nullptr ? atoi(g4) : 3;
+    if (ch == 5)
+      launch_pdl(gate4_topk_kernel<5>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
+                 gates, scores, status, step, layer, d);
+    else if (ch == 2)
+      launch_pdl(gate4_topk_kernel<2>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
+                 gates, scores, status, step, layer, d);
+    else
+      launch_pdl(gate4_topk_kernel<3>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
+                 gates, scores, status, step, layer, d);
+    return launch_ok();
+  }
   if ((E == 8 && k <= 8) || (E == 16 && k <= 16)) {
     const int64_t gw = ((n + 1) / 2 + 7) / 8;     // 8 warps per block, a row pair each
     const int grid = (int)(gw < 1 ? 1 : gw);
