@@ -223,8 +223,6 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
             work, kind = 4.0 * h * e * P, "tensor"
         elif name == "grouped_ffn+shared_gemm1":
             work, kind = 4.0 * h * e * P + 2.0 * R * h * S * e, "tensor"
-        elif name == "shared_gemm2_consume+local_gemm":
-            work, kind = 2.0 * R * h * S * e + 2.0 * R * h * h, "tensor"
         else:
             continue
         a = agg.setdefault(name, [0.0, 0, 0.0, kind])

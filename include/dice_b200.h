@@ -198,16 +198,6 @@ int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const
 int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
                       int ep, const int32_t* tile_offsets, uint16_t* y, void* stream);
 
-/* The consume of layer l and the local_block of layer l+1 in ONE persistent
- * launch: h = u + (A1 B1^T + addend) (schedules.py:308-317, the shared-FFN
- * GEMM2 epilogue) -> h32 / h16, then u' = gelu(h16 B2^T) + h32 (model.py:244-252,
- * B2 = W_mix^T of layer l+1) -> u32_out / u16_out, each 256-row m-tile of the
- * second GEMM starting as soon as the first has stored that m-tile. All
- * matrices have N = hidden columns (hp). */
-int dice_consume_then_local(const uint16_t* A1, int64_t M, const uint16_t* B1, int N, int K1,
-                            float* h32, uint16_t* h16, const float* u32, const float* addend,
-                            const uint16_t* B2, float* u32_out, uint16_t* u16_out, void* stream);
-
 /* out[t] = base[t] + sum_s gates[t, s] * rows[s, t] (f32, combine_outputs
  * model.py:279-298 and the consume residual, schedules.py:317). rows f32
  * [k, n, hp]; base f32 [n, hp]; optional residual adds u first:

@@ -37,7 +37,6 @@ SIGNATURES = {
     "dice_expert_gemm1_with_dense": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P, c_int64,
                                              P, c_int, P, P]),
     "dice_expert_gemm2": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P]),
-    "dice_consume_then_local": (c_int, [P, c_int64, P, c_int, c_int, P, P, P, P, P, P, P, P]),
     "dice_gemm_local_gate": (c_int, [P, c_int64, P, c_int, c_int, P, c_int64, P, c_int64, P,
                                      c_int64, P, c_int, P, P]),
     "dice_gate_parts": (c_int, [c_int64, c_int, c_int, c_int]),
@@ -120,7 +119,6 @@ KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSE
                     "dice_grouped_ffn": 2 * (1 + _SK), "dice_gemm": 1 + _SK,
                     "dice_gemm_local_gate": 1, "dice_gate_parts": 0, "dice_event_create": 0,
                     "dice_expert_gemm1_with_dense": 1 + _SK, "dice_expert_gemm2": 1 + _SK,
-                    "dice_consume_then_local": 1,
                     "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,

@@ -20,7 +20,6 @@
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
-#include <vector>
 
 namespace dice {
 
@@ -68,7 +67,7 @@ __device__ __forceinline__ int find_group(const int* off, int groups, int m_tile
 // one output row, a warp covers 4 rows per pass, so residual loads and f32 /
 // bf16 stores are coalesced 128-byte / 64-byte row segments. All 8 passes'
 // global loads are issued before any math so their latencies overlap.
-template <int EPI, bool WRITE_BACK = false, bool CG = false>
+template <int EPI, bool WRITE_BACK = false>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, float* stage, int lane,
                                                int row0, int row_limit, int col0) {
   const int q = lane & 7;
@@ -86,11 +85,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, float* stage, 
       for (int it = 0; it < 4; ++it) {
         const int64_t row = row0 + (half * 4 + it) * 4 + (lane >> 3);
         if (row < row_limit) {
-          // (CG: the residual was written by another SM during this launch)
-          if constexpr (CG)
-            r[it] = __ldcg(reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col));
-          else
-            r[it] = __ldg(reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col));
+          r[it] = __ldg(reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col));
           if constexpr (EPI == EPI_CONSUME)
             ad[it] = __ldg(reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col));
         }
@@ -523,7 +518,7 @@ __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_
   for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
 
-template <int BN, int EPI, bool DIRECT, int NSUB, int EPI2>
+template <int BN, int EPI, bool DIRECT, int NSUB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const GemmArgs args, const __grid_constant__ CUtensorMap tmA2,
@@ -594,17 +589,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     plan.init_chain(num_tiles, k_blocks, num_pairs, args.ksplit);
   else
     plan.init(num_tiles, k_blocks, num_pairs, args.sk_workspace != nullptr);
-  // host-planned order (dependent launches): tile ids from a per-pair list
-  const int* sched = args.sched;
-  const int sched_base = sched != nullptr ? args.sched_off[pair] : 0;
-  const int n_items = sched != nullptr ? args.sched_off[pair + 1] - sched_base : plan.items(pair);
-  auto item = [&](int i, int& tile, int& k0, int& k1, int& slot) {
-    if (sched != nullptr) {
-      tile = sched[sched_base + i]; k0 = 0; k1 = k_blocks; slot = -1;
-    } else {
-      plan.item(pair, i, tile, k0, k1, slot);
-    }
-  };
+  const int n_items = plan.items(pair);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -612,7 +597,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       uint32_t phase = 0;
       for (int it = 0; it < n_items; ++it) {
         int tile, k0, k1, slot;
-        item(it, tile, k0, k1, slot);
+        plan.item(pair, it, tile, k0, k1, slot);
         int prob, n_blk, m_tile;   // N-fastest: resident tiles share A rows
         locate(tile, prob, n_blk, m_tile);
         const int g = prob == 0 ? find_group(sh->group_off, groups, m_tile) : 0;
@@ -620,14 +605,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int b_row = g * (prob == 0 ? args.N : args2.N) + n_blk * TN + rank * (BN / 2);
         const CUtensorMap* mA = prob == 0 ? &tmA : &tmA2;
         const CUtensorMap* mB = prob == 0 ? &tmB : &tmB2;
-        const int kend = prob == 0 ? k1 : args2.num_k_blocks;
-        if (prob == 1 && args2.dep != nullptr) {
-          // the A rows of this m-tile are the first problem's output: wait until
-          // all its tiles of the m-tile are stored, then order the TMA reads after
-          while (ld_acquire_u32(args2.dep + m_tile) < args2.dep_target) __nanosleep(40);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        for (int kb = k0; kb < kend; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0), C::kStageBytes);
           tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
@@ -646,16 +624,13 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       uint32_t phase = 0;
       for (int local = 0; local < n_items; ++local) {
         int tile, k0, k1, slot;
-        item(local, tile, k0, k1, slot);
+        plan.item(pair, local, tile, k0, k1, slot);
         const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
         const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
         mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * TN;
-        int mprob, mn, mm;
-        locate(tile, mprob, mn, mm);
-        const int kend = mprob == 0 ? k1 : args2.num_k_blocks;
-        for (int kb = k0; kb < kend; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::kABytes);
@@ -684,7 +659,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
     for (int local = 0; local < n_items; ++local) {
       int tile, k0, k1, slot;
-      item(local, tile, k0, k1, slot);
+      plan.item(pair, local, tile, k0, k1, slot);
       int prob, n_blk, m_tile;
       locate(tile, prob, n_blk, m_tile);
       const GemmArgs& ar = prob == 0 ? args : args2;
@@ -719,11 +694,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (col0 >= ar.N) continue;  // warp-uniform
         if constexpr (DIRECT) {   // (the host never enables stream-K for DIRECT)
           const int64_t row = row0 + lane;
-          if (prob == 0) {
-            if (row < rl) epilogue_direct<EPI>(ar, r, row, col0);
-          } else {
-            if (row < rl) epilogue_direct<EPI2>(ar, r, row, col0);
-          }
+          if (row < rl) epilogue_direct<EPI>(ar, r, row, col0);
           continue;
         }
 #pragma unroll
@@ -747,29 +718,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             chain_store(stage, lane, cws, TN, rank * BM + sub * 32, col_in_tile);
           else
             epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
-        } else if (prob == 0) {
-          epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
-        } else if (args2.dep != nullptr) {
-          epilogue_chunk<EPI2, false, true>(ar, stage, lane, row0, rl, col0);
         } else {
-          epilogue_chunk<EPI2>(ar, stage, lane, row0, rl, col0);
+          epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         }
         __syncwarp();
-      }
-      if (prob == 0 && args.dep != nullptr) {
-        // this warp's rows of the m-tile are stored: count it for the dependent problem
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(args.dep + m_tile, 1u);
-      } else if (prob == 1 && args2.dep != nullptr) {
-        __syncwarp();
-        // the last dependent warp of the m-tile returns its counters to 0
-        if (lane == 0 &&
-            atomicAdd(args2.dep_done + m_tile, 1u) == (unsigned)n_blocks2 * 2u * kEpiWarps - 1u) {
-          args2.dep[m_tile] = 0;
-          args2.dep_done[m_tile] = 0;
-        }
       }
       if (!DIRECT && csplit >= 0) {
         if (csplit < args.ksplit - 1) {
@@ -972,14 +924,14 @@ int chain_workspace(cudaStream_t stream, int tiles, int tile_n, float** ws, unsi
   return 0;
 }
 
-template <int BN, int EPI, bool DIRECT, int NSUB = 1, int EPI2 = EPI>
+template <int BN, int EPI, bool DIRECT, int NSUB = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
                 const CUtensorMap* tb2 = nullptr, const GemmArgs* a2 = nullptr) {
   using C = PairCfg<BN, DIRECT, NSUB>;
   static bool attr_done = false;
   if (!attr_done) {
-    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT, NSUB, EPI2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kSmemBytes) != cudaSuccess)
       return DICE_ERR_CUDA;
     attr_done = true;
@@ -989,7 +941,6 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   static const int cta_cap = env_int("DICE_GEMM_MAX_CTAS", 1 << 30);   // experiment hook
   const int sms = num_sms() < cta_cap ? num_sms() : cta_cap;
   int grid = 2 * items < sms ? 2 * items : sms;
-  if (a.sched != nullptr) grid = 2 * (num_sms() / 2);   // one CTA pair per planned list
   grid &= ~1;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
@@ -1011,7 +962,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
       return DICE_ERR_CONTRACT;
     bb = *a2;
   }
-  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB, EPI2>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
+  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
              ta, tb, aa, a2 != nullptr ? *ta2 : ta, a2 != nullptr ? *tb2 : tb, bb);
   if (aa.sk_workspace != nullptr)
     launch_pdl(stream_k_fixup_kernel<EPI>, dim3(num_sms() * 2), dim3(256), 0, stream, aa, aa.sk_workspace, BN, grid / 2);
@@ -1225,156 +1176,6 @@ int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t st
   return p1.epi_kind == EPI_GELU_BF16
              ? launch_pair<192, EPI_GELU_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2)
              : launch_pair<192, EPI_STORE_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2);
-}
-
-// Dependent pair in one launch: p2 reads p1's output rows (A operand and/or
-// residual) m-tile by m-tile (the shared-FFN GEMM2 + consume of layer l, then
-// the local_block GEMM of layer l+1). Requires the same M and tile width and
-// staged epilogues; otherwise two launches.
-struct DepWs {
-  unsigned* c = nullptr;
-  int n = 0;
-};
-
-// List schedule of a dependent launch (host-simulated, cached per shape): the
-// first problem's tiles in index order, each on the pair that frees first;
-// then the second problem's tiles m-tile by m-tile, each on the pair where it
-// can start earliest (its m-tile is ready when the last first-problem tile of
-// that m-tile ends). Tile cost ~ its k-blocks (+ an epilogue term).
-struct SchedKey {
-  int t1, n1, kb1, t2, n2, kb2, pairs;
-  bool operator==(const SchedKey& o) const {
-    return t1 == o.t1 && n1 == o.n1 && kb1 == o.kb1 && t2 == o.t2 && n2 == o.n2 &&
-           kb2 == o.kb2 && pairs == o.pairs;
-  }
-};
-struct SchedKeyHash {
-  size_t operator()(const SchedKey& k) const {
-    return ((size_t)k.t1 * 1000003u) ^ ((size_t)k.t2 * 10007u) ^ ((size_t)k.kb1 << 20) ^
-           ((size_t)k.kb2 << 8) ^ (size_t)k.pairs ^ ((size_t)k.n1 << 40) ^ ((size_t)k.n2 << 48);
-  }
-};
-std::mutex g_sched_mu;
-std::unordered_map<SchedKey, int*, SchedKeyHash> g_sched;   // device [t1 + t2 + pairs + 1]
-
-int plan_then_schedule(int t1, int n1, int kb1, int t2, int n2, int kb2, int pairs,
-                       cudaStream_t stream, const int** sched, const int** sched_off) {
-  const SchedKey key{t1, n1, kb1, t2, n2, kb2, pairs};
-  std::lock_guard<std::mutex> lk(g_sched_mu);
-  auto it = g_sched.find(key);
-  if (it == g_sched.end()) {
-    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &st);
-    if (st != cudaStreamCaptureStatusNone) return DICE_ERR_CONTRACT;   // plan it before capture
-    const double c1 = kb1 + 4.0, c2 = kb2 + 4.0;      // k-blocks + epilogue/turnaround
-    std::vector<double> fr(pairs, 0.0);
-    std::vector<std::vector<int>> lists(pairs);
-    const int m_tiles = t1 / n1;
-    std::vector<double> ready(m_tiles, 0.0);
-    for (int t = 0; t < t1; ++t) {
-      int best = 0;
-      for (int p = 1; p < pairs; ++p)
-        if (fr[p] < fr[best]) best = p;
-      lists[best].push_back(t);
-      fr[best] += c1;
-      const int m = t / n1;
-      if (fr[best] > ready[m]) ready[m] = fr[best];
-    }
-    for (int t = 0; t < t2; ++t) {
-      const int m = t / n2;
-      const double r = m < m_tiles ? ready[m] : 0.0;
-      int best = 0;
-      double bs = 1e300;
-      for (int p = 0; p < pairs; ++p) {
-        const double start = fr[p] > r ? fr[p] : r;
-        if (start < bs) { bs = start; best = p; }
-      }
-      lists[best].push_back(t1 + t);
-      fr[best] = bs + c2;
-    }
-    std::vector<int> host;
-    std::vector<int> off(pairs + 1, 0);
-    for (int p = 0; p < pairs; ++p) {
-      off[p] = (int)host.size();
-      host.insert(host.end(), lists[p].begin(), lists[p].end());
-    }
-    off[pairs] = (int)host.size();
-    host.insert(host.end(), off.begin(), off.end());
-    int* d = nullptr;
-    if (cudaMalloc(&d, sizeof(int) * host.size()) != cudaSuccess ||
-        cudaMemcpy(d, host.data(), sizeof(int) * host.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-      cudaGetLastError();
-      return DICE_ERR_CUDA;
-    }
-    it = g_sched.emplace(key, d).first;
-  }
-  *sched = it->second;
-  *sched_off = it->second + t1 + t2;
-  return 0;
-}
-std::mutex g_dep_mu;
-std::unordered_map<cudaStream_t, DepWs> g_dep;
-
-int gemm_bf16_then(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t stream) {
-  static const int mode = env_int("DICE_GEMM_THEN", 1);
-  const TileChoice c1 = choose_tile(p1), c2 = choose_tile(p2);
-  const bool ok = mode != 0 && p1.group_tile_offsets == nullptr && p2.group_tile_offsets == nullptr &&
-                  p1.M == p2.M && c1.pair && c2.pair && !c1.wide && !c2.wide && c1.bn == c2.bn &&
-                  c1.ksplit == 1 && c2.ksplit == 1 && (c1.bn == 192 || c1.bn == 256) &&
-                  p1.epi_kind == EPI_CONSUME && p2.epi_kind == EPI_GELU_RESID;
-  if (!ok) {
-    const int rc = gemm_bf16(p1, stream);
-    return rc ? rc : gemm_bf16(p2, stream);
-  }
-  CUtensorMap ta1, tb1, ta2, tb2;
-  GemmArgs a1, a2;
-  int rc = prepare(p1, c1, &ta1, &tb1, &a1);
-  if (rc) return rc;
-  rc = prepare(p2, c2, &ta2, &tb2, &a2);
-  if (rc) return rc;
-  const int m_tiles = a1.num_m_tiles;
-  if (m_tiles * a1.num_n_blocks == 0) return 0;
-  unsigned* dep = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_dep_mu);
-    DepWs& w = g_dep[stream];
-    if (w.n < m_tiles) {
-      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(stream, &st);
-      if (st != cudaStreamCaptureStatusNone) return DICE_ERR_CONTRACT;   // size it before capture
-      cudaStreamSynchronize(stream);
-      if (w.c) cudaFree(w.c);
-      w.c = nullptr;
-      if (cudaMalloc(&w.c, sizeof(unsigned) * 2 * m_tiles) != cudaSuccess ||
-          cudaMemset(w.c, 0, sizeof(unsigned) * 2 * m_tiles) != cudaSuccess) {
-        cudaGetLastError();
-        w.n = 0;
-        return DICE_ERR_CUDA;
-      }
-      cudaDeviceSynchronize();
-      w.n = m_tiles;
-    }
-    dep = w.c;
-  }
-  a1.dep = dep;
-  a2.dep = dep;
-  a2.dep_done = dep + m_tiles;
-  a2.dep_target = (unsigned)a1.num_n_blocks * 2u * kEpiWarps;
-  const int t1 = m_tiles * a1.num_n_blocks;
-  const int t2 = a2.num_m_tiles * a2.num_n_blocks;
-  const int pairs = num_sms() / 2;
-  const int* sched = nullptr;
-  const int* sched_off = nullptr;
-  rc = plan_then_schedule(t1, a1.num_n_blocks, a1.num_k_blocks, t2, a2.num_n_blocks,
-                          a2.num_k_blocks, pairs, stream, &sched, &sched_off);
-  if (rc) return rc;
-  a1.sched = sched;
-  a1.sched_off = sched_off;
-  if (c1.bn == 256)
-    return launch_pair<256, EPI_CONSUME, false, 1, EPI_GELU_RESID>(ta1, tb1, a1, t1, stream, &ta2,
-                                                                   &tb2, &a2);
-  return launch_pair<192, EPI_CONSUME, false, 1, EPI_GELU_RESID>(ta1, tb1, a1, t1, stream, &ta2,
-                                                                 &tb2, &a2);
 }
 
 }  // namespace dice

@@ -65,17 +65,6 @@ struct GemmArgs {
   int ksplit;
   float* chain_ws;       // f32 [tiles, 256, tile_n] partials
   unsigned* chain_flags; // [tiles, 2] arrival counters (zero between launches)
-  // dependent second problem (gemm_bf16_then): the first problem's epilogue
-  // warps count finished tiles per m-tile into dep; the second problem's tile
-  // (m, n) starts once dep[m] == dep_target (its A rows / residual are the first
-  // problem's output rows); dep_done returns both counters to 0
-  unsigned* dep;
-  unsigned* dep_done;
-  unsigned dep_target;
-  // optional host-planned tile order: pair p runs tiles sched[sched_off[p] ..
-  // sched_off[p+1]) (list scheduling of unequal / dependent tiles)
-  const int* sched;
-  const int* sched_off;
 };
 
 struct GemmProblem {
@@ -93,9 +82,6 @@ struct GemmProblem {
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream);
 // two independent problems (same K, bf16-only epilogue) in one persistent launch
 int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t stream);
-// p2's m-tile m consumes p1's output rows of m-tile m (same M, same tile width):
-// one persistent launch, p2 tiles start as their rows are finished
-int gemm_bf16_then(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t stream);
 // number of partial-logit slots a GATE epilogue writes for this problem
 int gemm_gate_parts(const GemmProblem& p);
 

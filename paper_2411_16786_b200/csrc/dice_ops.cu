@@ -1381,29 +1381,6 @@ int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const
   return gemm_bf16_dual(p, q, (cudaStream_t)stream);
 }
 
-int dice_consume_then_local(const uint16_t* A1, int64_t M, const uint16_t* B1, int N, int K1,
-                            float* h32, uint16_t* h16, const float* u32, const float* addend,
-                            const uint16_t* B2, float* u32_out, uint16_t* u16_out, void* stream) {
-  if (M < 0 || M > INT_MAX || N % 64 != 0 || K1 % 64 != 0) return DICE_ERR_CONTRACT;
-  if (M == 0) return DICE_OK;
-  GemmProblem p{};
-  p.A = A1; p.A_rows = M; p.B = B1; p.M = (int)M; p.N = N; p.K = K1;
-  p.num_groups = 1; p.group_tile_offsets = nullptr; p.max_m_tiles = 0;
-  p.epi_kind = EPI_CONSUME;
-  p.epi.out_f32 = h32; p.epi.ld_f32 = N;
-  p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(h16); p.epi.ld_bf16 = N;
-  p.epi.residual = u32; p.epi.ld_res = N;
-  p.epi.addend = addend; p.epi.ld_add = N;
-  GemmProblem q{};
-  q.A = h16; q.A_rows = M; q.B = B2; q.M = (int)M; q.N = N; q.K = N;
-  q.num_groups = 1; q.group_tile_offsets = nullptr; q.max_m_tiles = 0;
-  q.epi_kind = EPI_GELU_RESID;
-  q.epi.out_f32 = u32_out; q.epi.ld_f32 = N;
-  q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(u16_out); q.epi.ld_bf16 = N;
-  q.epi.residual = h32; q.epi.ld_res = N;
-  return gemm_bf16_then(p, q, (cudaStream_t)stream);
-}
-
 int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
                       int ep, const int32_t* tile_offsets, uint16_t* y, void* stream) {
   if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0)

@@ -202,16 +202,6 @@ def expert_gemm2(hbuf, w2_t, E, tile_offsets, y):
               _ptr(y), _stream())
 
 
-def consume_then_local(hsh, ws2_t, h32, h16, u32, slot, w_mix_next_t, u32_out, u16_out):
-    """h = u + (shared + routed) (shared-FFN GEMM2 epilogue) then the next
-    layer's local_block u' = gelu(h W_mix) + h, in one persistent launch whose
-    second GEMM starts on each m-tile as soon as the first has stored it."""
-    M, K1 = hsh.shape
-    N = ws2_t.shape[0]
-    _lib.call("dice_consume_then_local", _ptr(hsh), M, _ptr(ws2_t), N, K1, _ptr(h32), _ptr(h16),
-              _ptr(u32), _ptr(slot), _ptr(w_mix_next_t), _ptr(u32_out), _ptr(u16_out), _stream())
-
-
 def cache_assemble(y, pos, active, write, gates, ids, routed, cache_rows=None, cache_gates=None,
                    cache_ids=None, rows_out=None, gates_out=None):
     n, k = pos.shape

@@ -223,14 +223,6 @@ class DeviceRunner:
         self.merge_gemm1 = (S > 0 and self.side is None
                             and strategy in (Strategy.SYNCHRONOUS, Strategy.INTERWEAVED)
                             and os.environ.get("DICE_MERGE_GEMM1", "1") != "0")
-        # DICE_MERGE_THEN=1: the consume of layer l and the local_block GEMM of layer
-        # l+1 in one launch, each local m-tile starting as the consume stores it
-        # (list-scheduled). Bit-identical, measured neutral in-step (266 vs 263 us:
-        # the step is power-capped, idle tail SMs already buy clock), so opt-in.
-        self.merge_then = (S > 0 and self.side is None and not self.fused_gate
-                           and strategy in (Strategy.SYNCHRONOUS, Strategy.INTERWEAVED)
-                           and os.environ.get("DICE_MERGE_THEN", "0") == "1")
-        self._local_done = False
 
     # ------------------------------------------------------------ helpers
     def _reset_state(self, x0_device=None):
@@ -255,7 +247,6 @@ class DeviceRunner:
         for p in (self.payloads if self.strategy is Strategy.INTERWEAVED else []):
             p.done = None
         self.occupied = set()
-        self._local_done = False
         self.peak_buffer_bytes = 0
         self.ring = 0
         self.records = []
@@ -415,8 +406,6 @@ class DeviceRunner:
             self._track("c", prev.layer)
 
     def _consume(self, layer, step, gen, gemm1_done=False):
-        """(with merge_then and a next layer: that layer's local_block GEMM rides in
-        the same launch)"""
         """u + (shared + routed) fused into the shared-FFN GEMM2 epilogue
         (_consume, schedules.py:308-317; combine_outputs, model.py:279-298)."""
         lw = self.model.layers[layer]
@@ -426,30 +415,13 @@ class DeviceRunner:
             if not gemm1_done:
                 with self._op("shared_gemm1", step, layer):
                     ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
-            nxt = layer + 1 if (self.merge_then and layer + 1 < self.cfg.num_layers) else None
-            if nxt is not None:
-                with self._op("shared_gemm2_consume+local_gemm", step, layer):
-                    ops.consume_then_local(self.hsh, lw.ws2_t, self.h32, self.h16, self.u32, slot,
-                                           self.model.layers[nxt].w_mix_t, self.u32, self.u16)
-                self._local_done = True
-            else:
-                with self._op("shared_gemm2_consume", step, layer):
-                    ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32,
-                             out_bf16=self.h16, residual=self.u32, addend=slot)
+            with self._op("shared_gemm2_consume", step, layer):
+                ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
+                         residual=self.u32, addend=slot)
         else:
             empty = slot.new_empty(self.n, 0)
             ops.combine(slot, slot, empty, self.h32, residual=self.u32, out_bf16=self.h16)
         self.records.append(StalenessRecord(layer=layer, used_step=step, generated_step=gen))
-
-    def _local_gemm(self, step, layer, lw, hin32, hin16):
-        """local_block (model.py:244-252): u = gelu(h W_mix) + h."""
-        with self._op("local_gemm", step, layer):
-            if self.fused_gate:
-                ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
-                                    self.gparts)
-            else:
-                ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
-                         out_bf16=self.u16, residual=hin32)
 
     def _run_step(self, step):
         cfg = self.cfg
@@ -458,10 +430,13 @@ class DeviceRunner:
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
             self._mark(f"local s{step} L{layer}")
-            if self._local_done:       # ran inside the previous layer's consume launch
-                self._local_done = False
-            else:
-                self._local_gemm(step, layer, lw, hin32, hin16)
+            with self._op("local_gemm", step, layer):
+                if self.fused_gate:
+                    ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
+                                        self.gparts)
+                else:
+                    ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
+                             out_bf16=self.u16, residual=hin32)
             self._mark(f"gate+dispatch s{step} L{layer}")
             sync = self._stage_is_sync(step, layer)
             if sync and self.strategy is Strategy.INTERWEAVED:

@@ -357,54 +357,3 @@ def test_expert_gemm1_with_shared_dual_launch():
     nt = int(tiles[-1].item()) * 256
     assert torch.equal(h_a[:nt], h_b[:nt]) and torch.equal(y_a[:nt], y_b[:nt])
     assert torch.equal(hs_a, hs_b)
-
-
-@pytest.mark.parametrize("M,hp", [(8192, 1152), (1000, 1152), (300, 768), (2048, 1792)])
-def test_consume_then_local_dependent_launch(M, hp):
-    """The consume of layer l and the local GEMM of layer l+1 in one launch with
-    per-m-tile dependencies: bit-identical to the two separate launches, also on
-    repeated launches and CUDA-graph replays (counters return to zero)."""
-    g = torch.Generator(device=dev).manual_seed(M + hp)
-    K1 = 2 * 512
-    hsh = (torch.randn(M, K1, device=dev, generator=g) * 0.5).to(torch.bfloat16)
-    ws2 = (torch.randn(hp, K1, device=dev, generator=g) / 32).to(torch.bfloat16)
-    wmix = (torch.randn(hp, hp, device=dev, generator=g) / np.sqrt(hp)).to(torch.bfloat16)
-    u32 = torch.randn(M, hp, device=dev, generator=g)
-    slot = torch.randn(M, hp, device=dev, generator=g)
-    # reference: two launches
-    h32a = torch.empty(M, hp, device=dev); h16a = torch.empty(M, hp, device=dev, dtype=torch.bfloat16)
-    ua = torch.empty(M, hp, device=dev); u16a = torch.empty(M, hp, device=dev, dtype=torch.bfloat16)
-    ops.gemm(ops.EPI_CONSUME, hsh, ws2, out_f32=h32a, out_bf16=h16a, residual=u32, addend=slot)
-    ops.gemm(ops.EPI_GELU_RESID, h16a, wmix, out_f32=ua, out_bf16=u16a, residual=h32a)
-
-    def fused():
-        h32 = torch.full((M, hp), float("nan"), device=dev)
-        h16 = torch.zeros(M, hp, device=dev, dtype=torch.bfloat16)
-        u = u32.clone()            # consume reads u; the local GEMM overwrites it in place
-        u16 = torch.zeros(M, hp, device=dev, dtype=torch.bfloat16)
-        ops.consume_then_local(hsh, ws2, h32, h16, u, slot, wmix, u, u16)
-        return h32, h16, u, u16
-
-    for _ in range(3):
-        h32, h16, u, u16 = fused()
-        torch.cuda.synchronize()
-        assert torch.equal(h32, h32a) and torch.equal(h16, h16a)
-        assert torch.equal(u, ua) and torch.equal(u16, u16a)
-    # graph replay
-    h32 = torch.empty(M, hp, device=dev); h16 = torch.empty(M, hp, device=dev, dtype=torch.bfloat16)
-    u = torch.empty(M, hp, device=dev); u16 = torch.empty(M, hp, device=dev, dtype=torch.bfloat16)
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        u.copy_(u32)
-        ops.consume_then_local(hsh, ws2, h32, h16, u, slot, wmix, u, u16)
-    torch.cuda.synchronize()
-    gr = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gr, stream=s):
-        u.copy_(u32)
-        ops.consume_then_local(hsh, ws2, h32, h16, u, slot, wmix, u, u16)
-    for _ in range(3):
-        h32.zero_(); u16.zero_()
-        gr.replay()
-        torch.cuda.synchronize()
-        assert torch.equal(h32, h32a) and torch.equal(u, ua) and torch.equal(u16, u16a)

@@ -360,21 +360,3 @@ def test_merged_gemm1_engine_bit_identical(strategy, monkeypatch):
         assert r.merge_gemm1 == (merge == "1")
         finals[merge] = r.run().final.values.cpu()
     assert torch.equal(finals["1"], finals["0"])
-
-
-@pytest.mark.parametrize("strategy", ["synchronous", "interweaved"])
-def test_consume_then_local_engine_bit_identical(strategy, monkeypatch):
-    """The engine with layer l's consume and layer l+1's local GEMM in one
-    dependent launch reproduces the separate-launch engine bit for bit."""
-    cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=256,
-                        expert_dim=512, num_tokens=256, batch=4, num_steps=6, step_size=1e-3)
-    model = D.init_model(cfg, seed=9)
-    x0 = D.sample_x0(cfg, 9)
-    pol = D.dice_policy(refresh_interval=2, warmup=2, period=3)
-    finals = {}
-    for merge in ("1", "0"):
-        monkeypatch.setenv("DICE_MERGE_THEN", merge)
-        r = D.DeviceRunner(model, x0, D.Strategy(strategy), pol, D.ClusterConfig(num_devices=1), 9)
-        assert r.merge_then == (merge == "1")
-        finals[merge] = r.run().final.values.cpu()
-    assert torch.equal(finals["1"], finals["0"])
