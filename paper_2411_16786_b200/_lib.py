@@ -113,8 +113,8 @@ def check(rc: int, what: str) -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches count)
-# (stream-K, opt-in, adds a fixup kernel per GEMM; the single-launch permute is the default)
-_SK = 1 if os.environ.get("DICE_GEMM_STREAMK") == "1" else 0
+# (the three-kernel permute is the default; DICE_PERMUTE_FUSED=1 is one launch)
+_SK = 0
 KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSED") == "1" else 3,
                     "dice_grouped_ffn": 2 * (1 + _SK), "dice_gemm": 1 + _SK,
                     "dice_gemm_local_gate": 1, "dice_gate_parts": 0, "dice_event_create": 0,

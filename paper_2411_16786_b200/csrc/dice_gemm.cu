@@ -288,193 +288,6 @@ __device__ __forceinline__ void gate_accumulate(const GemmArgs& a, const float* 
   }
 }
 
-// --------------------------------------------------------------- stream-K
-// Persistent pairs first run whole waves of tiles (data parallel), then split
-// the k-loops of the R < P remainder tiles evenly over all P pairs. A
-// remainder tile is covered by consecutive segments (pair q, tile j); each
-// segment stores its fp32 partial to workspace slot q + j, and a fixup kernel
-// sums the slots of each tile in pair order (deterministic) and applies the
-// epilogue. No CTA ever waits on another, so no co-residency assumption.
-struct SkPlan {
-  int T, KB, P, DP, R;
-  long long I;
-  bool on;
-  int S = 1;   // chained split-K factor (> 1 replaces stream-K)
-  __device__ __forceinline__ void init_chain(int T_, int KB_, int P_, int S_) {
-    T = T_; KB = KB_; P = P_; S = S_; on = false; DP = T; R = 0; I = 0;
-  }
-  __device__ __forceinline__ void init(int T_, int KB_, int P_, bool allow) {
-    T = T_; KB = KB_; P = P_;
-    R = T % P;
-    // only where the partial last wave costs more than the partial sums
-    on = allow && R > 0 && T >= P && T < 8 * P && (long long)R * KB >= 2LL * P;
-    DP = on ? T - R : T;
-    I = on ? (long long)R * KB : 0;
-  }
-  __device__ __forceinline__ long long begin(int q) const { return (long long)q * I / P; }
-  __device__ __forceinline__ int pair_of(long long x) const {
-    int q = (int)(x * P / I);
-    while (q + 1 < P && begin(q + 1) <= x) ++q;
-    while (q > 0 && begin(q) > x) --q;
-    return q;
-  }
-  // number of work items of pair p
-  __device__ __forceinline__ int items(int p) const {
-    if (S > 1) return p < T * S ? (T * S - 1 - p) / P + 1 : 0;
-    int n = p < DP ? (DP - 1 - p) / P + 1 : 0;
-    if (on) {
-      const long long b = begin(p), e = begin(p + 1);
-      if (e > b) n += (int)((e - 1) / KB - b / KB + 1);
-    }
-    return n;
-  }
-  // item i of pair p: tile, k-range [k0, k1), workspace slot (-1 = whole tile)
-  // (chain items: slot = -2 - split)
-  __device__ __forceinline__ void item(int p, int i, int& tile, int& k0, int& k1, int& slot) const {
-    if (S > 1) {
-      // split-major order: item (t, s) follows (t, s-1) by T items (more than a
-      // wave when T >= P), so the partial it adds is usually already written
-      const int idx = p + i * P;
-      const int s = idx / T;
-      tile = idx - s * T;
-      k0 = s * KB / S;
-      k1 = (s + 1) * KB / S;
-      slot = -2 - s;
-      return;
-    }
-    const int ndp = p < DP ? (DP - 1 - p) / P + 1 : 0;
-    if (i < ndp) { tile = p + i * P; k0 = 0; k1 = KB; slot = -1; return; }
-    const long long b = begin(p), e = begin(p + 1);
-    const int jl = (int)(b / KB) + (i - ndp);
-    const long long s0 = (long long)jl * KB > b ? (long long)jl * KB : b;
-    const long long s1 = (long long)(jl + 1) * KB < e ? (long long)(jl + 1) * KB : e;
-    tile = DP + jl;
-    k0 = (int)(s0 - (long long)jl * KB);
-    k1 = (int)(s1 - (long long)jl * KB);
-    slot = p + jl;
-  }
-};
-
-constexpr int kSkMaxSlots = 160;   // >= pairs + remainder tiles (<= 74 + 73)
-
-// fp32 partial of this CTA's 128 rows x 32 columns into the tile's workspace slot
-__device__ __forceinline__ void epilogue_partial(const float* stage, int lane, float* ws_tile,
-                                                 int bn, int row_in_tile0, int col_in_tile) {
-  const int q = lane & 7;
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int rr = it * 4 + (lane >> 3);
-    const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
-    *reinterpret_cast<float4*>(ws_tile + (int64_t)(row_in_tile0 + rr) * bn + col_in_tile + 4 * q) = v;
-  }
-}
-
-// Chained split-K helpers. Partial layout: f32 [tile][256 rows][ld] (this
-// CTA's rows at rank*128). stage += partial of the previous split (L2 reads:
-// the partial was written by another SM during this launch).
-__device__ __forceinline__ void chain_add_prev(float* stage, int lane, const float* ws, int ld,
-                                               int row_in_tile0, int col_in_tile) {
-  const int q = lane & 7;
-  float4 pv[8];
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int rr = it * 4 + (lane >> 3);
-    pv[it] = __ldcg(reinterpret_cast<const float4*>(ws + (int64_t)(row_in_tile0 + rr) * ld +
-                                                    col_in_tile + 4 * q));
-  }
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int rr = it * 4 + (lane >> 3);
-    float4* sp = reinterpret_cast<float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
-    const float4 a = *sp;   // prev + acc: the fixed summation order of the chain
-    *sp = make_float4(pv[it].x + a.x, pv[it].y + a.y, pv[it].z + a.z, pv[it].w + a.w);
-  }
-}
-
-__device__ __forceinline__ void chain_store(const float* stage, int lane, float* ws, int ld,
-                                            int row_in_tile0, int col_in_tile) {
-  const int q = lane & 7;
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int rr = it * 4 + (lane >> 3);
-    const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
-    __stcg(reinterpret_cast<float4*>(ws + (int64_t)(row_in_tile0 + rr) * ld + col_in_tile + 4 * q), v);
-  }
-}
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Sum each remainder tile's partial slots in pair order and apply the epilogue.
-// One block per (remainder tile, 16-row band); the tile's slot range is
-// computed once per block.
-template <int EPI>
-__global__ void __launch_bounds__(256) stream_k_fixup_kernel(const GemmArgs a, const float* ws,
-                                                             int bn, int pairs) {
-  pdl_enter();
-  __shared__ int info[4];   // m_tiles, q0, q1, on
-  if (threadIdx.x == 0)
-    info[0] = a.group_tile_offsets != nullptr ? a.group_tile_offsets[a.num_groups] : a.num_m_tiles;
-  __syncthreads();
-  SkPlan plan;
-  plan.init(info[0] * a.num_n_blocks, a.num_k_blocks, pairs, true);
-  if (!plan.on) return;
-  const int row_limit = a.group_tile_offsets != nullptr ? INT_MAX : a.M_valid;
-  const int c4n = bn / 4;
-  constexpr int kBand = 16;
-  const int bands = plan.R * (256 / kBand);
-  for (int b = blockIdx.x; b < bands; b += gridDim.x) {
-    const int jl = b / (256 / kBand);
-    const int row_base = (b - jl * (256 / kBand)) * kBand;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      info[1] = plan.pair_of((long long)jl * plan.KB);
-      info[2] = plan.pair_of((long long)(jl + 1) * plan.KB - 1);
-    }
-    __syncthreads();
-    const int q0 = info[1], q1 = info[2];
-    const int tile = plan.DP + jl;
-    const int n_blk = tile % a.num_n_blocks, m_tile = tile / a.num_n_blocks;
-    for (int e = threadIdx.x; e < kBand * c4n; e += blockDim.x) {
-      const int rr = e / c4n;
-      const int c4 = e - rr * c4n;
-      const int row_in = row_base + rr;
-      const int col = n_blk * bn + 4 * c4;
-      const int64_t row = (int64_t)m_tile * 256 + row_in;
-      if (col >= a.N || row >= row_limit) continue;
-      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int q = q0; q <= q1; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(
-            ws + ((int64_t)(q + jl) * 256 + row_in) * bn + 4 * c4);
-        x.x += v.x; x.y += v.y; x.z += v.z; x.w += v.w;
-      }
-      if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_GELU_RESID) {
-        const float2 lo = gelu_erf2(make_float2(x.x, x.y));
-        const float2 hi = gelu_erf2(make_float2(x.z, x.w));
-        x = make_float4(lo.x, lo.y, hi.x, hi.y);
-      }
-      if constexpr (EPI == EPI_GELU_RESID) {
-        const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
-        x.x += r.x; x.y += r.y; x.z += r.z; x.w += r.w;
-      }
-      if constexpr (EPI == EPI_CONSUME) {
-        const float4 r = *reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col);
-        const float4 q = *reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col);
-        x.x = r.x + (x.x + q.x); x.y = r.y + (x.y + q.y); x.z = r.z + (x.z + q.z); x.w = r.w + (x.w + q.w);
-      }
-      if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
-      if (a.out_bf16 != nullptr) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
-        *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
-            make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-      }
-    }
-  }
-}
-
 // --------------------------------------------------------- CTA-pair kernel
 // cta_group::2: a cluster of two CTAs computes a 256 x BN tile. Each CTA
 // stages its own 128 rows of A and half (BN/2 rows) of B, so per-CTA operand
@@ -584,20 +397,14 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   };
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
-  SkPlan plan;
-  if (args.ksplit > 1)
-    plan.init_chain(num_tiles, k_blocks, num_pairs, args.ksplit);
-  else
-    plan.init(num_tiles, k_blocks, num_pairs, args.sk_workspace != nullptr);
-  const int n_items = plan.items(pair);
+  const int n_items = pair < num_tiles ? (num_tiles - 1 - pair) / num_pairs + 1 : 0;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0; it < n_items; ++it) {
-        int tile, k0, k1, slot;
-        plan.item(pair, it, tile, k0, k1, slot);
+        const int tile = pair + it * num_pairs, k0 = 0, k1 = k_blocks;
         int prob, n_blk, m_tile;   // N-fastest: resident tiles share A rows
         locate(tile, prob, n_blk, m_tile);
         const int g = prob == 0 ? find_group(sh->group_off, groups, m_tile) : 0;
@@ -623,8 +430,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int stage = 0;
       uint32_t phase = 0;
       for (int local = 0; local < n_items; ++local) {
-        int tile, k0, k1, slot;
-        plan.item(pair, local, tile, k0, k1, slot);
+        const int k0 = 0, k1 = k_blocks;
         const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
         const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
         mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
@@ -658,8 +464,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
     for (int local = 0; local < n_items; ++local) {
-      int tile, k0, k1, slot;
-      plan.item(pair, local, tile, k0, k1, slot);
+      const int tile = pair + local * num_pairs;
       int prob, n_blk, m_tile;
       locate(tile, prob, n_blk, m_tile);
       const GemmArgs& ar = prob == 0 ? args : args2;
@@ -669,17 +474,6 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_wait(&sh->tfull[acc], acc_phase);
       tc_fence_after();
       const int row0 = m_tile * kPairM + rank * BM + sub * 32;
-      float* ws_tile = slot >= 0 ? args.sk_workspace + (int64_t)slot * kPairM * BN : nullptr;
-      // chained split-K item: split index, partial buffer, wait for split - 1
-      const int csplit = slot <= -2 ? -2 - slot : -1;
-      float* cws = csplit >= 0 ? args.chain_ws + (int64_t)tile * kPairM * TN : nullptr;
-      if (!DIRECT && csplit > 0) {
-        if (lane == 0) {
-          const unsigned want = (unsigned)(2 * kEpiWarps * csplit);
-          while (ld_acquire_u32(args.chain_flags + 2 * tile) < want) __nanosleep(64);
-        }
-        __syncwarp();
-      }
       constexpr int GE = EpiTraits<EPI>::gate_e;
       float2 gacc[GE > 0 ? GE / 2 : 1];
 #pragma unroll
@@ -692,7 +486,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * TN + col_in_tile, r);
         tmem_ld_wait();
         if (col0 >= ar.N) continue;  // warp-uniform
-        if constexpr (DIRECT) {   // (the host never enables stream-K for DIRECT)
+        if constexpr (DIRECT) {
           const int64_t row = row0 + lane;
           if (row < rl) epilogue_direct<EPI>(ar, r, row, col0);
           continue;
@@ -703,39 +497,14 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         __syncwarp();
-        if constexpr (GE > 0) {     // (the host never enables stream-K for GATE)
+        if constexpr (GE > 0) {
           epilogue_chunk<EpiTraits<EPI>::base, true>(args, stage, lane, row0, row_limit, col0);
           __syncwarp();
           gate_accumulate<GE>(args, stage, lane, col0, gacc);
-        } else if (ws_tile != nullptr) {
-          epilogue_partial(stage, lane, ws_tile, BN, rank * BM + sub * 32, col_in_tile);
-        } else if (csplit >= 0) {
-          if (csplit > 0) {
-            chain_add_prev(stage, lane, cws, TN, rank * BM + sub * 32, col_in_tile);
-            __syncwarp();
-          }
-          if (csplit < args.ksplit - 1)
-            chain_store(stage, lane, cws, TN, rank * BM + sub * 32, col_in_tile);
-          else
-            epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         } else {
           epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         }
         __syncwarp();
-      }
-      if (!DIRECT && csplit >= 0) {
-        if (csplit < args.ksplit - 1) {
-          __threadfence();           // partial visible before the arrival
-          __syncwarp();
-          if (lane == 0) atomicAdd(args.chain_flags + 2 * tile, 1u);
-        } else {
-          __syncwarp();
-          // the last of the final item's warps returns the tile's counters to 0
-          if (lane == 0 && atomicAdd(args.chain_flags + 2 * tile + 1, 1u) == 2u * kEpiWarps - 1) {
-            args.chain_flags[2 * tile] = 0;
-            args.chain_flags[2 * tile + 1] = 0;
-          }
-        }
       }
       if constexpr (GE > 0) {
         const int64_t row = row0 + lane;
@@ -852,76 +621,9 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int 
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 
-// One stream-K partial-sum workspace per stream (concurrent GEMMs on different
-// streams must not share it). Allocated on first use, before any graph capture.
-std::mutex g_ws_mu;
-std::unordered_map<cudaStream_t, float*> g_ws;
-
-float* stream_k_workspace(cudaStream_t stream) {
-  static int mode = -1;
-  if (mode < 0) {
-    // measured slower on the MoE shapes (partial sums + fixup cost more than the
-    // last-wave tail), so opt-in only: DICE_GEMM_STREAMK=1
-    const char* e = getenv("DICE_GEMM_STREAMK");
-    mode = (e != nullptr && e[0] == '1') ? 1 : 0;
-  }
-  if (mode == 0) return nullptr;
-  std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto it = g_ws.find(stream);
-  if (it != g_ws.end()) return it->second;
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(stream, &st);
-  if (st != cudaStreamCaptureStatusNone) return nullptr;   // never allocate while capturing
-  float* p = nullptr;
-  if (cudaMalloc(&p, sizeof(float) * (size_t)kSkMaxSlots * 256 * 256) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  g_ws[stream] = p;
-  return p;
-}
-
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return (e != nullptr && e[0] != 0) ? atoi(e) : dflt;
-}
-
-// Chained split-K partials + counters, one set per stream, grown only outside
-// graph capture (the warm-up run before capture sizes it).
-struct ChainWs {
-  float* ws = nullptr;
-  unsigned* flags = nullptr;
-  size_t ws_bytes = 0;
-  int tiles = 0;
-};
-std::mutex g_chain_mu;
-std::unordered_map<cudaStream_t, ChainWs> g_chain;
-
-int chain_workspace(cudaStream_t stream, int tiles, int tile_n, float** ws, unsigned** flags) {
-  std::lock_guard<std::mutex> lk(g_chain_mu);
-  ChainWs& c = g_chain[stream];
-  const size_t need = (size_t)tiles * 256 * tile_n * sizeof(float);
-  if (c.ws_bytes < need || c.tiles < tiles) {
-    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &st);
-    if (st != cudaStreamCaptureStatusNone) return DICE_ERR_CONTRACT;   // size it before capture
-    cudaStreamSynchronize(stream);
-    if (c.ws) cudaFree(c.ws);
-    if (c.flags) cudaFree(c.flags);
-    c.ws = nullptr; c.flags = nullptr;
-    if (cudaMalloc(&c.ws, need) != cudaSuccess || cudaMalloc(&c.flags, sizeof(unsigned) * 2 * tiles) != cudaSuccess ||
-        cudaMemset(c.flags, 0, sizeof(unsigned) * 2 * tiles) != cudaSuccess) {
-      cudaGetLastError();
-      c.ws_bytes = 0; c.tiles = 0;
-      return DICE_ERR_CUDA;
-    }
-    cudaDeviceSynchronize();
-    c.ws_bytes = need;
-    c.tiles = tiles;
-  }
-  *ws = c.ws;
-  *flags = c.flags;
-  return 0;
 }
 
 template <int BN, int EPI, bool DIRECT, int NSUB = 1>
@@ -936,36 +638,23 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
       return DICE_ERR_CUDA;
     attr_done = true;
   }
-  const int items = max_tiles * (a.ksplit > 1 ? a.ksplit : 1) +
-                    (a2 != nullptr ? a2->num_m_tiles * a2->num_n_blocks : 0);
+  const int items = max_tiles + (a2 != nullptr ? a2->num_m_tiles * a2->num_n_blocks : 0);
   static const int cta_cap = env_int("DICE_GEMM_MAX_CTAS", 1 << 30);   // experiment hook
   const int sms = num_sms() < cta_cap ? num_sms() : cta_cap;
   int grid = 2 * items < sms ? 2 * items : sms;
   grid &= ~1;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
-  aa.sk_workspace = (DIRECT || NSUB > 1 || EpiTraits<EPI>::gate_e > 0) ? nullptr
-                                                                       : stream_k_workspace(stream);
-  if (aa.ksplit > 1) {
-    if (DIRECT) return DICE_ERR_CONTRACT;
-    const int rc = chain_workspace(stream, max_tiles, NSUB * BN, &aa.chain_ws, &aa.chain_flags);
-    if (rc) return rc;
-  } else {
-    aa.ksplit = 1;
-  }
   // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
   static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
   aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
   GemmArgs bb{};
   if (a2 != nullptr) {
-    if (aa.ksplit > 1 || aa.sk_workspace != nullptr || EpiTraits<EPI>::gate_e > 0)
-      return DICE_ERR_CONTRACT;
+    if (EpiTraits<EPI>::gate_e > 0) return DICE_ERR_CONTRACT;
     bb = *a2;
   }
   launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
              ta, tb, aa, a2 != nullptr ? *ta2 : ta, a2 != nullptr ? *tb2 : tb, bb);
-  if (aa.sk_workspace != nullptr)
-    launch_pdl(stream_k_fixup_kernel<EPI>, dim3(num_sms() * 2), dim3(256), 0, stream, aa, aa.sk_workspace, BN, grid / 2);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 
@@ -1033,7 +722,6 @@ struct TileChoice {
   int tile_n;    // output columns per tile (bn, or 384 for the wide tiles)
   bool pair;     // CTA-pair kernel (256-row tiles)
   bool wide;
-  int ksplit;    // chained split-K factor (wide staged epilogues), 1 = off
 };
 
 TileChoice choose_tile(const GemmProblem& p) {
@@ -1058,7 +746,6 @@ TileChoice choose_tile(const GemmProblem& p) {
   // only when the wave count does not lose what the wider tile gains.
   static const int wide_mode = env_int("DICE_GEMM_WIDE", 1);
   c.wide = false;
-  c.ksplit = 1;
   if (c.pair && c.bn == 192 && p.N % 384 == 0 && wide_mode != 0 && !gate) {
     const int64_t m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + 255) / 256;
     const int pairs = num_sms() / 2;
@@ -1069,24 +756,6 @@ TileChoice choose_tile(const GemmProblem& p) {
     const double narrow = wave_eff(m_tiles * (p.N / 192));
     c.wide = wide_mode == 2 ||
              (direct_epi && p.K >= 2048 && 1.15 * wave_eff(m_tiles * (p.N / 384)) >= narrow);
-    // long-K dense staged epilogues (the shared-FFN GEMM2 + consume): wide tiles
-    // with a chained split-K factor that fills the last wave. Opt-in
-    // (DICE_GEMM_CHAIN=1; 2 forces it): measured slower at the XL consume shape
-    // (172 vs 162 us) because the single TMEM buffer of a 384-wide tile exposes
-    // the heavy f32 consume epilogue of every item.
-    static const int chain_mode = env_int("DICE_GEMM_CHAIN", 0);
-    const bool staged = p.epi_kind == EPI_CONSUME || p.epi_kind == EPI_STORE_F32;
-    if (!c.wide && chain_mode != 0 && staged && p.group_tile_offsets == nullptr && p.K >= 4096) {
-      const int64_t T = m_tiles * (p.N / 384);
-      const int KB = (p.K + BK - 1) / BK;
-      double best = 1.15 * wave_eff(T) - 0.0;
-      int best_s = 1;
-      for (int S = 2; S <= 4 && KB / S >= 16; ++S) {
-        const double e = 1.15 * wave_eff(T * S) - 0.03 * (S - 1);
-        if (e > best) { best = e; best_s = S; }
-      }
-      if (chain_mode == 2 || best > narrow) { c.wide = true; c.ksplit = best_s; }
-    }
   }
   c.tile_n = c.wide ? 384 : c.bn;
   return c;
@@ -1117,7 +786,6 @@ int prepare(const GemmProblem& p, const TileChoice& tc, CUtensorMap* ta, CUtenso
   a->group_tile_offsets = p.group_tile_offsets;
   a->num_groups = p.num_groups;
   a->num_m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + tile_m - 1) / tile_m;
-  a->ksplit = tc.ksplit;
   return 0;
 }
 }  // namespace
@@ -1154,7 +822,7 @@ int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t st
   const bool ok = dual_mode != 0 && direct && p1.K == p2.K && p1.epi_kind == p2.epi_kind &&
                   (p1.epi_kind == EPI_STORE_BF16 || p1.epi_kind == EPI_GELU_BF16) &&
                   p2.group_tile_offsets == nullptr && c1.pair && c2.pair && !c1.wide &&
-                  !c2.wide && c1.bn == c2.bn && c1.ksplit == 1 && c2.ksplit == 1 &&
+                  !c2.wide && c1.bn == c2.bn &&
                   (c1.bn == 256 || c1.bn == 192);
   if (!ok) {
     const int rc = gemm_bf16(p1, stream);

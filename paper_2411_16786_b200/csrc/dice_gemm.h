@@ -55,16 +55,9 @@ struct GemmArgs {
   int64_t ld_res;
   const float* addend;
   int64_t ld_add;
-  float* sk_workspace;   // stream-K partials (pair kernel); null disables stream-K
   int stages;            // operand ring depth actually used (pair kernel; set by the host)
   const float* gate_w;   // GATE epilogues: W_gate f32 [N, E] (row c = hidden column c)
   float* gate_part;      // GATE epilogues: partial logits f32 [P, M, E], P = gemm_gate_parts()
-  // chained split-K (pair kernel, staged epilogues): tile t's k-range is cut
-  // into ksplit items; item s > 0 adds item s-1's fp32 partial (in order, so
-  // deterministic) and the last item applies the epilogue
-  int ksplit;
-  float* chain_ws;       // f32 [tiles, 256, tile_n] partials
-  unsigned* chain_flags; // [tiles, 2] arrival counters (zero between launches)
 };
 
 struct GemmProblem {

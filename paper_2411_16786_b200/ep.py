@@ -528,7 +528,7 @@ class EPRunner:
         control flow is host-deterministic and every buffer is static, so the
         graph replays the identical kernel sequence; x0 is read from a static
         staging buffer (see sample()). The warm-up run uses the capture stream
-        so per-stream library state (stream-K workspace) exists before capture."""
+        so per-stream library state (tensor maps, kernel attributes) exists before capture."""
         self._x0_graph = torch.as_tensor(self.x0.values).to(
             device=self.dev, dtype=torch.float32).contiguous().clone()
         self._cap_stream = torch.cuda.Stream(device=self.dev)
