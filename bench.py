@@ -187,7 +187,8 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
       denoise         14Rh
       local_gemm      2Rh^2;  shared_gemm1 / shared_gemm2_consume 2RhSe each;  grouped_ffn 4heP
       (grouped_ffn+shared_gemm1: the expert FFN launches that also carry the stage's
-       shared GEMM1, 4heP + 2RhSe)
+       shared GEMM1, 4heP + 2RhSe; +combine: the routed combine in the GEMM2 epilogue)
+      slot_init       4Rh (combine slot) + 2h(Rk - P) (cached rows) + 10Rk
     """
     import torch
     r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed, time_ops=True,
@@ -219,10 +220,12 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
             work, kind = 2.0 * R * h * h, "tensor"
         elif name in ("shared_gemm1", "shared_gemm2_consume"):
             work, kind = 2.0 * R * h * S * e, "tensor"
-        elif name == "grouped_ffn":
-            work, kind = 4.0 * h * e * P, "tensor"
-        elif name == "grouped_ffn+shared_gemm1":
-            work, kind = 4.0 * h * e * P + 2.0 * R * h * S * e, "tensor"
+        elif name.startswith("grouped_ffn"):
+            # (+shared_gemm1: the stage's shared GEMM1 rides in the launch;
+            #  +combine: the routed combine is the GEMM2 epilogue)
+            work, kind = 4.0 * h * e * P + (2.0 * R * h * S * e if "shared" in name else 0.0), "tensor"
+        elif name == "slot_init":
+            work, kind = 4 * R * h + 2 * h * (R * k - P) + 10 * R * k, "hbm"
         else:
             continue
         a = agg.setdefault(name, [0.0, 0, 0.0, kind])

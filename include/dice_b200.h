@@ -148,7 +148,7 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
                        const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows,
                        int32_t* pos, int32_t* tile_offsets, int64_t* counters,
                        int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
-                       void* stream);
+                       int32_t* row_pair, void* stream);
 
 /* Upper bound of rows of the padded permuted buffer for n*k pairs over E experts. */
 int64_t dice_permute_max_rows(int64_t n, int k, int E);
@@ -197,6 +197,23 @@ int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const
                                  const uint16_t* B2, int N2, uint16_t* out2, void* stream);
 int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
                       int ep, const int32_t* tile_offsets, uint16_t* y, void* stream);
+
+/* Routed combine fused into the expert GEMM2 (k <= 2; TokenCache.assemble
+ * policies.py:188-208 + the routed part of combine_outputs model.py:295-298).
+ * dice_slot_init: slot[t] = the cached terms of t's inactive pairs, summed in
+ * slot order as acc + round(g * row) (0 when all pairs are fresh); refreshed
+ * pairs' gates / ids persisted. dice_expert_gemm2_combine: y = hbuf W2_e per
+ * expert tile; each output row (pair p = t*k + s, row_pair from
+ * dice_route_permute) is rounded to bf16, written to cache_rows [k, n, hp] when
+ * write[p], and round(gates[p] * row) is added into slot[t] (order-free for
+ * k <= 2, so equal to dice_cache_assemble's result). */
+int dice_slot_init(const uint8_t* active, const uint8_t* write, const float* gates,
+                   const int32_t* ids, int64_t n, int k, int hp, const uint16_t* cache_rows,
+                   float* cache_gates, int32_t* cache_ids, float* slot, void* stream);
+int dice_expert_gemm2_combine(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
+                              int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
+                              const float* gates, const uint8_t* write, int k, int64_t n,
+                              float* slot, uint16_t* cache_rows, void* stream);
 
 /* out[t] = base[t] + sum_s gates[t, s] * rows[s, t] (f32, combine_outputs
  * model.py:279-298 and the consume residual, schedules.py:317). rows f32

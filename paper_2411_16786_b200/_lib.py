@@ -46,7 +46,10 @@ SIGNATURES = {
     "dice_cond_decide": (c_int, [P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int, c_uint64,
                                  P, P, P, P, P, P, P]),
     "dice_route_permute": (c_int, [P, P, c_int64, c_int, c_int, P, c_int, P, c_int64, P, P, P,
-                                   c_int, c_int64, c_int64, P, P]),
+                                   c_int, c_int64, c_int64, P, P, P]),
+    "dice_slot_init": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P]),
+    "dice_expert_gemm2_combine": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P, P, c_int,
+                                          c_int64, P, P, P]),
     "dice_permute_max_rows": (c_int64, [c_int64, c_int, c_int]),
     "dice_permute_scratch_ints": (c_int64, [c_int64, c_int, c_int]),
     "dice_grouped_ffn": (c_int, [P, c_int64, P, P, c_int, c_int, c_int, P, P, P, P]),
@@ -119,6 +122,7 @@ KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSE
                     "dice_grouped_ffn": 2 * (1 + _SK), "dice_gemm": 1 + _SK,
                     "dice_gemm_local_gate": 1, "dice_gate_parts": 0, "dice_event_create": 0,
                     "dice_expert_gemm1_with_dense": 1 + _SK, "dice_expert_gemm2": 1 + _SK,
+                    "dice_slot_init": 1, "dice_expert_gemm2_combine": 1,
                     "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,

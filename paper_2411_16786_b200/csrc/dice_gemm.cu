@@ -314,10 +314,51 @@ struct PairCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 2048;
 };
 
+// Routed combine fused into the expert GEMM2 epilogue (EPI_COMBINE): this lane
+// owns permuted row `row` = pair p = (token t, slot s) and 32 columns. The row
+// is rounded to bf16 exactly as the expert output rows are (the on-wire width),
+// persisted to the token cache when the pair refreshes it (policies.py:203-207),
+// and round(g * row) is added to the token's combine slot with float4 atomics.
+// With k <= 2 terms per token onto a slot pre-initialised with the cached
+// terms, the float sum is order-independent (two terms commute; x + 0 == x),
+// so the result is deterministic and equals cache_assemble's.
+__device__ __forceinline__ void epilogue_combine(const GemmArgs& a, const uint32_t (&r)[32],
+                                                 int64_t row, int col0) {
+  const int p = a.row_pair[row];
+  if (p < 0) return;                       // padding row of an expert group
+  const int k = a.top_k;
+  const int64_t t = p / k;
+  const int s = p - (int)t * k;
+  const float g = a.pair_gates[p];
+  uint32_t w[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+    w[j] = *reinterpret_cast<uint32_t*>(&b);
+  }
+  if (a.pair_write != nullptr && a.pair_write[p] != 0) {
+    uint4* dst = reinterpret_cast<uint4*>(a.cache_rows + ((int64_t)s * a.n_tokens + t) * a.N + col0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+  float4* slot = reinterpret_cast<float4*>(a.slot + t * a.N + col0);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float v0 = __uint_as_float(w[2 * j] << 16), v1 = __uint_as_float(w[2 * j] & 0xFFFF0000u);
+    const float v2 = __uint_as_float(w[2 * j + 1] << 16), v3 = __uint_as_float(w[2 * j + 1] & 0xFFFF0000u);
+    atomicAdd(slot + j, make_float4(__fmul_rn(g, v0), __fmul_rn(g, v1), __fmul_rn(g, v2),
+                                    __fmul_rn(g, v3)));
+  }
+}
+
 // Direct bf16 epilogue: this lane owns one row and 32 consecutive columns.
 template <int EPI>
 __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_t (&r)[32],
                                                 int64_t row, int col0) {
+  if constexpr (EPI == EPI_COMBINE) {
+    epilogue_combine(a, r, row, col0);
+    return;
+  }
   uint32_t w[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -664,6 +705,7 @@ int dispatch_wide(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
   switch (epi) {
     case EPI_STORE_BF16: return launch_pair<192, EPI_STORE_BF16, true, 2>(ta, tb, a, max_tiles, s);
     case EPI_GELU_BF16: return launch_pair<192, EPI_GELU_BF16, true, 2>(ta, tb, a, max_tiles, s);
+    case EPI_COMBINE: return launch_pair<192, EPI_COMBINE, true, 2>(ta, tb, a, max_tiles, s);
     case EPI_STORE_F32: return launch_pair<192, EPI_STORE_F32, false, 2>(ta, tb, a, max_tiles, s);
     case EPI_GELU_RESID: return launch_pair<192, EPI_GELU_RESID, false, 2>(ta, tb, a, max_tiles, s);
     case EPI_CONSUME: return launch_pair<192, EPI_CONSUME, false, 2>(ta, tb, a, max_tiles, s);
@@ -683,6 +725,7 @@ int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
     case EPI_GELU_BF16:
       return direct ? launch_pair<BN, EPI_GELU_BF16, true>(ta, tb, a, max_tiles, s)
                     : launch_pair<BN, EPI_GELU_BF16, false>(ta, tb, a, max_tiles, s);
+    case EPI_COMBINE: return launch_pair<BN, EPI_COMBINE, true>(ta, tb, a, max_tiles, s);
     case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false>(ta, tb, a, max_tiles, s);
     case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false>(ta, tb, a, max_tiles, s);
     case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false>(ta, tb, a, max_tiles, s);
@@ -752,7 +795,8 @@ TileChoice choose_tile(const GemmProblem& p) {
     auto wave_eff = [&](int64_t tiles) {
       return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs);
     };
-    const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16;
+    const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16 ||
+                            p.epi_kind == EPI_COMBINE;
     const double narrow = wave_eff(m_tiles * (p.N / 192));
     c.wide = wide_mode == 2 ||
              (direct_epi && p.K >= 2048 && 1.15 * wave_eff(m_tiles * (p.N / 384)) >= narrow);

@@ -20,6 +20,11 @@ enum EpiKind : int {
   // u rows (gate fused into local_block's GEMM, E = 8 / 16 experts)
   EPI_GELU_RESID_GATE8 = 5,
   EPI_GELU_RESID_GATE16 = 6,
+  // expert GEMM2 with the routed combine fused (k <= 2): each output row (a
+  // (token, slot) pair) is rounded to bf16 as a fresh expert row, persisted to the
+  // token cache when the pair refreshes it, and g * row is added into the
+  // token's combine slot (pre-initialised with its cached terms)
+  EPI_COMBINE = 7,
 };
 
 template <int EPI>
@@ -58,6 +63,15 @@ struct GemmArgs {
   int stages;            // operand ring depth actually used (pair kernel; set by the host)
   const float* gate_w;   // GATE epilogues: W_gate f32 [N, E] (row c = hidden column c)
   float* gate_part;      // GATE epilogues: partial logits f32 [P, M, E], P = gemm_gate_parts()
+  // COMBINE: row -> pair map, per-pair gates / cache-write mask, slot [n, N] f32,
+  // cache rows of the layer bf16 [k, n, N]
+  const int32_t* row_pair;
+  const float* pair_gates;
+  const uint8_t* pair_write;
+  int top_k;
+  int64_t n_tokens;
+  float* slot;
+  __nv_bfloat16* cache_rows;
 };
 
 struct GemmProblem {
@@ -84,6 +98,6 @@ int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, 
                    int key_div, int row_tile, int experts_total, const uint16_t* rows, int hp,
                    uint16_t* x_perm, int32_t* pos, int32_t* tile_offsets, int64_t* counters,
                    int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
-                   cudaStream_t stream);
+                   cudaStream_t stream, int32_t* row_pair = nullptr);
 
 }  // namespace dice

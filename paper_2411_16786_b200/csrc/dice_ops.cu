@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
 __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
     int32_t* pos, const int32_t* __restrict__ block_counts, int32_t* tile_offsets, int key_div,
-    int row_tile) {
+    int row_tile, int32_t* row_pair) {
   pdl_enter();
   __shared__ int wcnt[32][64];
   __shared__ int base[64];
@@ -737,6 +737,15 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     if (blockIdx.x == 0) tile_offsets[E] = tiles;
   }
   __syncthreads();
+  if (row_pair != nullptr && blockIdx.x == 0) {
+    // padding rows of every expert group map to no pair (block 0's bases are
+    // the group starts)
+    for (int ex = 0; ex < E; ++ex) {
+      const int cnt = wcnt[0][ex];
+      const int pad_end = base[ex] + (cnt + row_tile - 1) / row_tile * row_tile;
+      for (int r = base[ex] + cnt + threadIdx.x; r < pad_end; r += blockDim.x) row_pair[r] = -1;
+    }
+  }
   const int64_t P = n * k;
   const int64_t p = (int64_t)blockIdx.x * kPermBlock + threadIdx.x;
   int e = 0, s = 0;
@@ -746,6 +755,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
   if (in_range) valid = pair_of(p, k, ids, active, key_div, e, t, s);
   const int r = block_rank(valid, e, E, wcnt);
   if (in_range) pos[p] = valid ? base[e] + r : -1;
+  if (row_pair != nullptr && valid) row_pair[base[e] + r] = (int32_t)p;   // row -> pair
 }
 
 // ------------------------------------------------- single-launch permute
@@ -983,7 +993,12 @@ __global__ void __launch_bounds__(256) cache_assemble_kernel(
           const uint16_t* hv = reinterpret_cast<const uint16_t*>(&raw[s][j]);
           float v[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) { v[q] = bf16_bits_to_f32(hv[q]); acc[q] = fmaf(g[s], v[q], acc[q]); }
+          // acc + round(g * row): the same two roundings an order-free
+          // (atomic) accumulation of the k <= 2 slot terms produces
+          for (int q = 0; q < 8; ++q) {
+            v[q] = bf16_bits_to_f32(hv[q]);
+            acc[q] = __fadd_rn(acc[q], __fmul_rn(g[s], v[q]));
+          }
           if (rows_out != nullptr) {
             float4* ro = reinterpret_cast<float4*>(rows_out + ((int64_t)s * n + t) * hp + c);
             ro[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -994,6 +1009,61 @@ __global__ void __launch_bounds__(256) cache_assemble_kernel(
         o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
         o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
       }
+    }
+  }
+}
+
+// ------------------------------------------- combine-slot initialisation
+// For the routed combine fused into the expert GEMM2 epilogue (EPI_COMBINE):
+// per token the cached terms of its inactive pairs (policies.py:197-202) summed
+// in slot order as acc + round(g * row), or 0 when every pair is fresh; the
+// refreshed pairs' gates / ids are persisted here (their rows by the epilogue,
+// policies.py:203-207). No entry is both read and written (write => active).
+template <int KMAX>
+__global__ void __launch_bounds__(256) slot_init_kernel(
+    const uint8_t* __restrict__ active, const uint8_t* __restrict__ write,
+    const float* __restrict__ gates, const int32_t* __restrict__ ids, int64_t n, int k, int hp,
+    const uint16_t* __restrict__ cache_rows, float* cache_gates, int32_t* cache_ids, float* slot) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int vec = hp / 8;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint16_t* src[KMAX];
+    float g[KMAX];
+    int cached = 0;
+    for (int s = 0; s < k && s < KMAX; ++s) {
+      const int64_t ps = t * k + s;
+      const bool act = active == nullptr || active[ps] != 0;
+      src[s] = nullptr;
+      g[s] = 0.f;
+      if (!act && cache_rows != nullptr) {
+        src[s] = cache_rows + ((int64_t)s * n + t) * hp;
+        g[s] = cache_gates[ps];
+        ++cached;
+      }
+      if (lane == 0 && act && write != nullptr && write[ps] != 0) {
+        cache_gates[ps] = gates[ps];
+        cache_ids[ps] = ids[ps];
+      }
+    }
+    for (int c8 = lane; c8 < vec; c8 += 32) {
+      float acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+      if (cached) {
+        for (int s = 0; s < k && s < KMAX; ++s) {
+          if (src[s] == nullptr) continue;
+          const uint4 raw = *reinterpret_cast<const uint4*>(src[s] + c8 * 8);
+          const uint16_t* hv = reinterpret_cast<const uint16_t*>(&raw);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            acc[q] = __fadd_rn(acc[q], __fmul_rn(g[s], bf16_bits_to_f32(hv[q])));
+        }
+      }
+      float4* o = reinterpret_cast<float4*>(slot + t * hp + c8 * 8);
+      o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
   }
 }
@@ -1063,11 +1133,6 @@ __global__ void pack_rows_kernel(const float* __restrict__ in, int64_t n, int co
   }
 }
 
-int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int groups,
-                   int key_div, int row_tile, int experts_total, const uint16_t* rows, int hp,
-                   uint16_t* x_perm, int32_t* pos, int32_t* tile_offsets, int64_t* counters,
-                   int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
-                   cudaStream_t s);
 
 static int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
@@ -1082,7 +1147,7 @@ int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, 
                    int key_div, int row_tile, int experts_total, const uint16_t* rows, int hp,
                    uint16_t* x_perm, int32_t* pos, int32_t* tile_offsets, int64_t* counters,
                    int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
-                   cudaStream_t s) {
+                   cudaStream_t s, int32_t* row_pair) {
   const int64_t P = n * k;
   const int blocks = (int)((P + kPermBlock - 1) / kPermBlock);
   if (blocks == 0) {
@@ -1094,7 +1159,7 @@ int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, 
                                                      row0, rows_total, scratch, key_div,
                                                      experts_total);
   launch_pdl(permute_scatter_kernel, dim3(blocks), dim3(kPermBlock), 0, s, ids, active, n, k, groups, pos, scratch,
-                                                       tile_offsets, key_div, row_tile);
+                                                       tile_offsets, key_div, row_tile, row_pair);
   if (x_perm != nullptr)
     launch_pdl(permute_gather_kernel, dim3(grid_for(P * 32, 256)), dim3(256), 0, s, pos, P, rows, k, hp, x_perm);
   return launch_ok();
@@ -1330,7 +1395,7 @@ int64_t dice_permute_scratch_ints(int64_t n, int k, int E) {
 int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
                        const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows, int32_t* pos,
                        int32_t* tile_offsets, int64_t* counters, int devices, int64_t row0,
-                       int64_t rows_total, int32_t* scratch, void* stream) {
+                       int64_t rows_total, int32_t* scratch, int32_t* row_pair, void* stream) {
   if (E < 1 || E > 64 || k < 1 || hp % 64 != 0 || devices < 1 || E % devices != 0)
     return DICE_ERR_CONTRACT;
   if (max_rows < dice_permute_max_rows(n, k, E)) return DICE_ERR_CONTRACT;
@@ -1346,7 +1411,7 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t P = n * k;
-  if (mode != 0 && P > 0 && x_perm != nullptr) {
+  if (mode != 0 && P > 0 && x_perm != nullptr && row_pair == nullptr) {
     int grid = (int)(sms < kFusedPermMaxBlocks ? sms : kFusedPermMaxBlocks);
     if (grid * E > 32 * 64) grid = (32 * 64) / E;   // all blocks' counts fit the smem stage
     unsigned* bar = reinterpret_cast<unsigned*>(scratch + dice_permute_scratch_ints(n, k, E) - 32);
@@ -1357,7 +1422,7 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
   }
   return dice::permute_launch(ids, active, n, k, E, 1, kRowTile, E, u16, hp, x_perm, pos,
                               tile_offsets, counters, devices, row0, rows_total, scratch,
-                              (cudaStream_t)stream);
+                              (cudaStream_t)stream, row_pair);
 }
 
 int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
@@ -1379,6 +1444,37 @@ int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const
   q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out2); q.epi.ld_bf16 = N2;
   if (M2 == 0) return gemm_bf16(p, (cudaStream_t)stream);
   return gemm_bf16_dual(p, q, (cudaStream_t)stream);
+}
+
+int dice_slot_init(const uint8_t* active, const uint8_t* write, const float* gates,
+                   const int32_t* ids, int64_t n, int k, int hp, const uint16_t* cache_rows,
+                   float* cache_gates, int32_t* cache_ids, float* slot, void* stream) {
+  if (hp % 64 != 0 || k < 1 || k > 2) return DICE_ERR_CONTRACT;
+  if (n == 0) return DICE_OK;
+  launch_pdl(slot_init_kernel<2>, dim3(grid_for(n * 32, 256)), dim3(256), 0, (cudaStream_t)stream,
+             active, write, gates, ids, n, k, hp, cache_rows, cache_gates, cache_ids, slot);
+  return launch_ok();
+}
+
+int dice_expert_gemm2_combine(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
+                              int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
+                              const float* gates, const uint8_t* write, int k, int64_t n,
+                              float* slot, uint16_t* cache_rows, void* stream) {
+  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0 ||
+      k < 1 || k > 2 || row_pair == nullptr || gates == nullptr || slot == nullptr)
+    return DICE_ERR_CONTRACT;
+  GemmProblem q{};
+  q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
+  q.num_groups = E; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / kRowTile);
+  q.epi_kind = EPI_COMBINE;
+  q.epi.row_pair = row_pair;
+  q.epi.pair_gates = gates;
+  q.epi.pair_write = write;
+  q.epi.top_k = k;
+  q.epi.n_tokens = n;
+  q.epi.slot = slot;
+  q.epi.cache_rows = reinterpret_cast<__nv_bfloat16*>(cache_rows);
+  return gemm_bf16(q, (cudaStream_t)stream);
 }
 
 int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,

@@ -170,12 +170,15 @@ def permute_scratch_ints(n, k, E):
 
 
 def route_permute(ids, active, u16, x_perm, pos, tile_offsets, counters, scratch, E,
-                  devices=1, row0=0, rows_total=None):
+                  devices=1, row0=0, rows_total=None, row_pair=None):
+    """row_pair (int32 [max_rows], optional): permuted row -> pair index t*k+s
+    (-1 on padding rows), for the fused expert GEMM2 combine."""
     n, k = ids.shape
     hp = u16.shape[1]
     _lib.call("dice_route_permute", _ptr(ids), _ptr(active), n, k, E, _ptr(u16), hp,
               _ptr(x_perm), x_perm.shape[0], _ptr(pos), _ptr(tile_offsets), _ptr(counters),
-              devices, row0, n if rows_total is None else rows_total, _ptr(scratch), _stream())
+              devices, row0, n if rows_total is None else rows_total, _ptr(scratch),
+              _ptr(row_pair), _stream())
 
 
 def grouped_ffn(x_perm, w1_t, w2_t, E, tile_offsets, hbuf, y):
@@ -200,6 +203,25 @@ def expert_gemm2(hbuf, w2_t, E, tile_offsets, y):
     hp = y.shape[1]
     _lib.call("dice_expert_gemm2", _ptr(hbuf), max_rows, _ptr(w2_t), E, hp, ep, _ptr(tile_offsets),
               _ptr(y), _stream())
+
+
+def slot_init(active, write, gates, ids, slot, cache_rows=None, cache_gates=None, cache_ids=None):
+    n, k = gates.shape
+    hp = slot.shape[1]
+    _lib.call("dice_slot_init", _ptr(active), _ptr(write), _ptr(gates), _ptr(ids), n, k, hp,
+              _ptr(cache_rows), _ptr(cache_gates), _ptr(cache_ids), _ptr(slot), _stream())
+
+
+def expert_gemm2_combine(hbuf, w2_t, E, tile_offsets, row_pair, gates, write, slot,
+                         cache_rows=None):
+    """Expert GEMM2 whose epilogue adds round(g * row) of every pair into its
+    token's combine slot and persists refreshed rows to the token cache."""
+    max_rows, ep = hbuf.shape
+    n, k = gates.shape
+    hp = slot.shape[1]
+    _lib.call("dice_expert_gemm2_combine", _ptr(hbuf), max_rows, _ptr(w2_t), E, hp, ep,
+              _ptr(tile_offsets), _ptr(row_pair), _ptr(gates), _ptr(write), k, n, _ptr(slot),
+              _ptr(cache_rows), _stream())
 
 
 def cache_assemble(y, pos, active, write, gates, ids, routed, cache_rows=None, cache_gates=None,

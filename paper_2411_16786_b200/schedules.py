@@ -122,7 +122,7 @@ class GpuTimeline:
 class _Payload:
     """Device buffers of one dispatch (DispatchPayload, schedules.py:48-57)."""
 
-    def __init__(self, n, k, E, hp, max_rows, device):
+    def __init__(self, n, k, E, hp, max_rows, device, row_pair=False):
         self.ids = torch.zeros(n, k, dtype=torch.int32, device=device)
         self.gates = torch.zeros(n, k, dtype=torch.float32, device=device)
         self.active = torch.ones(n, k, dtype=torch.uint8, device=device)
@@ -130,6 +130,9 @@ class _Payload:
         self.pos = torch.zeros(n, k, dtype=torch.int32, device=device)
         self.tiles = torch.zeros(E + 1, dtype=torch.int32, device=device)
         self.x_perm = torch.empty(max_rows, hp, dtype=torch.bfloat16, device=device)
+        # permuted row -> (token, slot) pair, for the combine fused into GEMM2
+        self.row_pair = (torch.full((max_rows,), -1, dtype=torch.int32, device=device)
+                         if row_pair else None)
         self.layer = -1
         self.gen = -1
         self.done = None     # side-stream event: expert FFN + merge of this payload finished
@@ -186,12 +189,19 @@ class DeviceRunner:
         L = cfg.num_layers
         nslots = 1 if strategy is Strategy.SYNCHRONOUS else L
         self.slots = torch.zeros(nslots, n, hp, dtype=f32, device=dev)
+        # DICE_FUSED_COMBINE=1: the routed combine (stale-cache merge + sum over
+        # slots) in the expert GEMM2 epilogue via float4 atomics onto a slot
+        # pre-initialised with the cached terms (k <= 2; bit-identical to the
+        # assemble kernel). Measured slower in-step (slot init 21 us + 19 us more
+        # GEMM2 epilogue vs a 26 us assemble), so opt-in.
+        self.fused_combine = k <= 2 and os.environ.get("DICE_FUSED_COMBINE", "0") == "1"
+        fc = self.fused_combine
         if strategy is Strategy.SYNCHRONOUS:
-            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev)]
+            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev, fc)]
         elif strategy is Strategy.INTERWEAVED:
-            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(3)]
+            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev, fc) for _ in range(3)]
         else:
-            self.payloads = [[_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(2)]
+            self.payloads = [[_Payload(n, k, E, hp, self.max_rows, dev, fc) for _ in range(2)]
                              for _ in range(L)]
         self.cache = None
         if policy.cond_strategy is not CondStrategy.OFF:
@@ -337,7 +347,8 @@ class DeviceRunner:
         with self._op("permute", step, layer):
             ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
                               self.counters[step, layer], self.scratch, self.E,
-                              devices=self.cluster.num_devices, row0=0, rows_total=self.n)
+                              devices=self.cluster.num_devices, row0=0, rows_total=self.n,
+                              row_pair=p.row_pair)
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 
@@ -371,31 +382,54 @@ class DeviceRunner:
         inside the expert GEMM1 launch."""
         self._mark(f"expert s{p.gen} L{p.layer}")
         lw = self.model.layers[p.layer]
+        c = self.cache
+        if self.fused_combine:
+            # combine slot <- cached terms of the inactive pairs; the GEMM2 epilogue
+            # adds the fresh ones (TokenCache.assemble, policies.py:188-208)
+            with self._op("slot_init", p.gen, p.layer):
+                ops.slot_init(None if c is None else p.active, None if c is None else p.write,
+                              p.gates, p.ids, self._slot(p.layer),
+                              None if c is None else c.rows[p.layer],
+                              None if c is None else c.gates[p.layer],
+                              None if c is None else c.expert_ids[p.layer])
         if self.time_experts:
             i = len(self._expert_events)
             if i >= len(self._event_pool):
                 self._event_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
             e0, e1 = self._event_pool[i]
             e0.record()
-        if shared_layer is None:
-            with self._op("grouped_ffn", p.gen, p.layer):
+        name = "grouped_ffn" if shared_layer is None else "grouped_ffn+shared_gemm1"
+        if self.fused_combine:
+            name += "+combine"
+        with self._op(name, p.gen, p.layer):
+            if shared_layer is None and not self.fused_combine:
                 ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
-        else:
-            with self._op("grouped_ffn+shared_gemm1", p.gen, p.layer):
-                ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
-                                             self.u16, self.model.layers[shared_layer].ws1_t,
-                                             self.hsh)
-                ops.expert_gemm2(self.hbuf, lw.w2_t, self.E, p.tiles, self.y)
+            else:
+                if shared_layer is None:
+                    ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
+                                                 self.u16[:0], lw.w1_t, self.hsh)
+                else:
+                    ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
+                                                 self.u16, self.model.layers[shared_layer].ws1_t,
+                                                 self.hsh)
+                if self.fused_combine:
+                    ops.expert_gemm2_combine(self.hbuf, lw.w2_t, self.E, p.tiles, p.row_pair,
+                                             p.gates, None if c is None else p.write,
+                                             self._slot(p.layer),
+                                             None if c is None else c.rows[p.layer])
+                else:
+                    ops.expert_gemm2(self.hbuf, lw.w2_t, self.E, p.tiles, self.y)
         if self.time_experts:
             e1.record()
             self._expert_events.append((e0, e1, p.gen, p.layer, shared_layer is not None))
-        c = self.cache
-        with self._op("cache_assemble", p.gen, p.layer):
-            ops.cache_assemble(self.y, p.pos, None if c is None else p.active,
-                               None if c is None else p.write, p.gates, p.ids, self._slot(p.layer),
-                               None if c is None else c.rows[p.layer],
-                               None if c is None else c.gates[p.layer],
-                               None if c is None else c.expert_ids[p.layer])
+        if not self.fused_combine:
+            with self._op("cache_assemble", p.gen, p.layer):
+                ops.cache_assemble(self.y, p.pos, None if c is None else p.active,
+                                   None if c is None else p.write, p.gates, p.ids,
+                                   self._slot(p.layer),
+                                   None if c is None else c.rows[p.layer],
+                                   None if c is None else c.gates[p.layer],
+                                   None if c is None else c.expert_ids[p.layer])
         self.slot_gen[p.layer] = p.gen
         self.combine_log.append((p.gen, p.layer))
 

@@ -157,6 +157,7 @@ class _FakeOps:
     status_reset = splitmix_fill = gate_topk = cond_decide = route_permute = _noop
     grouped_ffn = cache_assemble = gemm = combine = denoise = pack_rows = _noop
     gemm_local_gate = gate_finish = expert_gemm1_with_shared = expert_gemm2 = _noop
+    slot_init = expert_gemm2_combine = _noop
 
 
 def _cpu_model(cfg):

@@ -261,3 +261,56 @@ def test_expert_gemm1_with_shared_dual_launch():
     nt = int(tiles[-1].item()) * 256
     assert torch.equal(h_a[:nt], h_b[:nt]) and torch.equal(y_a[:nt], y_b[:nt])
     assert torch.equal(hs_a, hs_b)
+
+
+@pytest.mark.parametrize("k,masked", [(2, True), (2, False), (1, True)])
+def test_fused_combine_matches_cache_assemble(k, masked):
+    """Routed combine in the expert GEMM2 epilogue (slot init with the cached
+    terms + float4 atomic adds of round(g * row)) == expert GEMM2 then
+    cache_assemble: combine slot, cache rows, gates and ids bit-identical, and
+    run-to-run identical (k <= 2 terms per token commute)."""
+    n, E, hp, ep = 2000, 8, 1152, 512
+    g = torch.Generator(device=dev).manual_seed(21 + k)
+    ids = torch.randint(0, E, (n, k), dtype=torch.int32, device=dev, generator=g)
+    gates = torch.rand(n, k, device=dev, generator=g)
+    u16 = (torch.randn(n, hp, device=dev, generator=g) * 0.5).to(torch.bfloat16)
+    w1 = (torch.randn(E * ep, hp, device=dev, generator=g) / 34).to(torch.bfloat16)
+    w2 = (torch.randn(E * hp, ep, device=dev, generator=g) / 23).to(torch.bfloat16)
+    if masked:
+        active = (torch.rand(n, k, device=dev, generator=g) > 0.35).to(torch.uint8)
+        write = ((torch.rand(n, k, device=dev, generator=g) > 0.5).to(torch.uint8) * active)
+    else:
+        active = write = None
+    rows0 = (torch.randn(k, n, hp, device=dev, generator=g)).to(torch.bfloat16)
+    cg0 = torch.rand(n, k, device=dev, generator=g)
+    ci0 = torch.randint(0, E, (n, k), dtype=torch.int32, device=dev, generator=g)
+    max_rows = ops.permute_max_rows(n, k, E)
+    x_perm = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
+    pos = torch.empty(n, k, dtype=torch.int32, device=dev)
+    tiles = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    scr = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+    row_pair = torch.empty(max_rows, dtype=torch.int32, device=dev)
+    ops.route_permute(ids, active, u16, x_perm, pos, tiles, cnt, scr, E, row_pair=row_pair)
+    hbuf = torch.zeros(max_rows, ep, dtype=torch.bfloat16, device=dev)
+    y = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
+    # reference path
+    rows_a, cg_a, ci_a = rows0.clone(), cg0.clone(), ci0.clone()
+    slot_a = torch.full((n, hp), float("nan"), device=dev)
+    ops.grouped_ffn(x_perm, w1, w2, E, tiles, hbuf, y)
+    ops.cache_assemble(y, pos, active, write, gates, ids, slot_a, rows_a if masked else None,
+                       cg_a if masked else None, ci_a if masked else None)
+    outs = []
+    for _ in range(2):
+        rows_b, cg_b, ci_b = rows0.clone(), cg0.clone(), ci0.clone()
+        slot_b = torch.full((n, hp), float("nan"), device=dev)
+        ops.slot_init(active, write, gates, ids, slot_b, rows_b if masked else None,
+                      cg_b if masked else None, ci_b if masked else None)
+        ops.expert_gemm2_combine(hbuf, w2, E, tiles, row_pair, gates, write, slot_b,
+                                 rows_b if masked else None)
+        torch.cuda.synchronize()
+        outs.append(slot_b.clone())
+        assert torch.equal(slot_b, slot_a)
+        if masked:
+            assert torch.equal(rows_b, rows_a) and torch.equal(cg_b, cg_a) and torch.equal(ci_b, ci_a)
+    assert torch.equal(outs[0], outs[1])

@@ -360,3 +360,24 @@ def test_merged_gemm1_engine_bit_identical(strategy, monkeypatch):
         assert r.merge_gemm1 == (merge == "1")
         finals[merge] = r.run().final.values.cpu()
     assert torch.equal(finals["1"], finals["0"])
+
+
+@pytest.mark.parametrize("strategy", ["synchronous", "interweaved", "displaced"])
+def test_fused_combine_engine_bit_identical(strategy, monkeypatch):
+    """The engine with the routed combine in the expert GEMM2 epilogue reproduces
+    the separate cache_assemble engine bit for bit (DICE policy: stale cache
+    reads, refresh writes, strict off)."""
+    cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=256,
+                        expert_dim=512, num_tokens=256, batch=4, num_steps=8, step_size=1e-3)
+    model = D.init_model(cfg, seed=11)
+    x0 = D.sample_x0(cfg, 11)
+    pol = D.dice_policy(refresh_interval=2, warmup=2, period=3)
+    out = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("DICE_FUSED_COMBINE", fused)   # (opt-in path vs default)
+        r = D.DeviceRunner(model, x0, D.Strategy(strategy), pol, D.ClusterConfig(num_devices=2), 11)
+        assert r.fused_combine == (fused == "1")
+        res = r.run()
+        out[fused] = (res.final.values.cpu(), res.dispatch_bytes, res.active_pairs)
+    assert torch.equal(out["1"][0], out["0"][0])
+    assert out["1"][1:] == out["0"][1:]
