@@ -263,6 +263,66 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   }
 }
 
+// Residual prefetch for the local_block epilogue: the lane's 8 rows x 4 columns
+// of the chunk land by cp.async in the same XOR-swizzled 32x32 layout as the
+// accumulator staging tile (zero-filled past the last row).
+__device__ __forceinline__ void resid_prefetch(const GemmArgs& a, float* rbuf, int lane, int row0,
+                                               int row_limit, int col0) {
+  const int q = lane & 7;
+  const int col = col0 + 4 * q;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    const int64_t row = row0 + rr;
+    const bool ok = row < row_limit;
+    const float* src = a.residual + (ok ? row : 0) * a.ld_res + col;
+    const uint32_t dst = smem_u32(rbuf + rr * 32 + ((q ^ (rr & 7)) << 2));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "r"(ok ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void resid_wait() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
+// GELU_RESID epilogue with the residual already in smem (rbuf); when `next_col0`
+// is valid the next chunk's residual prefetch is issued once this chunk's has
+// been read into registers.
+__device__ __forceinline__ void epilogue_gelu_resid_pf(const GemmArgs& a, const float* stage,
+                                                       float* rbuf, int lane, int row0,
+                                                       int row_limit, int col0, int next_col0) {
+  const int q = lane & 7;
+  const int col = col0 + 4 * q;
+  float4 r[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    r[it] = *reinterpret_cast<const float4*>(rbuf + rr * 32 + ((q ^ (rr & 7)) << 2));
+  }
+  __syncwarp();
+  if (next_col0 >= 0) resid_prefetch(a, rbuf, lane, row0, row_limit, next_col0);
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    const float4 v = *reinterpret_cast<const float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2));
+    const float2 lo = gelu_erf2(make_float2(v.x, v.y));
+    const float2 hi = gelu_erf2(make_float2(v.z, v.w));
+    const float4 x = make_float4(lo.x + r[it].x, lo.y + r[it].y, hi.x + r[it].z, hi.y + r[it].w);
+    const int64_t row = row0 + rr;
+    if (row < row_limit) {
+      if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
+      if (a.out_bf16 != nullptr) {
+        __nv_bfloat162 l2 = __floats2bfloat162_rn(x.x, x.y), h2 = __floats2bfloat162_rn(x.z, x.w);
+        *reinterpret_cast<uint2*>(a.out_bf16 + row * a.ld_bf16 + col) =
+            make_uint2(*reinterpret_cast<uint32_t*>(&l2), *reinterpret_cast<uint32_t*>(&h2));
+      }
+    }
+  }
+}
+
 // Router logits of the finished u rows (gate, model.py:209-223, fused into the
 // local_block GEMM): the lane owning row `lane` of the transpose tile dots its
 // 32 finished values with W_gate[col0 .. col0+32, :] (warp-uniform broadcast
@@ -296,7 +356,7 @@ __device__ __forceinline__ void gate_accumulate(const GemmArgs& a, const float* 
 // NSUB > 1: a 256 x (NSUB*BN) tile of NSUB accumulators sharing each staged A
 // block (per-SM operand bytes per MMA cycle fall from 8192/BN + 32 to
 // 8192/(NSUB*BN) + 32), single-buffered in TMEM.
-template <int BN, bool DIRECT, int NSUB>
+template <int BN, bool DIRECT, int NSUB, bool RESID_PF = false>
 struct PairCfg {
   static constexpr int kTN = NSUB * BN;
   static constexpr int kAccBufs = NSUB == 1 ? 2 : 1;
@@ -306,7 +366,9 @@ struct PairCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   // bf16-only epilogues store straight from registers (64 contiguous bytes of
   // one row per lane, whole sectors), so their smem goes to the operand ring
-  static constexpr int kEpiBytes = DIRECT ? 0 : kEpiWarps * 32 * 32 * 4;
+  // RESID_PF (the local_block GELU_RESID epilogue): a second 32x32 f32 tile per
+  // epilogue warp receives the chunk's residual by cp.async ahead of its use
+  static constexpr int kEpiBytes = DIRECT ? 0 : kEpiWarps * 32 * 32 * 4 * (RESID_PF ? 2 : 1);
   static constexpr int kBudget = 232448 - kEpiBytes - 2048;
   static constexpr int kStages = kBudget / kStageBytes > kMaxStages ? kMaxStages : kBudget / kStageBytes;
   static constexpr int kTmemCols = kAccBufs * kTN <= 256 ? 256 : 512;
@@ -380,7 +442,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   // args2.num_m_tiles > 0: a second, dense problem with the same K and epilogue
   // kind runs in the same persistent launch; its tiles follow the first's
   // (one launch and one wave tail for two independent GEMMs)
-  using C = PairCfg<BN, DIRECT, NSUB>;
+  constexpr bool kResidPF = EPI == EPI_GELU_RESID;
+  using C = PairCfg<BN, DIRECT, NSUB, kResidPF>;
   constexpr int TN = C::kTN;
   const int kStages = args.stages;   // <= C::kStages (host-clamped)
   constexpr int kPairM = 2 * BM;
@@ -501,6 +564,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int sub = warp & 3;
     const int grp = (warp - 4) >> 2;
     float* stage = sm_epi + (warp - 4) * 1024;
+    float* rbuf = sm_epi + kEpiWarps * 1024 + (warp - 4) * 1024;   // (kResidPF only)
     const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
@@ -512,9 +576,13 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int rl = prob == 0 ? row_limit : args2.M_valid;
       const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
       const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
+      const int row0 = m_tile * kPairM + rank * BM + sub * 32;
+      if constexpr (kResidPF) {   // first chunk's residual while the MMAs run
+        if (grp * 32 < TN && n_blk * TN + grp * 32 < ar.N)
+          resid_prefetch(ar, rbuf, lane, row0, rl, n_blk * TN + grp * 32);
+      }
       mbar_wait(&sh->tfull[acc], acc_phase);
       tc_fence_after();
-      const int row0 = m_tile * kPairM + rank * BM + sub * 32;
       constexpr int GE = EpiTraits<EPI>::gate_e;
       float2 gacc[GE > 0 ? GE / 2 : 1];
 #pragma unroll
@@ -542,6 +610,12 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           epilogue_chunk<EpiTraits<EPI>::base, true>(args, stage, lane, row0, row_limit, col0);
           __syncwarp();
           gate_accumulate<GE>(args, stage, lane, col0, gacc);
+        } else if constexpr (kResidPF) {
+          resid_wait();
+          const int nci = ci + kEpiGroups;
+          const int ncol = n_blk * TN + nci * 32;
+          epilogue_gelu_resid_pf(ar, stage, rbuf, lane, row0, rl, col0,
+                                 (nci < TN / 32 && ncol < ar.N) ? ncol : -1);
         } else {
           epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         }
@@ -671,7 +745,7 @@ template <int BN, int EPI, bool DIRECT, int NSUB = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
                 const CUtensorMap* tb2 = nullptr, const GemmArgs* a2 = nullptr) {
-  using C = PairCfg<BN, DIRECT, NSUB>;
+  using C = PairCfg<BN, DIRECT, NSUB, EPI == EPI_GELU_RESID>;
   static bool attr_done = false;
   if (!attr_done) {
     if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
