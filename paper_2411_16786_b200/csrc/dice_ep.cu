@@ -166,13 +166,25 @@ int dice_stream_wait_eq(const uint64_t* addrs, int count, uint32_t value, void* 
   BatchMemOpFn fn = batch_memop();
   if (fn == nullptr || count < 0 || count > 64) return DICE_ERR_CUDA;
   if (count == 0) return DICE_OK;
+  // the ready flags are written by peer GPUs after their P2P row stores: where
+  // the device supports it, the wait also flushes outstanding remote writes so
+  // the rows are visible to the kernels behind it
+  static const unsigned flush = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev) != cudaSuccess) {
+      cudaGetLastError();
+      v = 0;
+    }
+    return v ? (unsigned)CU_STREAM_WAIT_VALUE_FLUSH : 0u;
+  }();
   CUstreamBatchMemOpParams ops[64];
   memset(ops, 0, sizeof(ops));
   for (int i = 0; i < count; ++i) {
     ops[i].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
     ops[i].waitValue.address = (CUdeviceptr)addrs[i];
     ops[i].waitValue.value = value;
-    ops[i].waitValue.flags = CU_STREAM_WAIT_VALUE_EQ;
+    ops[i].waitValue.flags = CU_STREAM_WAIT_VALUE_EQ | flush;
   }
   return fn((CUstream)stream, (unsigned)count, ops, 0) == CUDA_SUCCESS ? DICE_OK : DICE_ERR_CUDA;
 }
