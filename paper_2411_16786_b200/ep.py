@@ -536,9 +536,17 @@ class EPRunner:
         with torch.cuda.stream(self._cap_stream):
             self.launch(self._x0_graph)          # warm: kernel attributes, tensor maps
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=self._cap_stream):
-            self.launch(self._x0_graph)
+        # no garbage collection inside the capture: freeing an earlier runner's
+        # graph or events mid-capture would invalidate it
+        import gc
+        gc.collect()
+        gc.disable()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self._cap_stream):
+                self.launch(self._x0_graph)
+        finally:
+            gc.enable()
         torch.cuda.synchronize()
         self.graph = g
         return self
