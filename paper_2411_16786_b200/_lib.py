@@ -117,16 +117,15 @@ def check(rc: int, what: str) -> None:
 
 # kernels each entry point launches (for the bench's gpu_launches count)
 # (the three-kernel permute is the default; DICE_PERMUTE_FUSED=1 is one launch)
-_SK = 0
 KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSED") == "1" else 3,
-                    "dice_grouped_ffn": 2 * (1 + _SK), "dice_gemm": 1 + _SK,
+                    "dice_grouped_ffn": 2, "dice_gemm": 1,
                     "dice_gemm_local_gate": 1, "dice_gate_parts": 0, "dice_event_create": 0,
-                    "dice_expert_gemm1_with_dense": 1 + _SK, "dice_expert_gemm2": 1 + _SK,
+                    "dice_expert_gemm1_with_dense": 1, "dice_expert_gemm2": 1,
                     "dice_slot_init": 1, "dice_expert_gemm2_combine": 1,
                     "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,
-                    "dice_stream_write": 0, "dice_ep_dispatch": 3, "dice_ep_expert": 7 + 2 * _SK}
+                    "dice_stream_write": 0, "dice_ep_dispatch": 3, "dice_ep_expert": 7}
 launch_count = [0]
 
 
