@@ -968,9 +968,7 @@ __global__ void __launch_bounds__(256) cache_assemble_kernel(
         if (gates_out != nullptr) gates_out[ps] = g[s];
       }
     }
-    // 8-column chunks per lane per batch (k*CH loads in flight): one batch covers
-    // a 1280-wide row for k <= 2
-    constexpr int CH = KMAX <= 2 ? 5 : 3;
+    constexpr int CH = 3;  // 8-column chunks per lane per batch (k*CH loads in flight)
     for (int base = 0; base < vec; base += 32 * CH) {
       uint4 raw[KMAX][CH];
       for (int s = 0; s < k && s < KMAX; ++s) {
