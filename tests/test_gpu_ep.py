@@ -72,3 +72,43 @@ def test_ep_two_ranks_matches_single_gpu(strategy, policy, world):
         assert part["pairs"].tolist() == [ref.active_pairs, ref.total_pairs]
         assert part["per_step"].tolist() == ref.per_step_active_pairs
         assert int(part["peak"]) == ref.peak_buffer_bytes
+
+
+def test_ep_xl_widths_matches_single_gpu():
+    """Expert parallelism at the XL layer widths (h=1152, e=4608, 8 experts,
+    2 shared; 4 layers, 3 steps, full DICE policy): the 2-rank run over peer
+    memory reproduces the single-GPU engine bit-exactly — the bench geometry's
+    tile shapes (256x384 expert GEMM2, dual GEMM1 launches) on both sides."""
+    world = 2
+    cfg_kw = dict(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=1152,
+                  expert_dim=4608, num_tokens=256, batch=4, num_steps=3, step_size=2e-5)
+    same = torch.cuda.device_count() < world
+    port = free_port()
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "ep")
+        procs = []
+        for rank in range(world):
+            arg = json.dumps(dict(rank=rank, world=world, port=port, cfg_kwargs=cfg_kw,
+                                  strategy="interweaved", policy_name="dice", out_path=out,
+                                  same_device=same))
+            procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "ep_worker.py"), arg]))
+        for p in procs:
+            try:
+                p.wait(timeout=300)
+            except subprocess.TimeoutExpired:
+                for q in procs:
+                    q.kill()
+                pytest.fail("EP workers timed out")
+            assert p.returncode == 0
+        parts = [np.load(f"{out}.rank{r}.npz") for r in range(world)]
+    cfg = D.ModelConfig(**cfg_kw)
+    model = D.init_model(cfg, seed=5)
+    x0 = D.sample_x0(cfg, 5)
+    pol = D.dice_policy(refresh_interval=2, warmup=2, period=3)
+    ref = D.run_sampling(model, x0, D.Strategy.INTERWEAVED, pol, D.ClusterConfig(num_devices=world), 5)
+    fin = ref.final.values.cpu().numpy()
+    for part in parts:
+        a, b = part["rows"]
+        assert np.array_equal(part["final"], fin[a:b])
+        assert part["bytes"].tolist() == [ref.dispatch_bytes, ref.combine_bytes]
+        assert part["pairs"].tolist() == [ref.active_pairs, ref.total_pairs]
