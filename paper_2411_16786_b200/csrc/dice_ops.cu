@@ -1544,6 +1544,7 @@ int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, i
   p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out_bf16); p.epi.ld_bf16 = ld_bf16;
   p.epi.residual = residual; p.epi.ld_res = ld_res;
   p.epi.addend = addend; p.epi.ld_add = ld_add;
+  if (epi < EPI_STORE_BF16 || epi > EPI_CONSUME) return DICE_ERR_CONTRACT;   // public kinds only
   if ((epi == EPI_GELU_RESID || epi == EPI_CONSUME) && residual == nullptr) return DICE_ERR_CONTRACT;
   if (epi == EPI_CONSUME && addend == nullptr) return DICE_ERR_CONTRACT;
   return gemm_bf16(p, (cudaStream_t)stream);

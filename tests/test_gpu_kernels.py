@@ -314,3 +314,13 @@ def test_fused_combine_matches_cache_assemble(k, masked):
         if masked:
             assert torch.equal(rows_b, rows_a) and torch.equal(cg_b, cg_a) and torch.equal(ci_b, ci_a)
     assert torch.equal(outs[0], outs[1])
+
+
+def test_gemm_rejects_internal_epilogue_kinds():
+    A = torch.zeros(256, 64, device=dev, dtype=torch.bfloat16)
+    B = torch.zeros(64, 64, device=dev, dtype=torch.bfloat16)
+    o = torch.empty(256, 64, device=dev, dtype=torch.bfloat16)
+    from paper_2411_16786_b200.errors import ContractError
+    for epi in (-1, 5, 6, 7, 99):
+        with pytest.raises(ContractError):
+            ops.gemm(epi, A, B, out_bf16=o)
