@@ -595,6 +595,48 @@ class DeviceRunner:
         torch.cuda.current_stream().synchronize()
         return self._final_host
 
+    def sample_many(self, x0_hosts, out_hosts) -> None:
+        """Serve a sequence of batches (x0_hosts[i] -> out_hosts[i], pinned host
+        tensors [R, h] f32) with the copies off the critical path: batch i's H2D
+        and batch i-1's D2H run on a copy stream while batch i-1 / i replay, via
+        double-buffered device staging. Needs capture(). Returns when every
+        output has landed in host memory."""
+        if self.graph is None:
+            raise ContractError("sample_many needs a captured run (capture())")
+        h = self.cfg.hidden_dim
+        if not hasattr(self, "_pipe"):
+            mk = lambda: torch.empty(self.n, h, dtype=torch.float32, device=self.dev)
+            ev = lambda: torch.cuda.Event()
+            self._pipe = dict(copy=torch.cuda.Stream(device=self.dev),
+                              inb=[mk(), mk()], outb=[mk(), mk()],
+                              in_ready=[ev(), ev()], in_free=[ev(), ev()],
+                              out_ready=[ev(), ev()], out_free=[ev(), ev()], used=[False] * 4)
+        P = self._pipe
+        main, copy = torch.cuda.current_stream(), P["copy"]
+        for i, (xh, oh) in enumerate(zip(x0_hosts, out_hosts)):
+            b = i & 1
+            if P["used"][b]:
+                copy.wait_event(P["in_free"][b])        # replay i-2 took its input
+            with torch.cuda.stream(copy):
+                P["inb"][b].copy_(xh, non_blocking=True)
+                P["in_ready"][b].record(copy)
+            main.wait_event(P["in_ready"][b])
+            self._x0_graph.copy_(P["inb"][b])
+            P["in_free"][b].record(main)
+            P["used"][b] = True
+            self.graph.replay()
+            if P["used"][2 + b]:
+                main.wait_event(P["out_free"][b])       # D2H of batch i-2 done
+            P["outb"][b].copy_(self.x32[:, :h])
+            P["out_ready"][b].record(main)
+            P["used"][2 + b] = True
+            copy.wait_event(P["out_ready"][b])
+            with torch.cuda.stream(copy):
+                oh.copy_(P["outb"][b], non_blocking=True)
+                P["out_free"][b].record(copy)
+        copy.synchronize()
+        main.synchronize()
+
     def finish(self, gpu_seconds=None) -> RunResult:
         """One device->host read of status + counters; build the RunResult."""
         cfg = self.cfg

@@ -381,3 +381,22 @@ def test_fused_combine_engine_bit_identical(strategy, monkeypatch):
         out[fused] = (res.final.values.cpu(), res.dispatch_bytes, res.active_pairs)
     assert torch.equal(out["1"][0], out["0"][0])
     assert out["1"][1:] == out["0"][1:]
+
+
+def test_sample_many_matches_sample():
+    """Pipelined serving (copies of neighbouring batches overlapping the graph
+    replay) returns exactly what one sample() per batch returns."""
+    cfg = D.ModelConfig(num_layers=3, num_experts=8, num_shared=2, top_k=2, hidden_dim=128,
+                        expert_dim=256, num_tokens=64, batch=2, num_steps=4, step_size=1e-3)
+    model = D.init_model(cfg, seed=3)
+    x0 = D.sample_x0(cfg, 3)
+    r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, D.dice_policy(refresh_interval=2,
+                       warmup=1, period=2), D.ClusterConfig(num_devices=2), 3).capture()
+    g = torch.Generator().manual_seed(0)
+    xs = [(torch.rand(cfg.total_rows, cfg.hidden_dim, generator=g) * 2 - 1).pin_memory()
+          for _ in range(5)]
+    ref = [r.sample(x).clone() for x in xs]
+    outs = [torch.empty_like(x).pin_memory() for x in xs]
+    r.sample_many(xs, outs)
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
