@@ -198,14 +198,24 @@ def sample_x0_shard(config, seed: int, rows: tuple, device="cuda") -> Activation
 
 class EPRunner:
     """One rank of an expert-parallel sampling run (ScheduleRunner semantics,
-    schedules.py:142-490, for SYNCHRONOUS and INTERWEAVED)."""
+    schedules.py:142-490: SYNCHRONOUS, DISPLACED and INTERWEAVED).
+
+    DISPLACED (schedules.py:347-370) keeps each layer's dispatch in the peers'
+    receive windows for a whole step: stage (s, l) first expert-processes the
+    dispatch of step s-1 (its combine is assembled at the start of stage
+    (s+1, l), still after decide(s) as in the reference), then sends the new one
+    into the windows that processing just freed, so one window per layer
+    suffices; the slot consumed at (s, l) holds step s-2's combine (staleness
+    2). A dispatch a sync stage supersedes is drained unprocessed (the reference
+    drops it, its bytes stay counted), and a sync stage's own dispatch, which
+    the reference re-processes at the next stage, is already in the slot
+    (every pair of a forced refresh is active, so re-assembling it changes
+    nothing): only its combine bytes are counted again."""
 
     def __init__(self, model: ToyModel, x0_shard: ActivationBlock, strategy: Strategy,
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *, rank: int,
                  world: int, pg=None, time_waits: bool = False, time_experts: bool = False):
         cfg = model.config
-        if strategy is Strategy.DISPLACED:
-            raise ConfigurationError("expert-parallel runs support synchronous and interweaved")
         if cluster.num_devices != world:
             raise ConfigurationError(f"cluster.num_devices={cluster.num_devices} != world={world}")
         if cfg.num_experts % world:
@@ -269,7 +279,9 @@ class EPRunner:
         self.hsh = torch.empty(n, max(S, 1) * ep, dtype=bf, device=dev)
         nslots = 1 if strategy is Strategy.SYNCHRONOUS else L
         self.slots = torch.zeros(nslots, n, hp, dtype=f32, device=dev)
-        self.payloads = [_EPPayload(n, k, dev) for _ in range(L)]
+        # displaced: the dispatch in the windows and the new one coexist per layer
+        per_layer = 2 if strategy is Strategy.DISPLACED else 1
+        self.payloads = [[_EPPayload(n, k, dev) for _ in range(per_layer)] for _ in range(L)]
         self.cache = TokenCache(L, n, k, cfg.hidden_dim, device=dev) \
             if policy.cond_strategy is not CondStrategy.OFF else None
         self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
@@ -314,6 +326,7 @@ class EPRunner:
         L = cfg.num_layers
         self.slot_gen = [None] * L
         self.deferred = [None] * L    # payload whose combine is assembled at next stage l
+        self.disp = [None] * L        # displaced: (payload in the windows, processed at sync)
         self.pending = None
         self.occupied = set()
         self.peak_buffer_bytes = 0
@@ -321,8 +334,8 @@ class EPRunner:
         self._wait_events = []
         self._expert_events = []
 
-    def _track(self, layer):
-        self.occupied.add(("c", layer))
+    def _track(self, layer, kind="c"):
+        self.occupied.add((kind, layer))
         slot_bytes = self.cfg.total_rows * self.cfg.hidden_dim * self.cluster.bytes_per_element
         self.peak_buffer_bytes = max(self.peak_buffer_bytes, len(self.occupied) * slot_bytes)
 
@@ -333,7 +346,15 @@ class EPRunner:
             return True
         if layer in self.sync_layers:
             return True
+        if self.strategy is Strategy.DISPLACED:
+            return self.disp[layer] is None or self.slot_gen[layer] is None
         return self.slot_gen[layer] is None
+
+    def _payload(self, layer):
+        pair = self.payloads[layer]
+        if self.strategy is Strategy.DISPLACED and self.disp[layer] is not None:
+            return pair[1] if self.disp[layer][0] is pair[0] else pair[0]
+        return pair[0]
 
     # ------------------------------------------------------------- exchange
     def _send(self, step, layer, p: _EPPayload, force, decided=False):
@@ -397,6 +418,16 @@ class EPRunner:
         self.slot_gen[layer] = p.gen          # the combine is in flight (_store_combine)
         self.combine_log.append((p.gen, layer))
 
+    def _discard(self, p: _EPPayload):
+        """Expert side of a dispatch that is never processed (displaced, superseded
+        by a sync stage or left at the end of the run): release the receive
+        regions so the handshake state returns to its initial values."""
+        g, me, layer = self.grp, self.rank, p.layer
+        self._timed_wait([g.flag("rx_ready", me, layer, s) for s in self._peers()], 1)
+        g.write([g.flag("rx_ready", me, layer, s) for s in self._peers()], 0)
+        g.data("read", [("rx", me, layer, s) for s in self._peers()])
+        g.write([g.flag("rx_free", s, layer, me) for s in self._peers()], 1)
+
     def _shared_args(self, shared_layer):
         if shared_layer is None:
             return (None, 0, None, 0, None)
@@ -457,7 +488,7 @@ class EPRunner:
             if sync:
                 self._flush_pending()
             self._assemble(layer)            # previous step's combine, before decide(layer)
-            p = self.payloads[layer]
+            p = self._payload(layer)
             # the conditional-communication decision rides in the gate launch
             dec = None
             if self.cache is not None:
@@ -470,12 +501,35 @@ class EPRunner:
                               step, layer, decide=dec)
             decided = dec is not None
             if sync:
+                old = self.disp[layer]
+                if old is not None and not old[1]:
+                    self._discard(old[0])    # superseded, never processed (schedules.py:336)
                 self._send(step, layer, p, force=True, decided=decided)
                 self._expert(p, shared_layer=layer if self.merge_gemm1 else None)
                 self._assemble(layer)
-                if self.strategy is Strategy.INTERWEAVED:
+                if self.strategy is Strategy.DISPLACED:
+                    self.disp[layer] = (p, True)
+                    self._track(layer, "d")
+                    self._track(layer)
+                elif self.strategy is Strategy.INTERWEAVED:
                     self._track(layer)
                 self._consume(layer, step, step, gemm1_done=self.merge_gemm1)
+            elif self.strategy is Strategy.DISPLACED:
+                gen = self.slot_gen[layer]
+                old, processed = self.disp[layer]
+                merged = False
+                if processed:
+                    # the reference re-processes the sync stage's dispatch; its
+                    # rows are already in the slot, its combine bytes count again
+                    self.combine_log.append((old.gen, layer))
+                else:
+                    merged = self.merge_gemm1
+                    self._expert(old, shared_layer=layer if merged else None)
+                self._track(layer)
+                self._send(step, layer, p, force=False, decided=decided)
+                self.disp[layer] = (p, False)
+                self._track(layer, "d")
+                self._consume(layer, step, gen, gemm1_done=merged)
             else:
                 gen = self.slot_gen[layer]
                 self._send(step, layer, p, force=False, decided=decided)
@@ -493,6 +547,9 @@ class EPRunner:
         initial state (the run stays replayable)."""
         for layer in range(self.cfg.num_layers):
             self._assemble(layer)
+            if self.disp[layer] is not None and not self.disp[layer][1]:
+                self._discard(self.disp[layer][0])
+                self.disp[layer] = None
 
     # ------------------------------------------------------------- run API
     def launch(self, x0_device=None):

@@ -16,6 +16,8 @@ import tempfile
 
 import pytest
 
+from oracle import dice_oracle as O
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 FAKE_BASE = 1 << 40
 
@@ -103,7 +105,10 @@ def simulate(logs, seed):
 @pytest.mark.parametrize("world,strategy,policy", [(2, "synchronous", "neutral"),
                                                    (2, "interweaved", "dice"),
                                                    (4, "interweaved", "neutral"),
-                                                   (4, "interweaved", "deep")])
+                                                   (4, "interweaved", "deep"),
+                                                   (2, "displaced", "neutral"),
+                                                   (2, "displaced", "dice"),
+                                                   (4, "displaced", "deep")])
 def test_exchange_protocol_random_interleavings(world, strategy, policy):
     logs = collect(world, strategy, policy, runs=2)
     # the trace records kernel writes as ("write", [regions]) only when the
@@ -118,6 +123,13 @@ def test_exchange_protocol_random_interleavings(world, strategy, policy):
         lg["trace"] = fixed
     recs = [lg["records"] for lg in logs]
     assert all(r == recs[0] for r in recs), "ranks disagree on the schedule"
+    # ... and the schedule is the reference's (the oracle's staleness records;
+    # of the last of two runs back to back)
+    g = O.Geometry(**CFG)
+    pol = {"neutral": O.Policy(), "dice": O.dice_defaults(refresh_interval=2, warmup=2, period=3),
+           "deep": O.Policy(sync_strategy=O.SYNC_DEEP)}[policy]
+    ref = O.run_schedule(g, O.init_params(g, 3), O.initial_latent(g, 3), strategy, pol, world, 3)
+    assert recs[0] == [tuple(t) for t in ref.staleness]
     for seed in range(40):
         simulate(logs, seed)
 

@@ -35,7 +35,10 @@ CFG = dict(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=128, e
 @pytest.mark.parametrize("strategy,policy,world", [("synchronous", "neutral", 2),
                                                    ("interweaved", "neutral", 2),
                                                    ("interweaved", "dice", 2),
-                                                   ("interweaved", "dice", 4)])
+                                                   ("interweaved", "dice", 4),
+                                                   ("displaced", "neutral", 2),
+                                                   ("displaced", "dice", 2),
+                                                   ("displaced", "dice", 4)])
 def test_ep_two_ranks_matches_single_gpu(strategy, policy, world):
     same = torch.cuda.device_count() < world
     port = free_port()
