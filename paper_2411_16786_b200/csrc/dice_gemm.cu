@@ -493,32 +493,14 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int k_blocks = args.num_k_blocks;
   const int T1 = m_tiles * n_blocks;
   const int n_blocks2 = args2.num_n_blocks;
+  const int num_tiles = T1 + (args2.num_m_tiles > 0 ? args2.num_m_tiles * n_blocks2 : 0);
+  // tile -> (problem, n block, m tile); N-fastest within each problem
+  auto locate = [&](int tile, int& prob, int& n_blk, int& m_tile) {
+    if (tile < T1) { prob = 0; n_blk = tile % n_blocks; m_tile = tile / n_blocks; }
+    else { prob = 1; const int t2 = tile - T1; n_blk = t2 % n_blocks2; m_tile = t2 / n_blocks2; }
+  };
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
-  // NSUB = 2 tail split: when the last wave of wide tiles would occupy at most
-  // half of the pairs, its tiles are dealt as two 256 x BN halves each (the
-  // tile count is only known here, from the device tile prefix). A half moves
-  // 5/8 of a wide tile's operand bytes, so the tail finishes in ~0.6 of a wide
-  // tile's time instead of idling the other pairs for a whole one.
-  int full_w = T1, tail_w = 0;
-  if constexpr (NSUB == 2 && DIRECT) {
-    if (args.tail_split && args2.num_m_tiles == 0) {
-      const int r = T1 % num_pairs;
-      if (r > 0 && 2 * r <= num_pairs) { full_w = T1 - r; tail_w = r; }
-    }
-  }
-  const int T1s = full_w + 2 * tail_w;
-  const int num_tiles = T1s + (args2.num_m_tiles > 0 ? args2.num_m_tiles * n_blocks2 : 0);
-  // tile -> (problem, n block, m tile, half); N-fastest within each problem;
-  // half = -1: all NSUB accumulators, 0 / 1: only that one (tail split)
-  auto locate = [&](int tile, int& prob, int& n_blk, int& m_tile, int& half) {
-    half = -1;
-    if (tile < full_w) { prob = 0; n_blk = tile % n_blocks; m_tile = tile / n_blocks; }
-    else if (tile < T1s) {
-      const int j = tile - full_w, w = full_w + (j >> 1);
-      prob = 0; n_blk = w % n_blocks; m_tile = w / n_blocks; half = j & 1;
-    } else { prob = 1; const int t2 = tile - T1s; n_blk = t2 % n_blocks2; m_tile = t2 / n_blocks2; }
-  };
   const int n_items = pair < num_tiles ? (num_tiles - 1 - pair) / num_pairs + 1 : 0;
 
   if (warp == 0) {
@@ -527,9 +509,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       uint32_t phase = 0;
       for (int it = 0; it < n_items; ++it) {
         const int tile = pair + it * num_pairs, k0 = 0, k1 = k_blocks;
-        int prob, n_blk, m_tile, half;   // N-fastest: resident tiles share A rows
-        locate(tile, prob, n_blk, m_tile, half);
-        const int s_lo = half < 0 ? 0 : half, s_hi = half < 0 ? NSUB : half + 1;
+        int prob, n_blk, m_tile;   // N-fastest: resident tiles share A rows
+        locate(tile, prob, n_blk, m_tile);
         const int g = prob == 0 ? find_group(sh->group_off, groups, m_tile) : 0;
         const int a_row = m_tile * kPairM + rank * BM;
         const int b_row = g * (prob == 0 ? args.N : args2.N) + n_blk * TN + rank * (BN / 2);
@@ -537,10 +518,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const CUtensorMap* mB = prob == 0 ? &tmB : &tmB2;
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0),
-                                        C::kABytes + (s_hi - s_lo) * C::kSubBBytes);
+          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0), C::kStageBytes);
           tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
-          for (int sub = s_lo; sub < s_hi; ++sub)
+#pragma unroll
+          for (int sub = 0; sub < NSUB; ++sub)
             tma_load_2d_pair(smB + stage * C::kBBytes + sub * C::kSubBBytes, mB, &sh->full[stage],
                              kb * BK, b_row + sub * BN);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -554,9 +535,6 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       uint32_t phase = 0;
       for (int local = 0; local < n_items; ++local) {
         const int k0 = 0, k1 = k_blocks;
-        int prob_, n_blk_, m_tile_, half;
-        locate(pair + local * num_pairs, prob_, n_blk_, m_tile_, half);
-        const int s_lo = half < 0 ? 0 : half, s_hi = half < 0 ? NSUB : half + 1;
         const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
         const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
         mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
@@ -570,7 +548,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             const uint64_t ad = umma_desc_sw128(a_base + k * UMMA_K * 2);
-            for (int sub = s_lo; sub < s_hi; ++sub)
+#pragma unroll
+            for (int sub = 0; sub < NSUB; ++sub)
               umma_bf16_pair(d_tmem + sub * BN, ad,
                              umma_desc_sw128(b_base + sub * C::kSubBBytes + k * UMMA_K * 2), idesc,
                              (kb != k0 || k != 0) ? 1u : 0u);
@@ -591,10 +570,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
     for (int local = 0; local < n_items; ++local) {
       const int tile = pair + local * num_pairs;
-      int prob, n_blk, m_tile, half;
-      locate(tile, prob, n_blk, m_tile, half);
-      const int c_lo = half < 0 ? 0 : half * (BN / 32);
-      const int c_hi = half < 0 ? TN / 32 : (half + 1) * (BN / 32);
+      int prob, n_blk, m_tile;
+      locate(tile, prob, n_blk, m_tile);
       const GemmArgs& ar = prob == 0 ? args : args2;
       const int rl = prob == 0 ? row_limit : args2.M_valid;
       const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
@@ -611,7 +588,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
       for (int e = 0; e < (GE > 0 ? GE / 2 : 1); ++e) gacc[e] = make_float2(0.f, 0.f);
 #pragma unroll 1
-      for (int ci = c_lo + grp; ci < c_hi; ci += kEpiGroups) {
+      for (int ci = grp; ci < TN / 32; ci += kEpiGroups) {
         const int col_in_tile = ci * 32;
         const int col0 = n_blk * TN + col_in_tile;
         uint32_t r[32];
@@ -638,7 +615,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const int nci = ci + kEpiGroups;
           const int ncol = n_blk * TN + nci * 32;
           epilogue_gelu_resid_pf(ar, stage, rbuf, lane, row0, rl, col0,
-                                 (nci < c_hi && ncol < ar.N) ? ncol : -1);
+                                 (nci < TN / 32 && ncol < ar.N) ? ncol : -1);
         } else {
           epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         }
@@ -786,8 +763,6 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
   static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
   aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
-  const int tail = env_int("DICE_GEMM_TAIL", 1);   // wide-tile tail split (0: off; read per call)
-  aa.tail_split = tail;
   GemmArgs bb{};
   if (a2 != nullptr) {
     if (EpiTraits<EPI>::gate_e > 0) return DICE_ERR_CONTRACT;

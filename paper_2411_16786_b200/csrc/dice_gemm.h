@@ -61,7 +61,6 @@ struct GemmArgs {
   const float* addend;
   int64_t ld_add;
   int stages;            // operand ring depth actually used (pair kernel; set by the host)
-  int tail_split;        // NSUB = 2 pair kernel: deal a short last wave as half tiles
   const float* gate_w;   // GATE epilogues: W_gate f32 [N, E] (row c = hidden column c)
   float* gate_part;      // GATE epilogues: partial logits f32 [P, M, E], P = gemm_gate_parts()
   // COMBINE: row -> pair map, per-pair gates / cache-write mask, slot [n, N] f32,

@@ -324,33 +324,3 @@ def test_gemm_rejects_internal_epilogue_kinds():
     for epi in (-1, 5, 6, 7, 99):
         with pytest.raises(ContractError):
             ops.gemm(epi, A, B, out_bf16=o)
-
-
-@pytest.mark.parametrize("m_tiles", [30, 40, 50, 64])
-def test_wide_gemm_tail_split_bit_identical(m_tiles, monkeypatch):
-    """256x384 expert GEMM2 whose short last wave is dealt as 256x192 halves
-    (the device decides from the tile prefix: 30 and 50 m-tiles split, 40 and 64
-    do not) is bit-identical to the unsplit launch and matches torch."""
-    E, hp, ep = 8, 1152, 4608
-    max_rows = 64 * 256
-    g = torch.Generator(device=dev).manual_seed(5)
-    hbuf = (torch.randn(max_rows, ep, device=dev, generator=g) * 0.5).to(torch.bfloat16)
-    w2 = (torch.randn(E * hp, ep, device=dev, generator=g) / 68).to(torch.bfloat16)
-    per = [m_tiles // E + (1 if e < m_tiles % E else 0) for e in range(E)]
-    tiles = torch.tensor([0] + list(np.cumsum(per)), dtype=torch.int32, device=dev)
-    out = {}
-    for t in ("1", "0"):
-        monkeypatch.setenv("DICE_GEMM_TAIL", t)
-        y = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
-        ops.expert_gemm2(hbuf, w2, E, tiles, y)
-        torch.cuda.synchronize()
-        out[t] = y
-    assert torch.equal(out["1"], out["0"])
-    rows = m_tiles * 256
-    grp = np.repeat(np.arange(E), [p * 256 for p in per])
-    for e in (0, E - 1):
-        r = torch.as_tensor(np.nonzero(grp == e)[0], device=dev)
-        ref = hbuf[r].float() @ w2[e * hp:(e + 1) * hp].float().T
-        got = out["1"][r].float()
-        assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (got - ref).abs().max()
-    assert rows <= max_rows
