@@ -272,13 +272,16 @@ int dice_ep_dispatch(const int32_t* ids, const uint8_t* active, int64_t n, int k
  * every output row into its home rank's combine window at the home pair
  * index (cx: host array of D device pointers). A2 != NULL: the rank's dense
  * shared-expert GEMM1 out2 = gelu(A2 B2^T) [M2, N2] runs in the same GEMM1
- * launch (dice_expert_gemm1_with_dense). */
+ * launch (dice_expert_gemm1_with_dense). row_pair (int32 [max_rows]) != NULL:
+ * the combine all-to-all is fused into the expert GEMM2 epilogue (peer-memory
+ * stores of each finished tile; y unused); NULL: GEMM2 into y, then a
+ * peer-store kernel. */
 int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
                    int64_t cap, int El, int hp, int ep, const uint16_t* w1_t, const uint16_t* w2_t,
                    int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
                    uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
                    const uint64_t* cx, const uint16_t* A2, int64_t M2, const uint16_t* B2,
-                   int N2, uint16_t* out2, void* stream);
+                   int N2, uint16_t* out2, int32_t* row_pair, void* stream);
 
 /* out[i] = i for i < count (identity pair positions for the combine window). */
 int dice_iota(int32_t* out, int64_t count, void* stream);

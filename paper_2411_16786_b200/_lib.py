@@ -70,7 +70,8 @@ SIGNATURES = {
                                  c_int64, c_int64, P, ctypes.POINTER(c_uint64),
                                  ctypes.POINTER(c_uint64), ctypes.POINTER(c_uint64), P]),
     "dice_ep_expert": (c_int, [P, P, P, c_int, c_int64, c_int, c_int, c_int, P, P, P, P, P, P, P,
-                               c_int64, P, P, ctypes.POINTER(c_uint64), P, c_int64, P, c_int, P, P]),
+                               c_int64, P, P, ctypes.POINTER(c_uint64), P, c_int64, P, c_int, P, P,
+                               P]),
     "dice_iota": (c_int, [P, c_int64, P]),
 }
 
@@ -125,7 +126,9 @@ KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSE
                     "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,
-                    "dice_stream_write": 0, "dice_ep_dispatch": 3, "dice_ep_expert": 7}
+                    "dice_stream_write": 0, "dice_ep_dispatch": 3,
+                    # fused combine: the peer stores ride in the expert GEMM2 epilogue
+                    "dice_ep_expert": 7 if os.environ.get("DICE_EP_FUSED_COMBINE") == "0" else 6}
 launch_count = [0]
 
 

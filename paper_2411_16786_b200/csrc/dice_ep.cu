@@ -240,15 +240,37 @@ int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* 
                    int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
                    uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
                    const uint64_t* cx, const uint16_t* A2, int64_t M2, const uint16_t* B2,
-                   int N2, uint16_t* out2, void* stream) {
+                   int N2, uint16_t* out2, int32_t* row_pair, void* stream) {
   if (D < 1 || D > kMaxRanks || hp % 64 != 0 || ep % 64 != 0 || El < 1) return DICE_ERR_CONTRACT;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t total = (int64_t)D * cap;
+  // combine all-to-all fused into the expert GEMM2 epilogue (row_pair given;
+  // DICE_EP_FUSED_COMBINE=0: GEMM2 into y, then a separate peer-store kernel)
+  const char* fe = getenv("DICE_EP_FUSED_COMBINE");
+  const bool fused = row_pair != nullptr && !(fe != nullptr && fe[0] == '0');
   ep_rx_ids_kernel<<<(int)((total + 255) / 256 < 2368 ? (total + 255) / 256 : 2368), 256, 0, s>>>(
       static_cast<const int2*>(rx_meta), rx_count, D, cap, ids_rx);
   int rc = permute_launch(ids_rx, nullptr, total, 1, El, 1, 256, El, rx_rows, hp, x_perm, pos_rx,
-                          tile_offsets, nullptr, 1, 0, total, scratch, s);
+                          tile_offsets, nullptr, 1, 0, total, scratch, s,
+                          fused ? row_pair : nullptr);
   if (rc) return rc;
+  if (fused) {
+    // GEMM1 (+ the rank's shared GEMM1 in the same launch), then GEMM2 whose
+    // epilogue stores every finished row into its home rank's combine window
+    rc = dice_expert_gemm1_with_dense(x_perm, max_rows, w1_t, El, hp, ep, tile_offsets, hbuf,
+                                      A2, A2 != nullptr ? M2 : 0, B2, N2, out2, stream);
+    if (rc) return rc;
+    GemmProblem q{};
+    q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
+    q.num_groups = El; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / 256);
+    q.epi_kind = EPI_STORE_SCATTER;
+    q.epi.ld_bf16 = hp;
+    q.epi.row_pair = row_pair;
+    q.epi.scatter_meta = rx_meta;
+    q.epi.scatter_cap = cap;
+    for (int r = 0; r < D; ++r) q.epi.scatter_dst[r] = cx[r];
+    return gemm_bf16(q, s);
+  }
   if (A2 != nullptr && M2 > 0) {
     // this rank's shared-expert GEMM1 rides in the expert GEMM1 launch
     rc = dice_expert_gemm1_with_dense(x_perm, max_rows, w1_t, El, hp, ep, tile_offsets, hbuf, A2,

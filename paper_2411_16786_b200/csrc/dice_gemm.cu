@@ -429,7 +429,15 @@ __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_
     __nv_bfloat162 b = __floats2bfloat162_rn(v.x, v.y);
     w[j] = *reinterpret_cast<uint32_t*>(&b);
   }
-  uint4* dst = reinterpret_cast<uint4*>(a.out_bf16 + row * a.ld_bf16 + col0);
+  __nv_bfloat16* out = a.out_bf16 + row * a.ld_bf16;
+  if constexpr (EPI == EPI_STORE_SCATTER) {
+    const int i = a.row_pair[row];
+    if (i < 0) return;                       // padding row of an expert group
+    const int src = (int)(i / a.scatter_cap);
+    const int pair = reinterpret_cast<const int2*>(a.scatter_meta)[i].y;
+    out = reinterpret_cast<__nv_bfloat16*>(a.scatter_dst[src]) + (int64_t)pair * a.ld_bf16;
+  }
+  uint4* dst = reinterpret_cast<uint4*>(out + col0);
 #pragma unroll
   for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
@@ -780,6 +788,8 @@ int dispatch_wide(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
     case EPI_STORE_BF16: return launch_pair<192, EPI_STORE_BF16, true, 2>(ta, tb, a, max_tiles, s);
     case EPI_GELU_BF16: return launch_pair<192, EPI_GELU_BF16, true, 2>(ta, tb, a, max_tiles, s);
     case EPI_COMBINE: return launch_pair<192, EPI_COMBINE, true, 2>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_SCATTER:
+      return launch_pair<192, EPI_STORE_SCATTER, true, 2>(ta, tb, a, max_tiles, s);
     case EPI_STORE_F32: return launch_pair<192, EPI_STORE_F32, false, 2>(ta, tb, a, max_tiles, s);
     case EPI_GELU_RESID: return launch_pair<192, EPI_GELU_RESID, false, 2>(ta, tb, a, max_tiles, s);
     case EPI_CONSUME: return launch_pair<192, EPI_CONSUME, false, 2>(ta, tb, a, max_tiles, s);
@@ -800,6 +810,7 @@ int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
       return direct ? launch_pair<BN, EPI_GELU_BF16, true>(ta, tb, a, max_tiles, s)
                     : launch_pair<BN, EPI_GELU_BF16, false>(ta, tb, a, max_tiles, s);
     case EPI_COMBINE: return launch_pair<BN, EPI_COMBINE, true>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_SCATTER: return launch_pair<BN, EPI_STORE_SCATTER, true>(ta, tb, a, max_tiles, s);
     case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false>(ta, tb, a, max_tiles, s);
     case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false>(ta, tb, a, max_tiles, s);
     case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false>(ta, tb, a, max_tiles, s);
@@ -870,7 +881,7 @@ TileChoice choose_tile(const GemmProblem& p) {
       return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs);
     };
     const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16 ||
-                            p.epi_kind == EPI_COMBINE;
+                            p.epi_kind == EPI_COMBINE || p.epi_kind == EPI_STORE_SCATTER;
     const double narrow = wave_eff(m_tiles * (p.N / 192));
     c.wide = wide_mode == 2 ||
              (direct_epi && p.K >= 2048 && 1.15 * wave_eff(m_tiles * (p.N / 384)) >= narrow);

@@ -25,6 +25,11 @@ enum EpiKind : int {
   // token cache when the pair refreshes it, and g * row is added into the
   // token's combine slot (pre-initialised with its cached terms)
   EPI_COMBINE = 7,
+  // expert-parallel expert GEMM2 with the combine all-to-all fused: each output
+  // row (window entry i = row_pair[r] of source rank i / scatter_cap) is stored
+  // as bf16 straight into that rank's combine window (peer memory) at its home
+  // pair index scatter_meta[i].y, tile by tile as the GEMM finishes them
+  EPI_STORE_SCATTER = 8,
 };
 
 template <int EPI>
@@ -72,6 +77,11 @@ struct GemmArgs {
   int64_t n_tokens;
   float* slot;
   __nv_bfloat16* cache_rows;
+  // STORE_SCATTER: window metadata int2 [D * cap] (.y = home pair), entries per
+  // source rank, and the D combine-window bases (peer-mapped device pointers)
+  const void* scatter_meta;
+  int64_t scatter_cap;
+  uint64_t scatter_dst[16];
 };
 
 struct GemmProblem {

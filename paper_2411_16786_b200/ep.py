@@ -267,6 +267,9 @@ class EPRunner:
         self.hbuf = torch.empty(self.max_rows, ep, dtype=bf, device=dev)
         self.y = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
         self.x_perm = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
+        # permuted row -> window entry: the expert GEMM2 epilogue stores each finished
+        # row straight into its home rank's combine window (fused combine all-to-all)
+        self.row_pair_rx = torch.empty(self.max_rows, dtype=torch.int32, device=dev)
         self.ids_rx = torch.empty(total, dtype=torch.int32, device=dev)
         self.pos_rx = torch.empty(total, dtype=torch.int32, device=dev)
         self.tiles = torch.empty(El + 1, dtype=torch.int32, device=dev)
@@ -406,7 +409,7 @@ class EPRunner:
                   lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.ids_rx.data_ptr(),
                   self.pos_rx.data_ptr(), self.tiles.data_ptr(), self.scratch.data_ptr(),
                   self.x_perm.data_ptr(), self.max_rows, self.hbuf.data_ptr(), self.y.data_ptr(),
-                  cx, *self._shared_args(shared_layer), ops._stream())
+                  cx, *self._shared_args(shared_layer), self.row_pair_rx.data_ptr(), ops._stream())
         if self.time_experts:
             e1.record()
             self._expert_events.append((e0, e1, p.gen, layer, shared_layer is not None))
