@@ -152,10 +152,15 @@ def run_reference(args):
         return 0
     cores = os.cpu_count()
     vals = []
-    for i in range(args.warmup + args.steps):
+    # each step is a bounded sample (~10 s); at most one warm-up sample and at
+    # most ~150 s of timed samples, so any --steps / --warmup ends in minutes
+    t_start = time.perf_counter()
+    for i in range(min(args.warmup, 1) + args.steps):
         s = cpu_sample(f"{cores} host threads")
-        if i >= args.warmup:
+        if i >= min(args.warmup, 1):
             vals.append(s)
+            if time.perf_counter() - t_start > 150.0:
+                break
     v = statistics.median([s["value"] for s in vals])
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "img/s", "n_gpus": args.gpus,
