@@ -169,7 +169,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "parallelism": "cpu"},
         "cpu_baseline": {"value": v, "unit": "img/s", "cores": cores, "kind": "port",
-                         "sample": vals[0]["sample"]},
+                         "sample": vals[0]["sample"], "samples_timed": len(vals)},
         "e2e": {"value": v, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
