@@ -253,10 +253,43 @@ def config1():
         json.dump(meta, f, indent=1)
 
 
+def xl_width():
+    """The XL/2-8E2A layer widths (h=1152, e=4608, E=8, S=2, k=2) at a size the
+    fp64 reference runs in seconds: 3 layers, 64 tokens x batch 2, 4 steps, D=2,
+    eta=2e-5; synchronous and full DICE (Deep sync + LowScore R=2, W=1, P=3).
+    Stores float32 finals, the routing ids of every (step, layer) and the run
+    accounting (histograms, bytes, pairs)."""
+    cfg = ds.ModelConfig(num_layers=3, num_experts=8, num_shared=2, top_k=2, hidden_dim=1152,
+                         expert_dim=4608, num_tokens=64, batch=2, num_steps=4, step_size=2e-5)
+    model = ds.init_model(cfg, seed=7)
+    x0 = ds.sample_x0(cfg, seed=7)
+    out, meta = {}, {"config": cfg_dict(cfg), "seed": 7, "devices": 2}
+    runs = [("sync", ds.Strategy.SYNCHRONOUS, ds.NEUTRAL),
+            ("dice", ds.Strategy.INTERWEAVED,
+             ds.dice_policy(refresh_interval=2, warmup=1, period=3))]
+    for name, strategy, pol in runs:
+        t0 = time.time()
+        res = ds.run_sampling(model, x0, strategy, pol, ds.ClusterConfig(num_devices=2), 7,
+                              record_routes=True)
+        meta[name + "_seconds"] = time.time() - t0
+        meta[name + "_policy"] = pol_dict(pol)
+        out[name + "_final"] = res.final.values.astype(np.float32)
+        out[name + "_ids"] = np.array([[r.expert_ids for r in res.step_routes[s]]
+                                       for s in range(cfg.num_steps)]).astype(np.int8)
+        meta[name] = dict(histogram={str(k): v for k, v in res.staleness_histogram().items()},
+                          dispatch_bytes=res.dispatch_bytes, combine_bytes=res.combine_bytes,
+                          active_pairs=res.active_pairs, total_pairs=res.total_pairs,
+                          peak_buffer_bytes=res.peak_buffer_bytes)
+    np.savez_compressed(os.path.join(HERE, "xl_width.npz"), **out)
+    with open(os.path.join(HERE, "xl_width.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "init", "gate", "cache", "runs", "placement", "config1"]
+    which = sys.argv[1:] or ["kat", "init", "gate", "cache", "runs", "placement", "config1",
+                             "xl_width"]
     fns = dict(kat=kat, init=init_and_layers, gate=gate_cases, cache=cache_sequences,
-               runs=small_runs, placement=placement_bytes, config1=config1)
+               runs=small_runs, placement=placement_bytes, config1=config1, xl_width=xl_width)
     for w in which:
         t0 = time.time()
         fns[w]()

@@ -400,3 +400,36 @@ def test_sample_many_matches_sample():
     r.sample_many(xs, outs)
     for a, b in zip(outs, ref):
         assert torch.equal(a, b)
+
+
+def test_xl_width_runs_vs_reference():
+    """The engine at the XL/2-8E2A layer widths (h=1152, e=4608, the bench's tile
+    shapes) against the real reference's fp64 runs (3 layers, 128 rows, 4 steps,
+    synchronous and full DICE): update rel-L2 <= 2e-2, routing ids of every
+    (step, layer) agree for >= 98 % of the pairs (free-running: flips only near
+    ties), identical staleness histograms, pair counts and bytes."""
+    meta = json.load(open(os.path.join(G, "xl_width.json")))
+    z = load("xl_width.npz")
+    cfg = cfg_of(meta["config"])
+    model = D.init_model(cfg, seed=meta["seed"])
+    x0 = D.sample_x0(cfg, meta["seed"])
+    x0n = x0.values.cpu().numpy().astype(np.float64)
+    runs = {"sync": (D.Strategy.SYNCHRONOUS, D.NEUTRAL),
+            "dice": (D.Strategy.INTERWEAVED, D.dice_policy(refresh_interval=2, warmup=1,
+                                                           period=3))}
+    for name, (st, pol) in runs.items():
+        res = D.run_sampling(model, x0, st, pol, D.ClusterConfig(num_devices=meta["devices"]),
+                             meta["seed"], record_routes=True)
+        fin = res.final.values.cpu().numpy().astype(np.float64)
+        ref = z[name + "_final"].astype(np.float64)
+        drift = np.linalg.norm((fin - x0n) - (ref - x0n)) / np.linalg.norm(ref - x0n)
+        assert drift < 2e-2, (name, drift)
+        ids = np.array([[r.expert_ids.numpy() for r in res.step_routes[s]]
+                        for s in range(cfg.num_steps)])
+        agree = float(np.mean(ids == z[name + "_ids"]))
+        assert agree >= 0.98, (name, agree)
+        m = meta[name]
+        assert {str(k): v for k, v in res.staleness_histogram().items()} == m["histogram"]
+        assert (res.active_pairs, res.total_pairs) == (m["active_pairs"], m["total_pairs"])
+        assert (res.dispatch_bytes, res.combine_bytes) == (m["dispatch_bytes"], m["combine_bytes"])
+        print(f"{name}: update rel-L2 {drift:.2e}, id agreement {agree:.4f}")

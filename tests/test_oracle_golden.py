@@ -170,3 +170,27 @@ def test_gate_weight_matches_full_init():
     g, z = tiny()
     for l in range(2):
         assert np.array_equal(O.gate_weight(g, 7, l), z[f"l{l}_w_gate"])
+
+
+XL_POLICIES = {"sync": (O.SYNC, O.Policy()),
+               "dice": (O.INTERWEAVED, O.dice_defaults(refresh_interval=2, warmup=1, period=3))}
+
+
+def test_xl_width_runs_match_reference():
+    """The oracle at the XL/2-8E2A layer widths (h=1152, e=4608; 3 layers, 128
+    rows, 4 steps) against the real reference's runs: finals to the fp32 storage
+    rounding of the fixture, identical staleness histograms, pairs and bytes."""
+    meta = json.load(open(os.path.join(G, "xl_width.json")))
+    z = np.load(os.path.join(G, "xl_width.npz"))
+    g = O.Geometry(**meta["config"])
+    params = O.init_params(g, meta["seed"])
+    x0 = O.initial_latent(g, meta["seed"])
+    for name, (strategy, pol) in XL_POLICIES.items():
+        r = O.run_schedule(g, params, x0, strategy, pol, meta["devices"], meta["seed"])
+        ref = z[name + "_final"].astype(np.float64)
+        assert np.abs(r.final - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max())
+        m = meta[name]
+        assert {str(k): v for k, v in r.histogram().items()} == m["histogram"]
+        assert (r.active_pairs, r.total_pairs) == (m["active_pairs"], m["total_pairs"])
+        assert (r.dispatch_bytes, r.combine_bytes) == (m["dispatch_bytes"], m["combine_bytes"])
+        assert r.peak_buffer_bytes == m["peak_buffer_bytes"]
