@@ -285,11 +285,40 @@ def xl_width():
         json.dump(meta, f, indent=1)
 
 
+def g_width():
+    """The G-16E2A layer widths (h=1664, e=6656, E=16 experts, S=2, k=2; hidden
+    padded to 1792 on the GPU) at a size the fp64 reference runs in about a
+    minute: 2 layers, 32 tokens x batch 2, 3 steps, D=4, eta=2e-5, full DICE
+    (Deep sync + LowScore R=2, W=1, P=2). Float32 finals, ids and accounting."""
+    cfg = ds.ModelConfig(num_layers=2, num_experts=16, num_shared=2, top_k=2, hidden_dim=1664,
+                         expert_dim=6656, num_tokens=32, batch=2, num_steps=3, step_size=2e-5)
+    model = ds.init_model(cfg, seed=11)
+    x0 = ds.sample_x0(cfg, seed=11)
+    out, meta = {}, {"config": cfg_dict(cfg), "seed": 11, "devices": 4}
+    pol = ds.dice_policy(refresh_interval=2, warmup=1, period=2)
+    t0 = time.time()
+    res = ds.run_sampling(model, x0, ds.Strategy.INTERWEAVED, pol, ds.ClusterConfig(num_devices=4),
+                          11, record_routes=True)
+    meta["dice_seconds"] = time.time() - t0
+    meta["dice_policy"] = pol_dict(pol)
+    out["dice_final"] = res.final.values.astype(np.float32)
+    out["dice_ids"] = np.array([[r.expert_ids for r in res.step_routes[s]]
+                                for s in range(cfg.num_steps)]).astype(np.int8)
+    meta["dice"] = dict(histogram={str(k): v for k, v in res.staleness_histogram().items()},
+                        dispatch_bytes=res.dispatch_bytes, combine_bytes=res.combine_bytes,
+                        active_pairs=res.active_pairs, total_pairs=res.total_pairs,
+                        peak_buffer_bytes=res.peak_buffer_bytes)
+    np.savez_compressed(os.path.join(HERE, "g_width.npz"), **out)
+    with open(os.path.join(HERE, "g_width.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kat", "init", "gate", "cache", "runs", "placement", "config1",
-                             "xl_width"]
+                             "xl_width", "g_width"]
     fns = dict(kat=kat, init=init_and_layers, gate=gate_cases, cache=cache_sequences,
-               runs=small_runs, placement=placement_bytes, config1=config1, xl_width=xl_width)
+               runs=small_runs, placement=placement_bytes, config1=config1, xl_width=xl_width,
+               g_width=g_width)
     for w in which:
         t0 = time.time()
         fns[w]()

@@ -433,3 +433,33 @@ def test_xl_width_runs_vs_reference():
         assert (res.active_pairs, res.total_pairs) == (m["active_pairs"], m["total_pairs"])
         assert (res.dispatch_bytes, res.combine_bytes) == (m["dispatch_bytes"], m["combine_bytes"])
         print(f"{name}: update rel-L2 {drift:.2e}, id agreement {agree:.4f}")
+
+
+def test_g_width_run_vs_reference():
+    """The engine at the G-16E2A layer widths (h=1664 padded to 1792, e=6656, 16
+    experts: the E = 16 router and 16-group expert GEMMs) against the real
+    reference's fp64 run (2 layers, 64 rows, 3 steps, D=4, full DICE): update
+    rel-L2 <= 2e-2, ids >= 98 % identical, histogram / pairs / bytes exact."""
+    meta = json.load(open(os.path.join(G, "g_width.json")))
+    z = load("g_width.npz")
+    cfg = cfg_of(meta["config"])
+    model = D.init_model(cfg, seed=meta["seed"])
+    x0 = D.sample_x0(cfg, meta["seed"])
+    x0n = x0.values.cpu().numpy().astype(np.float64)
+    pol = D.dice_policy(refresh_interval=2, warmup=1, period=2)
+    res = D.run_sampling(model, x0, D.Strategy.INTERWEAVED, pol,
+                         D.ClusterConfig(num_devices=meta["devices"]), meta["seed"],
+                         record_routes=True)
+    fin = res.final.values.cpu().numpy().astype(np.float64)
+    ref = z["dice_final"].astype(np.float64)
+    drift = np.linalg.norm((fin - x0n) - (ref - x0n)) / np.linalg.norm(ref - x0n)
+    assert drift < 2e-2, drift
+    ids = np.array([[r.expert_ids.numpy() for r in res.step_routes[s]]
+                    for s in range(cfg.num_steps)])
+    agree = float(np.mean(ids == z["dice_ids"]))
+    assert agree >= 0.98, agree
+    m = meta["dice"]
+    assert {str(k): v for k, v in res.staleness_histogram().items()} == m["histogram"]
+    assert (res.active_pairs, res.total_pairs) == (m["active_pairs"], m["total_pairs"])
+    assert (res.dispatch_bytes, res.combine_bytes) == (m["dispatch_bytes"], m["combine_bytes"])
+    print(f"G widths: update rel-L2 {drift:.2e}, id agreement {agree:.4f}")
