@@ -77,14 +77,22 @@ def test_ep_two_ranks_matches_single_gpu(strategy, policy, world):
         assert int(part["peak"]) == ref.peak_buffer_bytes
 
 
-def test_ep_xl_widths_matches_single_gpu():
+@pytest.mark.parametrize("geometry", ["xl", "g"])
+def test_ep_xl_widths_matches_single_gpu(geometry):
     """Expert parallelism at the XL layer widths (h=1152, e=4608, 8 experts,
-    2 shared; 4 layers, 3 steps, full DICE policy): the 2-rank run over peer
-    memory reproduces the single-GPU engine bit-exactly — the bench geometry's
-    tile shapes (256x384 expert GEMM2, dual GEMM1 launches) on both sides."""
-    world = 2
-    cfg_kw = dict(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=1152,
-                  expert_dim=4608, num_tokens=256, batch=4, num_steps=3, step_size=2e-5)
+    2 shared; 4 layers, 3 steps, full DICE policy; 2 ranks) and at the G-16E2A
+    widths (h=1664 padded to 1792, e=6656, 16 experts; 4 ranks of 4 experts):
+    the run over peer memory reproduces the single-GPU engine bit-exactly — the
+    bench geometry's tile shapes (256x384 expert GEMM2 with the combine stored
+    into the peers' windows by its epilogue, dual GEMM1 launches) on both sides."""
+    if geometry == "xl":
+        world = 2
+        cfg_kw = dict(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=1152,
+                      expert_dim=4608, num_tokens=256, batch=4, num_steps=3, step_size=2e-5)
+    else:
+        world = 4
+        cfg_kw = dict(num_layers=2, num_experts=16, num_shared=2, top_k=2, hidden_dim=1664,
+                      expert_dim=6656, num_tokens=128, batch=4, num_steps=3, step_size=2e-5)
     same = torch.cuda.device_count() < world
     port = free_port()
     with tempfile.TemporaryDirectory() as td:
