@@ -150,6 +150,25 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
                        int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
                        int32_t* row_pair, void* stream);
 
+/* The permute's counting pass fused into the router (single-GPU engine, E = 8):
+ * dice_gate_topk(_decide) (decide = 0 / 1) that also writes, per block of 32
+ * tokens, the number of active pairs per expert (chunk_counts int32
+ * [ceil(n/32), 8]) and adds the run counters (as dice_route_permute's);
+ * dice_route_permute_counted then only scatters (+ gathers) with those counts
+ * (k must divide 32): the same positions, tile offsets and rows as
+ * dice_route_permute, one launch fewer. */
+int dice_gate_topk_counted(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                           int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                           int layer, int decide, int force, int refresh_interval, int strategy,
+                           int strict, uint64_t random_key, int32_t* last_refresh,
+                           uint8_t* primed, uint8_t* reduced, const int32_t* cached_ids,
+                           uint8_t* active, uint8_t* write, int32_t* chunk_counts,
+                           int64_t* counters, int devices, int64_t rows_total, void* stream);
+int dice_route_permute_counted(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
+                               const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows,
+                               int32_t* pos, int32_t* tile_offsets, const int32_t* chunk_counts,
+                               int32_t* row_pair, void* stream);
+
 /* Upper bound of rows of the padded permuted buffer for n*k pairs over E experts. */
 int64_t dice_permute_max_rows(int64_t n, int k, int E);
 

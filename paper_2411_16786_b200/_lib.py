@@ -37,6 +37,11 @@ SIGNATURES = {
     "dice_expert_gemm1_with_dense": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P, c_int64,
                                              P, c_int, P, P]),
     "dice_expert_gemm2": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P]),
+    "dice_gate_topk_counted": (c_int, [P, P, c_int64, c_int, c_int, c_int, P, P, P, P, c_int, c_int,
+                                       c_int, c_int, c_int, c_int, c_int, c_uint64, P, P, P, P, P,
+                                       P, P, P, c_int, c_int64, P]),
+    "dice_route_permute_counted": (c_int, [P, P, c_int64, c_int, c_int, P, c_int, P, c_int64, P,
+                                           P, P, P, P]),
     "dice_gemm_local_gate": (c_int, [P, c_int64, P, c_int, c_int, P, c_int64, P, c_int64, P,
                                      c_int64, P, c_int, P, P]),
     "dice_gate_parts": (c_int, [c_int64, c_int, c_int, c_int]),
@@ -119,6 +124,7 @@ def check(rc: int, what: str) -> None:
 # kernels each entry point launches (for the bench's gpu_launches count)
 # (the three-kernel permute is the default; DICE_PERMUTE_FUSED=1 is one launch)
 KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSED") == "1" else 3,
+                    "dice_route_permute_counted": 2,
                     "dice_grouped_ffn": 2, "dice_gemm": 1,
                     "dice_gemm_local_gate": 1, "dice_gate_parts": 0, "dice_event_create": 0,
                     "dice_expert_gemm1_with_dense": 1, "dice_expert_gemm2": 1,

@@ -229,6 +229,17 @@ struct DecideArgs {
   uint8_t* write;
 };
 
+// Permute counting fused into the gate launch (single-GPU engine): per block of
+// 32 tokens the number of active pairs per expert (the permute's per-chunk
+// counts) and the run counters (active pairs; remote pairs of the byte plan,
+// cluster.py:75-90), so the permute needs no counting pass of its own.
+struct CountArgs {
+  int32_t* chunk_counts;   // [ceil(n / 32), 8]; null: no counting
+  long long* counters;     // [2] (+=)
+  int devices;
+  int64_t rows_total;
+};
+
 // TokenCache.decide for token t (policies.py:159-186): cadence, mask redraw,
 // active / write masks (strict: also refresh reduced pairs whose expert changed)
 __device__ __forceinline__ void decide_token(int64_t t, int k, const int32_t* ids,
@@ -288,7 +299,14 @@ template <int CH>
 __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
     const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
     int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
-    int32_t* status, int step, int layer, const DecideArgs d) {
+    int32_t* status, int step, int layer, const DecideArgs d, const CountArgs c) {
+  __shared__ int s_cnt[8];
+  __shared__ unsigned long long s_red[2];
+  if (c.chunk_counts != nullptr) {   // (block-uniform) one block = 32 tokens
+    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
+    __syncthreads();
+  }
   pdl_enter();
   constexpr int E = 8;
   const int lane = threadIdx.x & 31;
@@ -389,6 +407,7 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
       ids[t * k + slot] = my_e;
       gates[t * k + slot] = my_s / psum;
     }
+    bool my_act = true;
     if (d.on && slot < k && row_ok) {
       if (d.strategy == DICE_COND_OFF) {
         d.active[t * k + slot] = 1;
@@ -408,7 +427,27 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
         if (d.strict && red && !due && my_e != d_cid) { act = true; wr = true; }
         d.active[t * k + slot] = act;
         d.write[t * k + slot] = wr;
+        my_act = act;
       }
+    }
+    if (c.chunk_counts != nullptr) {
+      const bool valid = slot < k && row_ok && my_act;
+      bool remote = false;
+      if (valid && c.devices > 1)
+        remote = (int)((t * c.devices) / c.rows_total) != my_e / (E / c.devices);
+      if (valid) atomicAdd(&s_cnt[my_e], 1);
+      const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
+      const unsigned nr = __popc(__ballot_sync(0xffffffffu, remote));
+      if (lane == 0 && nv) atomicAdd(&s_red[0], (unsigned long long)nv);
+      if (lane == 0 && nr) atomicAdd(&s_red[1], (unsigned long long)nr);
+    }
+  }
+  if (c.chunk_counts != nullptr) {
+    __syncthreads();
+    if (threadIdx.x < 8) c.chunk_counts[(int64_t)blockIdx.x * 8 + threadIdx.x] = s_cnt[threadIdx.x];
+    if (threadIdx.x == 0 && c.counters != nullptr) {
+      if (s_red[0]) atomicAdd(reinterpret_cast<unsigned long long*>(&c.counters[0]), s_red[0]);
+      if (s_red[1]) atomicAdd(reinterpret_cast<unsigned long long*>(&c.counters[1]), s_red[1]);
     }
   }
 }
@@ -711,16 +750,45 @@ __global__ void __launch_bounds__(kPermBlock) permute_count_kernel(
 __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
     const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
     int32_t* pos, const int32_t* __restrict__ block_counts, int32_t* tile_offsets, int key_div,
-    int row_tile, int32_t* row_pair) {
+    int row_tile, int32_t* row_pair, int count_rows, int rows_per_block) {
   pdl_enter();
   __shared__ int wcnt[32][64];
   __shared__ int base[64];
-  const int nb = gridDim.x;
-  if (threadIdx.x < E) {
+  // count rows: one per block of the counting pass (the count kernel: one per
+  // scatter block; the gate's fused counting: one per 32 tokens)
+  const int first_mine = (int)blockIdx.x * rows_per_block;
+  if (E == 8 && blockDim.x == 1024) {
+    // 128 row-strided partial sums per expert (thread = 8 part + e), reduced
+    // over the 4 parts of a warp by shuffles, then over the 32 warps in smem:
+    // no thread walks the count rows serially (the gate's fused counting
+    // produces one row per 32 tokens: 256 rows at 8192 tokens)
+    __shared__ int red_b[32][8], red_t[32][8];
+    const int e = threadIdx.x & 7, part = threadIdx.x >> 3;
     int before = 0, total = 0;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = part; b < count_rows; b += 128) {
+      const int c = block_counts[(int64_t)b * 8 + e];
+      if (b < first_mine) before += c;
+      total += c;
+    }
+#pragma unroll
+    for (int off = 8; off < 32; off <<= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, off);
+      total += __shfl_xor_sync(0xffffffffu, total, off);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane < 8) { red_b[warp][lane] = before; red_t[warp][lane] = total; }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      int b = 0, t = 0;
+      for (int w = 0; w < 32; ++w) { b += red_b[w][threadIdx.x]; t += red_t[w][threadIdx.x]; }
+      wcnt[0][threadIdx.x] = t;
+      base[threadIdx.x] = b;
+    }
+  } else if (threadIdx.x < E) {
+    int before = 0, total = 0;
+    for (int b = 0; b < count_rows; ++b) {
       const int c = block_counts[(int64_t)b * E + threadIdx.x];
-      if (b < (int)blockIdx.x) before += c;
+      if (b < first_mine) before += c;
       total += c;
     }
     wcnt[0][threadIdx.x] = total;
@@ -1159,7 +1227,7 @@ int permute_launch(const int32_t* ids, const uint8_t* active, int64_t n, int k, 
                                                      row0, rows_total, scratch, key_div,
                                                      experts_total);
   launch_pdl(permute_scatter_kernel, dim3(blocks), dim3(kPermBlock), 0, s, ids, active, n, k, groups, pos, scratch,
-                                                       tile_offsets, key_div, row_tile, row_pair);
+                                                       tile_offsets, key_div, row_tile, row_pair, blocks, 1);
   if (x_perm != nullptr)
     launch_pdl(permute_gather_kernel, dim3(grid_for(P * 32, 256)), dim3(256), 0, s, pos, P, rows, k, hp, x_perm);
   return launch_ok();
@@ -1223,27 +1291,30 @@ int dice_splitmix_bits(uint64_t seed, uint64_t start, int64_t count, uint64_t* o
 namespace {
 int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
                      int32_t* ids, float* gates, float* scores, int32_t* status, int step,
-                     int layer, const DecideArgs& d, cudaStream_t s) {
+                     int layer, const DecideArgs& d, cudaStream_t s,
+                     const CountArgs& c = CountArgs{nullptr, nullptr, 1, 1}) {
   if (E < 1 || E > 64 || k < 1 || k > E || hp % 64 != 0) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
+  // the fused permute counting lives in the E = 8 row-quad kernel only
+  if (c.chunk_counts != nullptr && (E != 8 || k > 8)) return DICE_ERR_CONTRACT;
   const size_t smem = (size_t)E * hp * sizeof(float);
   const int threads = 512;
   int64_t want = ((n + 1) / 2 + 15) / 16;
   if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
   const char* g4 = getenv("DICE_GATE4");        // 0: the row-pair kernel for E = 8
-  if (E == 8 && k <= 8 && !(g4 != nullptr && g4[0] == '0')) {
+  if (E == 8 && k <= 8 && (c.chunk_counts != nullptr || !(g4 != nullptr && g4[0] == '0'))) {
     const int64_t gw = ((n + 3) / 4 + 7) / 8;     // 8 warps per block, four rows each
     const int grid = (int)(gw < 1 ? 1 : gw);
-    const int ch = g4 != nullptr ? atoi(g4) : 3;
+    const int ch = g4 != nullptr && c.chunk_counts == nullptr ? atoi(g4) : 3;
     if (ch == 5)
       launch_pdl(gate4_topk_kernel<5>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
-                 gates, scores, status, step, layer, d);
+                 gates, scores, status, step, layer, d, c);
     else if (ch == 2)
       launch_pdl(gate4_topk_kernel<2>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
-                 gates, scores, status, step, layer, d);
+                 gates, scores, status, step, layer, d, c);
     else
       launch_pdl(gate4_topk_kernel<3>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
-                 gates, scores, status, step, layer, d);
+                 gates, scores, status, step, layer, d, c);
     return launch_ok();
   }
   if ((E == 8 && k <= 8) || (E == 16 && k <= 16)) {
@@ -1314,6 +1385,47 @@ int dice_gate_topk_decide(const float* u, const float* w_gate_t, int64_t n, int 
                      last_refresh, primed, reduced, cached_ids, active, write};
   return gate_topk_launch(u, w_gate_t, n, hp, E, k, ids, gates, scores, status, step, layer, d,
                           (cudaStream_t)stream);
+}
+
+int dice_gate_topk_counted(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                           int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                           int layer, int decide, int force, int refresh_interval, int strategy,
+                           int strict, uint64_t random_key, int32_t* last_refresh,
+                           uint8_t* primed, uint8_t* reduced, const int32_t* cached_ids,
+                           uint8_t* active, uint8_t* write, int32_t* chunk_counts,
+                           int64_t* counters, int devices, int64_t rows_total, void* stream) {
+  if (decide && (refresh_interval < 1 || strategy < 0 || strategy > 3)) return DICE_ERR_CONFIG;
+  if (chunk_counts == nullptr || devices < 1 || E % devices != 0 || rows_total < 1)
+    return DICE_ERR_CONTRACT;
+  const DecideArgs d{decide ? 1 : 0, step, force, refresh_interval, strategy, strict, random_key,
+                     last_refresh, primed, reduced, cached_ids, active, write};
+  const CountArgs c{chunk_counts, reinterpret_cast<long long*>(counters), devices, rows_total};
+  return gate_topk_launch(u, w_gate_t, n, hp, E, k, ids, gates, scores, status, step, layer, d,
+                          (cudaStream_t)stream, c);
+}
+
+int dice_route_permute_counted(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
+                               const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows,
+                               int32_t* pos, int32_t* tile_offsets, const int32_t* chunk_counts,
+                               int32_t* row_pair, void* stream) {
+  if (E != 8 || k < 1 || hp % 64 != 0 || chunk_counts == nullptr) return DICE_ERR_CONTRACT;
+  if (kPermBlock % (32 * k) != 0) return DICE_ERR_CONTRACT;
+  if (max_rows < dice_permute_max_rows(n, k, E)) return DICE_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t P = n * k;
+  const int blocks = (int)((P + kPermBlock - 1) / kPermBlock);
+  if (blocks == 0) {
+    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (E + 1), s);
+    return launch_ok();
+  }
+  const int count_rows = (int)((n + 31) / 32);
+  launch_pdl(permute_scatter_kernel, dim3(blocks), dim3(kPermBlock), 0, s, ids, active, n, k, E,
+             pos, chunk_counts, tile_offsets, 1, kRowTile, row_pair, count_rows,
+             kPermBlock / (32 * k));
+  if (x_perm != nullptr)
+    launch_pdl(permute_gather_kernel, dim3(grid_for(P * 32, 256)), dim3(256), 0, s, pos, P, u16, k,
+               hp, x_perm);
+  return launch_ok();
 }
 
 int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, int refresh_interval,

@@ -93,12 +93,27 @@ def splitmix_bits(seed, start, count, device="cuda"):
 
 
 def gate_topk(u32, w_gate_t, k, ids, gates, scores=None, status=None, step=0, layer=0,
-              decide=None):
+              decide=None, count=None):
     """Fused gate (softmax + stable top-k); ``decide`` = TokenCache.decide_args(...)
-    also runs the conditional-communication decision in the same kernel."""
+    also runs the conditional-communication decision in the same kernel;
+    ``count`` = (chunk_counts, counters, devices, rows_total) also runs the
+    permute's counting pass (E = 8; then route_permute(chunk_counts=...))."""
     n, hp = u32.shape
     E = w_gate_t.shape[0]
     _need(u32, torch.float32, "gate u")
+    if count is not None:
+        chunk_counts, counters, devices, rows_total = count
+        _need(chunk_counts, torch.int32, "chunk_counts")
+        if decide is None:
+            args = (0, 0, 1, 0, 0, 0, None, None, None, None, None, None)
+        else:
+            (force, R, strat, strict, key, last, primed, reduced, cached, active, write) = decide
+            args = (1, int(force), R, strat, int(strict), key & 0xFFFFFFFFFFFFFFFF, _ptr(last),
+                    _ptr(primed), _ptr(reduced), _ptr(cached), _ptr(active), _ptr(write))
+        _lib.call("dice_gate_topk_counted", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids),
+                  _ptr(gates), _ptr(scores), _ptr(status), step, layer, *args,
+                  _ptr(chunk_counts), _ptr(counters), devices, rows_total, _stream())
+        return
     if decide is None:
         _lib.call("dice_gate_topk", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids),
                   _ptr(gates), _ptr(scores), _ptr(status), step, layer, _stream())
@@ -170,11 +185,18 @@ def permute_scratch_ints(n, k, E):
 
 
 def route_permute(ids, active, u16, x_perm, pos, tile_offsets, counters, scratch, E,
-                  devices=1, row0=0, rows_total=None, row_pair=None):
+                  devices=1, row0=0, rows_total=None, row_pair=None, chunk_counts=None):
     """row_pair (int32 [max_rows], optional): permuted row -> pair index t*k+s
-    (-1 on padding rows), for the fused expert GEMM2 combine."""
+    (-1 on padding rows), for the fused expert GEMM2 combine. chunk_counts: the
+    per-32-token expert counts the gate launch produced (gate_topk(count=...));
+    the counting pass and its counters are then already done."""
     n, k = ids.shape
     hp = u16.shape[1]
+    if chunk_counts is not None:
+        _lib.call("dice_route_permute_counted", _ptr(ids), _ptr(active), n, k, E, _ptr(u16), hp,
+                  _ptr(x_perm), x_perm.shape[0], _ptr(pos), _ptr(tile_offsets),
+                  _ptr(chunk_counts), _ptr(row_pair), _stream())
+        return
     _lib.call("dice_route_permute", _ptr(ids), _ptr(active), n, k, E, _ptr(u16), hp,
               _ptr(x_perm), x_perm.shape[0], _ptr(pos), _ptr(tile_offsets), _ptr(counters),
               devices, row0, n if rows_total is None else rows_total, _ptr(scratch),

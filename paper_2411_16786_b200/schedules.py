@@ -212,6 +212,12 @@ class DeviceRunner:
         # its critical path); default: standalone persistent gate kernel. Either
         # way the conditional-communication decision runs inside the gate launch.
         self.fused_gate = E in (8, 16) and os.environ.get("DICE_FUSED_GATE", "0") == "1"
+        # the permute's counting pass rides in the gate launch (E = 8 row-quad
+        # kernel; DICE_GATE_COUNT=0: separate count kernel)
+        self.gate_count = (E == 8 and not self.fused_gate and 32 % k == 0
+                           and os.environ.get("DICE_GATE_COUNT", "1") != "0")
+        self.chunk_counts = (torch.zeros((n + 31) // 32 * 8, dtype=torch.int32, device=dev)
+                             if self.gate_count else None)
         if self.fused_gate:
             self.gparts = torch.empty(ops.gate_parts(n, hp, hp, E), n, E, dtype=f32, device=dev)
         self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
@@ -348,7 +354,7 @@ class DeviceRunner:
             ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
                               self.counters[step, layer], self.scratch, self.E,
                               devices=self.cluster.num_devices, row0=0, rows_total=self.n,
-                              row_pair=p.row_pair)
+                              row_pair=p.row_pair, chunk_counts=self.chunk_counts)
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 
@@ -488,8 +494,10 @@ class DeviceRunner:
                     ops.gate_finish(self.gparts, p.ids, p.gates, self.scores, self.status, step,
                                     layer, decide=dec)
                 else:
+                    cnt = ((self.chunk_counts, self.counters[step, layer],
+                            self.cluster.num_devices, self.n) if self.gate_count else None)
                     ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
-                                  self.status, step, layer, decide=dec)
+                                  self.status, step, layer, decide=dec, count=cnt)
             decided = dec is not None
             if self.record_inputs:
                 inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu())

@@ -324,3 +324,38 @@ def test_gemm_rejects_internal_epilogue_kinds():
     for epi in (-1, 5, 6, 7, 99):
         with pytest.raises(ContractError):
             ops.gemm(epi, A, B, out_bf16=o)
+
+
+@pytest.mark.parametrize("n,k,devices", [(8192, 2, 2), (1000, 2, 1), (777, 1, 4), (300, 4, 8)])
+def test_gate_counted_permute_matches_count_kernel(n, k, devices):
+    """dice_gate_topk_counted + dice_route_permute_counted == dice_gate_topk +
+    dice_route_permute: ids, gates, positions, tile offsets, permuted rows and
+    the run counters (active / remote pairs under D simulated devices). (The
+    engine test covers the decide-masked path.)"""
+    E, hp = 8, 256
+    g = torch.Generator(device=dev).manual_seed(n + k)
+    u = torch.randn(n, hp, device=dev, generator=g)
+    wg = torch.randn(E, hp, device=dev, generator=g) * 0.1
+    u16 = u.to(torch.bfloat16)
+    max_rows = ops.permute_max_rows(n, k, E)
+    res = {}
+    for mode in ("count", "plain"):
+        ids = torch.empty(n, k, dtype=torch.int32, device=dev)
+        gates = torch.empty(n, k, device=dev)
+        cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+        pos = torch.empty(n, k, dtype=torch.int32, device=dev)
+        tiles = torch.empty(E + 1, dtype=torch.int32, device=dev)
+        x_perm = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
+        if mode == "count":
+            cc = torch.zeros((n + 31) // 32 * 8, dtype=torch.int32, device=dev)
+            ops.gate_topk(u, wg, k, ids, gates, count=(cc, cnt, devices, n))
+            ops.route_permute(ids, None, u16, x_perm, pos, tiles, cnt, None, E, chunk_counts=cc)
+        else:
+            scr = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+            ops.gate_topk(u, wg, k, ids, gates)
+            ops.route_permute(ids, None, u16, x_perm, pos, tiles, cnt, scr, E, devices=devices,
+                              rows_total=n)
+        torch.cuda.synchronize()
+        res[mode] = (ids, gates, pos, tiles, x_perm, cnt)
+    for a, b in zip(res["count"], res["plain"]):
+        assert torch.equal(a, b)

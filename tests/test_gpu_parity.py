@@ -463,3 +463,27 @@ def test_g_width_run_vs_reference():
     assert (res.active_pairs, res.total_pairs) == (m["active_pairs"], m["total_pairs"])
     assert (res.dispatch_bytes, res.combine_bytes) == (m["dispatch_bytes"], m["combine_bytes"])
     print(f"G widths: update rel-L2 {drift:.2e}, id agreement {agree:.4f}")
+
+
+@pytest.mark.parametrize("strategy,devices", [("interweaved", 2), ("displaced", 4),
+                                              ("synchronous", 1)])
+def test_gate_counted_permute_engine_bit_identical(strategy, devices, monkeypatch):
+    """The permute's counting pass fused into the gate launch (per-32-token expert
+    counts + run counters) reproduces the separate count kernel bit for bit:
+    latents, bytes (remote-pair counters under D simulated devices) and pairs."""
+    cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=256,
+                        expert_dim=512, num_tokens=200, batch=3, num_steps=6, step_size=1e-3)
+    model = D.init_model(cfg, seed=13)
+    x0 = D.sample_x0(cfg, 13)
+    pol = D.dice_policy(refresh_interval=2, warmup=1, period=3)
+    out = {}
+    for g in ("1", "0"):
+        monkeypatch.setenv("DICE_GATE_COUNT", g)
+        r = D.DeviceRunner(model, x0, D.Strategy(strategy), pol,
+                           D.ClusterConfig(num_devices=devices), 13)
+        assert r.gate_count == (g == "1")
+        res = r.run()
+        out[g] = (res.final.values.cpu(), res.dispatch_bytes, res.combine_bytes,
+                  res.active_pairs, res.per_step_active_pairs)
+    assert torch.equal(out["1"][0], out["0"][0])
+    assert out["1"][1:] == out["0"][1:]
