@@ -430,6 +430,11 @@ def run_gpu(args):
                    "l2": "inputs larger than L2: 6.0 GB of bf16 weights streamed per denoising step"},
         "moe_layer_us": ms_per_step * 1e3 / (cfg.num_steps * cfg.num_layers),
         "exposed_a2a_us": exposed_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
+        # the reference's logical buffer accounting (R*h*2 per occupied slot,
+        # schedules.py:185) next to the physical bytes this rank's run holds
+        "buffers": {"logical_peak_bytes": int(res.peak_buffer_bytes),
+                    "device_bytes": (int(runner.device_bytes())
+                                     if hasattr(runner, "device_bytes") else None)},
         "roofline": {"bound": "tensor", "kernel": "grouped expert FFN (tcgen05 GEMM1+GELU, GEMM2; the stage's shared-expert GEMM1 shares the GEMM1 launch)",
                      "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": traffic,

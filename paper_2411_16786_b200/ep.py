@@ -554,6 +554,29 @@ class EPRunner:
                 self._discard(self.disp[layer][0])
                 self.disp[layer] = None
 
+    def device_bytes(self) -> int:
+        """Physical device bytes of this rank's run: its buffers, payloads, token
+        cache and its exchange window (not the model weights)."""
+        seen, total = set(), int(self.win.nbytes)
+
+        def visit(v, depth):
+            nonlocal total
+            if isinstance(v, torch.Tensor):
+                if v.is_cuda and v.untyped_storage().data_ptr() not in seen:
+                    seen.add(v.untyped_storage().data_ptr())
+                    total += v.untyped_storage().nbytes()
+            elif isinstance(v, (list, tuple)):
+                for x in v:
+                    visit(x, depth)
+            elif depth < 2 and isinstance(v, (_EPPayload, TokenCache)):
+                for x in vars(v).values():
+                    visit(x, depth + 1)
+
+        for key, v in vars(self).items():
+            if key != "model":
+                visit(v, 0)
+        return total
+
     # ------------------------------------------------------------- run API
     def launch(self, x0_device=None):
         if self.graph is not None:

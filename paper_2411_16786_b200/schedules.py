@@ -304,6 +304,31 @@ class DeviceRunner:
                     runner._op_events.append((name, self_.ev[0], self_.ev[1], step, layer))
         return _Ctx()
 
+    def device_bytes(self) -> int:
+        """Physical device bytes of the run's own buffers (activations, payloads,
+        combine slots, token cache, scratch; not the model weights): every CUDA
+        tensor reachable from the runner, its payloads and its cache, counted
+        once per storage."""
+        seen, total = set(), 0
+
+        def visit(v, depth):
+            nonlocal total
+            if isinstance(v, torch.Tensor):
+                if v.is_cuda and v.untyped_storage().data_ptr() not in seen:
+                    seen.add(v.untyped_storage().data_ptr())
+                    total += v.untyped_storage().nbytes()
+            elif isinstance(v, (list, tuple)):
+                for x in v:
+                    visit(x, depth)
+            elif depth < 2 and isinstance(v, (_Payload, TokenCache)):
+                for x in vars(v).values():
+                    visit(x, depth + 1)
+
+        for key, v in vars(self).items():
+            if key != "model":
+                visit(v, 0)
+        return total
+
     def op_times(self):
         """[(op, ms, step, layer)] of the last run / replay (time_ops)."""
         return [(n, a.elapsed_ms(b), s, l) for n, a, b, s, l in self._op_events]
