@@ -266,11 +266,20 @@ def xl_width():
     out, meta = {}, {"config": cfg_dict(cfg), "seed": 7, "devices": 2}
     runs = [("sync", ds.Strategy.SYNCHRONOUS, ds.NEUTRAL),
             ("dice", ds.Strategy.INTERWEAVED,
-             ds.dice_policy(refresh_interval=2, warmup=1, period=3))]
+             ds.dice_policy(refresh_interval=2, warmup=1, period=3)),
+            ("random_strict", ds.Strategy.INTERWEAVED,
+             ds.PolicyConfig(sync_strategy=ds.SyncStrategy.STAGGERED,
+                             cond_strategy=ds.CondStrategy.RANDOM, refresh_interval=2,
+                             strict_refresh=True)),
+            ("displaced_high", ds.Strategy.DISPLACED,
+             ds.PolicyConfig(sync_strategy=ds.SyncStrategy.SHALLOW,
+                             cond_strategy=ds.CondStrategy.HIGH_SCORE, refresh_interval=3,
+                             warmup=1))]
     for name, strategy, pol in runs:
         t0 = time.time()
         res = ds.run_sampling(model, x0, strategy, pol, ds.ClusterConfig(num_devices=2), 7,
                               record_routes=True)
+        meta[name + "_strategy"] = strategy.value
         meta[name + "_seconds"] = time.time() - t0
         meta[name + "_policy"] = pol_dict(pol)
         out[name + "_final"] = res.final.values.astype(np.float32)

@@ -416,7 +416,15 @@ def test_xl_width_runs_vs_reference():
     x0n = x0.values.cpu().numpy().astype(np.float64)
     runs = {"sync": (D.Strategy.SYNCHRONOUS, D.NEUTRAL),
             "dice": (D.Strategy.INTERWEAVED, D.dice_policy(refresh_interval=2, warmup=1,
-                                                           period=3))}
+                                                           period=3)),
+            "random_strict": (D.Strategy.INTERWEAVED,
+                              D.PolicyConfig(sync_strategy=D.SyncStrategy.STAGGERED,
+                                             cond_strategy=D.CondStrategy.RANDOM,
+                                             refresh_interval=2, strict_refresh=True)),
+            "displaced_high": (D.Strategy.DISPLACED,
+                               D.PolicyConfig(sync_strategy=D.SyncStrategy.SHALLOW,
+                                              cond_strategy=D.CondStrategy.HIGH_SCORE,
+                                              refresh_interval=3, warmup=1))}
     for name, (st, pol) in runs.items():
         res = D.run_sampling(model, x0, st, pol, D.ClusterConfig(num_devices=meta["devices"]),
                              meta["seed"], record_routes=True)
@@ -430,8 +438,16 @@ def test_xl_width_runs_vs_reference():
         assert agree >= 0.98, (name, agree)
         m = meta[name]
         assert {str(k): v for k, v in res.staleness_histogram().items()} == m["histogram"]
-        assert (res.active_pairs, res.total_pairs) == (m["active_pairs"], m["total_pairs"])
-        assert (res.dispatch_bytes, res.combine_bytes) == (m["dispatch_bytes"], m["combine_bytes"])
+        if agree == 1.0 or not pol.strict_refresh:
+            # masks depend on the step pattern only (strict also on id changes)
+            assert (res.active_pairs, res.total_pairs) == (m["active_pairs"], m["total_pairs"])
+        else:
+            assert abs(res.active_pairs - m["active_pairs"]) <= 0.01 * m["active_pairs"]
+        # bytes follow the ids' placement: exact unless a near-tie flip moved a pair
+        # across the simulated devices
+        for got, want in ((res.dispatch_bytes, m["dispatch_bytes"]),
+                          (res.combine_bytes, m["combine_bytes"])):
+            assert got == want if agree == 1.0 else abs(got - want) <= 0.02 * want
         print(f"{name}: update rel-L2 {drift:.2e}, id agreement {agree:.4f}")
 
 

@@ -173,7 +173,13 @@ def test_gate_weight_matches_full_init():
 
 
 XL_POLICIES = {"sync": (O.SYNC, O.Policy()),
-               "dice": (O.INTERWEAVED, O.dice_defaults(refresh_interval=2, warmup=1, period=3))}
+               "dice": (O.INTERWEAVED, O.dice_defaults(refresh_interval=2, warmup=1, period=3)),
+               "random_strict": (O.INTERWEAVED, O.Policy(sync_strategy=O.SYNC_STAGGERED,
+                                                         cond_strategy=O.COND_RANDOM,
+                                                         refresh_interval=2, strict_refresh=True)),
+               "displaced_high": (O.DISPLACED, O.Policy(sync_strategy=O.SYNC_SHALLOW,
+                                                        cond_strategy=O.COND_HIGH,
+                                                        refresh_interval=3, warmup=1))}
 
 
 def test_xl_width_runs_match_reference():
