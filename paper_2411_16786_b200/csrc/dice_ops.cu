@@ -814,6 +814,7 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
       for (int r = base[ex] + cnt + threadIdx.x; r < pad_end; r += blockDim.x) row_pair[r] = -1;
     }
   }
+  __syncthreads();   // block_rank() reuses wcnt[0][*] (the group totals read above)
   const int64_t P = n * k;
   const int64_t p = (int64_t)blockIdx.x * kPermBlock + threadIdx.x;
   int e = 0, s = 0;

@@ -269,7 +269,7 @@ class EPRunner:
         self.x_perm = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
         # permuted row -> window entry: the expert GEMM2 epilogue stores each finished
         # row straight into its home rank's combine window (fused combine all-to-all)
-        self.row_pair_rx = torch.empty(self.max_rows, dtype=torch.int32, device=dev)
+        self.row_pair_rx = torch.full((self.max_rows,), -1, dtype=torch.int32, device=dev)
         self.ids_rx = torch.empty(total, dtype=torch.int32, device=dev)
         self.pos_rx = torch.empty(total, dtype=torch.int32, device=dev)
         self.tiles = torch.empty(El + 1, dtype=torch.int32, device=dev)
@@ -366,7 +366,8 @@ class EPRunner:
         g, me, D = self.grp, self.rank, self.world
         if self.cache is not None:
             if not decided:
-                self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write)
+                self.cache.decide_into(layer, step, p.ids, self.policy, force, p.active, p.write,
+                                       row0=self.r0)
             act = p.active
         else:
             act = None
@@ -495,7 +496,8 @@ class EPRunner:
             # the conditional-communication decision rides in the gate launch
             dec = None
             if self.cache is not None:
-                dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write)
+                dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write,
+                                             row0=self.r0)
             if self.fused_gate:
                 ops.gate_finish(self.gparts, p.ids, p.gates, None, self.status, step, layer,
                                 decide=dec)

@@ -6,6 +6,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def policy_by_name(D, name):
+    """Policies of the EP parity cases (shared with tests/test_gpu_ep.py)."""
+    import dataclasses
+    dice = D.dice_policy(refresh_interval=2, warmup=2, period=3)
+    return {"neutral": D.NEUTRAL, "dice": dice,
+            # Random: the kept slot is drawn per GLOBAL row (policies.py:107-115)
+            "random": dataclasses.replace(dice, cond_strategy=D.CondStrategy.RANDOM,
+                                          sync_strategy=D.SyncStrategy.STAGGERED),
+            "high_strict": dataclasses.replace(dice, cond_strategy=D.CondStrategy.HIGH_SCORE,
+                                               strict_refresh=True,
+                                               sync_strategy=D.SyncStrategy.SHALLOW)}[name]
+
+
 def run(rank, world, port, cfg_kwargs, strategy, policy_name, out_path, same_device):
     import numpy as np
     import torch
@@ -22,7 +35,7 @@ def run(rank, world, port, cfg_kwargs, strategy, policy_name, out_path, same_dev
     model = D.init_model(cfg, seed=5, experts=(rank * El, (rank + 1) * El))
     rows = shard_rows(cfg.total_rows, world, rank)
     x0 = sample_x0_shard(cfg, 5, rows)
-    policy = {"neutral": D.NEUTRAL, "dice": D.dice_policy(refresh_interval=2, warmup=2, period=3)}[policy_name]
+    policy = policy_by_name(D, policy_name)
     r = EPRunner(model, x0, D.Strategy(strategy), policy, D.ClusterConfig(num_devices=world), 5,
                  rank=rank, world=world, time_waits=True)
     res = r.run()

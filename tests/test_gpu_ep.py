@@ -36,6 +36,10 @@ CFG = dict(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=128, e
                                                    ("interweaved", "neutral", 2),
                                                    ("interweaved", "dice", 2),
                                                    ("interweaved", "dice", 4),
+                                                   ("interweaved", "random", 2),
+                                                   ("interweaved", "random", 4),
+                                                   ("interweaved", "high_strict", 2),
+                                                   ("displaced", "random", 4),
                                                    ("displaced", "neutral", 2),
                                                    ("displaced", "dice", 2),
                                                    ("displaced", "dice", 4)])
@@ -62,7 +66,8 @@ def test_ep_two_ranks_matches_single_gpu(strategy, policy, world):
     cfg = D.ModelConfig(**CFG)
     model = D.init_model(cfg, seed=5)
     x0 = D.sample_x0(cfg, 5)
-    pol = {"neutral": D.NEUTRAL, "dice": D.dice_policy(refresh_interval=2, warmup=2, period=3)}[policy]
+    from tests.ep_worker import policy_by_name
+    pol = policy_by_name(D, policy)
     ref = D.run_sampling(model, x0, D.Strategy(strategy), pol, D.ClusterConfig(num_devices=world), 5)
     fin = ref.final.values.cpu().numpy()
     for r, part in enumerate(parts):
