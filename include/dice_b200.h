@@ -43,12 +43,11 @@ extern "C" {
 #define DICE_COND_HIGH_SCORE 2
 #define DICE_COND_RANDOM 3
 
-/* GEMM epilogues. */
+/* GEMM epilogues of dice_gemm. */
 #define DICE_EPI_STORE_BF16 0
 #define DICE_EPI_GELU_BF16 1
 #define DICE_EPI_STORE_F32 2
 #define DICE_EPI_GELU_RESID 3
-#define DICE_EPI_CONSUME 4
 
 /* Library version / build identification (sm_100a). */
 int dice_version(void);
@@ -87,30 +86,6 @@ int dice_gate_topk(const float* u, const float* w_gate_t, int64_t n, int hp, int
                    int32_t* ids, float* gates, float* scores, int32_t* status, int step,
                    int layer, void* stream);
 
-/* local_block with the gate fused into its GEMM epilogue (model.py:244-252 then
- * model.py:209-223): the GELU_RESID GEMM (u = gelu(A B^T) + residual -> out_f32,
- * out_bf16) also dots each finished u row with w_gate (f32 [N, E], row c =
- * hidden column c, E = 8 or 16) and stores partial logits f32 [P, M, E],
- * P = dice_gate_parts(M, N, K, E), one slot per (column tile, epilogue warp
- * group). The router never re-reads u from HBM. */
-int dice_gemm_local_gate(const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
-                         float* out_f32, int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16,
-                         const float* residual, int64_t ld_res, const float* w_gate, int E,
-                         float* parts, void* stream);
-int dice_gate_parts(int64_t M, int N, int K, int E);
-
-/* Router finish over those partials: logits = sum of the P slots in slot order,
- * softmax, stable top-k, renormalised gates (same outputs and non-finite rule as
- * dice_gate_topk). decide != 0 also runs the conditional-communication decision
- * (dice_cond_decide's arguments and semantics) on the fresh ids in the same
- * kernel. */
-int dice_gate_finish(const float* parts, int P, int64_t n, int E, int k, int32_t* ids,
-                     float* gates, float* scores, int32_t* status, int step, int layer,
-                     int decide, int force, int refresh_interval, int strategy, int strict,
-                     uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
-                     uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
-                     uint8_t* write, void* stream);
-
 /* dice_gate_topk followed, in the same kernel, by the conditional-communication
  * decision of each token on its fresh ids (dice_cond_decide's arguments and
  * semantics; the engine's gate + TokenCache.decide in one launch). */
@@ -126,7 +101,10 @@ int dice_gate_topk_decide(const float* u, const float* w_gate_t, int64_t n, int 
  * State (this layer): last_refresh int32 [n] (init -1e9), primed uint8 [n],
  * reduced uint8 [n, k], cached_ids int32 [n, k] (read only when strict).
  * random_key = mix64(mix64(mix64(seed ^ TAG) + layer) + step), computed by
- * the caller (policies.py:113-114). Outputs active / write uint8 [n, k]. */
+ * the caller (policies.py:113-114); token t's kept slot is
+ * splitmix64(random_key, t+1) % k, so a shard whose first token is global row
+ * row0 passes random_key + row0 * 0x9E3779B97F4A7C15 (mod 2^64).
+ * Outputs active / write uint8 [n, k]. */
 int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force,
                      int refresh_interval, int strategy, int strict, uint64_t random_key,
                      int32_t* last_refresh, uint8_t* primed, uint8_t* reduced,
@@ -184,12 +162,13 @@ int dice_grouped_ffn(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w
                      uint16_t* hbuf, uint16_t* y, void* stream);
 
 /* Stale-activation cache merge + weighted routed sum (TokenCache.assemble,
- * policies.py:188-208; combine_outputs' routed part, model.py:295-298).
+ * policies.py:188-208; combine_outputs' routed part, model.py:295-298) — the
+ * functional API form (policies.TokenCache.assemble, model.routed_rows).
  * For each token t: routed[t] = sum_s g_s * row_s (slots left to right, f32)
  * where active pairs take row y[pos[t,s]] and gate gates[t,s], inactive pairs
  * take the cached row/gate. Pairs with write[t,s] store their fresh row/gate/id
  * into the cache. cache_* may be NULL (cond-comm off). rows_out (f32 [k, n, hp])
- * and gates_out (f32 [n, k]) are optional (functional API). */
+ * and gates_out (f32 [n, k]) are optional. */
 int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* active,
                         const uint8_t* write, const float* gates, const int32_t* ids,
                         int64_t n, int k, int hp, uint16_t* cache_rows, float* cache_gates,
@@ -199,11 +178,10 @@ int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* ac
 /* Dense bf16 GEMM C[M, N] = A[M, K] @ B[N, K]^T with a fused epilogue (see
  * DICE_EPI_*): local_block (model.py:244-252) = GELU_RESID with residual h;
  * shared_forward GEMM1 (model.py:235-241) = GELU_BF16 with the S experts
- * concatenated on N, GEMM2 = STORE_F32 or CONSUME (u + (shared + routed)). */
+ * concatenated on N, GEMM2 = STORE_F32. */
 int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
               float* out_f32, int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16,
-              const float* residual, int64_t ld_res, const float* addend, int64_t ld_add,
-              void* stream);
+              const float* residual, int64_t ld_res, void* stream);
 
 /* The two halves of dice_grouped_ffn, the first merged with a dense GELU GEMM
  * of the same K in ONE persistent launch: hbuf = gelu(x_perm W1_e) over the
@@ -217,22 +195,40 @@ int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const
 int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
                       int ep, const int32_t* tile_offsets, uint16_t* y, void* stream);
 
-/* Routed combine fused into the expert GEMM2 (k <= 2; TokenCache.assemble
- * policies.py:188-208 + the routed part of combine_outputs model.py:295-298).
- * dice_slot_init: slot[t] = the cached terms of t's inactive pairs, summed in
- * slot order as acc + round(g * row) (0 when all pairs are fresh); refreshed
- * pairs' gates / ids persisted. dice_expert_gemm2_combine: y = hbuf W2_e per
- * expert tile; each output row (pair p = t*k + s, row_pair from
- * dice_route_permute) is rounded to bf16, written to cache_rows [k, n, hp] when
- * write[p], and round(gates[p] * row) is added into slot[t] (order-free for
- * k <= 2, so equal to dice_cache_assemble's result). */
-int dice_slot_init(const uint8_t* active, const uint8_t* write, const float* gates,
-                   const int32_t* ids, int64_t n, int k, int hp, const uint16_t* cache_rows,
-                   float* cache_gates, int32_t* cache_ids, float* slot, void* stream);
-int dice_expert_gemm2_combine(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
-                              int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
-                              const float* gates, const uint8_t* write, int k, int64_t n,
-                              float* slot, uint16_t* cache_rows, void* stream);
+/* The engine's routed combine, split between the producer and the consumer of
+ * a layer's expert rows (TokenCache.assemble policies.py:188-208 +
+ * combine_outputs model.py:279-298 + _consume schedules.py:308-317), with no
+ * kernel in between:
+ *
+ * dice_expert_gemm2_pairs: the expert GEMM2 (y = hbuf W2_e per expert tile)
+ * whose epilogue stores the bf16 row of permuted row r (pair p = row_pair[r] =
+ * t*k + s from dice_route_permute, -1 on padding) into pair_rows[s][t]
+ * ([k, n, hp]: the layer's token-cache rows) and persists gates[p] / ids[p]
+ * into cache_gates[p] / cache_ids[p] (either may be NULL). Every computed
+ * pair is persisted: a cached entry is only ever read for a reduced pair that
+ * is not due, and a pair enters the reduced set only at a refresh, which
+ * writes it (policies.py:171-186), so persisting the other fresh pairs too
+ * leaves every value the reference reads unchanged — the rows / gates then
+ * hold, per pair, its latest computed row and gate: for an active pair the
+ * fresh one, for an inactive pair the cached one (policies.py:197-202).
+ *
+ * dice_gemm_consume: out = residual + ((A B^T + g_0 row_0) + g_1 row_1 ...)
+ * with row_s = pair_rows[s][t], g_s = pair_gates[t][s] — the shared-expert
+ * GEMM2 with the layer's consume in its epilogue (slots left to right, the
+ * product and each sum rounded; then the residual, schedules.py:317) ->
+ * out_f32 / out_bf16. dice_consume_rows: the same without shared experts
+ * (S = 0): out = residual + ((0 + g_0 row_0) + ...). */
+int dice_expert_gemm2_pairs(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
+                            int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
+                            const float* gates, const int32_t* ids, int k, int64_t n,
+                            uint16_t* pair_rows, float* cache_gates, int32_t* cache_ids,
+                            void* stream);
+int dice_gemm_consume(const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
+                      const float* residual, int64_t ld_res, const uint16_t* pair_rows,
+                      const float* pair_gates, int k, float* out_f32, int64_t ld_f32,
+                      uint16_t* out_bf16, int64_t ld_bf16, void* stream);
+int dice_consume_rows(const float* residual, const uint16_t* pair_rows, const float* pair_gates,
+                      int64_t n, int k, int hp, float* out, uint16_t* out_bf16, void* stream);
 
 /* out[t] = base[t] + sum_s gates[t, s] * rows[s, t] (f32, combine_outputs
  * model.py:279-298 and the consume residual, schedules.py:317). rows f32
@@ -276,34 +272,34 @@ int dice_stream_write(const uint64_t* addrs, int count, uint32_t value, void* st
 /* Dispatch all-to-all send of one layer: groups this rank's active pairs by
  * destination rank (expert e lives on rank e/(E/D)), accumulates
  * {active pairs, remote pairs} in counters, and stores each pair's bf16 row
- * and int2 (local expert, pair index) into the destination's window region for
- * source `me`, plus the per-destination row count. rx_*: host arrays of D
- * device pointers to those regions. pos_dest int32 [n*k], dest_offsets int32
- * [D+1], scratch >= dice_permute_scratch_ints(n, k, D). */
-int dice_ep_dispatch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E, int D,
-                     int me, const uint16_t* u16, int hp, int32_t* pos_dest, int32_t* dest_offsets,
-                     int64_t* counters, int64_t row0, int64_t rows_total, int32_t* scratch,
-                     const uint64_t* rx_rows, const uint64_t* rx_meta, const uint64_t* rx_count,
-                     void* stream);
+ * and int4 metadata {local expert, home pair index t*k+s, gate (f32 bits),
+ * expert id} into the destination's window region for source `me`, plus the
+ * per-destination row count. rx_*: host arrays of D device pointers to those
+ * regions. gates f32 [n, k]; pos_dest int32 [n*k], dest_offsets int32 [D+1],
+ * scratch >= dice_permute_scratch_ints(n, k, D). */
+int dice_ep_dispatch(const int32_t* ids, const float* gates, const uint8_t* active, int64_t n,
+                     int k, int E, int D, int me, const uint16_t* u16, int hp, int32_t* pos_dest,
+                     int32_t* dest_offsets, int64_t* counters, int64_t row0, int64_t rows_total,
+                     int32_t* scratch, const uint64_t* rx_rows, const uint64_t* rx_meta,
+                     const uint64_t* rx_count, void* stream);
 
 /* Expert side of one layer: groups the D*cap window rows by local expert,
- * runs the grouped expert FFN (expert_forward, model.py:226-232) and stores
- * every output row into its home rank's combine window at the home pair
- * index (cx: host array of D device pointers). A2 != NULL: the rank's dense
- * shared-expert GEMM1 out2 = gelu(A2 B2^T) [M2, N2] runs in the same GEMM1
- * launch (dice_expert_gemm1_with_dense). row_pair (int32 [max_rows]) != NULL:
- * the combine all-to-all is fused into the expert GEMM2 epilogue (peer-memory
- * stores of each finished tile; y unused); NULL: GEMM2 into y, then a
- * peer-store kernel. */
+ * runs the grouped expert FFN (expert_forward, model.py:226-232); the expert
+ * GEMM2's epilogue stores every finished row straight into its home rank's
+ * pair rows [k, n_home, hp] at [s][t] with its gate and expert id (the combine
+ * all-to-all fused into the GEMM, as peer-memory stores; the persistence rule
+ * of dice_expert_gemm2_pairs). home_rows / home_gates / home_ids: host arrays
+ * of D device pointers (the layer's pair rows / cache gates / cache ids of
+ * every rank, peer-mapped), home_n: host array of the D ranks' row counts.
+ * A2 != NULL: the rank's dense shared-expert GEMM1 out2 = gelu(A2 B2^T)
+ * [M2, N2] runs in the same GEMM1 launch. row_pair: int32 [max_rows]. */
 int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
-                   int64_t cap, int El, int hp, int ep, const uint16_t* w1_t, const uint16_t* w2_t,
-                   int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
-                   uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
-                   const uint64_t* cx, const uint16_t* A2, int64_t M2, const uint16_t* B2,
-                   int N2, uint16_t* out2, int32_t* row_pair, void* stream);
-
-/* out[i] = i for i < count (identity pair positions for the combine window). */
-int dice_iota(int32_t* out, int64_t count, void* stream);
+                   int64_t cap, int El, int hp, int ep, int k, const uint16_t* w1_t,
+                   const uint16_t* w2_t, int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets,
+                   int32_t* scratch, uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf,
+                   int32_t* row_pair, const uint64_t* home_rows, const uint64_t* home_gates,
+                   const uint64_t* home_ids, const int64_t* home_n, const uint16_t* A2,
+                   int64_t M2, const uint16_t* B2, int N2, uint16_t* out2, void* stream);
 
 #ifdef __cplusplus
 }

@@ -42,25 +42,21 @@ SIGNATURES = {
                                        P, P, P, c_int, c_int64, P]),
     "dice_route_permute_counted": (c_int, [P, P, c_int64, c_int, c_int, P, c_int, P, c_int64, P,
                                            P, P, P, P]),
-    "dice_gemm_local_gate": (c_int, [P, c_int64, P, c_int, c_int, P, c_int64, P, c_int64, P,
-                                     c_int64, P, c_int, P, P]),
-    "dice_gate_parts": (c_int, [c_int64, c_int, c_int, c_int]),
-    "dice_gate_finish": (c_int, [P, c_int, c_int64, c_int, c_int, P, P, P, P, c_int, c_int,
-                                 c_int, c_int, c_int, c_int, c_int, c_uint64, P, P, P, P, P, P,
-                                 P]),
     "dice_cond_decide": (c_int, [P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int, c_uint64,
                                  P, P, P, P, P, P, P]),
     "dice_route_permute": (c_int, [P, P, c_int64, c_int, c_int, P, c_int, P, c_int64, P, P, P,
                                    c_int, c_int64, c_int64, P, P, P]),
-    "dice_slot_init": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P]),
-    "dice_expert_gemm2_combine": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P, P, c_int,
-                                          c_int64, P, P, P]),
     "dice_permute_max_rows": (c_int64, [c_int64, c_int, c_int]),
     "dice_permute_scratch_ints": (c_int64, [c_int64, c_int, c_int]),
     "dice_grouped_ffn": (c_int, [P, c_int64, P, P, c_int, c_int, c_int, P, P, P, P]),
     "dice_cache_assemble": (c_int, [P, P, P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P, P, P]),
     "dice_gemm": (c_int, [c_int, P, c_int64, P, c_int, c_int, P, c_int64, P, c_int64, P, c_int64,
-                          P, c_int64, P]),
+                          P]),
+    "dice_expert_gemm2_pairs": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P, P, c_int,
+                                        c_int64, P, P, P, P]),
+    "dice_gemm_consume": (c_int, [P, c_int64, P, c_int, c_int, P, c_int64, P, P, c_int, P,
+                                  c_int64, P, c_int64, P]),
+    "dice_consume_rows": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, P]),
     "dice_combine": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P]),
     "dice_denoise": (c_int, [P, P, P, c_float, c_int64, c_int, P, c_int, P]),
     "dice_pack_rows": (c_int, [P, c_int64, c_int, c_int64, c_int, P, P, P]),
@@ -71,13 +67,13 @@ SIGNATURES = {
     "dice_ipc_close": (c_int, [P]),
     "dice_stream_wait_eq": (c_int, [ctypes.POINTER(c_uint64), c_int, ctypes.c_uint32, P]),
     "dice_stream_write": (c_int, [ctypes.POINTER(c_uint64), c_int, ctypes.c_uint32, P]),
-    "dice_ep_dispatch": (c_int, [P, P, c_int64, c_int, c_int, c_int, c_int, P, c_int, P, P, P,
+    "dice_ep_dispatch": (c_int, [P, P, P, c_int64, c_int, c_int, c_int, c_int, P, c_int, P, P, P,
                                  c_int64, c_int64, P, ctypes.POINTER(c_uint64),
                                  ctypes.POINTER(c_uint64), ctypes.POINTER(c_uint64), P]),
-    "dice_ep_expert": (c_int, [P, P, P, c_int, c_int64, c_int, c_int, c_int, P, P, P, P, P, P, P,
-                               c_int64, P, P, ctypes.POINTER(c_uint64), P, c_int64, P, c_int, P, P,
-                               P]),
-    "dice_iota": (c_int, [P, c_int64, P]),
+    "dice_ep_expert": (c_int, [P, P, P, c_int, c_int64, c_int, c_int, c_int, c_int, P, P, P, P, P,
+                               P, P, c_int64, P, P, ctypes.POINTER(c_uint64),
+                               ctypes.POINTER(c_uint64), ctypes.POINTER(c_uint64),
+                               ctypes.POINTER(c_int64), P, c_int64, P, c_int, P, P]),
 }
 
 _lock = threading.Lock()
@@ -122,19 +118,18 @@ def check(rc: int, what: str) -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches count)
-# (the three-kernel permute is the default; DICE_PERMUTE_FUSED=1 is one launch)
-KERNELS_PER_CALL = {"dice_route_permute": 1 if os.environ.get("DICE_PERMUTE_FUSED") == "1" else 3,
-                    "dice_route_permute_counted": 2,
-                    "dice_grouped_ffn": 2, "dice_gemm": 1,
-                    "dice_gemm_local_gate": 1, "dice_gate_parts": 0, "dice_event_create": 0,
-                    "dice_expert_gemm1_with_dense": 1, "dice_expert_gemm2": 1,
-                    "dice_slot_init": 1, "dice_expert_gemm2_combine": 1,
-                    "dice_event_destroy": 0, "dice_event_record": 0, "dice_event_elapsed_ms": 0,
+KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_route_permute_counted": 2,
+                    "dice_grouped_ffn": 2, "dice_event_create": 0, "dice_event_destroy": 0,
+                    "dice_event_record": 0, "dice_event_elapsed_ms": 0,
+                    "dice_permute_max_rows": 0, "dice_permute_scratch_ints": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,
-                    "dice_stream_write": 0, "dice_ep_dispatch": 3,
-                    # fused combine: the peer stores ride in the expert GEMM2 epilogue
-                    "dice_ep_expert": 7 if os.environ.get("DICE_EP_FUSED_COMBINE") == "0" else 6}
+                    "dice_stream_write": 0, "dice_version": 0,
+                    # count + scatter + send
+                    "dice_ep_dispatch": 3,
+                    # receive ids + count + scatter + gather + GEMM1 + GEMM2 (the
+                    # combine's peer stores ride in the GEMM2 epilogue)
+                    "dice_ep_expert": 6}
 launch_count = [0]
 
 

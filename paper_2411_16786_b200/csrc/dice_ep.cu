@@ -21,19 +21,18 @@
 
 namespace dice {
 
-constexpr int kMaxRanks = 16;
-
 struct PeerPtrs {
   void* p[kMaxRanks];
 };
 
 // Sender: warp per active pair; rows go to the destination rank's window at
-// the pair's compact index within (me -> dest), metadata (local expert, pair).
+// the pair's compact index within (me -> dest), metadata {local expert, home
+// pair, gate bits, expert id}.
 __global__ void __launch_bounds__(256) ep_send_kernel(
-    const int32_t* __restrict__ ids, const int32_t* __restrict__ pos_dest,
-    const int32_t* __restrict__ dest_offsets, int64_t pairs, int k, int El,
-    const uint16_t* __restrict__ u16, int hp, PeerPtrs rx_rows, PeerPtrs rx_meta, PeerPtrs rx_count,
-    int D) {
+    const int32_t* __restrict__ ids, const float* __restrict__ gates,
+    const int32_t* __restrict__ pos_dest, const int32_t* __restrict__ dest_offsets,
+    int64_t pairs, int k, int El, const uint16_t* __restrict__ u16, int hp, PeerPtrs rx_rows,
+    PeerPtrs rx_meta, PeerPtrs rx_count, int D) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x < D) {
@@ -52,12 +51,12 @@ __global__ void __launch_bounds__(256) ep_send_kernel(
     uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(rx_rows.p[d]) + (int64_t)idx * hp);
     for (int c = lane; c < vec; c += 32) dst[c] = src[c];
     if (lane == 0)
-      static_cast<int2*>(rx_meta.p[d])[idx] = make_int2(e - d * El, (int)q);
+      static_cast<int4*>(rx_meta.p[d])[idx] = make_int4(e - d * El, (int)q, __float_as_int(gates[q]), e);
   }
 }
 
 // Receiver: expert key of every received row (-1 beyond each source's count).
-__global__ void ep_rx_ids_kernel(const int2* __restrict__ meta, const int32_t* __restrict__ counts,
+__global__ void ep_rx_ids_kernel(const int4* __restrict__ meta, const int32_t* __restrict__ counts,
                                  int D, int64_t cap, int32_t* ids_rx) {
   pdl_enter();
   const int64_t total = (int64_t)D * cap;
@@ -67,33 +66,6 @@ __global__ void ep_rx_ids_kernel(const int2* __restrict__ meta, const int32_t* _
     const int64_t j = g - (int64_t)src * cap;
     ids_rx[g] = j < counts[src] ? meta[g].x : -1;
   }
-}
-
-// Owner -> home: expert output row of received row g goes back to its source
-// rank's combine window at the source's pair index.
-__global__ void __launch_bounds__(256) ep_combine_send_kernel(
-    const int32_t* __restrict__ pos_rx, const int2* __restrict__ meta, int64_t total, int64_t cap,
-    const uint16_t* __restrict__ y, int hp, PeerPtrs cx) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int vec = hp / 8;
-  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < total;
-       g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int pr = pos_rx[g];
-    if (pr < 0) continue;
-    const int src = (int)(g / cap);
-    const int pair = meta[g].y;
-    const uint4* s = reinterpret_cast<const uint4*>(y + (int64_t)pr * hp);
-    uint4* d = reinterpret_cast<uint4*>(static_cast<uint16_t*>(cx.p[src]) + (int64_t)pair * hp);
-    for (int c = lane; c < vec; c += 32) d[c] = s[c];
-  }
-}
-
-__global__ void iota_pairs_kernel(int32_t* out, int64_t count) {
-  pdl_enter();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (int32_t)i;
 }
 
 namespace {
@@ -207,90 +179,75 @@ int dice_stream_write(const uint64_t* addrs, int count, uint32_t value, void* st
 
 // Dispatch send for one layer (TokenCache.decide has produced `active`).
 // Groups this rank's active pairs by destination rank (compact, no padding),
-// counts bytes of remote pairs, and stores every row + (local expert, pair)
-// into the destination's window region reserved for this source rank.
-// rx_rows/rx_meta/rx_count: per-destination device pointers (peer-mapped) to
-// this layer's region for source `me`.
-int dice_ep_dispatch(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E, int D,
-                     int me, const uint16_t* u16, int hp, int32_t* pos_dest, int32_t* dest_offsets,
-                     int64_t* counters, int64_t row0, int64_t rows_total, int32_t* scratch,
-                     const uint64_t* rx_rows, const uint64_t* rx_meta, const uint64_t* rx_count,
-                     void* stream) {
-  if (D < 1 || D > kMaxRanks || E % D != 0 || hp % 64 != 0 || me < 0 || me >= D)
+// counts bytes of remote pairs, and stores every row + {local expert, pair,
+// gate, expert} into the destination's window region reserved for this source
+// rank. rx_rows/rx_meta/rx_count: per-destination device pointers (peer-mapped)
+// to this layer's region for source `me`.
+int dice_ep_dispatch(const int32_t* ids, const float* gates, const uint8_t* active, int64_t n,
+                     int k, int E, int D, int me, const uint16_t* u16, int hp, int32_t* pos_dest,
+                     int32_t* dest_offsets, int64_t* counters, int64_t row0, int64_t rows_total,
+                     int32_t* scratch, const uint64_t* rx_rows, const uint64_t* rx_meta,
+                     const uint64_t* rx_count, void* stream) {
+  if (D < 1 || D > kMaxRanks || E % D != 0 || hp % 64 != 0 || me < 0 || me >= D ||
+      gates == nullptr)
     return DICE_ERR_CONTRACT;
   cudaStream_t s = (cudaStream_t)stream;
   const int El = E / D;
   int rc = permute_launch(ids, active, n, k, D, El, 1, E, nullptr, hp, nullptr, pos_dest,
                           dest_offsets, counters, D, row0, rows_total, scratch, s);
   if (rc) return rc;
-  ep_send_kernel<<<grid_warps(n * k), 256, 0, s>>>(ids, pos_dest, dest_offsets, n * k, k, El, u16, hp,
-                                                   table(rx_rows, D, 0), table(rx_meta, D, 0),
-                                                   table(rx_count, D, 0), D);
+  // plain launches on the exchange path: these kernels follow stream memory
+  // operations (flag waits), not kernels
+  ep_send_kernel<<<grid_warps(n * k), 256, 0, s>>>(ids, gates, pos_dest, dest_offsets, n * k, k,
+                                                   El, u16, hp, table(rx_rows, D, 0),
+                                                   table(rx_meta, D, 0), table(rx_count, D, 0), D);
   return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
 }
 
 // Receive side of one layer: group the rows every source rank stored in this
 // rank's window by local expert (256-row padded tiles), run the grouped
-// expert FFN, and store each output row into its home rank's combine window
-// at the home's pair index. rx_rows [D*cap, hp], rx_meta [D*cap] (int2),
-// rx_count [D] are this rank's window for the layer; cx: per-source pointer to
-// the layer's combine window base [n_src*k, hp].
+// expert FFN, and let the expert GEMM2's epilogue store each output row into
+// its home rank's pair rows (with gate and expert id) over peer memory.
+// rx_rows [D*cap, hp], rx_meta [D*cap] (int4), rx_count [D] are this rank's
+// window for the layer.
 int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
-                   int64_t cap, int El, int hp, int ep, const uint16_t* w1_t, const uint16_t* w2_t,
-                   int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets, int32_t* scratch,
-                   uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf, uint16_t* y,
-                   const uint64_t* cx, const uint16_t* A2, int64_t M2, const uint16_t* B2,
-                   int N2, uint16_t* out2, int32_t* row_pair, void* stream) {
-  if (D < 1 || D > kMaxRanks || hp % 64 != 0 || ep % 64 != 0 || El < 1) return DICE_ERR_CONTRACT;
+                   int64_t cap, int El, int hp, int ep, int k, const uint16_t* w1_t,
+                   const uint16_t* w2_t, int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets,
+                   int32_t* scratch, uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf,
+                   int32_t* row_pair, const uint64_t* home_rows, const uint64_t* home_gates,
+                   const uint64_t* home_ids, const int64_t* home_n, const uint16_t* A2,
+                   int64_t M2, const uint16_t* B2, int N2, uint16_t* out2, void* stream) {
+  if (D < 1 || D > kMaxRanks || hp % 64 != 0 || ep % 64 != 0 || El < 1 || k < 1 ||
+      row_pair == nullptr)
+    return DICE_ERR_CONTRACT;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t total = (int64_t)D * cap;
-  // combine all-to-all fused into the expert GEMM2 epilogue (row_pair given;
-  // DICE_EP_FUSED_COMBINE=0: GEMM2 into y, then a separate peer-store kernel)
-  const char* fe = getenv("DICE_EP_FUSED_COMBINE");
-  const bool fused = row_pair != nullptr && !(fe != nullptr && fe[0] == '0');
   ep_rx_ids_kernel<<<(int)((total + 255) / 256 < 2368 ? (total + 255) / 256 : 2368), 256, 0, s>>>(
-      static_cast<const int2*>(rx_meta), rx_count, D, cap, ids_rx);
+      static_cast<const int4*>(rx_meta), rx_count, D, cap, ids_rx);
   int rc = permute_launch(ids_rx, nullptr, total, 1, El, 1, 256, El, rx_rows, hp, x_perm, pos_rx,
-                          tile_offsets, nullptr, 1, 0, total, scratch, s,
-                          fused ? row_pair : nullptr);
+                          tile_offsets, nullptr, 1, 0, total, scratch, s, row_pair);
   if (rc) return rc;
-  if (fused) {
-    // GEMM1 (+ the rank's shared GEMM1 in the same launch), then GEMM2 whose
-    // epilogue stores every finished row into its home rank's combine window
-    rc = dice_expert_gemm1_with_dense(x_perm, max_rows, w1_t, El, hp, ep, tile_offsets, hbuf,
-                                      A2, A2 != nullptr ? M2 : 0, B2, N2, out2, stream);
-    if (rc) return rc;
-    GemmProblem q{};
-    q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
-    q.num_groups = El; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / 256);
-    q.epi_kind = EPI_STORE_SCATTER;
-    q.epi.ld_bf16 = hp;
-    q.epi.row_pair = row_pair;
-    q.epi.scatter_meta = rx_meta;
-    q.epi.scatter_cap = cap;
-    for (int r = 0; r < D; ++r) q.epi.scatter_dst[r] = cx[r];
-    return gemm_bf16(q, s);
-  }
-  if (A2 != nullptr && M2 > 0) {
-    // this rank's shared-expert GEMM1 rides in the expert GEMM1 launch
-    rc = dice_expert_gemm1_with_dense(x_perm, max_rows, w1_t, El, hp, ep, tile_offsets, hbuf, A2,
-                                      M2, B2, N2, out2, stream);
-    if (rc) return rc;
-    rc = dice_expert_gemm2(hbuf, max_rows, w2_t, El, hp, ep, tile_offsets, y, stream);
-  } else {
-    rc = dice_grouped_ffn(x_perm, max_rows, w1_t, w2_t, El, hp, ep, tile_offsets, hbuf, y, stream);
-  }
+  // GEMM1 (+ the rank's shared GEMM1 in the same launch), then GEMM2 whose
+  // epilogue stores every finished row into its home rank's pair rows
+  rc = dice_expert_gemm1_with_dense(x_perm, max_rows, w1_t, El, hp, ep, tile_offsets, hbuf,
+                                    A2, A2 != nullptr ? M2 : 0, B2, N2, out2, stream);
   if (rc) return rc;
-  ep_combine_send_kernel<<<grid_warps(total), 256, 0, s>>>(
-      pos_rx, static_cast<const int2*>(rx_meta), total, cap, y, hp, table(cx, D, 0));
-  return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
-}
-
-int dice_iota(int32_t* out, int64_t count, void* stream) {
-  if (count <= 0) return DICE_OK;
-  iota_pairs_kernel<<<(int)((count + 255) / 256 < 2368 ? (count + 255) / 256 : 2368), 256, 0,
-                      (cudaStream_t)stream>>>(out, count);
-  return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+  GemmProblem q{};
+  q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
+  q.num_groups = El; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / 256);
+  q.epi_kind = EPI_STORE_SCATTER;
+  q.epi.ld_bf16 = hp;
+  q.epi.row_pair = row_pair;
+  q.epi.top_k = k;
+  q.epi.scatter_meta = rx_meta;
+  q.epi.scatter_cap = cap;
+  for (int r = 0; r < D; ++r) {
+    q.epi.scatter_rows[r] = home_rows[r];
+    q.epi.scatter_gates[r] = home_gates[r];
+    q.epi.scatter_ids[r] = home_ids[r];
+    q.epi.scatter_n[r] = home_n[r];
+  }
+  return gemm_bf16(q, s);
 }
 
 }  // extern "C"

@@ -1,7 +1,8 @@
 // Warp-specialised tcgen05 GEMM for sm_100a: C[M,N] = A[M,K] * B[N,K]^T
 // (both operands K-major bf16, fp32 accumulation in TMEM), persistent over
-// 128 x BN output tiles, TMA-fed multi-stage smem ring, double-buffered TMEM
-// accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
+// 256 x BN output tiles computed by CTA pairs (cta_group::2), TMA-fed
+// multi-stage smem ring, double-buffered TMEM accumulators so the epilogue of
+// tile i overlaps the MMAs of tile i+1.
 //
 // One kernel serves every dense contraction of the MoE layer:
 //   * grouped expert FFN (expert_forward, model.py:226-232): rows of A are the
@@ -11,8 +12,10 @@
 //   * shared FFN (shared_forward, model.py:235-241) with the S shared experts
 //     concatenated along N (GEMM1) / K (GEMM2).
 //   * mixing block (local_block, model.py:244-252).
-// Epilogues fuse exact-erf GELU, the residual add of local_block, and the
-// consume step u + (shared + routed) (schedules.py:308-317, model.py:279-298).
+// Epilogues fuse exact-erf GELU, the residual add of local_block, the expert
+// rows' store into the layer's pair rows (TokenCache rows, policies.py:188-208)
+// and the consume step u + (shared + sum_s g_s row_s) (schedules.py:308-317,
+// model.py:279-298) that reads them back.
 #include "dice_gemm.h"
 #include "dice_ptx.cuh"
 
@@ -29,21 +32,6 @@ constexpr int UMMA_K = 16;
 constexpr int kEpiWarps = 12;   // 3 per TMEM lane quadrant
 constexpr int kEpiGroups = kEpiWarps / 4;
 constexpr int kThreads = 128 + 32 * kEpiWarps;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4.. epilogue
-
-template <int BN>
-struct GemmCfg {
-  static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesFit = (232448 - kEpiWarps * 4096 - 2048) / kStageBytes;
-  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
-  // two accumulator buffers; allocation is a power of two >= 32 columns
-  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  // per epilogue warp: a 32x32 fp32 transpose tile (XOR-swizzled, conflict free)
-  static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;
-  static constexpr int kSmemBytes =
-      kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 1024 /*barriers*/;
-};
 
 constexpr int kMaxStages = 12;
 
@@ -65,16 +53,30 @@ __device__ __forceinline__ int find_group(const int* off, int groups, int m_tile
 
 // Epilogue on 4 consecutive columns per lane: 8 lanes cover the 32 columns of
 // one output row, a warp covers 4 rows per pass, so residual loads and f32 /
-// bf16 stores are coalesced 128-byte / 64-byte row segments. All 8 passes'
+// bf16 stores are coalesced 128-byte / 64-byte row segments. All passes'
 // global loads are issued before any math so their latencies overlap.
-template <int EPI, bool WRITE_BACK = false>
+__device__ __forceinline__ float4 bf16x4_to_f32(uint2 w) {
+  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                     __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+}
+__device__ __forceinline__ float4 add_scaled(float4 x, float g, float4 r) {
+  // x + g * r with the product and the sum each rounded (combine_outputs,
+  // model.py:295-297: out += gates[:, s] * rows[s])
+  return make_float4(__fadd_rn(x.x, __fmul_rn(g, r.x)), __fadd_rn(x.y, __fmul_rn(g, r.y)),
+                     __fadd_rn(x.z, __fmul_rn(g, r.z)), __fadd_rn(x.w, __fmul_rn(g, r.w)));
+}
+
+template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, float* stage, int lane,
                                                int row0, int row_limit, int col0) {
   const int q = lane & 7;
   const int col = col0 + 4 * q;
+  constexpr int KF = 2;   // consume: routed slots prefetched with the residual (more: in turn)
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    float4 v[4], r[4], ad[4];
+    float4 v[4], r[4];
+    uint2 pr[KF][4];
+    float pg[KF][4];
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int rr = (half * 4 + it) * 4 + (lane >> 3);
@@ -86,8 +88,16 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, float* stage, 
         const int64_t row = row0 + (half * 4 + it) * 4 + (lane >> 3);
         if (row < row_limit) {
           r[it] = __ldg(reinterpret_cast<const float4*>(a.residual + row * a.ld_res + col));
-          if constexpr (EPI == EPI_CONSUME)
-            ad[it] = __ldg(reinterpret_cast<const float4*>(a.addend + row * a.ld_add + col));
+          if constexpr (EPI == EPI_CONSUME) {
+#pragma unroll
+            for (int s = 0; s < KF; ++s) {
+              if (s < a.top_k) {
+                pr[s][it] = __ldg(reinterpret_cast<const uint2*>(
+                    a.pair_rows + ((int64_t)s * a.n_tokens + row) * a.N + col));
+                pg[s][it] = __ldg(a.pair_gates + row * a.top_k + s);
+              }
+            }
+          }
         }
       }
     }
@@ -104,13 +114,18 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, float* stage, 
         x.x += r[it].x; x.y += r[it].y; x.z += r[it].z; x.w += r[it].w;
       }
       if constexpr (EPI == EPI_CONSUME) {
-        x.x = r[it].x + (x.x + ad[it].x); x.y = r[it].y + (x.y + ad[it].y);
-        x.z = r[it].z + (x.z + ad[it].z); x.w = r[it].w + (x.w + ad[it].w);
-      }
-      if constexpr (WRITE_BACK) {
-        // the finished values replace the accumulators in the transpose tile
-        const int rr = (half * 4 + it) * 4 + (lane >> 3);
-        *reinterpret_cast<float4*>(stage + rr * 32 + ((q ^ (rr & 7)) << 2)) = x;
+        if (row < row_limit) {
+#pragma unroll
+          for (int s = 0; s < KF; ++s)
+            if (s < a.top_k) x = add_scaled(x, pg[s][it], bf16x4_to_f32(pr[s][it]));
+          for (int s = KF; s < a.top_k; ++s) {
+            const uint2 w = __ldg(reinterpret_cast<const uint2*>(
+                a.pair_rows + ((int64_t)s * a.n_tokens + row) * a.N + col));
+            x = add_scaled(x, __ldg(a.pair_gates + row * a.top_k + s), bf16x4_to_f32(w));
+          }
+          x = make_float4(__fadd_rn(r[it].x, x.x), __fadd_rn(r[it].y, x.y),
+                          __fadd_rn(r[it].z, x.z), __fadd_rn(r[it].w, x.w));
+        }
       }
       if (row < row_limit) {
         if (a.out_f32 != nullptr) *reinterpret_cast<float4*>(a.out_f32 + row * a.ld_f32 + col) = x;
@@ -121,145 +136,6 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& a, float* stage, 
         }
       }
     }
-  }
-}
-
-template <int BN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
-gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const GemmArgs args) {
-  pdl_enter();
-  using C = GemmCfg<BN>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smA = smem;
-  uint8_t* smB = smem + C::kStages * C::kABytes;
-  float* sm_epi = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
-  GemmShared* sh = reinterpret_cast<GemmShared*>(smem + C::kStages * C::kStageBytes + C::kEpiBytes);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) { mbar_init(&sh->full[s], 1); mbar_init(&sh->empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], kEpiWarps); }
-    fence_barrier_init();
-    if (args.group_tile_offsets != nullptr) {
-      for (int g = 0; g <= args.num_groups; ++g) sh->group_off[g] = args.group_tile_offsets[g];
-      sh->m_tiles = sh->group_off[args.num_groups];
-    } else {
-      sh->group_off[0] = 0;
-      sh->group_off[1] = args.num_m_tiles;
-      sh->m_tiles = args.num_m_tiles;
-    }
-  }
-  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(&sh->tmem_base);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-
-  const uint32_t tmem_base = sh->tmem_base;
-  const int m_tiles = sh->m_tiles;
-  const int groups = args.group_tile_offsets != nullptr ? args.num_groups : 1;
-  const int n_blocks = args.num_n_blocks;
-  const int k_blocks = args.num_k_blocks;
-  const int num_tiles = m_tiles * n_blocks;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int n_blk = tile % n_blocks;   // N-fastest: resident tiles share A rows
-        const int m_tile = tile / n_blocks;
-        const int g = find_group(sh->group_off, groups, m_tile);
-        const int a_row = m_tile * BM;
-        const int b_row = g * args.N + n_blk * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&sh->empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&sh->full[stage], C::kStageBytes);
-          tma_load_2d(smA + stage * C::kABytes, &tmA, &sh->full[stage], kb * BK, a_row);
-          tma_load_2d(smB + stage * C::kBBytes, &tmB, &sh->full[stage], kb * BK, b_row);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&sh->tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&sh->full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(smA + stage * C::kABytes);
-          const uint32_t b_base = smem_u32(smB + stage * C::kBBytes);
-#pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            const uint64_t ad = umma_desc_sw128(a_base + k * UMMA_K * 2);
-            const uint64_t bd = umma_desc_sw128(b_base + k * UMMA_K * 2);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-          }
-          umma_commit(&sh->empty[stage]);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-        }
-        umma_commit(&sh->tfull[acc]);
-      }
-    }
-  } else if (warp >= 4) {
-    // --------------------------------------------------------------- epilogue
-    const int sub = warp & 3;            // TMEM lane quadrant this warp may access
-    const int grp = (warp - 4) >> 2;     // which 32-column chunks of the tile (round robin)
-    float* stage = sm_epi + (warp - 4) * 1024;
-    const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
-    int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int n_blk = tile % n_blocks;
-      const int m_tile = tile / n_blocks;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&sh->tfull[acc], acc_phase);
-      tc_fence_after();
-      const int row0 = m_tile * BM + sub * 32;
-#pragma unroll 1
-      for (int ci = grp; ci < BN / 32; ci += kEpiGroups) {
-        const int col_in_tile = ci * 32;
-        const int col0 = n_blk * BN + col_in_tile;
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN + col_in_tile, r);
-        tmem_ld_wait();
-        if (col0 >= args.N) continue;  // warp-uniform
-        // transpose through shared memory (16-byte chunks XOR-swizzled by row):
-        // thread = row on the way in, 8 lanes per row x 4 columns on the way out
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(stage + lane * 32 + ((q ^ (lane & 7)) << 2)) =
-              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-        __syncwarp();
-        epilogue_chunk<EPI>(args, stage, lane, row0, row_limit, col0);
-        __syncwarp();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh->tempty[acc]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
@@ -323,31 +199,6 @@ __device__ __forceinline__ void epilogue_gelu_resid_pf(const GemmArgs& a, const 
   }
 }
 
-// Router logits of the finished u rows (gate, model.py:209-223, fused into the
-// local_block GEMM): the lane owning row `lane` of the transpose tile dots its
-// 32 finished values with W_gate[col0 .. col0+32, :] (warp-uniform broadcast
-// loads) into GE partial logits, accumulated over this warp's chunks of the tile.
-template <int GE>
-__device__ __forceinline__ void gate_accumulate(const GemmArgs& a, const float* stage, int lane,
-                                                int col0, float2 (&g)[GE / 2]) {
-  const float4* w = reinterpret_cast<const float4*>(a.gate_w + (int64_t)col0 * GE);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 xv = *reinterpret_cast<const float4*>(stage + lane * 32 + ((q ^ (lane & 7)) << 2));
-    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 xx = make_float2(xs[j], xs[j]);
-#pragma unroll
-      for (int e4 = 0; e4 < GE / 4; ++e4) {
-        const float4 wv = __ldg(w + (4 * q + j) * (GE / 4) + e4);
-        g[2 * e4] = __ffma2_rn(xx, make_float2(wv.x, wv.y), g[2 * e4]);
-        g[2 * e4 + 1] = __ffma2_rn(xx, make_float2(wv.z, wv.w), g[2 * e4 + 1]);
-      }
-    }
-  }
-}
-
 // --------------------------------------------------------- CTA-pair kernel
 // cta_group::2: a cluster of two CTAs computes a 256 x BN tile. Each CTA
 // stages its own 128 rows of A and half (BN/2 rows) of B, so per-CTA operand
@@ -376,51 +227,10 @@ struct PairCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 2048;
 };
 
-// Routed combine fused into the expert GEMM2 epilogue (EPI_COMBINE): this lane
-// owns permuted row `row` = pair p = (token t, slot s) and 32 columns. The row
-// is rounded to bf16 exactly as the expert output rows are (the on-wire width),
-// persisted to the token cache when the pair refreshes it (policies.py:203-207),
-// and round(g * row) is added to the token's combine slot with float4 atomics.
-// With k <= 2 terms per token onto a slot pre-initialised with the cached
-// terms, the float sum is order-independent (two terms commute; x + 0 == x),
-// so the result is deterministic and equals cache_assemble's.
-__device__ __forceinline__ void epilogue_combine(const GemmArgs& a, const uint32_t (&r)[32],
-                                                 int64_t row, int col0) {
-  const int p = a.row_pair[row];
-  if (p < 0) return;                       // padding row of an expert group
-  const int k = a.top_k;
-  const int64_t t = p / k;
-  const int s = p - (int)t * k;
-  const float g = a.pair_gates[p];
-  uint32_t w[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-    w[j] = *reinterpret_cast<uint32_t*>(&b);
-  }
-  if (a.pair_write != nullptr && a.pair_write[p] != 0) {
-    uint4* dst = reinterpret_cast<uint4*>(a.cache_rows + ((int64_t)s * a.n_tokens + t) * a.N + col0);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-  }
-  float4* slot = reinterpret_cast<float4*>(a.slot + t * a.N + col0);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float v0 = __uint_as_float(w[2 * j] << 16), v1 = __uint_as_float(w[2 * j] & 0xFFFF0000u);
-    const float v2 = __uint_as_float(w[2 * j + 1] << 16), v3 = __uint_as_float(w[2 * j + 1] & 0xFFFF0000u);
-    atomicAdd(slot + j, make_float4(__fmul_rn(g, v0), __fmul_rn(g, v1), __fmul_rn(g, v2),
-                                    __fmul_rn(g, v3)));
-  }
-}
-
 // Direct bf16 epilogue: this lane owns one row and 32 consecutive columns.
 template <int EPI>
 __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_t (&r)[32],
                                                 int64_t row, int col0) {
-  if constexpr (EPI == EPI_COMBINE) {
-    epilogue_combine(a, r, row, col0);
-    return;
-  }
   uint32_t w[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -430,12 +240,31 @@ __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_
     w[j] = *reinterpret_cast<uint32_t*>(&b);
   }
   __nv_bfloat16* out = a.out_bf16 + row * a.ld_bf16;
+  if constexpr (EPI == EPI_STORE_PAIR) {
+    // (token, slot) pair of this expert row -> the layer's pair rows [s][t]
+    const int p = a.row_pair[row];
+    if (p < 0) return;                       // padding row of an expert group
+    const int64_t t = p / a.top_k;
+    const int s = p - (int)t * a.top_k;
+    out = a.out_bf16 + ((int64_t)s * a.n_tokens + t) * a.ld_bf16;
+    if (col0 == 0) {
+      if (a.cache_gates != nullptr) a.cache_gates[p] = a.pair_gates[p];
+      if (a.cache_ids != nullptr) a.cache_ids[p] = a.pair_ids[p];
+    }
+  }
   if constexpr (EPI == EPI_STORE_SCATTER) {
     const int i = a.row_pair[row];
     if (i < 0) return;                       // padding row of an expert group
     const int src = (int)(i / a.scatter_cap);
-    const int pair = reinterpret_cast<const int2*>(a.scatter_meta)[i].y;
-    out = reinterpret_cast<__nv_bfloat16*>(a.scatter_dst[src]) + (int64_t)pair * a.ld_bf16;
+    const int4 m = reinterpret_cast<const int4*>(a.scatter_meta)[i];   // {e_local, pair, gate, expert}
+    const int64_t t = m.y / a.top_k;
+    const int s = m.y - (int)t * a.top_k;
+    out = reinterpret_cast<__nv_bfloat16*>(a.scatter_rows[src]) +
+          ((int64_t)s * a.scatter_n[src] + t) * a.ld_bf16;
+    if (col0 == 0) {
+      reinterpret_cast<float*>(a.scatter_gates[src])[m.y] = __int_as_float(m.z);
+      reinterpret_cast<int32_t*>(a.scatter_ids[src])[m.y] = m.w;
+    }
   }
   uint4* dst = reinterpret_cast<uint4*>(out + col0);
 #pragma unroll
@@ -591,10 +420,6 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       mbar_wait(&sh->tfull[acc], acc_phase);
       tc_fence_after();
-      constexpr int GE = EpiTraits<EPI>::gate_e;
-      float2 gacc[GE > 0 ? GE / 2 : 1];
-#pragma unroll
-      for (int e = 0; e < (GE > 0 ? GE / 2 : 1); ++e) gacc[e] = make_float2(0.f, 0.f);
 #pragma unroll 1
       for (int ci = grp; ci < TN / 32; ci += kEpiGroups) {
         const int col_in_tile = ci * 32;
@@ -614,11 +439,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         __syncwarp();
-        if constexpr (GE > 0) {
-          epilogue_chunk<EpiTraits<EPI>::base, true>(args, stage, lane, row0, row_limit, col0);
-          __syncwarp();
-          gate_accumulate<GE>(args, stage, lane, col0, gacc);
-        } else if constexpr (kResidPF) {
+        if constexpr (kResidPF) {
           resid_wait();
           const int nci = ci + kEpiGroups;
           const int ncol = n_blk * TN + nci * 32;
@@ -628,16 +449,6 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           epilogue_chunk<EPI>(ar, stage, lane, row0, rl, col0);
         }
         __syncwarp();
-      }
-      if constexpr (GE > 0) {
-        const int64_t row = row0 + lane;
-        if (row < row_limit) {
-          float4* dst = reinterpret_cast<float4*>(
-              args.gate_part + ((int64_t)(n_blk * kEpiGroups + grp) * args.M_valid + row) * GE);
-#pragma unroll
-          for (int e4 = 0; e4 < GE / 4; ++e4)
-            dst[e4] = make_float4(gacc[2 * e4].x, gacc[2 * e4].y, gacc[2 * e4 + 1].x, gacc[2 * e4 + 1].y);
-        }
       }
       tc_fence_before();
       __syncwarp();
@@ -727,28 +538,6 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int EPI>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
-           cudaStream_t stream) {
-  using C = GemmCfg<BN>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::kSmemBytes) != cudaSuccess)
-      return DICE_ERR_CUDA;
-    attr_done = true;
-  }
-  int grid = max_tiles < num_sms() ? max_tiles : num_sms();
-  if (grid <= 0) return 0;
-  launch_pdl(gemm_bf16_tcgen05<BN, EPI>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ta, tb, a);
-  return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
-}
-
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return (e != nullptr && e[0] != 0) ? atoi(e) : dflt;
-}
-
 template <int BN, int EPI, bool DIRECT, int NSUB = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
@@ -762,20 +551,14 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
     attr_done = true;
   }
   const int items = max_tiles + (a2 != nullptr ? a2->num_m_tiles * a2->num_n_blocks : 0);
-  static const int cta_cap = env_int("DICE_GEMM_MAX_CTAS", 1 << 30);   // experiment hook
-  const int sms = num_sms() < cta_cap ? num_sms() : cta_cap;
+  const int sms = num_sms();
   int grid = 2 * items < sms ? 2 * items : sms;
   grid &= ~1;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
-  // experiment hook: DICE_GEMM_STAGES caps the operand ring depth
-  static const int cap = env_int("DICE_GEMM_STAGES", kMaxStages);
-  aa.stages = C::kStages < cap ? C::kStages : (cap < 2 ? 2 : cap);
+  aa.stages = C::kStages;
   GemmArgs bb{};
-  if (a2 != nullptr) {
-    if (EpiTraits<EPI>::gate_e > 0) return DICE_ERR_CONTRACT;
-    bb = *a2;
-  }
+  if (a2 != nullptr) bb = *a2;
   launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
              ta, tb, aa, a2 != nullptr ? *ta2 : ta, a2 != nullptr ? *tb2 : tb, bb);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
@@ -787,12 +570,9 @@ int dispatch_wide(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
   switch (epi) {
     case EPI_STORE_BF16: return launch_pair<192, EPI_STORE_BF16, true, 2>(ta, tb, a, max_tiles, s);
     case EPI_GELU_BF16: return launch_pair<192, EPI_GELU_BF16, true, 2>(ta, tb, a, max_tiles, s);
-    case EPI_COMBINE: return launch_pair<192, EPI_COMBINE, true, 2>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_PAIR: return launch_pair<192, EPI_STORE_PAIR, true, 2>(ta, tb, a, max_tiles, s);
     case EPI_STORE_SCATTER:
       return launch_pair<192, EPI_STORE_SCATTER, true, 2>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_F32: return launch_pair<192, EPI_STORE_F32, false, 2>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_RESID: return launch_pair<192, EPI_GELU_RESID, false, 2>(ta, tb, a, max_tiles, s);
-    case EPI_CONSUME: return launch_pair<192, EPI_CONSUME, false, 2>(ta, tb, a, max_tiles, s);
     default: return DICE_ERR_CONTRACT;
   }
 }
@@ -800,99 +580,49 @@ int dispatch_wide(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
 template <int BN>
 int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                   int max_tiles, cudaStream_t s) {
-  // bf16-only epilogues default to direct register stores (DICE_GEMM_EPI_DIRECT=0: staged)
-  static const bool direct = env_int("DICE_GEMM_EPI_DIRECT", 1) != 0;
   switch (epi) {
-    case EPI_STORE_BF16:
-      return direct ? launch_pair<BN, EPI_STORE_BF16, true>(ta, tb, a, max_tiles, s)
-                    : launch_pair<BN, EPI_STORE_BF16, false>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_BF16:
-      return direct ? launch_pair<BN, EPI_GELU_BF16, true>(ta, tb, a, max_tiles, s)
-                    : launch_pair<BN, EPI_GELU_BF16, false>(ta, tb, a, max_tiles, s);
-    case EPI_COMBINE: return launch_pair<BN, EPI_COMBINE, true>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_BF16: return launch_pair<BN, EPI_STORE_BF16, true>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_BF16: return launch_pair<BN, EPI_GELU_BF16, true>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_PAIR: return launch_pair<BN, EPI_STORE_PAIR, true>(ta, tb, a, max_tiles, s);
     case EPI_STORE_SCATTER: return launch_pair<BN, EPI_STORE_SCATTER, true>(ta, tb, a, max_tiles, s);
     case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false>(ta, tb, a, max_tiles, s);
     case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false>(ta, tb, a, max_tiles, s);
     case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_RESID_GATE8: return launch_pair<BN, EPI_GELU_RESID_GATE8, false>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_RESID_GATE16:
-      return launch_pair<BN, EPI_GELU_RESID_GATE16, false>(ta, tb, a, max_tiles, s);
-    default: return DICE_ERR_CONTRACT;
-  }
-}
-
-template <int BN>
-int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                 int max_tiles, cudaStream_t s) {
-  switch (epi) {
-    case EPI_STORE_BF16: return launch<BN, EPI_STORE_BF16>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_BF16: return launch<BN, EPI_GELU_BF16>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_F32: return launch<BN, EPI_STORE_F32>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_RESID: return launch<BN, EPI_GELU_RESID>(ta, tb, a, max_tiles, s);
-    case EPI_CONSUME: return launch<BN, EPI_CONSUME>(ta, tb, a, max_tiles, s);
     default: return DICE_ERR_CONTRACT;
   }
 }
 
 }  // namespace
 
-bool use_pair_kernel() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("DICE_GEMM_PAIR");
-    mode = (e != nullptr && e[0] == '0') ? 0 : 1;
-  }
-  return mode == 1;
-}
-
 struct TileChoice {
   int bn;        // MMA N per accumulator
   int tile_n;    // output columns per tile (bn, or 384 for the wide tiles)
-  bool pair;     // CTA-pair kernel (256-row tiles)
   bool wide;
 };
 
+// Every GEMM runs on the CTA-pair kernel (256-row tiles: the permute pads
+// expert groups to 256 rows). Tile width: 256 when N allows, else 192 / 128;
+// N = 1152-class long-K bf16 GEMMs take 256 x 384 tiles (measured, XL shapes:
+// 16384x1152x4608 1148 -> 1348 TF/s) when the wave count does not lose what
+// the wider tile gains (its single TMEM buffer exposes each tile's epilogue,
+// so only for the register-direct bf16 epilogues).
 TileChoice choose_tile(const GemmProblem& p) {
   TileChoice c{};
   c.bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
-  if (const char* e = getenv("DICE_GEMM_BN")) {
-    // experiment hook: force the tile width (128 / 192 / 256)
-    const int f = atoi(e);
-    if (f == 128 || f == 192 || f == 256) c.bn = f;
-  }
-  if (const char* e = getenv("DICE_GEMM_BN_NARROW")) {
-    // experiment hook: use 128-wide tiles for N not divisible by 256 (wave quantisation)
-    if (e[0] == '1' && p.N % 256 != 0) c.bn = 128;
-  }
-  const bool gate = p.epi_kind == EPI_GELU_RESID_GATE8 || p.epi_kind == EPI_GELU_RESID_GATE16;
-  // grouped GEMMs always use 256-row tiles (the permute pads experts to 256 rows);
-  // the gate-fused epilogue exists only in the pair kernel
-  c.pair = p.group_tile_offsets != nullptr || gate || use_pair_kernel();
-  // N = 1152-class shapes: 256 x 384 tiles (DICE_GEMM_WIDE=0 disables)
-  // (measured, XL shapes: 16384x1152x4608 1148 -> 1348 TF/s). The single TMEM
-  // buffer exposes each tile's epilogue, so only for long-K bf16 epilogues, and
-  // only when the wave count does not lose what the wider tile gains.
-  static const int wide_mode = env_int("DICE_GEMM_WIDE", 1);
   c.wide = false;
-  if (c.pair && c.bn == 192 && p.N % 384 == 0 && wide_mode != 0 && !gate) {
+  if (c.bn == 192 && p.N % 384 == 0) {
     const int64_t m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + 255) / 256;
     const int pairs = num_sms() / 2;
     auto wave_eff = [&](int64_t tiles) {
       return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs);
     };
     const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16 ||
-                            p.epi_kind == EPI_COMBINE || p.epi_kind == EPI_STORE_SCATTER;
+                            p.epi_kind == EPI_STORE_PAIR || p.epi_kind == EPI_STORE_SCATTER;
     const double narrow = wave_eff(m_tiles * (p.N / 192));
-    c.wide = wide_mode == 2 ||
-             (direct_epi && p.K >= 2048 && 1.15 * wave_eff(m_tiles * (p.N / 384)) >= narrow);
+    c.wide = direct_epi && p.K >= 2048 && 1.15 * wave_eff(m_tiles * (p.N / 384)) >= narrow;
   }
   c.tile_n = c.wide ? 384 : c.bn;
   return c;
-}
-
-int gemm_gate_parts(const GemmProblem& p) {
-  const TileChoice c = choose_tile(p);
-  return ((p.N + c.tile_n - 1) / c.tile_n) * kEpiGroups;
 }
 
 namespace {
@@ -901,10 +631,10 @@ int prepare(const GemmProblem& p, const TileChoice& tc, CUtensorMap* ta, CUtenso
             GemmArgs* a) {
   if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
   if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
-  const int tile_m = tc.pair ? 2 * BM : BM;
+  const int tile_m = 2 * BM;
   int rc = tensor_map(p.A, p.A_rows, p.K, BM, ta);
   if (rc) return rc;
-  rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, tc.pair ? tc.bn / 2 : tc.bn, tb);
+  rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, tc.bn / 2, tb);
   if (rc) return rc;
   *a = p.epi;
   a->M_valid = p.M;
@@ -922,7 +652,7 @@ int prepare(const GemmProblem& p, const TileChoice& tc, CUtensorMap* ta, CUtenso
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   const TileChoice tc = choose_tile(p);
   const int bn = tc.bn;
-  const bool pair = tc.pair, wide = tc.wide;
+  const bool wide = tc.wide;
   CUtensorMap ta, tb;
   GemmArgs a;
   int rc = prepare(p, tc, &ta, &tb, &a);
@@ -930,27 +660,20 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   const int max_tiles = a.num_m_tiles * a.num_n_blocks;
   if (max_tiles == 0) return 0;
   if (wide) return dispatch_wide(p.epi_kind, ta, tb, a, max_tiles, stream);
-  if (pair) {
-    if (bn == 256) return dispatch_pair<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
-    if (bn == 192) return dispatch_pair<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
-    return dispatch_pair<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
-  }
-  if (bn == 256) return dispatch_epi<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
-  if (bn == 192) return dispatch_epi<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
-  return dispatch_epi<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
+  if (bn == 256) return dispatch_pair<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
+  if (bn == 192) return dispatch_pair<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
+  return dispatch_pair<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
 }
 
 // Two independent GEMMs with the same K and bf16-only epilogue kind in ONE
 // persistent launch (p1 may be grouped, p2 dense): the grouped expert GEMM1
 // and the shared-expert GEMM1 of a stage. Falls back to two launches when the
-// tile choices differ (or DICE_GEMM_DUAL=0).
+// tile choices differ.
 int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t stream) {
-  static const int dual_mode = env_int("DICE_GEMM_DUAL", 1);
   const TileChoice c1 = choose_tile(p1), c2 = choose_tile(p2);
-  static const bool direct = env_int("DICE_GEMM_EPI_DIRECT", 1) != 0;
-  const bool ok = dual_mode != 0 && direct && p1.K == p2.K && p1.epi_kind == p2.epi_kind &&
+  const bool ok = p1.K == p2.K && p1.epi_kind == p2.epi_kind &&
                   (p1.epi_kind == EPI_STORE_BF16 || p1.epi_kind == EPI_GELU_BF16) &&
-                  p2.group_tile_offsets == nullptr && c1.pair && c2.pair && !c1.wide &&
+                  p2.group_tile_offsets == nullptr && !c1.wide &&
                   !c2.wide && c1.bn == c2.bn &&
                   (c1.bn == 256 || c1.bn == 192);
   if (!ok) {

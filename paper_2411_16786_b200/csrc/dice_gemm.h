@@ -15,38 +15,26 @@ enum EpiKind : int {
   EPI_GELU_BF16 = 1,   // out_bf16 = gelu(acc)
   EPI_STORE_F32 = 2,   // out_f32 = acc (and out_bf16 if set)
   EPI_GELU_RESID = 3,  // v = gelu(acc) + residual -> out_f32, out_bf16   (local_block)
-  EPI_CONSUME = 4,     // v = residual + (acc + addend) -> out_f32, out_bf16 (consume)
-  // GELU_RESID whose epilogue also emits partial router logits of the finished
-  // u rows (gate fused into local_block's GEMM, E = 8 / 16 experts)
-  EPI_GELU_RESID_GATE8 = 5,
-  EPI_GELU_RESID_GATE16 = 6,
-  // expert GEMM2 with the routed combine fused (k <= 2): each output row (a
-  // (token, slot) pair) is rounded to bf16 as a fresh expert row, persisted to the
-  // token cache when the pair refreshes it, and g * row is added into the
-  // token's combine slot (pre-initialised with its cached terms)
-  EPI_COMBINE = 7,
-  // expert-parallel expert GEMM2 with the combine all-to-all fused: each output
-  // row (window entry i = row_pair[r] of source rank i / scatter_cap) is stored
-  // as bf16 straight into that rank's combine window (peer memory) at its home
-  // pair index scatter_meta[i].y, tile by tile as the GEMM finishes them
-  EPI_STORE_SCATTER = 8,
+  // consume (schedules.py:308-317, model.py:279-298): the shared-expert GEMM2
+  // accumulator plus the token's routed rows, slots left to right, then the
+  // residual: v = residual + ((acc + g_0 * row_0) + g_1 * row_1 ...) with
+  // row_s = pair_rows[s][t] (bf16 [k, n, N]) and g_s = pair_gates[t][s]
+  // (f32 [n, k]) -> out_f32, out_bf16
+  EPI_CONSUME = 4,
+  // single-GPU expert GEMM2: the finished row of permuted row r (pair p =
+  // row_pair[r] = t*k + s; -1 on padding rows) is stored as bf16 at
+  // out_bf16[s][t] ([k, n, N]: the layer's pair rows, i.e. the token cache
+  // rows), and its gate / expert id at cache_gates[p] / cache_ids[p]
+  EPI_STORE_PAIR = 5,
+  // expert-parallel expert GEMM2 with the combine all-to-all fused: the row of
+  // window entry i = row_pair[r] (source rank i / scatter_cap, metadata int4
+  // {local expert, home pair, gate bits, global expert}) is stored as bf16
+  // straight into that rank's pair rows (peer memory) at [s][t] of its home
+  // pair, with the gate and expert id, tile by tile as the GEMM finishes them
+  EPI_STORE_SCATTER = 6,
 };
 
-template <int EPI>
-struct EpiTraits {
-  static constexpr int base = EPI;
-  static constexpr int gate_e = 0;
-};
-template <>
-struct EpiTraits<EPI_GELU_RESID_GATE8> {
-  static constexpr int base = EPI_GELU_RESID;
-  static constexpr int gate_e = 8;
-};
-template <>
-struct EpiTraits<EPI_GELU_RESID_GATE16> {
-  static constexpr int base = EPI_GELU_RESID;
-  static constexpr int gate_e = 16;
-};
+constexpr int kMaxRanks = 16;
 
 struct GemmArgs {
   int M_valid;
@@ -63,25 +51,27 @@ struct GemmArgs {
   int64_t ld_f32;
   const float* residual;
   int64_t ld_res;
-  const float* addend;
-  int64_t ld_add;
-  int stages;            // operand ring depth actually used (pair kernel; set by the host)
-  const float* gate_w;   // GATE epilogues: W_gate f32 [N, E] (row c = hidden column c)
-  float* gate_part;      // GATE epilogues: partial logits f32 [P, M, E], P = gemm_gate_parts()
-  // COMBINE: row -> pair map, per-pair gates / cache-write mask, slot [n, N] f32,
-  // cache rows of the layer bf16 [k, n, N]
+  int stages;            // operand ring depth actually used (set by the host)
+  // CONSUME: pair_rows bf16 [k, n_tokens, ld_bf16-wide rows], pair_gates f32 [n, k]
+  // STORE_PAIR: row -> pair map, source gates / ids of the pairs [n, k], the
+  // cache gates / ids they are persisted to
+  const __nv_bfloat16* pair_rows;
   const int32_t* row_pair;
   const float* pair_gates;
-  const uint8_t* pair_write;
+  const int32_t* pair_ids;
+  float* cache_gates;
+  int32_t* cache_ids;
   int top_k;
   int64_t n_tokens;
-  float* slot;
-  __nv_bfloat16* cache_rows;
-  // STORE_SCATTER: window metadata int2 [D * cap] (.y = home pair), entries per
-  // source rank, and the D combine-window bases (peer-mapped device pointers)
+  // STORE_SCATTER: window metadata int4 [D * cap], entries per source rank, and
+  // per source rank the (peer-mapped) pair rows / gates / ids of the layer and
+  // its row count
   const void* scatter_meta;
   int64_t scatter_cap;
-  uint64_t scatter_dst[16];
+  uint64_t scatter_rows[kMaxRanks];
+  uint64_t scatter_gates[kMaxRanks];
+  uint64_t scatter_ids[kMaxRanks];
+  int64_t scatter_n[kMaxRanks];
 };
 
 struct GemmProblem {
@@ -99,8 +89,6 @@ struct GemmProblem {
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream);
 // two independent problems (same K, bf16-only epilogue) in one persistent launch
 int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t stream);
-// number of partial-logit slots a GATE epilogue writes for this problem
-int gemm_gate_parts(const GemmProblem& p);
 
 // Count + scatter (+ optional row gather) of (token, slot) pairs grouped by
 // key = ids[p] / key_div, groups padded to row_tile rows (dice_ops.cu).

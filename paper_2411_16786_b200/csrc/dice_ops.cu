@@ -601,71 +601,6 @@ __global__ void __launch_bounds__(256, MINB) gate_topk_fast_kernel(
   }
 }
 
-// Gate finish over the partial logits the local_block GEMM epilogue emitted
-// (EPI_GELU_RESID_GATE*): logit = sum of the P slot partials in slot order,
-// softmax over E, stable top-k (ties -> lower id), gates renormalised over the
-// k picked in pick order (model.py:209-223); non-finite logits record
-// (step, layer) (model.py:212-213). One thread per token; optionally the
-// conditional-communication decision for the token follows in the same thread.
-template <int E>
-__global__ void __launch_bounds__(64) gate_parts_kernel(
-    const float* __restrict__ parts, int P, int64_t n, int k, int32_t* __restrict__ ids,
-    float* __restrict__ gates, float* __restrict__ scores, int32_t* status, int step, int layer,
-    const DecideArgs d) {
-  pdl_enter();
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    float l[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) l[e] = 0.f;
-    for (int p = 0; p < P; ++p) {
-      const float4* src = reinterpret_cast<const float4*>(parts + ((int64_t)p * n + t) * E);
-#pragma unroll
-      for (int e4 = 0; e4 < E / 4; ++e4) {
-        const float4 v = __ldg(src + e4);
-        l[4 * e4] += v.x; l[4 * e4 + 1] += v.y; l[4 * e4 + 2] += v.z; l[4 * e4 + 3] += v.w;
-      }
-    }
-    bool finite = true;
-    float mx = l[0];
-#pragma unroll
-    for (int e = 0; e < E; ++e) { finite = finite && isfinite(l[e]); mx = fmaxf(mx, l[e]); }
-    if (!finite) record_nonfinite(status, step, layer);
-    float sc[E], sum = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) { sc[e] = expf(l[e] - mx); sum += sc[e]; }
-#pragma unroll
-    for (int e = 0; e < E; ++e) sc[e] = sc[e] / sum;
-    if (scores != nullptr) {
-      float4* dst = reinterpret_cast<float4*>(scores + t * E);
-#pragma unroll
-      for (int e4 = 0; e4 < E / 4; ++e4)
-        dst[e4] = make_float4(sc[4 * e4], sc[4 * e4 + 1], sc[4 * e4 + 2], sc[4 * e4 + 3]);
-    }
-    uint32_t taken = 0;
-    float psum = 0.f, pick_s[E];
-    int pick_e[E];
-    for (int j = 0; j < k; ++j) {
-      int best = -1;
-      float bs = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const bool free_e = ((taken >> e) & 1u) == 0;
-        if (free_e && (best < 0 || sc[e] > bs)) { best = e; bs = sc[e]; }
-      }
-      taken |= 1u << best;
-      pick_e[j] = best;
-      pick_s[j] = bs;
-      psum += bs;
-    }
-    for (int j = 0; j < k; ++j) {
-      ids[t * k + j] = pick_e[j];
-      gates[t * k + j] = pick_s[j] / psum;
-    }
-    if (d.on) decide_token(t, k, ids, d);
-  }
-}
-
 // ------------------------------------------------------------- permute
 // Pairs are visited in token-major order p = t*k + s; within an expert the
 // rows are ordered by p, a deterministic order (the GEMM rows are independent,
@@ -827,151 +762,6 @@ __global__ void __launch_bounds__(kPermBlock) permute_scatter_kernel(
   if (row_pair != nullptr && valid) row_pair[base[e] + r] = (int32_t)p;   // row -> pair
 }
 
-// ------------------------------------------------- single-launch permute
-// The engine's route_permute as ONE persistent launch (grid <= #SMs, every
-// block co-resident): count per (block, expert) -> grid barrier -> 256-row
-// padded expert bases + positions in pair order (the same deterministic order
-// as the three-kernel path) -> grid barrier -> row gather by all warps.
-constexpr int kFusedPermMaxBlocks = 160;
-constexpr int kFusedPermThreads = 1024;
-
-// Sense-free generation barrier; state {arrivals, generation} persists across
-// launches (and CUDA-graph replays): arrivals return to 0 at every barrier.
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned gen;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      unsigned g;
-      do {
-        __nanosleep(32);
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
-      } while (g == gen);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kFusedPermThreads, 1) route_permute_fused_kernel(
-    const int32_t* __restrict__ ids, const uint8_t* __restrict__ active, int64_t n, int k, int E,
-    const uint16_t* __restrict__ u16, int hp, uint16_t* __restrict__ x_perm, int32_t* pos,
-    int32_t* tile_offsets, long long* counters, int devices, int64_t row0, int64_t rows_total,
-    int32_t* block_counts, unsigned* bar) {
-  pdl_enter();
-  __shared__ int cnt[64];
-  __shared__ int base[64];
-  __shared__ int wcnt[32][64];
-  __shared__ int stride_tot[64];
-  __shared__ unsigned long long red[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t P = n * k;
-  const int64_t chunk = (P + gridDim.x - 1) / gridDim.x;
-  const int64_t p0 = (int64_t)blockIdx.x * chunk;
-  const int64_t p1 = p0 + chunk < P ? p0 + chunk : P;
-  if (tid < 64) cnt[tid] = 0;
-  if (tid < 2) red[tid] = 0;
-  __syncthreads();
-  // phase 1: per-(block, expert) counts and the byte-plan counters (cluster.py:75-90)
-  for (int64_t q0 = p0; q0 < p1; q0 += blockDim.x) {
-    const int64_t p = q0 + tid;
-    int e = 0, s = 0;
-    int64_t t = 0;
-    const bool valid = p < p1 && pair_of(p, k, ids, active, 1, e, t, s);
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : -1);
-    if (valid && __popc(peers & ((1u << lane) - 1)) == 0) atomicAdd(&cnt[e], __popc(peers));
-    bool remote = false;
-    if (valid && devices > 1) {
-      const int home = (int)(((row0 + t) * devices) / rows_total);
-      remote = home != e / (E / devices);
-    }
-    const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
-    const unsigned nr = __popc(__ballot_sync(0xffffffffu, remote));
-    if (lane == 0 && nv) atomicAdd(&red[0], (unsigned long long)nv);
-    if (lane == 0 && nr) atomicAdd(&red[1], (unsigned long long)nr);
-  }
-  __syncthreads();
-  if (tid < E) block_counts[(int64_t)blockIdx.x * E + tid] = cnt[tid];
-  if (tid == 0 && counters != nullptr) {
-    if (red[0]) atomicAdd(reinterpret_cast<unsigned long long*>(&counters[0]), red[0]);
-    if (red[1]) atomicAdd(reinterpret_cast<unsigned long long*>(&counters[1]), red[1]);
-  }
-  grid_barrier(bar);
-  // phase 2: expert bases (groups padded to 256-row GEMM tiles), positions.
-  // All blocks' counts are staged in smem with one coalesced pass (wcnt as
-  // scratch: gridDim.x * E <= 32 * 64 ints), then summed per expert.
-  int* all_counts = &wcnt[0][0];
-  for (int i = tid; i < (int)gridDim.x * E; i += blockDim.x) all_counts[i] = __ldcg(block_counts + i);
-  __syncthreads();
-  if (tid < E) {
-    int before = 0, total = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      const int c = all_counts[b * E + tid];
-      if (b < (int)blockIdx.x) before += c;
-      total += c;
-    }
-    cnt[tid] = total;
-    base[tid] = before;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int tiles = 0;
-    for (int ex = 0; ex < E; ++ex) {
-      if (blockIdx.x == 0) tile_offsets[ex] = tiles;
-      base[ex] += tiles * kRowTile;
-      tiles += (cnt[ex] + kRowTile - 1) / kRowTile;
-    }
-    if (blockIdx.x == 0) tile_offsets[E] = tiles;
-  }
-  __syncthreads();
-  for (int64_t q0 = p0; q0 < p1; q0 += blockDim.x) {
-    const int64_t p = q0 + tid;
-    int e = 0, s = 0;
-    int64_t t = 0;
-    const bool in_range = p < p1;
-    const bool valid = in_range && pair_of(p, k, ids, active, 1, e, t, s);
-    // rank in pair order within this stride: warp match ranks + per-warp prefixes
-    for (int i = tid; i < 32 * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
-    __syncthreads();
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : -1);
-    const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
-    if (valid && rank_in_warp == 0) wcnt[warp][e] = __popc(peers);
-    __syncthreads();
-    if (tid < E) {
-      int acc = 0;
-      for (int w = 0; w < 32; ++w) { const int c = wcnt[w][tid]; wcnt[w][tid] = acc; acc += c; }
-      stride_tot[tid] = acc;
-    }
-    __syncthreads();
-    if (in_range) pos[p] = valid ? base[e] + wcnt[warp][e] + rank_in_warp : -1;
-    __syncthreads();
-    if (tid < E) base[tid] += stride_tot[tid];   // running bases for the next stride
-    __syncthreads();
-  }
-  grid_barrier(bar);
-  // phase 3: row gather by every warp of the grid, one pair per warp iteration
-  const int vec = hp / 8;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; q < P; q += warps_total) {
-    const int d = __ldcg(pos + q);
-    if (d < 0) continue;
-    const uint4* src = reinterpret_cast<const uint4*>(u16 + (q / k) * hp);
-    uint4* out = reinterpret_cast<uint4*>(x_perm + (int64_t)d * hp);
-    uint4 v[5];
-#pragma unroll
-    for (int j = 0; j < 5; ++j) if (lane + 32 * j < vec) v[j] = src[lane + 32 * j];
-#pragma unroll
-    for (int j = 0; j < 5; ++j) if (lane + 32 * j < vec) out[lane + 32 * j] = v[j];
-    for (int c = lane + 160; c < vec; c += 32) out[c] = src[c];
-  }
-}
-
 // Row gather x_perm[pos[t, s]] = u16[t]: one warp per (token, slot) pair,
 // 16-byte vector copies, grid over all pairs.
 __global__ void __launch_bounds__(256) permute_gather_kernel(
@@ -1082,61 +872,6 @@ __global__ void __launch_bounds__(256) cache_assemble_kernel(
   }
 }
 
-// ------------------------------------------- combine-slot initialisation
-// For the routed combine fused into the expert GEMM2 epilogue (EPI_COMBINE):
-// per token the cached terms of its inactive pairs (policies.py:197-202) summed
-// in slot order as acc + round(g * row), or 0 when every pair is fresh; the
-// refreshed pairs' gates / ids are persisted here (their rows by the epilogue,
-// policies.py:203-207). No entry is both read and written (write => active).
-template <int KMAX>
-__global__ void __launch_bounds__(256) slot_init_kernel(
-    const uint8_t* __restrict__ active, const uint8_t* __restrict__ write,
-    const float* __restrict__ gates, const int32_t* __restrict__ ids, int64_t n, int k, int hp,
-    const uint16_t* __restrict__ cache_rows, float* cache_gates, int32_t* cache_ids, float* slot) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int vec = hp / 8;
-  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
-       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const uint16_t* src[KMAX];
-    float g[KMAX];
-    int cached = 0;
-    for (int s = 0; s < k && s < KMAX; ++s) {
-      const int64_t ps = t * k + s;
-      const bool act = active == nullptr || active[ps] != 0;
-      src[s] = nullptr;
-      g[s] = 0.f;
-      if (!act && cache_rows != nullptr) {
-        src[s] = cache_rows + ((int64_t)s * n + t) * hp;
-        g[s] = cache_gates[ps];
-        ++cached;
-      }
-      if (lane == 0 && act && write != nullptr && write[ps] != 0) {
-        cache_gates[ps] = gates[ps];
-        cache_ids[ps] = ids[ps];
-      }
-    }
-    for (int c8 = lane; c8 < vec; c8 += 32) {
-      float acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-      if (cached) {
-        for (int s = 0; s < k && s < KMAX; ++s) {
-          if (src[s] == nullptr) continue;
-          const uint4 raw = *reinterpret_cast<const uint4*>(src[s] + c8 * 8);
-          const uint16_t* hv = reinterpret_cast<const uint16_t*>(&raw);
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            acc[q] = __fadd_rn(acc[q], __fmul_rn(g[s], bf16_bits_to_f32(hv[q])));
-        }
-      }
-      float4* o = reinterpret_cast<float4*>(slot + t * hp + c8 * 8);
-      o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-    }
-  }
-}
-
 // ---------------------------------------------------------------- combine
 __global__ void combine_kernel(const float* __restrict__ base, const float* __restrict__ rows,
                                const float* __restrict__ gates, const float* __restrict__ residual,
@@ -1163,6 +898,41 @@ __global__ void combine_kernel(const float* __restrict__ base, const float* __re
       __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
       uint2 w = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
       *reinterpret_cast<uint2*>(out16 + t * hp + c) = w;
+    }
+  }
+}
+
+// Consume without shared experts (S = 0): h = u + ((0 + g_0 row_0) + g_1 row_1 ...)
+// over the layer's bf16 pair rows [k, n, hp] and gates [n, k] (schedules.py:308-317,
+// model.py:279-298), in the shared-GEMM consume epilogue's arithmetic order.
+__global__ void consume_rows_kernel(const float* __restrict__ residual,
+                                    const uint16_t* __restrict__ rows,
+                                    const float* __restrict__ gates, int64_t n, int k, int hp,
+                                    float* out, __nv_bfloat16* out16) {
+  pdl_enter();
+  const int vec = hp / 4;
+  const int64_t total = n * vec;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / vec;
+    const int c = (int)(i - t * vec) * 4;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < k; ++s) {
+      const float g = gates[t * k + s];
+      const uint2 w = *reinterpret_cast<const uint2*>(rows + ((int64_t)s * n + t) * hp + c);
+      const float r0 = bf16_bits_to_f32(w.x & 0xFFFFu), r1 = bf16_bits_to_f32(w.x >> 16);
+      const float r2 = bf16_bits_to_f32(w.y & 0xFFFFu), r3 = bf16_bits_to_f32(w.y >> 16);
+      a = make_float4(__fadd_rn(a.x, __fmul_rn(g, r0)), __fadd_rn(a.y, __fmul_rn(g, r1)),
+                      __fadd_rn(a.z, __fmul_rn(g, r2)), __fadd_rn(a.w, __fmul_rn(g, r3)));
+    }
+    const float4 u = *reinterpret_cast<const float4*>(residual + t * hp + c);
+    a = make_float4(__fadd_rn(u.x, a.x), __fadd_rn(u.y, a.y), __fadd_rn(u.z, a.z),
+                    __fadd_rn(u.w, a.w));
+    *reinterpret_cast<float4*>(out + t * hp + c) = a;
+    if (out16 != nullptr) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+      *reinterpret_cast<uint2*>(out16 + t * hp + c) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
     }
   }
 }
@@ -1302,46 +1072,22 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
   const int threads = 512;
   int64_t want = ((n + 1) / 2 + 15) / 16;
   if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
-  const char* g4 = getenv("DICE_GATE4");        // 0: the row-pair kernel for E = 8
-  if (E == 8 && k <= 8 && (c.chunk_counts != nullptr || !(g4 != nullptr && g4[0] == '0'))) {
+  if (E == 8 && k <= 8) {
     const int64_t gw = ((n + 3) / 4 + 7) / 8;     // 8 warps per block, four rows each
     const int grid = (int)(gw < 1 ? 1 : gw);
-    const int ch = g4 != nullptr && c.chunk_counts == nullptr ? atoi(g4) : 3;
-    if (ch == 5)
-      launch_pdl(gate4_topk_kernel<5>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
-                 gates, scores, status, step, layer, d, c);
-    else if (ch == 2)
-      launch_pdl(gate4_topk_kernel<2>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
-                 gates, scores, status, step, layer, d, c);
-    else
-      launch_pdl(gate4_topk_kernel<3>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
-                 gates, scores, status, step, layer, d, c);
+    launch_pdl(gate4_topk_kernel<3>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
+               gates, scores, status, step, layer, d, c);
     return launch_ok();
   }
-  if ((E == 8 && k <= 8) || (E == 16 && k <= 16)) {
+  if (E == 16 && k <= 16) {
     const int64_t gw = ((n + 1) / 2 + 7) / 8;     // 8 warps per block, a row pair each
     const int grid = (int)(gw < 1 ? 1 : gw);
-    const int ch = hp / 128 <= 9 ? 9 : 4;   // 16-byte loads in flight per lane and row
-    static const int minb = [] {
-      const char* e = getenv("DICE_GATE_MINB");   // experiment hook (1 / 2 / 3)
-      return e != nullptr ? atoi(e) : 2;
-    }();
-#define DICE_GATE_FAST(EE, CC, MB)                                                             \
-    launch_pdl(gate_topk_fast_kernel<EE, CC, MB>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids, gates,  \
-                                                           scores, status, step, layer, d)
-#define DICE_GATE_FAST_MB(EE, CC)                                                              \
-    {                                                                                          \
-      if (minb == 1) DICE_GATE_FAST(EE, CC, 1);                                                \
-      else if (minb == 3) DICE_GATE_FAST(EE, CC, 3);                                           \
-      else DICE_GATE_FAST(EE, CC, 2);                                                          \
-    }
-    if (E == 8) {
-      if (ch == 9) DICE_GATE_FAST_MB(8, 9) else DICE_GATE_FAST_MB(8, 4)
-    } else {
-      if (ch == 9) DICE_GATE_FAST_MB(16, 9) else DICE_GATE_FAST_MB(16, 4)
-    }
-#undef DICE_GATE_FAST_MB
-#undef DICE_GATE_FAST
+    if (hp / 128 <= 9)   // 16-byte loads in flight per lane and row
+      launch_pdl(gate_topk_fast_kernel<16, 9, 2>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp,
+                 k, ids, gates, scores, status, step, layer, d);
+    else
+      launch_pdl(gate_topk_fast_kernel<16, 4, 2>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp,
+                 k, ids, gates, scores, status, step, layer, d);
     return launch_ok();
   }
   const int grid = (int)(want < 2 * 148 ? (want < 1 ? 1 : want) : 2 * 148);
@@ -1441,68 +1187,15 @@ int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, 
   return launch_ok();
 }
 
-int dice_gemm_local_gate(const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
-                         float* out_f32, int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16,
-                         const float* residual, int64_t ld_res, const float* w_gate, int E,
-                         float* parts, void* stream) {
-  if (M < 0 || M > INT_MAX || (E != 8 && E != 16) || residual == nullptr || w_gate == nullptr ||
-      parts == nullptr)
-    return DICE_ERR_CONTRACT;
-  if (M == 0) return DICE_OK;
-  GemmProblem p{};
-  p.A = A; p.A_rows = M; p.B = B; p.M = (int)M; p.N = N; p.K = K;
-  p.num_groups = 1; p.group_tile_offsets = nullptr; p.max_m_tiles = 0;
-  p.epi_kind = E == 8 ? EPI_GELU_RESID_GATE8 : EPI_GELU_RESID_GATE16;
-  p.epi.out_f32 = out_f32; p.epi.ld_f32 = ld_f32;
-  p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out_bf16); p.epi.ld_bf16 = ld_bf16;
-  p.epi.residual = residual; p.epi.ld_res = ld_res;
-  p.epi.gate_w = w_gate;
-  p.epi.gate_part = parts;
-  return gemm_bf16(p, (cudaStream_t)stream);
-}
-
-int dice_gate_parts(int64_t M, int N, int K, int E) {
-  if (E != 8 && E != 16) return -DICE_ERR_CONTRACT;
-  GemmProblem p{};
-  p.M = (int)M; p.N = N; p.K = K; p.num_groups = 1;
-  p.epi_kind = E == 8 ? EPI_GELU_RESID_GATE8 : EPI_GELU_RESID_GATE16;
-  return gemm_gate_parts(p);
-}
-
-int dice_gate_finish(const float* parts, int P, int64_t n, int E, int k, int32_t* ids,
-                     float* gates, float* scores, int32_t* status, int step, int layer,
-                     int decide, int force, int refresh_interval, int strategy, int strict,
-                     uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
-                     uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
-                     uint8_t* write, void* stream) {
-  if ((E != 8 && E != 16) || k < 1 || k > E || P < 1) return DICE_ERR_CONTRACT;
-  if (decide && (refresh_interval < 1 || strategy < 0 || strategy > 3)) return DICE_ERR_CONFIG;
-  if (n == 0) return DICE_OK;
-  const DecideArgs d{decide ? 1 : 0, step, force, refresh_interval, strategy, strict, random_key,
-                     last_refresh, primed, reduced, cached_ids, active, write};
-  // one token per thread, small blocks so every SM gets some
-  const int grid = grid_for(n, 64);
-  if (E == 8)
-    launch_pdl(gate_parts_kernel<8>, dim3(grid), dim3(64), 0, (cudaStream_t)stream, parts, P, n, k, ids, gates, scores,
-                                                                status, step, layer, d);
-  else
-    launch_pdl(gate_parts_kernel<16>, dim3(grid), dim3(64), 0, (cudaStream_t)stream, parts, P, n, k, ids, gates,
-                                                                 scores, status, step, layer, d);
-  return launch_ok();
-}
-
 int64_t dice_permute_max_rows(int64_t n, int k, int E) {
   const int64_t tiles = (n * k + (kRowTile - 1) * (int64_t)E + kRowTile - 1) / kRowTile;
   return (tiles < 1 ? 1 : tiles) * kRowTile;
 }
 
 int64_t dice_permute_scratch_ints(int64_t n, int k, int E) {
-  // three-kernel path: per-1024-pair block counts; single-launch path: per-block
-  // counts of up to kFusedPermMaxBlocks blocks; + 32 ints of grid-barrier state
+  // per-1024-pair block counts of the counting pass
   const int64_t blocks = (n * k + kPermBlock - 1) / kPermBlock;
-  const int64_t a = (blocks < 1 ? 1 : blocks) * E;
-  const int64_t b = (int64_t)kFusedPermMaxBlocks * E;
-  return (a > b ? a : b) + 32;
+  return (blocks < 1 ? 1 : blocks) * E;
 }
 
 int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
@@ -1512,27 +1205,6 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
   if (E < 1 || E > 64 || k < 1 || hp % 64 != 0 || devices < 1 || E % devices != 0)
     return DICE_ERR_CONTRACT;
   if (max_rows < dice_permute_max_rows(n, k, E)) return DICE_ERR_CONTRACT;
-  // DICE_PERMUTE_FUSED=1: the single-launch permute (measured slower inside the
-  // step than the three kernels: its two grid barriers serialise more than the
-  // launches they save); read per call
-  const char* fe = getenv("DICE_PERMUTE_FUSED");
-  const int mode = fe != nullptr ? atoi(fe) : 0;
-  int sms = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int64_t P = n * k;
-  if (mode != 0 && P > 0 && x_perm != nullptr && row_pair == nullptr) {
-    int grid = (int)(sms < kFusedPermMaxBlocks ? sms : kFusedPermMaxBlocks);
-    if (grid * E > 32 * 64) grid = (32 * 64) / E;   // all blocks' counts fit the smem stage
-    unsigned* bar = reinterpret_cast<unsigned*>(scratch + dice_permute_scratch_ints(n, k, E) - 32);
-    launch_pdl(route_permute_fused_kernel, dim3(grid), dim3(kFusedPermThreads), 0, (cudaStream_t)stream, 
-        ids, active, n, k, E, u16, hp, x_perm, pos, tile_offsets,
-        reinterpret_cast<long long*>(counters), devices, row0, rows_total, scratch, bar);
-    return launch_ok();
-  }
   return dice::permute_launch(ids, active, n, k, E, 1, kRowTile, E, u16, hp, x_perm, pos,
                               tile_offsets, counters, devices, row0, rows_total, scratch,
                               (cudaStream_t)stream, row_pair);
@@ -1559,37 +1231,6 @@ int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const
   return gemm_bf16_dual(p, q, (cudaStream_t)stream);
 }
 
-int dice_slot_init(const uint8_t* active, const uint8_t* write, const float* gates,
-                   const int32_t* ids, int64_t n, int k, int hp, const uint16_t* cache_rows,
-                   float* cache_gates, int32_t* cache_ids, float* slot, void* stream) {
-  if (hp % 64 != 0 || k < 1 || k > 2) return DICE_ERR_CONTRACT;
-  if (n == 0) return DICE_OK;
-  launch_pdl(slot_init_kernel<2>, dim3(grid_for(n * 32, 256)), dim3(256), 0, (cudaStream_t)stream,
-             active, write, gates, ids, n, k, hp, cache_rows, cache_gates, cache_ids, slot);
-  return launch_ok();
-}
-
-int dice_expert_gemm2_combine(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
-                              int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
-                              const float* gates, const uint8_t* write, int k, int64_t n,
-                              float* slot, uint16_t* cache_rows, void* stream) {
-  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0 ||
-      k < 1 || k > 2 || row_pair == nullptr || gates == nullptr || slot == nullptr)
-    return DICE_ERR_CONTRACT;
-  GemmProblem q{};
-  q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
-  q.num_groups = E; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / kRowTile);
-  q.epi_kind = EPI_COMBINE;
-  q.epi.row_pair = row_pair;
-  q.epi.pair_gates = gates;
-  q.epi.pair_write = write;
-  q.epi.top_k = k;
-  q.epi.n_tokens = n;
-  q.epi.slot = slot;
-  q.epi.cache_rows = reinterpret_cast<__nv_bfloat16*>(cache_rows);
-  return gemm_bf16(q, (cudaStream_t)stream);
-}
-
 int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
                       int ep, const int32_t* tile_offsets, uint16_t* y, void* stream) {
   if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0)
@@ -1600,6 +1241,62 @@ int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2
   q.epi_kind = EPI_STORE_BF16;
   q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(y); q.epi.ld_bf16 = hp;
   return gemm_bf16(q, (cudaStream_t)stream);
+}
+
+int dice_expert_gemm2_pairs(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
+                            int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
+                            const float* gates, const int32_t* ids, int k, int64_t n,
+                            uint16_t* pair_rows, float* cache_gates, int32_t* cache_ids,
+                            void* stream) {
+  if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0 ||
+      k < 1 || n < 0 || row_pair == nullptr || pair_rows == nullptr ||
+      (cache_gates != nullptr && gates == nullptr) || (cache_ids != nullptr && ids == nullptr))
+    return DICE_ERR_CONTRACT;
+  GemmProblem q{};
+  q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
+  q.num_groups = E; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / kRowTile);
+  q.epi_kind = EPI_STORE_PAIR;
+  q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(pair_rows); q.epi.ld_bf16 = hp;
+  q.epi.row_pair = row_pair;
+  q.epi.pair_gates = gates;
+  q.epi.pair_ids = ids;
+  q.epi.cache_gates = cache_gates;
+  q.epi.cache_ids = cache_ids;
+  q.epi.top_k = k;
+  q.epi.n_tokens = n;
+  return gemm_bf16(q, (cudaStream_t)stream);
+}
+
+int dice_gemm_consume(const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
+                      const float* residual, int64_t ld_res, const uint16_t* pair_rows,
+                      const float* pair_gates, int k, float* out_f32, int64_t ld_f32,
+                      uint16_t* out_bf16, int64_t ld_bf16, void* stream) {
+  if (M < 0 || M > INT_MAX || residual == nullptr || k < 0 ||
+      (k > 0 && (pair_rows == nullptr || pair_gates == nullptr)))
+    return DICE_ERR_CONTRACT;
+  if (M == 0) return DICE_OK;
+  GemmProblem p{};
+  p.A = A; p.A_rows = M; p.B = B; p.M = (int)M; p.N = N; p.K = K;
+  p.num_groups = 1; p.group_tile_offsets = nullptr; p.max_m_tiles = 0;
+  p.epi_kind = EPI_CONSUME;
+  p.epi.out_f32 = out_f32; p.epi.ld_f32 = ld_f32;
+  p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out_bf16); p.epi.ld_bf16 = ld_bf16;
+  p.epi.residual = residual; p.epi.ld_res = ld_res;
+  p.epi.pair_rows = reinterpret_cast<const __nv_bfloat16*>(pair_rows);
+  p.epi.pair_gates = pair_gates;
+  p.epi.top_k = k;
+  p.epi.n_tokens = M;
+  return gemm_bf16(p, (cudaStream_t)stream);
+}
+
+int dice_consume_rows(const float* residual, const uint16_t* pair_rows, const float* pair_gates,
+                      int64_t n, int k, int hp, float* out, uint16_t* out_bf16, void* stream) {
+  if (hp % 4 != 0 || k < 0 || residual == nullptr || out == nullptr) return DICE_ERR_CONTRACT;
+  if (n == 0) return DICE_OK;
+  launch_pdl(consume_rows_kernel, dim3(grid_for(n * (hp / 4), 256)), dim3(256), 0,
+             (cudaStream_t)stream, residual, pair_rows, pair_gates, n, k, hp, out,
+             reinterpret_cast<__nv_bfloat16*>(out_bf16));
+  return launch_ok();
 }
 
 int dice_grouped_ffn(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
@@ -1646,7 +1343,7 @@ int dice_cache_assemble(const uint16_t* y, const int32_t* pos, const uint8_t* ac
 
 int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, int K, float* out_f32,
               int64_t ld_f32, uint16_t* out_bf16, int64_t ld_bf16, const float* residual,
-              int64_t ld_res, const float* addend, int64_t ld_add, void* stream) {
+              int64_t ld_res, void* stream) {
   if (M < 0 || M > INT_MAX) return DICE_ERR_CONTRACT;
   if (M == 0) return DICE_OK;
   GemmProblem p{};
@@ -1656,10 +1353,8 @@ int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, i
   p.epi.out_f32 = out_f32; p.epi.ld_f32 = ld_f32;
   p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out_bf16); p.epi.ld_bf16 = ld_bf16;
   p.epi.residual = residual; p.epi.ld_res = ld_res;
-  p.epi.addend = addend; p.epi.ld_add = ld_add;
-  if (epi < EPI_STORE_BF16 || epi > EPI_CONSUME) return DICE_ERR_CONTRACT;   // public kinds only
-  if ((epi == EPI_GELU_RESID || epi == EPI_CONSUME) && residual == nullptr) return DICE_ERR_CONTRACT;
-  if (epi == EPI_CONSUME && addend == nullptr) return DICE_ERR_CONTRACT;
+  if (epi < EPI_STORE_BF16 || epi > EPI_GELU_RESID) return DICE_ERR_CONTRACT;   // public kinds only
+  if (epi == EPI_GELU_RESID && residual == nullptr) return DICE_ERR_CONTRACT;
   return gemm_bf16(p, (cudaStream_t)stream);
 }
 

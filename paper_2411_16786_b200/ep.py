@@ -8,18 +8,22 @@ Exchange: every rank cudaMallocs one window allocation, exports it with CUDA
 IPC and maps every peer's (handles travel through torch.distributed object
 collectives; that is the only use of the process group on the data path's
 setup). The dispatch kernel stores each active pair's bf16 row straight into
-the expert rank's window; the expert rank's combine kernel stores each
-output row straight into the home rank's combine window. Completion uses
-constant-valued flags (ready / free per layer and peer) driven by batched
-stream memory operations, so the schedule keeps host-deterministic control
-flow and a whole run captures into one CUDA graph per rank.
+the expert rank's window; the expert rank's GEMM2 epilogue stores each
+output row, with its gate and expert id, straight into the home rank's pair
+rows — which live in the home's window and ARE its token cache rows / combine
+slot (see DeviceRunner), so the combine needs no kernel at the home.
+Completion uses constant-valued flags (ready / free per layer and peer)
+driven by batched stream memory operations, so the schedule keeps
+host-deterministic control flow and a whole run captures into one CUDA graph
+per rank.
 
 Schedule (schedules.py:372-402, PAPER §4.1): dispatch(l) is sent in stage l and
-expert-processed in stage l+1 (or at a flush); its combine is assembled at the
-start of stage l of the next step, right before decide(l) so the TokenCache
-sees the reference's decide/assemble order (policies.py:159-208), and consumed
-with one-step staleness. Selective-sync / warmup / periodic stages run the
-blocking dispatch -> experts -> combine -> assemble sequence.
+expert-processed in stage l+1 (or at a flush); its combine arrival is awaited
+at the start of stage l of the next step, right before decide(l) so the
+TokenCache sees the reference's decide/assemble order (policies.py:159-208),
+and consumed with one-step staleness; once the consume has read the layer's
+pair rows, the home frees them for the next combine. Selective-sync / warmup
+/ periodic stages run the blocking dispatch -> experts -> combine sequence.
 """
 from __future__ import annotations
 
@@ -53,21 +57,24 @@ _TYPESTR = {torch.float32: "<f4", torch.bfloat16: "<V2", torch.int32: "<i4", tor
 
 
 class Window:
-    """One cudaMalloc'd allocation: receive windows, combine window and flags."""
+    """One cudaMalloc'd allocation: receive windows, the rank's pair rows /
+    gates / ids (written by the expert ranks) and flags. Every rank uses the
+    same layout (sized by the largest shard, nmax rows), so peers compute
+    addresses from the base pointer alone."""
 
-    def __init__(self, L, D, cap, ncap, hp, device):
-        self._layout(L, D, cap, ncap, hp)
+    def __init__(self, L, D, cap, k, nmax, hp, device):
+        self._layout(L, D, cap, k, nmax, hp)
         h = ctypes.c_void_p()
         torch.cuda.set_device(device)
         _lib.call("dice_device_alloc", self.nbytes, ctypes.byref(h))
         self.ptr = int(h.value)
-        # free flags start at 1 (regions free), ready flags at 0
-        for o in (self.o_rx_free, self.o_cx_free):
-            self.view(o, (L * D,), torch.int32).fill_(1)
+        # receive regions start free (rx_free = 1); pair rows are freed by their
+        # home right before each expert call of the layer (cx_free starts at 0)
+        self.view(self.o_rx_free, (L * D,), torch.int32).fill_(1)
         torch.cuda.synchronize()
 
-    def _layout(self, L, D, cap, ncap, hp):
-        self.L, self.D, self.cap, self.ncap, self.hp = L, D, cap, ncap, hp
+    def _layout(self, L, D, cap, k, nmax, hp):
+        self.L, self.D, self.cap, self.k, self.nmax, self.hp = L, D, cap, k, nmax, hp
         off = 0
 
         def take(nbytes):
@@ -77,14 +84,29 @@ class Window:
             return start
 
         self.o_rx_rows = take(L * D * cap * hp * 2)
-        self.o_rx_meta = take(L * D * cap * 8)
+        self.o_rx_meta = take(L * D * cap * 16)
         self.o_rx_count = take(L * D * 4)
-        self.o_cx_rows = take(L * ncap * hp * 2)
+        self.row_block = k * nmax * hp * 2        # bytes of one layer's pair rows
+        self.o_cx_rows = take(L * self.row_block)
+        self.o_cx_gates = take(L * nmax * k * 4)
+        self.o_cx_ids = take(L * nmax * k * 4)
         self.o_rx_ready = take(L * D * 4)
         self.o_cx_ready = take(L * D * 4)
         self.o_rx_free = take(L * D * 4)
         self.o_cx_free = take(L * D * 4)
         self.nbytes = off
+
+    def pair_views(self, n):
+        """This rank's pair rows bf16 [L, k, n, hp], gates f32 [L, n, k], ids
+        int32 [L, n, k] (layer blocks sized for nmax rows)."""
+        L, k, hp, nmax = self.L, self.k, self.hp, self.nmax
+        flat = self.view(self.o_cx_rows, (L * k * nmax * hp,), torch.bfloat16)
+        rows = torch.as_strided(flat, (L, k, n, hp), (k * nmax * hp, n * hp, hp, 1))
+        g = self.view(self.o_cx_gates, (L * nmax * k,), torch.float32)
+        gates = torch.as_strided(g, (L, n, k), (nmax * k, k, 1))
+        i = self.view(self.o_cx_ids, (L * nmax * k,), torch.int32)
+        ids = torch.as_strided(i, (L, n, k), (nmax * k, k, 1))
+        return rows, gates, ids
 
     def view(self, offset, shape, dtype):
         if dtype is torch.bfloat16:
@@ -148,7 +170,15 @@ class EPGroup:
 
     def cx_rows(self, owner, layer):
         w = self.win
-        return self.base[owner] + w.o_cx_rows + layer * w.ncap * w.hp * 2
+        return self.base[owner] + w.o_cx_rows + layer * w.row_block
+
+    def cx_gates(self, owner, layer):
+        w = self.win
+        return self.base[owner] + w.o_cx_gates + layer * w.nmax * w.k * 4
+
+    def cx_ids(self, owner, layer):
+        w = self.win
+        return self.base[owner] + w.o_cx_ids + layer * w.nmax * w.k * 4
 
     def flag(self, kind, owner, layer, peer):
         w = self.win
@@ -171,10 +201,11 @@ class EPGroup:
         arr = _u64_array(addrs)
         _lib.call("dice_stream_write", arr, len(addrs), value, ops._stream())
 
-    def data(self, kind, regions):
-        """Record a data access of a kernel (test tracing only)."""
+    def data(self, kind, regions, gen=None):
+        """Record a data access of a kernel (test tracing only); gen: the step
+        whose combine a pair-row store writes / a consume expects."""
         if self.trace is not None:
-            self.trace.append((kind, regions))
+            self.trace.append((kind, regions, gen))
 
 
 class _EPPayload:
@@ -201,12 +232,11 @@ class EPRunner:
     schedules.py:142-490: SYNCHRONOUS, DISPLACED and INTERWEAVED).
 
     DISPLACED (schedules.py:347-370) keeps each layer's dispatch in the peers'
-    receive windows for a whole step: stage (s, l) first expert-processes the
-    dispatch of step s-1 (its combine is assembled at the start of stage
-    (s+1, l), still after decide(s) as in the reference), then sends the new one
-    into the windows that processing just freed, so one window per layer
-    suffices; the slot consumed at (s, l) holds step s-2's combine (staleness
-    2). A dispatch a sync stage supersedes is drained unprocessed (the reference
+    receive windows for a whole step: stage (s, l) consumes the layer's pair
+    rows (step s-2's combine, staleness 2), then expert-processes the dispatch
+    of step s-1 (its combine arrival is awaited at the start of stage (s+1, l),
+    still after decide(s) as in the reference), then sends the new one into the
+    windows that processing just freed, so one window per layer suffices. A dispatch a sync stage supersedes is drained unprocessed (the reference
     drops it, its bytes stay counted), and a sync stage's own dispatch, which
     the reference re-processes at the next stage, is already in the slot
     (every pair of a forced refresh is active, so re-assembling it changes
@@ -240,11 +270,12 @@ class EPRunner:
         self.dev = dev
         k, E, S, hp, ep = cfg.top_k, cfg.num_experts, cfg.num_shared, model.hp, model.ep
         self.n, self.k, self.E, self.S, self.hp, self.ep = n, k, E, S, hp, ep
-        n_max = max(shard_rows(cfg.total_rows, world, r)[1] - shard_rows(cfg.total_rows, world, r)[0]
-                    for r in range(world))
+        self.shard_n = [shard_rows(cfg.total_rows, world, r)[1] - shard_rows(cfg.total_rows, world, r)[0]
+                        for r in range(world)]
+        n_max = max(self.shard_n)
         self.cap = n_max * k
         L = cfg.num_layers
-        self.win = Window(L, world, self.cap, self.cap, hp,
+        self.win = Window(L, world, self.cap, k, n_max, hp,
                           torch.cuda.current_device() if str(dev).startswith("cuda") else None)
         self.grp = EPGroup(self.win, rank, world, pg)
         f32, bf = torch.float32, torch.bfloat16
@@ -255,37 +286,31 @@ class EPRunner:
         self.u32 = torch.zeros(n, hp, dtype=f32, device=dev)
         self.u16 = torch.zeros(n, hp, dtype=bf, device=dev)
         # the shared-expert GEMM1 rides in the expert GEMM1 launch (see DeviceRunner)
-        self.merge_gemm1 = cfg.num_shared > 0 and os.environ.get("DICE_MERGE_GEMM1", "1") != "0"
-        # router fused into the local_block GEMM epilogue (see DeviceRunner)
-        E_all = cfg.num_experts
-        self.fused_gate = E_all in (8, 16) and os.environ.get("DICE_FUSED_GATE", "0") == "1"
-        if self.fused_gate:
-            self.gparts = torch.empty(ops.gate_parts(n, hp, hp, E_all), n, E_all, dtype=f32,
-                                      device=dev)
+        self.merge_gemm1 = cfg.num_shared > 0
         total = world * self.cap
         self.max_rows = ops.permute_max_rows(total, 1, El)
         self.hbuf = torch.empty(self.max_rows, ep, dtype=bf, device=dev)
-        self.y = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
         self.x_perm = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
         # permuted row -> window entry: the expert GEMM2 epilogue stores each finished
-        # row straight into its home rank's combine window (fused combine all-to-all)
+        # row straight into its home rank's pair rows (fused combine all-to-all)
         self.row_pair_rx = torch.full((self.max_rows,), -1, dtype=torch.int32, device=dev)
         self.ids_rx = torch.empty(total, dtype=torch.int32, device=dev)
         self.pos_rx = torch.empty(total, dtype=torch.int32, device=dev)
         self.tiles = torch.empty(El + 1, dtype=torch.int32, device=dev)
         self.pos_dest = torch.empty(n, k, dtype=torch.int32, device=dev)
         self.dest_off = torch.empty(world + 1, dtype=torch.int32, device=dev)
-        self.pair_pos = torch.empty(n, k, dtype=torch.int32, device=dev)
-        _lib.call("dice_iota", self.pair_pos.data_ptr(), n * k, ops._stream())
         sc = max(ops.permute_scratch_ints(n, k, world), ops.permute_scratch_ints(total, 1, El))
         self.scratch = torch.zeros(sc, dtype=torch.int32, device=dev)
         self.hsh = torch.empty(n, max(S, 1) * ep, dtype=bf, device=dev)
-        nslots = 1 if strategy is Strategy.SYNCHRONOUS else L
-        self.slots = torch.zeros(nslots, n, hp, dtype=f32, device=dev)
         # displaced: the dispatch in the windows and the new one coexist per layer
         per_layer = 2 if strategy is Strategy.DISPLACED else 1
         self.payloads = [[_EPPayload(n, k, dev) for _ in range(per_layer)] for _ in range(L)]
-        self.cache = TokenCache(L, n, k, cfg.hidden_dim, device=dev) \
+        # this rank's pair rows / gates / ids live in its window (the expert ranks
+        # write them); with conditional communication they are the token cache's
+        rows, gates, ids = self.win.pair_views(n)
+        self.pair_rows, self.pair_gates, self.pair_ids = rows, gates, ids
+        self.cache = TokenCache(L, n, k, cfg.hidden_dim, device=dev, rows=rows, gates=gates,
+                                expert_ids=ids) \
             if policy.cond_strategy is not CondStrategy.OFF else None
         self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
         self.status = torch.empty(4, dtype=torch.int32, device=dev)
@@ -299,7 +324,7 @@ class EPRunner:
 
     # --------------------------------------------------------------- helpers
     def _slot(self, layer):
-        return self.slots[0] if self.strategy is Strategy.SYNCHRONOUS else self.slots[layer]
+        return self.pair_rows[layer], self.pair_gates[layer]
 
     def _peers(self):
         return range(self.world)
@@ -377,7 +402,8 @@ class EPRunner:
         rx_rows = _u64_array([g.rx_rows(d, layer, me) for d in self._peers()])
         rx_meta = _u64_array([g.rx_meta(d, layer, me) for d in self._peers()])
         rx_cnt = _u64_array([g.rx_count(d, layer, me) for d in self._peers()])
-        _lib.call("dice_ep_dispatch", p.ids.data_ptr(), None if act is None else act.data_ptr(),
+        _lib.call("dice_ep_dispatch", p.ids.data_ptr(), p.gates.data_ptr(),
+                  None if act is None else act.data_ptr(),
                   self.n, self.k, self.E, D, me, self.u16.data_ptr(), self.hp,
                   self.pos_dest.data_ptr(), self.dest_off.data_ptr(),
                   self.counters[step, layer].data_ptr(), self.r0, self.cfg.total_rows,
@@ -389,16 +415,25 @@ class EPRunner:
 
     def _expert(self, p: _EPPayload, shared_layer=None):
         """Expert side of dispatch(p.layer): wait for every source, grouped FFN,
-        combine rows straight back to their home ranks. shared_layer: that
-        layer's shared-expert GEMM1 (u16 -> hsh) rides in the expert GEMM1 launch."""
+        rows (with gates and expert ids) stored straight into their home ranks'
+        pair rows by the GEMM2 epilogue. shared_layer: that layer's
+        shared-expert GEMM1 (u16 -> hsh) rides in the expert GEMM1 launch."""
         g, me, layer = self.grp, self.rank, p.layer
+        # as a home: every read of this layer's pair rows precedes this point in
+        # the schedule (the rows are next written by this expert call), so free
+        # them for every expert rank
+        g.write([g.flag("cx_free", r, layer, me) for r in self._peers()], 1)
         self._timed_wait([g.flag("rx_ready", me, layer, s) for s in self._peers()], 1)
         g.write([g.flag("rx_ready", me, layer, s) for s in self._peers()], 0)
+        # as an expert rank: every home has freed its rows of this layer
         self._timed_wait([g.flag("cx_free", me, layer, h) for h in self._peers()], 1)
         g.write([g.flag("cx_free", me, layer, h) for h in self._peers()], 0)
         lw = self.model.layers[layer]
-        win = self.win
-        cx = _u64_array([g.cx_rows(h, layer) for h in self._peers()])
+        homes = self._peers()
+        rows = _u64_array([g.cx_rows(h, layer) for h in homes])
+        gates = _u64_array([g.cx_gates(h, layer) for h in homes])
+        ids = _u64_array([g.cx_ids(h, layer) for h in homes])
+        hn = (ctypes.c_int64 * len(self.shard_n))(*self.shard_n)
         if self.time_experts:
             i = len(self._expert_events)
             if i >= len(self._expert_pool):
@@ -407,19 +442,20 @@ class EPRunner:
             e0.record()
         _lib.call("dice_ep_expert", g.rx_rows(me, layer, 0), g.rx_meta(me, layer, 0),
                   g.rx_count(me, layer, 0), self.world, self.cap, self.El, self.hp, self.ep,
-                  lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.ids_rx.data_ptr(),
+                  self.k, lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.ids_rx.data_ptr(),
                   self.pos_rx.data_ptr(), self.tiles.data_ptr(), self.scratch.data_ptr(),
-                  self.x_perm.data_ptr(), self.max_rows, self.hbuf.data_ptr(), self.y.data_ptr(),
-                  cx, *self._shared_args(shared_layer), self.row_pair_rx.data_ptr(), ops._stream())
+                  self.x_perm.data_ptr(), self.max_rows, self.hbuf.data_ptr(),
+                  self.row_pair_rx.data_ptr(), rows, gates, ids, hn,
+                  *self._shared_args(shared_layer), ops._stream())
         if self.time_experts:
             e1.record()
             self._expert_events.append((e0, e1, p.gen, layer, shared_layer is not None))
         g.data("read", [("rx", me, layer, s) for s in self._peers()])
-        g.data("write", [("cx", h, layer, me) for h in self._peers()])
+        g.data("write", [("cx", h, layer, me) for h in self._peers()], gen=p.gen)
         g.write([g.flag("rx_free", s, layer, me) for s in self._peers()], 1)
         g.write([g.flag("cx_ready", h, layer, me) for h in self._peers()], 1)
         self.deferred[layer] = p
-        self.slot_gen[layer] = p.gen          # the combine is in flight (_store_combine)
+        self.slot_gen[layer] = p.gen          # the combine is in flight
         self.combine_log.append((p.gen, layer))
 
     def _discard(self, p: _EPPayload):
@@ -439,23 +475,16 @@ class EPRunner:
         return (self.u16.data_ptr(), self.n, ws1.data_ptr(), ws1.shape[0], self.hsh.data_ptr())
 
     def _assemble(self, layer):
-        """Combine arrival at the home rank: stale-cache merge into slot[layer]."""
+        """Combine arrival at the home rank: every expert rank has stored its
+        rows into this layer's pair rows (TokenCache.assemble needs no kernel:
+        the rows are the cache, inactive pairs keep their cached entries)."""
         p = self.deferred[layer]
         if p is None:
             return
         g, me = self.grp, self.rank
         self._timed_wait([g.flag("cx_ready", me, layer, r) for r in self._peers()], 1)
         g.write([g.flag("cx_ready", me, layer, r) for r in self._peers()], 0)
-        cxv = self.win.view(self.win.o_cx_rows + layer * self.cap * self.hp * 2,
-                            (self.cap, self.hp), torch.bfloat16)
-        c = self.cache
-        ops.cache_assemble(cxv, self.pair_pos, None if c is None else p.active,
-                           None if c is None else p.write, p.gates, p.ids, self._slot(layer),
-                           None if c is None else c.rows[layer],
-                           None if c is None else c.gates[layer],
-                           None if c is None else c.expert_ids[layer])
-        g.data("read", [("cx", me, layer, r) for r in self._peers()])
-        g.write([g.flag("cx_free", r, layer, me) for r in self._peers()], 1)
+        g.data("arrive", [("cx", me, layer, r) for r in self._peers()])
         self.deferred[layer] = None
 
     def _flush_pending(self):
@@ -465,16 +494,17 @@ class EPRunner:
             self._track(prev.layer)
 
     def _consume(self, layer, step, gen, gemm1_done=False):
+        """u + (shared + sum_s g_s row_s) over the layer's pair rows (step `gen`'s
+        combine; the rows are freed at the layer's next expert call)."""
         lw = self.model.layers[layer]
-        slot = self._slot(layer)
+        rows, gates = self._slot(layer)
         if self.S > 0:
             if not gemm1_done:
                 ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
-            ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
-                     residual=self.u32, addend=slot)
+            ops.gemm_consume(self.hsh, lw.ws2_t, self.u32, rows, gates, self.h32, self.h16)
         else:
-            ops.combine(slot, slot, slot.new_empty(self.n, 0), self.h32, residual=self.u32,
-                        out_bf16=self.h16)
+            ops.consume_rows(self.u32, rows, gates, self.h32, self.h16)
+        self.grp.data("consume", [("cx", self.rank, layer, r) for r in self._peers()], gen=gen)
         self.records.append(StalenessRecord(layer=layer, used_step=step, generated_step=gen))
 
     def _run_step(self, step):
@@ -482,12 +512,8 @@ class EPRunner:
         for layer in range(cfg.num_layers):
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
-            if self.fused_gate:
-                ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
-                                    self.gparts)
-            else:
-                ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
-                         out_bf16=self.u16, residual=hin32)
+            ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
+                     out_bf16=self.u16, residual=hin32)
             sync = self._stage_is_sync(step, layer)
             if sync:
                 self._flush_pending()
@@ -498,12 +524,8 @@ class EPRunner:
             if self.cache is not None:
                 dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write,
                                              row0=self.r0)
-            if self.fused_gate:
-                ops.gate_finish(self.gparts, p.ids, p.gates, None, self.status, step, layer,
-                                decide=dec)
-            else:
-                ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, None, self.status,
-                              step, layer, decide=dec)
+            ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, None, self.status,
+                          step, layer, decide=dec)
             decided = dec is not None
             if sync:
                 old = self.disp[layer]
@@ -522,19 +544,19 @@ class EPRunner:
             elif self.strategy is Strategy.DISPLACED:
                 gen = self.slot_gen[layer]
                 old, processed = self.disp[layer]
-                merged = False
+                # consume the pair rows (step s-2's combine) before the old
+                # dispatch's combine overwrites them
+                self._consume(layer, step, gen)
                 if processed:
                     # the reference re-processes the sync stage's dispatch; its
                     # rows are already in the slot, its combine bytes count again
                     self.combine_log.append((old.gen, layer))
                 else:
-                    merged = self.merge_gemm1
-                    self._expert(old, shared_layer=layer if merged else None)
+                    self._expert(old)
                 self._track(layer)
                 self._send(step, layer, p, force=False, decided=decided)
                 self.disp[layer] = (p, False)
                 self._track(layer, "d")
-                self._consume(layer, step, gen, gemm1_done=merged)
             else:
                 gen = self.slot_gen[layer]
                 self._send(step, layer, p, force=False, decided=decided)

@@ -122,7 +122,6 @@ class LayerWeights:
     w2_t: torch.Tensor
     ws1_t: torch.Tensor | None
     ws2_t: torch.Tensor | None
-    w_gate_c: torch.Tensor | None = None   # f32 [hp, E] = W_gate (gate fused into local_block)
 
 
 @dataclass
@@ -183,8 +182,7 @@ def init_model(config: ModelConfig, seed: int, device="cuda", experts=None) -> T
                 ops.splitmix_fill(ws1_t[i * ep:(i + 1) * ep], seed, pos, h, e, a_h, transpose=True)
                 _fill_columns(ws2_t, i * ep, seed, pos + h * e, e, h, a_e)
                 pos += 2 * h * e
-        layers.append(LayerWeights(w_mix_t, w_gate_t, w1_t, w2_t, ws1_t, ws2_t,
-                                   w_gate_t.t().contiguous()))
+        layers.append(LayerWeights(w_mix_t, w_gate_t, w1_t, w2_t, ws1_t, ws2_t))
     return ToyModel(config=config, seed=seed, layers=layers, experts=(first, last), hp=hp, ep=ep,
                     device=str(device))
 

@@ -11,7 +11,7 @@ import torch
 from . import _lib
 from .errors import ContractError
 
-EPI_STORE_BF16, EPI_GELU_BF16, EPI_STORE_F32, EPI_GELU_RESID, EPI_CONSUME = range(5)
+EPI_STORE_BF16, EPI_GELU_BF16, EPI_STORE_F32, EPI_GELU_RESID = range(4)
 COND_CODES = {"off": 0, "low_score": 1, "high_score": 2, "random": 3}
 
 
@@ -125,49 +125,6 @@ def gate_topk(u32, w_gate_t, k, ids, gates, scores=None, status=None, step=0, la
               _ptr(cached), _ptr(active), _ptr(write), _stream())
 
 
-def gate_parts(M, N, K, E):
-    """Partial-logit slots the gate-fused local GEMM writes (dice_gate_parts)."""
-    P = int(_lib.load().dice_gate_parts(M, N, K, E))
-    if P < 1:
-        raise ContractError(f"gate-fused GEMM: unsupported E={E}")
-    return P
-
-
-def gemm_local_gate(A, B, w_gate_c, out_f32, out_bf16, residual, parts):
-    """local_block GEMM (u = gelu(A @ B^T) + residual) with the router's partial
-    logits of the finished u rows fused into the epilogue: parts [P, M, E]."""
-    _need(A, torch.bfloat16, "gemm A")
-    _need(B, torch.bfloat16, "gemm B")
-    _need(w_gate_c, torch.float32, "w_gate")
-    _need(parts, torch.float32, "gate parts")
-    M, K = A.shape
-    N = B.shape[0]
-    E = w_gate_c.shape[1]
-    if B.shape[1] != K or w_gate_c.shape[0] != N or parts.shape[1:] != (M, E):
-        raise ContractError(f"gemm_local_gate: A {tuple(A.shape)} B {tuple(B.shape)} "
-                            f"w_gate {tuple(w_gate_c.shape)} parts {tuple(parts.shape)}")
-    _lib.call("dice_gemm_local_gate", _ptr(A), M, _ptr(B), N, K, _ptr(out_f32), out_f32.shape[-1],
-              _ptr(out_bf16), out_bf16.shape[-1], _ptr(residual), residual.shape[-1],
-              _ptr(w_gate_c), E, _ptr(parts), _stream())
-
-
-def gate_finish(parts, ids, gates, scores=None, status=None, step=0, layer=0, decide=None):
-    """Router finish over the fused partial logits (softmax, stable top-k,
-    renormalised gates); ``decide`` = TokenCache.decide_args(...) also runs the
-    conditional-communication decision in the same kernel."""
-    P, n, E = parts.shape
-    k = ids.shape[1]
-    if decide is None:
-        d = (0, 0, 1, 0, 0, 0, None, None, None, None, None, None)
-    else:
-        d = (1,) + tuple(decide)
-    (on, force, R, strat, strict, key, last, primed, reduced, cached, active, write) = d
-    _lib.call("dice_gate_finish", _ptr(parts), P, n, E, k, _ptr(ids), _ptr(gates), _ptr(scores),
-              _ptr(status), step, layer, on, int(force), R, strat, int(strict),
-              key & 0xFFFFFFFFFFFFFFFF, _ptr(last), _ptr(primed), _ptr(reduced), _ptr(cached),
-              _ptr(active), _ptr(write), _stream())
-
-
 def cond_decide(ids, step, force, refresh_interval, strategy, strict, random_key, last, primed,
                 reduced, cached_ids, active, write):
     n, k = ids.shape
@@ -187,7 +144,7 @@ def permute_scratch_ints(n, k, E):
 def route_permute(ids, active, u16, x_perm, pos, tile_offsets, counters, scratch, E,
                   devices=1, row0=0, rows_total=None, row_pair=None, chunk_counts=None):
     """row_pair (int32 [max_rows], optional): permuted row -> pair index t*k+s
-    (-1 on padding rows), for the fused expert GEMM2 combine. chunk_counts: the
+    (-1 on padding rows), for the expert GEMM2's pair-row stores. chunk_counts: the
     per-32-token expert counts the gate launch produced (gate_topk(count=...));
     the counting pass and its counters are then already done."""
     n, k = ids.shape
@@ -227,23 +184,44 @@ def expert_gemm2(hbuf, w2_t, E, tile_offsets, y):
               _ptr(y), _stream())
 
 
-def slot_init(active, write, gates, ids, slot, cache_rows=None, cache_gates=None, cache_ids=None):
-    n, k = gates.shape
-    hp = slot.shape[1]
-    _lib.call("dice_slot_init", _ptr(active), _ptr(write), _ptr(gates), _ptr(ids), n, k, hp,
-              _ptr(cache_rows), _ptr(cache_gates), _ptr(cache_ids), _ptr(slot), _stream())
-
-
-def expert_gemm2_combine(hbuf, w2_t, E, tile_offsets, row_pair, gates, write, slot,
-                         cache_rows=None):
-    """Expert GEMM2 whose epilogue adds round(g * row) of every pair into its
-    token's combine slot and persists refreshed rows to the token cache."""
+def expert_gemm2_pairs(hbuf, w2_t, E, tile_offsets, row_pair, gates, ids, pair_rows,
+                       cache_gates=None, cache_ids=None):
+    """Expert GEMM2 whose epilogue stores each row of pair p = t*k + s into
+    pair_rows[s, t] (bf16 [k, n, hp]) and persists the pair's gate / expert id
+    (dice_expert_gemm2_pairs)."""
     max_rows, ep = hbuf.shape
     n, k = gates.shape
-    hp = slot.shape[1]
-    _lib.call("dice_expert_gemm2_combine", _ptr(hbuf), max_rows, _ptr(w2_t), E, hp, ep,
-              _ptr(tile_offsets), _ptr(row_pair), _ptr(gates), _ptr(write), k, n, _ptr(slot),
-              _ptr(cache_rows), _stream())
+    hp = pair_rows.shape[-1]
+    _need(pair_rows, torch.bfloat16, "pair rows")
+    if tuple(pair_rows.shape) != (k, n, hp):
+        raise ContractError(f"pair rows {tuple(pair_rows.shape)} != {(k, n, hp)}")
+    _lib.call("dice_expert_gemm2_pairs", _ptr(hbuf), max_rows, _ptr(w2_t), E, hp, ep,
+              _ptr(tile_offsets), _ptr(row_pair), _ptr(gates), _ptr(ids), k, n, _ptr(pair_rows),
+              _ptr(cache_gates), _ptr(cache_ids), _stream())
+
+
+def gemm_consume(A, B, residual, pair_rows, pair_gates, out_f32, out_bf16=None):
+    """out = residual + ((A @ B^T + g_0 row_0) + g_1 row_1 ...): the shared-expert
+    GEMM2 with the layer's consume fused (dice_gemm_consume)."""
+    _need(A, torch.bfloat16, "gemm A")
+    _need(B, torch.bfloat16, "gemm B")
+    M, K = A.shape
+    N = B.shape[0]
+    k = pair_gates.shape[1]
+    if B.shape[1] != K or tuple(pair_rows.shape) != (k, M, N):
+        raise ContractError(f"gemm_consume: A {tuple(A.shape)} B {tuple(B.shape)} "
+                            f"rows {tuple(pair_rows.shape)}")
+    _lib.call("dice_gemm_consume", _ptr(A), M, _ptr(B), N, K, _ptr(residual), residual.shape[-1],
+              _ptr(pair_rows), _ptr(pair_gates), k, _ptr(out_f32), out_f32.shape[-1],
+              _ptr(out_bf16), 0 if out_bf16 is None else out_bf16.shape[-1], _stream())
+
+
+def consume_rows(residual, pair_rows, pair_gates, out_f32, out_bf16=None):
+    """out = residual + ((0 + g_0 row_0) + ...) (no shared experts)."""
+    n, hp = residual.shape
+    k = pair_gates.shape[1]
+    _lib.call("dice_consume_rows", _ptr(residual), _ptr(pair_rows), _ptr(pair_gates), n, k, hp,
+              _ptr(out_f32), _ptr(out_bf16), _stream())
 
 
 def cache_assemble(y, pos, active, write, gates, ids, routed, cache_rows=None, cache_gates=None,
@@ -255,7 +233,7 @@ def cache_assemble(y, pos, active, write, gates, ids, routed, cache_rows=None, c
               _ptr(routed), _ptr(rows_out), _ptr(gates_out), _stream())
 
 
-def gemm(epi, A, B, out_f32=None, out_bf16=None, residual=None, addend=None):
+def gemm(epi, A, B, out_f32=None, out_bf16=None, residual=None):
     """C[M, N] = A[M, K] @ B[N, K]^T (bf16 operands, fp32 accumulate) + fused epilogue."""
     _need(A, torch.bfloat16, "gemm A")
     _need(B, torch.bfloat16, "gemm B")
@@ -265,8 +243,7 @@ def gemm(epi, A, B, out_f32=None, out_bf16=None, residual=None, addend=None):
         raise ContractError(f"gemm: A {tuple(A.shape)} vs B {tuple(B.shape)}")
     ld = lambda t: 0 if t is None else t.shape[-1]
     _lib.call("dice_gemm", epi, _ptr(A), M, _ptr(B), N, K, _ptr(out_f32), ld(out_f32),
-              _ptr(out_bf16), ld(out_bf16), _ptr(residual), ld(residual), _ptr(addend),
-              ld(addend), _stream())
+              _ptr(out_bf16), ld(out_bf16), _ptr(residual), ld(residual), _stream())
 
 
 def combine(base, rows, gates, out, residual=None, out_bf16=None):

@@ -10,16 +10,19 @@ non-finite status word are read once at the end of the run.
 
 Buffers (all HBM-resident, allocated once per runner):
 * a dispatch payload = gate ids/gates, cond masks, permute positions/tile
-  offsets and the expert-sorted bf16 token rows (DispatchPayload, 48-57);
-* one combine slot per layer = the gate-weighted routed sum in f32
-  (CombinePayload + LayerBuffers, 60-79). It is consumed by the fused
-  shared-FFN epilogue u + (shared + routed).
+  offsets, the row -> pair map and the expert-sorted bf16 token rows
+  (DispatchPayload, 48-57);
+* per layer, the pair rows bf16 [k, n, hp] and pair gates f32 [n, k]: the
+  latest computed expert row and gate of every (token, slot) pair — the token
+  cache's rows / gates when conditional communication is on (TokenCache,
+  policies.py:142-208) — which together are the layer's combine slot
+  (CombinePayload + LayerBuffers, 60-79). The expert GEMM2 epilogue writes
+  them; the shared-FFN GEMM2 epilogue consumes them, u + (shared + sum g row).
 """
 from __future__ import annotations
 
 import dataclasses
 import hashlib
-import os
 from collections import Counter
 from dataclasses import dataclass
 from enum import Enum
@@ -122,7 +125,7 @@ class GpuTimeline:
 class _Payload:
     """Device buffers of one dispatch (DispatchPayload, schedules.py:48-57)."""
 
-    def __init__(self, n, k, E, hp, max_rows, device, row_pair=False):
+    def __init__(self, n, k, E, hp, max_rows, device):
         self.ids = torch.zeros(n, k, dtype=torch.int32, device=device)
         self.gates = torch.zeros(n, k, dtype=torch.float32, device=device)
         self.active = torch.ones(n, k, dtype=torch.uint8, device=device)
@@ -130,12 +133,12 @@ class _Payload:
         self.pos = torch.zeros(n, k, dtype=torch.int32, device=device)
         self.tiles = torch.zeros(E + 1, dtype=torch.int32, device=device)
         self.x_perm = torch.empty(max_rows, hp, dtype=torch.bfloat16, device=device)
-        # permuted row -> (token, slot) pair, for the combine fused into GEMM2
-        self.row_pair = (torch.full((max_rows,), -1, dtype=torch.int32, device=device)
-                         if row_pair else None)
+        # permuted row -> (token, slot) pair (-1 on padding rows), for the expert
+        # GEMM2's pair-row stores
+        self.row_pair = torch.full((max_rows,), -1, dtype=torch.int32, device=device)
         self.layer = -1
         self.gen = -1
-        self.done = None     # side-stream event: expert FFN + merge of this payload finished
+        self.done = None     # side-stream event: expert FFN of this payload finished
 
 
 class DeviceRunner:
@@ -183,43 +186,31 @@ class DeviceRunner:
         self.u32 = torch.zeros(n, hp, dtype=f32, device=dev)
         self.u16 = torch.zeros(n, hp, dtype=bf, device=dev)
         self.hbuf = torch.empty(self.max_rows, ep, dtype=bf, device=dev)
-        self.y = torch.empty(self.max_rows, hp, dtype=bf, device=dev)
         self.hsh = torch.empty(n, max(S, 1) * ep, dtype=bf, device=dev)
         self.scores = torch.empty(n, E, dtype=f32, device=dev) if record_routes else None
         L = cfg.num_layers
-        nslots = 1 if strategy is Strategy.SYNCHRONOUS else L
-        self.slots = torch.zeros(nslots, n, hp, dtype=f32, device=dev)
-        # DICE_FUSED_COMBINE=1: the routed combine (stale-cache merge + sum over
-        # slots) in the expert GEMM2 epilogue via float4 atomics onto a slot
-        # pre-initialised with the cached terms (k <= 2; bit-identical to the
-        # assemble kernel). Measured slower in-step (slot init 21 us + 19 us more
-        # GEMM2 epilogue vs a 26 us assemble), so opt-in.
-        self.fused_combine = k <= 2 and os.environ.get("DICE_FUSED_COMBINE", "0") == "1"
-        fc = self.fused_combine
         if strategy is Strategy.SYNCHRONOUS:
-            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev, fc)]
+            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev)]
         elif strategy is Strategy.INTERWEAVED:
-            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev, fc) for _ in range(3)]
+            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(3)]
         else:
-            self.payloads = [[_Payload(n, k, E, hp, self.max_rows, dev, fc) for _ in range(2)]
+            self.payloads = [[_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(2)]
                              for _ in range(L)]
         self.cache = None
         if policy.cond_strategy is not CondStrategy.OFF:
             self.cache = TokenCache(L, n, k, cfg.hidden_dim, device=dev)
+            self.pair_rows, self.pair_gates = self.cache.rows, self.cache.gates
+            self.pair_ids = self.cache.expert_ids
+        else:
+            nslots = 1 if strategy is Strategy.SYNCHRONOUS else L
+            self.pair_rows = torch.zeros(nslots, k, n, hp, dtype=bf, device=dev)
+            self.pair_gates = torch.zeros(nslots, n, k, dtype=f32, device=dev)
+            self.pair_ids = None
         self.scratch = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
-        # DICE_FUSED_GATE=1: router partial logits fused into the local_block GEMM
-        # epilogue (measured slower at the XL shape: the local GEMM's epilogue is
-        # its critical path); default: standalone persistent gate kernel. Either
-        # way the conditional-communication decision runs inside the gate launch.
-        self.fused_gate = E in (8, 16) and os.environ.get("DICE_FUSED_GATE", "0") == "1"
-        # the permute's counting pass rides in the gate launch (E = 8 row-quad
-        # kernel; DICE_GATE_COUNT=0: separate count kernel)
-        self.gate_count = (E == 8 and not self.fused_gate and 32 % k == 0
-                           and os.environ.get("DICE_GATE_COUNT", "1") != "0")
+        # the permute's counting pass rides in the gate launch (E = 8 row-quad kernel)
+        self.gate_count = E == 8 and 32 % k == 0
         self.chunk_counts = (torch.zeros((n + 31) // 32 * 8, dtype=torch.int32, device=dev)
                              if self.gate_count else None)
-        if self.fused_gate:
-            self.gparts = torch.empty(ops.gate_parts(n, hp, hp, E), n, E, dtype=f32, device=dev)
         self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
         self.status = torch.empty(4, dtype=torch.int32, device=dev)
         self.sync_layers = select_sync_layers(policy.sync_strategy, L, policy.explicit_layers)
@@ -235,10 +226,9 @@ class DeviceRunner:
         if overlap and strategy is Strategy.INTERWEAVED and str(dev).startswith("cuda") and not timeline:
             self.side = torch.cuda.Stream(device=dev)
         # the processed dispatch's expert GEMM1 and the stage's shared-expert GEMM1
-        # are independent: one persistent launch for both (DICE_MERGE_GEMM1=0 off)
+        # are independent: one persistent launch for both
         self.merge_gemm1 = (S > 0 and self.side is None
-                            and strategy in (Strategy.SYNCHRONOUS, Strategy.INTERWEAVED)
-                            and os.environ.get("DICE_MERGE_GEMM1", "1") != "0")
+                            and strategy in (Strategy.SYNCHRONOUS, Strategy.INTERWEAVED))
 
     # ------------------------------------------------------------ helpers
     def _reset_state(self, x0_device=None):
@@ -364,7 +354,10 @@ class DeviceRunner:
         return pair[1] if self.dispatch_slot[layer] is pair[0] else pair[0]
 
     def _slot(self, layer):
-        return self.slots[0] if self.strategy is Strategy.SYNCHRONOUS else self.slots[layer]
+        """(pair rows [k, n, hp], pair gates [n, k], cached ids or None) of a layer."""
+        i = 0 if self.pair_rows.shape[0] == 1 else layer
+        return (self.pair_rows[i], self.pair_gates[i],
+                None if self.pair_ids is None else self.pair_ids[i])
 
     # -------------------------------------------------------------- stages
     def _dispatch(self, step, layer, p: _Payload, force: bool, decided: bool = False):
@@ -409,20 +402,13 @@ class DeviceRunner:
             self.side_tail = None
 
     def _process_body(self, p: _Payload, shared_layer=None):
-        """shared_layer: also run that layer's shared-expert GEMM1 (u16 -> hsh)
-        inside the expert GEMM1 launch."""
+        """Expert FFN of a dispatch; the GEMM2 epilogue stores every computed
+        pair's row / gate / id into the layer's pair rows (the stale-cache merge
+        of TokenCache.assemble, policies.py:188-208, needs no kernel: inactive
+        pairs keep their cached entries). shared_layer: also run that layer's
+        shared-expert GEMM1 (u16 -> hsh) inside the expert GEMM1 launch."""
         self._mark(f"expert s{p.gen} L{p.layer}")
         lw = self.model.layers[p.layer]
-        c = self.cache
-        if self.fused_combine:
-            # combine slot <- cached terms of the inactive pairs; the GEMM2 epilogue
-            # adds the fresh ones (TokenCache.assemble, policies.py:188-208)
-            with self._op("slot_init", p.gen, p.layer):
-                ops.slot_init(None if c is None else p.active, None if c is None else p.write,
-                              p.gates, p.ids, self._slot(p.layer),
-                              None if c is None else c.rows[p.layer],
-                              None if c is None else c.gates[p.layer],
-                              None if c is None else c.expert_ids[p.layer])
         if self.time_experts:
             i = len(self._expert_events)
             if i >= len(self._event_pool):
@@ -430,37 +416,20 @@ class DeviceRunner:
             e0, e1 = self._event_pool[i]
             e0.record()
         name = "grouped_ffn" if shared_layer is None else "grouped_ffn+shared_gemm1"
-        if self.fused_combine:
-            name += "+combine"
+        rows, gates, ids = self._slot(p.layer)
         with self._op(name, p.gen, p.layer):
-            if shared_layer is None and not self.fused_combine:
-                ops.grouped_ffn(p.x_perm, lw.w1_t, lw.w2_t, self.E, p.tiles, self.hbuf, self.y)
+            if shared_layer is None:
+                ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
+                                             self.u16[:0], lw.w1_t, self.hsh)
             else:
-                if shared_layer is None:
-                    ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
-                                                 self.u16[:0], lw.w1_t, self.hsh)
-                else:
-                    ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
-                                                 self.u16, self.model.layers[shared_layer].ws1_t,
-                                                 self.hsh)
-                if self.fused_combine:
-                    ops.expert_gemm2_combine(self.hbuf, lw.w2_t, self.E, p.tiles, p.row_pair,
-                                             p.gates, None if c is None else p.write,
-                                             self._slot(p.layer),
-                                             None if c is None else c.rows[p.layer])
-                else:
-                    ops.expert_gemm2(self.hbuf, lw.w2_t, self.E, p.tiles, self.y)
+                ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
+                                             self.u16, self.model.layers[shared_layer].ws1_t,
+                                             self.hsh)
+            ops.expert_gemm2_pairs(self.hbuf, lw.w2_t, self.E, p.tiles, p.row_pair, p.gates,
+                                   p.ids, rows, gates, ids)
         if self.time_experts:
             e1.record()
             self._expert_events.append((e0, e1, p.gen, p.layer, shared_layer is not None))
-        if not self.fused_combine:
-            with self._op("cache_assemble", p.gen, p.layer):
-                ops.cache_assemble(self.y, p.pos, None if c is None else p.active,
-                                   None if c is None else p.write, p.gates, p.ids,
-                                   self._slot(p.layer),
-                                   None if c is None else c.rows[p.layer],
-                                   None if c is None else c.gates[p.layer],
-                                   None if c is None else c.expert_ids[p.layer])
         self.slot_gen[p.layer] = p.gen
         self.combine_log.append((p.gen, p.layer))
 
@@ -471,21 +440,20 @@ class DeviceRunner:
             self._track("c", prev.layer)
 
     def _consume(self, layer, step, gen, gemm1_done=False):
-        """u + (shared + routed) fused into the shared-FFN GEMM2 epilogue
-        (_consume, schedules.py:308-317; combine_outputs, model.py:279-298)."""
+        """u + (shared + sum_s g_s row_s) fused into the shared-FFN GEMM2 epilogue
+        over the layer's pair rows (_consume, schedules.py:308-317;
+        combine_outputs, model.py:279-298)."""
         lw = self.model.layers[layer]
-        slot = self._slot(layer)
+        rows, gates, _ = self._slot(layer)
         self._mark(f"shared+consume s{step} L{layer}")
         if self.S > 0:
             if not gemm1_done:
                 with self._op("shared_gemm1", step, layer):
                     ops.gemm(ops.EPI_GELU_BF16, self.u16, lw.ws1_t, out_bf16=self.hsh)
             with self._op("shared_gemm2_consume", step, layer):
-                ops.gemm(ops.EPI_CONSUME, self.hsh, lw.ws2_t, out_f32=self.h32, out_bf16=self.h16,
-                         residual=self.u32, addend=slot)
+                ops.gemm_consume(self.hsh, lw.ws2_t, self.u32, rows, gates, self.h32, self.h16)
         else:
-            empty = slot.new_empty(self.n, 0)
-            ops.combine(slot, slot, empty, self.h32, residual=self.u32, out_bf16=self.h16)
+            ops.consume_rows(self.u32, rows, gates, self.h32, self.h16)
         self.records.append(StalenessRecord(layer=layer, used_step=step, generated_step=gen))
 
     def _run_step(self, step):
@@ -496,12 +464,8 @@ class DeviceRunner:
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
             self._mark(f"local s{step} L{layer}")
             with self._op("local_gemm", step, layer):
-                if self.fused_gate:
-                    ops.gemm_local_gate(hin16, lw.w_mix_t, lw.w_gate_c, self.u32, self.u16, hin32,
-                                        self.gparts)
-                else:
-                    ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
-                             out_bf16=self.u16, residual=hin32)
+                ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
+                         out_bf16=self.u16, residual=hin32)
             self._mark(f"gate+dispatch s{step} L{layer}")
             sync = self._stage_is_sync(step, layer)
             if sync and self.strategy is Strategy.INTERWEAVED:
@@ -515,14 +479,10 @@ class DeviceRunner:
             if self.cache is not None:
                 dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write)
             with self._op("gate_decide", step, layer):
-                if self.fused_gate:
-                    ops.gate_finish(self.gparts, p.ids, p.gates, self.scores, self.status, step,
-                                    layer, decide=dec)
-                else:
-                    cnt = ((self.chunk_counts, self.counters[step, layer],
-                            self.cluster.num_devices, self.n) if self.gate_count else None)
-                    ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
-                                  self.status, step, layer, decide=dec, count=cnt)
+                cnt = ((self.chunk_counts, self.counters[step, layer],
+                        self.cluster.num_devices, self.n) if self.gate_count else None)
+                ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
+                              self.status, step, layer, decide=dec, count=cnt)
             decided = dec is not None
             if self.record_inputs:
                 inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu())

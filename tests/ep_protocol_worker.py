@@ -19,8 +19,8 @@ FAKE_BASE = 1 << 40
 
 
 class FakeWindow(ep.Window):
-    def __init__(self, L, Dn, cap, ncap, hp, device):
-        self._layout(L, Dn, cap, ncap, hp)
+    def __init__(self, L, Dn, cap, k, nmax, hp, device):
+        self._layout(L, Dn, cap, k, nmax, hp)
         self.ptr = FAKE_BASE * (dist.get_rank() + 1)
 
     def view(self, offset, shape, dtype):
@@ -41,7 +41,7 @@ def fake_call(name, *args):
 
 
 class FakeOps:
-    EPI_STORE_BF16, EPI_GELU_BF16, EPI_STORE_F32, EPI_GELU_RESID, EPI_CONSUME = range(5)
+    EPI_STORE_BF16, EPI_GELU_BF16, EPI_STORE_F32, EPI_GELU_RESID = range(4)
     pad64 = staticmethod(ops.pad64)
     pad_hidden = staticmethod(ops.pad_hidden)
     COND_CODES = ops.COND_CODES
@@ -57,10 +57,6 @@ class FakeOps:
     @staticmethod
     def permute_scratch_ints(n, k, E):
         return max(1, (n * k + 1023) // 1024) * E
-
-    @staticmethod
-    def gate_parts(M, N, K, E):
-        return 1
 
     class DeviceEvent:
         def record(self):

@@ -45,10 +45,9 @@ def test_permute_sizing_helpers():
     lib = _lib.load()
     rows = lib.dice_permute_max_rows(8192, 2, 8)
     assert rows % 256 == 0 and rows >= 8192 * 2 + 8 * 255
-    # per-block counts of the three-kernel path (16 blocks of 1024 pairs) or of the
-    # single-launch path (<= 160 blocks), whichever is larger, + 32 barrier ints
-    assert lib.dice_permute_scratch_ints(8192, 2, 8) == max(16 * 8, 160 * 8) + 32
-    assert lib.dice_permute_scratch_ints(1 << 20, 2, 8) == 2048 * 8 + 32
+    # per-block expert counts of the counting pass (blocks of 1024 pairs)
+    assert lib.dice_permute_scratch_ints(8192, 2, 8) == 16 * 8
+    assert lib.dice_permute_scratch_ints(1 << 20, 2, 8) == 2048 * 8
 
 
 def test_missing_library_fails_loudly(monkeypatch, tmp_path):
@@ -156,8 +155,8 @@ class _FakeOps:
 
     status_reset = splitmix_fill = gate_topk = cond_decide = route_permute = _noop
     grouped_ffn = cache_assemble = gemm = combine = denoise = pack_rows = _noop
-    gemm_local_gate = gate_finish = expert_gemm1_with_shared = expert_gemm2 = _noop
-    slot_init = expert_gemm2_combine = _noop
+    expert_gemm1_with_shared = expert_gemm2 = expert_gemm2_pairs = _noop
+    gemm_consume = consume_rows = _noop
 
 
 def _cpu_model(cfg):

@@ -1,10 +1,12 @@
 """CPU, world_size 2 and 4 over gloo: the expert-parallel exchange protocol
 (EPRunner host control flow, IPC-handle rendezvous through torch.distributed,
 ready/free flag handshakes) is simulated under many random interleavings of
-the ranks' stream operations. Checks: no deadlock, every window region is
-written exactly once before it is read and read before it is rewritten (no
-data race), every flag returns to its initial value (graph-replay safe), and
-all ranks follow the reference staleness law."""
+the ranks' stream operations. Checks: no deadlock; every receive region is
+written exactly once before it is read and read before it is rewritten; every
+consume of a home's pair rows finds, from every expert rank, the combine of
+exactly the step it consumes (stored and signalled; never a newer one) — no
+data race; every flag returns to its initial value (graph-replay safe); all
+ranks follow the reference staleness law."""
 import json
 import os
 import pickle
@@ -54,7 +56,7 @@ def initial_flags(logs):
     for lg in logs:
         lay, b = lg["layout"], FAKE_BASE * (lg["rank"] + 1)
         n = lay["L"] * lay["D"]
-        for key, init in (("o_rx_ready", 0), ("o_cx_ready", 0), ("o_rx_free", 1), ("o_cx_free", 1)):
+        for key, init in (("o_rx_ready", 0), ("o_cx_ready", 0), ("o_rx_free", 1), ("o_cx_free", 0)):
             for i in range(n):
                 flags[b + lay[key] + 4 * i] = init
     return flags
@@ -64,7 +66,8 @@ def simulate(logs, seed):
     rng = random.Random(seed)
     flags = initial_flags(logs)
     init = dict(flags)
-    full = set()            # window regions holding unread data
+    full = set()            # receive regions holding unread data
+    cx = {}                 # pair-row region -> (step of its combine, signalled)
     pcs = [0] * len(logs)
     traces = [lg["trace"] for lg in logs]
     steps = 0
@@ -87,17 +90,29 @@ def simulate(logs, seed):
                 flags[a] = op[2]
         elif op[0] == "kwrite":                   # kernel stores into window regions
             for reg in map(tuple, op[1]):
+                if reg[0] == "cx":                # pair rows: the combine of step op[2]
+                    cx[reg] = (op[2], False)
+                    continue
                 assert reg not in full, f"rank {r} overwrites unread {reg}"
                 full.add(reg)
-        elif op[0] == "read":                     # kernel reads window regions
+        elif op[0] == "read":                     # kernel reads receive regions
             for reg in map(tuple, op[1]):
                 assert reg in full, f"rank {r} reads {reg} before it was written"
                 full.discard(reg)
+        elif op[0] == "arrive":                   # home: combine stores signalled
+            for reg in map(tuple, op[1]):
+                assert reg in cx and not cx[reg][1], f"rank {r}: {reg} arrives without a store"
+                cx[reg] = (cx[reg][0], True)
+        elif op[0] == "consume":                  # home reads its pair rows
+            for reg in map(tuple, op[1]):
+                got = cx.get(reg)
+                assert got == (op[2], True), f"rank {r} consumes {reg}: has {got}, wants step {op[2]}"
         pcs[r] += 1
         steps += 1
     done = all(pcs[r] >= len(t) for r, t in enumerate(traces))
     assert done, f"deadlock: pcs={pcs}"
     assert not full, f"unread regions at the end: {sorted(full)[:4]}"
+    assert all(arrived for _, arrived in cx.values())
     assert flags == init, "flags not restored"
     return steps
 
@@ -117,7 +132,7 @@ def test_exchange_protocol_random_interleavings(world, strategy, policy):
         fixed = []
         for op in lg["trace"]:
             if op[0] == "write" and op[1] and not isinstance(op[1][0], int):
-                fixed.append(("kwrite", op[1]))
+                fixed.append(("kwrite", op[1], op[2]))
             else:
                 fixed.append(op)
         lg["trace"] = fixed

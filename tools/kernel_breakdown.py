@@ -11,7 +11,7 @@ sys.path.insert(0, ".")
 import paper_2411_16786_b200 as D  # noqa: E402
 from paper_2411_16786_b200 import ops, schedules  # noqa: E402
 
-EPI = {0: "store_bf16", 1: "gelu_bf16", 2: "store_f32", 3: "gelu_resid", 4: "consume"}
+EPI = {0: "store_bf16", 1: "gelu_bf16", 2: "store_f32", 3: "gelu_resid"}
 records = []
 pool = []
 
@@ -34,8 +34,8 @@ def gemm_label(epi, A, B, **kw):
     return f"gemm {EPI[epi]} {A.shape[0]}x{B.shape[0]}x{A.shape[1]}"
 
 
-for name in ("gate_topk", "route_permute", "cache_assemble", "denoise", "grouped_ffn",
-             "gemm_local_gate", "gate_finish"):
+for name in ("gate_topk", "route_permute", "denoise", "expert_gemm1_with_shared",
+             "expert_gemm2_pairs", "gemm_consume"):
     setattr(ops, name, wrap(name, getattr(ops, name)))
 ops.gemm = wrap("gemm", ops.gemm, gemm_label)
 _decide = D.policies.TokenCache.decide_into
