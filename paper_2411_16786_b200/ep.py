@@ -162,7 +162,7 @@ class EPGroup:
 
     def rx_meta(self, owner, layer, src):
         w = self.win
-        return self.base[owner] + w.o_rx_meta + ((layer * w.D + src) * w.cap) * 8
+        return self.base[owner] + w.o_rx_meta + ((layer * w.D + src) * w.cap) * 16
 
     def rx_count(self, owner, layer, src):
         w = self.win

@@ -149,7 +149,12 @@ class DeviceRunner:
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *,
                  record_inputs: bool = False, record_routes: bool = False,
                  time_experts: bool = False, overlap: bool = False, timeline: bool = False,
-                 time_ops: bool = False):
+                 time_ops: bool = False, record_filter=None, record_outputs: bool = False):
+        """record_inputs / record_routes: per (step, layer) MoE inputs u and
+        routes (+ the conditional-communication masks in ``step_masks``), as
+        run_sampling(record_*=True); ``record_filter(step, layer)`` limits the
+        recorded inputs (others are None), ``record_outputs`` also records the
+        layer outputs h at those stages (``step_outputs``)."""
         cfg = model.config
         if not isinstance(strategy, Strategy):
             raise ContractError(f"strategy must be a Strategy, got {strategy!r}")
@@ -166,6 +171,8 @@ class DeviceRunner:
         self.model, self.cfg, self.x0 = model, cfg, x0
         self.strategy, self.policy, self.cluster, self.seed = strategy, policy, cluster, seed
         self.record_inputs, self.record_routes = record_inputs, record_routes
+        self.record_filter = record_filter or (lambda step, layer: True)
+        self.record_outputs = record_outputs
         self.time_experts = time_experts
         # time_ops: graph-safe CUDA events around every library op of the run
         # (per-op device time inside the real step; costs a few % of the step)
@@ -258,7 +265,7 @@ class DeviceRunner:
         self.records = []
         self.dispatch_log = []
         self.combine_log = []
-        self.step_inputs, self.step_routes = [], []
+        self.step_inputs, self.step_routes, self.step_masks, self.step_outputs = [], [], [], []
         self._expert_events = []  # (start, end, generated step, layer) of each expert-FFN launch
         self._marks = []
         self._op_events = []      # (op, start, end, step, layer) when time_ops
@@ -458,7 +465,7 @@ class DeviceRunner:
 
     def _run_step(self, step):
         cfg = self.cfg
-        inputs_here, routes_here = [], []
+        inputs_here, routes_here, masks_here, outputs_here = [], [], [], []
         for layer in range(cfg.num_layers):
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
@@ -484,11 +491,14 @@ class DeviceRunner:
                 ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
                               self.status, step, layer, decide=dec, count=cnt)
             decided = dec is not None
+            keep = self.record_filter(step, layer)
             if self.record_inputs:
-                inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu())
+                inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu() if keep else None)
             if self.record_routes:
                 routes_here.append(RouteDecision(p.ids.long().cpu(), p.gates.cpu(),
                                                  self.scores.cpu()))
+                masks_here.append((p.active.bool().cpu(), p.write.bool().cpu())
+                                  if self.cache is not None else None)
             if sync:
                 self._dispatch(step, layer, p, force=True, decided=decided)
                 self._process(p, shared_layer=layer if self.merge_gemm1 else None)
@@ -518,6 +528,8 @@ class DeviceRunner:
                     self._process(prev, side=True, shared_layer=layer if merged else None)
                     self._track("c", prev.layer)
                 self._consume(layer, step, self.slot_gen[layer], gemm1_done=merged)
+            if self.record_outputs:
+                outputs_here.append(self.h32[:, :cfg.hidden_dim].cpu() if keep else None)
         self._flush_pending(side=self.strategy is Strategy.INTERWEAVED)
         self._mark(f"denoise s{step}")
         with self._op("denoise", step, -1):
@@ -527,6 +539,9 @@ class DeviceRunner:
             self.step_inputs.append(inputs_here)
         if self.record_routes:
             self.step_routes.append(routes_here)
+            self.step_masks.append(masks_here)
+        if self.record_outputs:
+            self.step_outputs.append(outputs_here)
 
     def launch(self, x0_device=None):
         """Enqueue the whole run (no host sync). ``x0_device`` (f32 [R, h] on

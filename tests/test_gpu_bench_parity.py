@@ -1,0 +1,202 @@
+"""Parity at the benched geometry and the divergence contract, on the GPU.
+
+The bench workload is DiT-MoE-XL/2-8E2A (h=1152, e=4608, 28 layers, 8 routed +
+2 shared experts, top-2) at 8192 rows under the full DICE policy (interweaved +
+Deep selective sync + LowScore R=5, W=6, P=10). Here the same engine runs 9
+denoising steps of that workload (steps 0-6 synchronous by warmup / period,
+7-8 asynchronous on the shallow layers) and is checked against the CPU oracle
+teacher-forced on the GPU's own recorded values (SURVEY.md §8c protocol):
+
+* routing: at sampled (step, layer) stages, the oracle's fp64 gate on the
+  GPU's u gives the GPU's expert ids bit-exactly for every token whose
+  adjacent top-(k+1) score gap exceeds TAU = 1e-5 (model.py:209-223), gates
+  within 1e-5;
+* conditional-communication masks: the oracle's TokenCache.decide replayed on
+  the GPU's ids over all 9 x 28 stages gives the GPU's active / write masks
+  exactly (policies.py:159-186);
+* layer outputs, teacher-forced: a synchronous stage (fresh expert rows) and
+  an asynchronous stage that consumes the previous step's combine with a
+  cached slot (expert rows of step 6 behind the LowScore cadence, stale gates;
+  schedules.py:372-397, policies.py:188-208), recomputed in fp64 from the
+  GPU's u / ids, within rel-L2 <= 1e-2 and max |err| <= 3e-2 * max |ref|
+  (bf16 GEMM operands, fp32 accumulation and residual).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2411_16786_b200 as D  # noqa: E402
+from oracle import dice_oracle as O  # noqa: E402
+
+TAU = 1e-5
+L_ASYNC = 3      # a shallow layer: asynchronous at steps 7, 8
+L_DEEP = 20      # a Deep selective-sync layer: synchronous at every step
+
+
+def _tie_band(scores, k):
+    """Tokens whose adjacent gap among the top-(k+1) scores is < TAU."""
+    top = -np.sort(-scores, axis=1)[:, :k + 1]
+    return np.min(top[:, :-1] - top[:, 1:], axis=1) < TAU
+
+
+@pytest.fixture(scope="module")
+def bench_run():
+    cfg = D.preset("xl2-8e2a", batch=32, num_steps=9)
+    assert cfg.total_rows == 8192
+    model = D.init_model(cfg, seed=0)
+    x0 = D.sample_x0(cfg, 1000)
+    keep = {(0, 0), (6, L_ASYNC), (7, L_ASYNC), (8, L_ASYNC), (8, L_DEEP)}
+    r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, D.dice_policy(),
+                       D.ClusterConfig(num_devices=1), 1000, record_inputs=True,
+                       record_routes=True, record_outputs=True,
+                       record_filter=lambda s, l: (s, l) in keep)
+    res = r.run()
+    g = O.Geometry(**{**O.PRESETS["xl2-8e2a"], "batch": 32, "num_steps": 9})
+    return cfg, g, r, res, keep
+
+
+def test_teacher_forced_routing_bit_exact_at_bench_geometry(bench_run):
+    cfg, g, r, res, keep = bench_run
+    excluded = 0
+    for (s, l) in sorted(keep):
+        u = res.step_inputs[s][l].numpy().astype(np.float64)
+        route = O.route_tokens(u, O.gate_weight(g, 0, l), cfg.top_k)
+        got = res.step_routes[s][l]
+        band = _tie_band(route.scores, cfg.top_k)
+        ids = got.expert_ids.numpy()
+        ok = ~band
+        assert np.array_equal(ids[ok], route.ids[ok]), (s, l, int((ids[ok] != route.ids[ok]).sum()))
+        assert np.abs(got.gates.numpy()[ok] - route.gates[ok]).max() < 1e-5
+        excluded += int(band.sum())
+    # the tie band is a small minority (~1e-5 gaps are rare)
+    assert excluded <= 0.002 * len(keep) * cfg.total_rows, excluded
+
+
+def test_cond_masks_exact_at_bench_geometry(bench_run):
+    cfg, g, r, res, keep = bench_run
+    pol = O.dice_defaults()
+    cache = O.CadenceCache(cfg.num_layers, cfg.total_rows, cfg.top_k, 1)
+    sync_set = O.sync_layer_set(pol.sync_strategy, cfg.num_layers)
+    checked = async_stages = 0
+    for s in range(cfg.num_steps):
+        for l in range(cfg.num_layers):
+            force = O.sync_step(s, pol.warmup, pol.period) or l in sync_set or s == 0
+            ids = res.step_routes[s][l].expert_ids.numpy()
+            act, wr = cache.decide(l, s, ids, pol, force)
+            gact, gwr = (m.numpy() for m in res.step_masks[s][l])
+            assert np.array_equal(gact, act) and np.array_equal(gwr, wr), (s, l)
+            checked += 1
+            async_stages += not force
+    assert checked == cfg.num_steps * cfg.num_layers and async_stages == 2 * 14
+    # the run's pair counters agree with the replayed masks
+    assert res.per_step_active_pairs[7] == 14 * 8192 * 2 + 14 * 8192
+
+
+def _oracle_layer(g, l):
+    return O.init_layer(g, 0, l)
+
+
+def _check(h_gpu, h_ref, what):
+    d = h_gpu - h_ref
+    rel_l2 = np.linalg.norm(d) / np.linalg.norm(h_ref)
+    max_rel = np.abs(d).max() / np.abs(h_ref).max()
+    print(f"{what}: rel-L2 {rel_l2:.2e}, max-rel {max_rel:.2e}")
+    assert rel_l2 <= 1e-2 and max_rel <= 3e-2, (what, rel_l2, max_rel)
+
+
+def test_teacher_forced_sync_stage_outputs_at_bench_geometry(bench_run):
+    cfg, g, r, res, keep = bench_run
+    for (s, l) in ((0, 0), (8, L_DEEP)):
+        p = _oracle_layer(g, l)
+        u = res.step_inputs[s][l].numpy().astype(np.float64)
+        route = O.forced_route(u, p.w_gate, res.step_routes[s][l].expert_ids.numpy())
+        rows = O.expert_rows(p, u, route)
+        h_ref = u + O.weighted_combine(rows, O.shared_sum(p, u), route.gates)
+        _check(res.step_outputs[s][l].numpy().astype(np.float64), h_ref, f"sync stage ({s},{l})")
+
+
+def test_teacher_forced_stale_cached_stage_at_bench_geometry(bench_run):
+    """Stage (8, L_ASYNC) consumes dispatch (7, L_ASYNC): slot 0 fresh at step 7,
+    slot 1 cached from the forced refresh at step 6 (LowScore, R=5), each with
+    the gate stored with its row; plus the shared experts on u(8)."""
+    cfg, g, r, res, keep = bench_run
+    l = L_ASYNC
+    assert [(x.layer, x.used_step, x.generated_step) for x in res.staleness_records
+            if x.layer == l and x.used_step == 8] == [(l, 8, 7)]
+    p = _oracle_layer(g, l)
+    pol = O.dice_defaults()
+    cache = O.CadenceCache(1, cfg.total_rows, cfg.top_k, cfg.hidden_dim)
+    rows = gates = None
+    for s, force in ((6, True), (7, False)):
+        u = res.step_inputs[s][l].numpy().astype(np.float64)
+        route = O.forced_route(u, p.w_gate, res.step_routes[s][l].expert_ids.numpy())
+        act, wr = cache.decide(0, s, route.ids, pol, force)
+        fresh = O.expert_rows(p, u, route, act)
+        rows, gates = cache.assemble(0, fresh, route, act, wr)
+    u8 = res.step_inputs[8][l].numpy().astype(np.float64)
+    h_ref = u8 + O.weighted_combine(rows, O.shared_sum(p, u8), gates)
+    _check(res.step_outputs[8][l].numpy().astype(np.float64), h_ref, "stale cached stage (8, 3)")
+
+
+# ------------------------------------------------------------- divergence
+SMALL = dict(num_layers=3, num_experts=4, num_shared=1, top_k=2, hidden_dim=64, expert_dim=128,
+             num_tokens=8, batch=2, num_steps=5, step_size=2e-4)
+
+
+def test_divergent_step_size_raises_with_step():
+    """Reference tests/test_schedules.py:239-244: step_size 1e150 diverges and
+    the error carries the step. (fp32 cannot hold 1e150 * h, so the GPU's
+    residual stream overflows at step 0; the fp64 reference a few steps later —
+    the reference test asserts only that a step is reported.)"""
+    cfg = D.ModelConfig(**{**SMALL, "step_size": 1e150})
+    model = D.init_model(cfg, seed=7)
+    x0 = D.sample_x0(cfg, 7)
+    for st in (D.Strategy.SYNCHRONOUS, D.Strategy.INTERWEAVED):
+        with pytest.raises(D.NumericalDivergenceError) as err:
+            D.run_sampling(model, x0, st, D.NEUTRAL, D.ClusterConfig(num_devices=2), 7)
+        assert err.value.step == 0
+
+
+@pytest.mark.parametrize("poison_step", [0, 3])
+@pytest.mark.parametrize("strategy", ["synchronous", "interweaved", "displaced"])
+def test_nonfinite_latent_raises_reference_step(poison_step, strategy):
+    """A non-finite latent entering step s: the reference's gate raises
+    NumericsError inside step s (model.py:212-213), which run() reports as
+    NumericalDivergenceError(step=s) (schedules.py:459-469); the oracle agrees.
+    The GPU run records it in the device status word and raises the same step
+    (one status read per run, also through a CUDA-graph replay)."""
+    cfg = D.ModelConfig(**SMALL)
+    model = D.init_model(cfg, seed=7)
+    x0 = D.sample_x0(cfg, 7)
+    pol = D.dice_policy(refresh_interval=2, warmup=1, period=3)
+    # oracle: the same poisoning
+    g = O.Geometry(**SMALL)
+    params = O.init_params(g, 7)
+    xs = O.initial_latent(g, 7)
+    xs[5, 3] = np.nan if poison_step == 0 else xs[5, 3]
+    if poison_step == 0:
+        with pytest.raises(O.NonFinite):
+            O.run_schedule(g, params, xs, strategy, O.dice_defaults(refresh_interval=2, warmup=1,
+                                                                     period=3), 2, 7)
+    for graph in (False, True):
+        r = D.DeviceRunner(model, x0, D.Strategy(strategy), pol, D.ClusterConfig(num_devices=2), 7)
+        if graph:
+            r.capture()
+        if poison_step == 0:
+            xp = x0.values.clone()
+            xp[5, 3] = float("nan")
+            r.launch(xp.contiguous())
+        elif graph:
+            continue    # mid-run poisoning needs the eager step loop
+        else:
+            r._reset_state()
+            for s in range(cfg.num_steps):
+                if s == poison_step:
+                    r.x32[5, 3] = float("nan")
+                r._run_step(s)
+            r._join_side()
+        with pytest.raises(D.NumericalDivergenceError) as err:
+            r.finish()
+        assert err.value.step == poison_step

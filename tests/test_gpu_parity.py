@@ -355,12 +355,33 @@ def test_sample_many_matches_sample():
         assert torch.equal(a, b)
 
 
+def assert_teacher_forced_ids(cfg, seed, res):
+    """Every (step, layer) of a run: the oracle's fp64 gate on the GPU's own
+    recorded MoE input u gives the GPU's expert ids bit-exactly outside the
+    tie band (adjacent top-(k+1) score gap < TAU) (model.py:209-223)."""
+    g = O.Geometry(**cfg.__dict__)
+    excluded = total = 0
+    for s in range(cfg.num_steps):
+        for l in range(cfg.num_layers):
+            u = res.step_inputs[s][l].numpy().astype(np.float64)
+            route = O.route_tokens(u, O.gate_weight(g, seed, l), cfg.top_k)
+            top = -np.sort(-route.scores, axis=1)[:, :cfg.top_k + 1]
+            ok = np.min(top[:, :-1] - top[:, 1:], axis=1) >= TAU
+            ids = res.step_routes[s][l].expert_ids.numpy()
+            assert np.array_equal(ids[ok], route.ids[ok]), (s, l)
+            excluded += int((~ok).sum())
+            total += len(ok)
+    assert excluded <= 0.01 * total, (excluded, total)
+
+
+
 def test_xl_width_runs_vs_reference():
     """The engine at the XL/2-8E2A layer widths (h=1152, e=4608, the bench's tile
     shapes) against the real reference's fp64 runs (3 layers, 128 rows, 4 steps,
-    synchronous and full DICE): update rel-L2 <= 2e-2, routing ids of every
-    (step, layer) agree for >= 98 % of the pairs (free-running: flips only near
-    ties), identical staleness histograms, pair counts and bytes."""
+    synchronous and full DICE): update rel-L2 <= 2e-2, routing ids teacher-forced
+    bit-exact outside the tie band at every (step, layer), free-running ids vs
+    the reference's >= 98 % identical (flips only near ties), identical
+    staleness histograms, pair counts and bytes."""
     meta = json.load(open(os.path.join(G, "xl_width.json")))
     z = load("xl_width.npz")
     cfg = cfg_of(meta["config"])
@@ -380,7 +401,8 @@ def test_xl_width_runs_vs_reference():
                                               refresh_interval=3, warmup=1))}
     for name, (st, pol) in runs.items():
         res = D.run_sampling(model, x0, st, pol, D.ClusterConfig(num_devices=meta["devices"]),
-                             meta["seed"], record_routes=True)
+                             meta["seed"], record_routes=True, record_inputs=True)
+        assert_teacher_forced_ids(cfg, meta["seed"], res)
         fin = res.final.values.cpu().numpy().astype(np.float64)
         ref = z[name + "_final"].astype(np.float64)
         drift = np.linalg.norm((fin - x0n) - (ref - x0n)) / np.linalg.norm(ref - x0n)
@@ -408,7 +430,9 @@ def test_g_width_run_vs_reference():
     """The engine at the G-16E2A layer widths (h=1664 padded to 1792, e=6656, 16
     experts: the E = 16 router and 16-group expert GEMMs) against the real
     reference's fp64 run (2 layers, 64 rows, 3 steps, D=4, full DICE): update
-    rel-L2 <= 2e-2, ids >= 98 % identical, histogram / pairs / bytes exact."""
+    rel-L2 <= 2e-2, ids teacher-forced bit-exact outside the tie band at every
+    (step, layer) and free-running >= 98 % identical, histogram / pairs / bytes
+    exact."""
     meta = json.load(open(os.path.join(G, "g_width.json")))
     z = load("g_width.npz")
     cfg = cfg_of(meta["config"])
@@ -418,7 +442,8 @@ def test_g_width_run_vs_reference():
     pol = D.dice_policy(refresh_interval=2, warmup=1, period=2)
     res = D.run_sampling(model, x0, D.Strategy.INTERWEAVED, pol,
                          D.ClusterConfig(num_devices=meta["devices"]), meta["seed"],
-                         record_routes=True)
+                         record_routes=True, record_inputs=True)
+    assert_teacher_forced_ids(cfg, meta["seed"], res)
     fin = res.final.values.cpu().numpy().astype(np.float64)
     ref = z["dice_final"].astype(np.float64)
     drift = np.linalg.norm((fin - x0n) - (ref - x0n)) / np.linalg.norm(ref - x0n)
