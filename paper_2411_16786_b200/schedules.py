@@ -379,7 +379,8 @@ class DeviceRunner:
             ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
                               self.counters[step, layer], self.scratch, self.E,
                               devices=self.cluster.num_devices, row0=0, rows_total=self.n,
-                              row_pair=p.row_pair, chunk_counts=self.chunk_counts)
+                              row_pair=p.row_pair,
+                              chunk_counts=self.chunk_counts if self.gate_count else None)
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 

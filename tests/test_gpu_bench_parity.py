@@ -86,7 +86,7 @@ def test_cond_masks_exact_at_bench_geometry(bench_run):
             force = O.sync_step(s, pol.warmup, pol.period) or l in sync_set or s == 0
             ids = res.step_routes[s][l].expert_ids.numpy()
             act, wr = cache.decide(l, s, ids, pol, force)
-            gact, gwr = (m.numpy() for m in res.step_masks[s][l])
+            gact, gwr = (m.numpy() for m in r.step_masks[s][l])
             assert np.array_equal(gact, act) and np.array_equal(gwr, wr), (s, l)
             checked += 1
             async_stages += not force
@@ -115,7 +115,7 @@ def test_teacher_forced_sync_stage_outputs_at_bench_geometry(bench_run):
         route = O.forced_route(u, p.w_gate, res.step_routes[s][l].expert_ids.numpy())
         rows = O.expert_rows(p, u, route)
         h_ref = u + O.weighted_combine(rows, O.shared_sum(p, u), route.gates)
-        _check(res.step_outputs[s][l].numpy().astype(np.float64), h_ref, f"sync stage ({s},{l})")
+        _check(r.step_outputs[s][l].numpy().astype(np.float64), h_ref, f"sync stage ({s},{l})")
 
 
 def test_teacher_forced_stale_cached_stage_at_bench_geometry(bench_run):
@@ -138,7 +138,7 @@ def test_teacher_forced_stale_cached_stage_at_bench_geometry(bench_run):
         rows, gates = cache.assemble(0, fresh, route, act, wr)
     u8 = res.step_inputs[8][l].numpy().astype(np.float64)
     h_ref = u8 + O.weighted_combine(rows, O.shared_sum(p, u8), gates)
-    _check(res.step_outputs[8][l].numpy().astype(np.float64), h_ref, "stale cached stage (8, 3)")
+    _check(r.step_outputs[8][l].numpy().astype(np.float64), h_ref, "stale cached stage (8, 3)")
 
 
 # ------------------------------------------------------------- divergence
