@@ -18,7 +18,8 @@ teacher-forced on the GPU's own recorded values (SURVEY.md §8c protocol):
   an asynchronous stage that consumes the previous step's combine with a
   cached slot (expert rows of step 6 behind the LowScore cadence, stale gates;
   schedules.py:372-397, policies.py:188-208), recomputed in fp64 from the
-  GPU's u / ids, within rel-L2 <= 1e-2 and max |err| <= 3e-2 * max |ref|
+  GPU's u / ids, within rel-L2 <= 5e-3 and max |err| <= 1e-2 * max |ref|
+  (measured: ~1e-3 both)
   (bf16 GEMM operands, fp32 accumulation and residual).
 """
 import numpy as np
@@ -104,7 +105,7 @@ def _check(h_gpu, h_ref, what):
     rel_l2 = np.linalg.norm(d) / np.linalg.norm(h_ref)
     max_rel = np.abs(d).max() / np.abs(h_ref).max()
     print(f"{what}: rel-L2 {rel_l2:.2e}, max-rel {max_rel:.2e}")
-    assert rel_l2 <= 1e-2 and max_rel <= 3e-2, (what, rel_l2, max_rel)
+    assert rel_l2 <= 5e-3 and max_rel <= 1e-2, (what, rel_l2, max_rel)
 
 
 def test_teacher_forced_sync_stage_outputs_at_bench_geometry(bench_run):
