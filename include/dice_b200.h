@@ -128,24 +128,29 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
                        int devices, int64_t row0, int64_t rows_total, int32_t* scratch,
                        int32_t* row_pair, void* stream);
 
-/* The permute's counting pass fused into the router (single-GPU engine, E = 8):
- * dice_gate_topk(_decide) (decide = 0 / 1) that also writes, per block of 32
- * tokens, the number of active pairs per expert (chunk_counts int32
- * [ceil(n/32), 8]) and adds the run counters (as dice_route_permute's);
- * dice_route_permute_counted then only scatters (+ gathers) with those counts
- * (k must divide 32): the same positions, tile offsets and rows as
- * dice_route_permute, one launch fewer. */
-int dice_gate_topk_counted(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
-                           int32_t* ids, float* gates, float* scores, int32_t* status, int step,
-                           int layer, int decide, int force, int refresh_interval, int strategy,
-                           int strict, uint64_t random_key, int32_t* last_refresh,
-                           uint8_t* primed, uint8_t* reduced, const int32_t* cached_ids,
-                           uint8_t* active, uint8_t* write, int32_t* chunk_counts,
-                           int64_t* counters, int devices, int64_t rows_total, void* stream);
-int dice_route_permute_counted(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
-                               const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows,
-                               int32_t* pos, int32_t* tile_offsets, const int32_t* chunk_counts,
-                               int32_t* row_pair, void* stream);
+/* Router + conditional-communication decision + token permute in ONE launch
+ * (single-GPU engine, E = 8, k <= 8): dice_gate_topk(_decide) (decide = 0 / 1)
+ * whose blocks of 32 tokens also group their active pairs by expert and copy
+ * the tokens' rows, rounded to bf16 from the fp32 u (the bits the local GEMM
+ * stores as its bf16 output), to their permuted rows. Expert e owns rows
+ * [e*cap, (e+1)*cap) of x_perm (bf16 [E*cap, hp], cap >= n, a multiple of
+ * 256); within an expert, rows follow pair order t*k+s (per-block offsets from
+ * a decoupled look-back over the blocks' counts). Outputs pos int32 [n, k]
+ * (-1 inactive), row_pair int32 [E*cap] (pair of each row, -1 on the padding
+ * rows up to each expert's 256-row tile end), tile_offsets int32 [E+1] (256-row
+ * tile prefix, for dice_expert_gemm1_with_dense(group_stride = cap)) and adds
+ * dice_route_permute's counters. route_state: uint64
+ * [dice_gate_route_state_words(n)], zero-filled once, then owned by these
+ * launches (look-back words and a launch generation). */
+int64_t dice_gate_route_state_words(int64_t n);
+int dice_gate_route(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                    int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                    int layer, int decide, int force, int refresh_interval, int strategy,
+                    int strict, uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
+                    uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
+                    uint8_t* write, uint16_t* x_perm, int64_t cap, int32_t* pos,
+                    int32_t* row_pair, int32_t* tile_offsets, int64_t* counters, int devices,
+                    int64_t rows_total, uint64_t* route_state, void* stream);
 
 /* Upper bound of rows of the padded permuted buffer for n*k pairs over E experts. */
 int64_t dice_permute_max_rows(int64_t n, int k, int E);
@@ -187,11 +192,16 @@ int dice_gemm(int epi, const uint16_t* A, int64_t M, const uint16_t* B, int N, i
  * of the same K in ONE persistent launch: hbuf = gelu(x_perm W1_e) over the
  * expert tiles AND out2 [M2, N2] = gelu(A2 B2^T) (the stage's shared-expert
  * GEMM1, shared_forward model.py:235-241, A2 = u bf16 [M2, hp], B2 = ws1_t);
- * then y = hbuf W2_e (expert_forward model.py:226-232). */
-int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
-                                 int E, int hp, int ep, const int32_t* tile_offsets,
-                                 uint16_t* hbuf, const uint16_t* A2, int64_t M2,
-                                 const uint16_t* B2, int N2, uint16_t* out2, void* stream);
+ * then y = hbuf W2_e (expert_forward model.py:226-232). group_stride = 0:
+ * x_perm holds the experts' 256-row tiles contiguously (dice_route_permute,
+ * max_rows rows); > 0: expert e's rows start at row e * group_stride
+ * (dice_gate_route's capacity regions, E * group_stride rows). hbuf is
+ * tile-contiguous either way (max_rows rows). */
+int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, int64_t group_stride,
+                                 const uint16_t* w1_t, int E, int hp, int ep,
+                                 const int32_t* tile_offsets, uint16_t* hbuf, const uint16_t* A2,
+                                 int64_t M2, const uint16_t* B2, int N2, uint16_t* out2,
+                                 void* stream);
 int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E, int hp,
                       int ep, const int32_t* tile_offsets, uint16_t* y, void* stream);
 
@@ -202,7 +212,9 @@ int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2
  *
  * dice_expert_gemm2_pairs: the expert GEMM2 (y = hbuf W2_e per expert tile)
  * whose epilogue stores the bf16 row of permuted row r (pair p = row_pair[r] =
- * t*k + s from dice_route_permute, -1 on padding) into pair_rows[s][t]
+ * t*k + s from dice_route_permute / dice_gate_route, -1 on padding; with
+ * pair_group_stride > 0 the map is indexed in dice_gate_route's capacity
+ * regions: tile j of expert e -> rows e * stride + 256 j ...) into pair_rows[s][t]
  * ([k, n, hp]: the layer's token-cache rows) and persists gates[p] / ids[p]
  * into cache_gates[p] / cache_ids[p] (either may be NULL). Every computed
  * pair is persisted: a cached entry is only ever read for a reduced pair that
@@ -220,9 +232,9 @@ int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2
  * (S = 0): out = residual + ((0 + g_0 row_0) + ...). */
 int dice_expert_gemm2_pairs(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
                             int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
-                            const float* gates, const int32_t* ids, int k, int64_t n,
-                            uint16_t* pair_rows, float* cache_gates, int32_t* cache_ids,
-                            void* stream);
+                            int64_t pair_group_stride, const float* gates, const int32_t* ids,
+                            int k, int64_t n, uint16_t* pair_rows, float* cache_gates,
+                            int32_t* cache_ids, void* stream);
 int dice_gemm_consume(const uint16_t* A, int64_t M, const uint16_t* B, int N, int K,
                       const float* residual, int64_t ld_res, const uint16_t* pair_rows,
                       const float* pair_gates, int k, float* out_f32, int64_t ld_f32,

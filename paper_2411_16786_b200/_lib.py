@@ -34,14 +34,13 @@ SIGNATURES = {
     "dice_gate_topk": (c_int, [P, P, c_int64, c_int, c_int, c_int, P, P, P, P, c_int, c_int, P]),
     "dice_gate_topk_decide": (c_int, [P, P, c_int64, c_int, c_int, c_int, P, P, P, P, c_int, c_int,
                                       c_int, c_int, c_int, c_int, c_uint64, P, P, P, P, P, P, P]),
-    "dice_expert_gemm1_with_dense": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P, c_int64,
-                                             P, c_int, P, P]),
+    "dice_expert_gemm1_with_dense": (c_int, [P, c_int64, c_int64, P, c_int, c_int, c_int, P, P, P,
+                                             c_int64, P, c_int, P, P]),
+    "dice_gate_route_state_words": (c_int64, [c_int64]),
+    "dice_gate_route": (c_int, [P, P, c_int64, c_int, c_int, c_int, P, P, P, P, c_int, c_int,
+                                c_int, c_int, c_int, c_int, c_int, c_uint64, P, P, P, P, P, P,
+                                P, c_int64, P, P, P, P, c_int, c_int64, P, P]),
     "dice_expert_gemm2": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P]),
-    "dice_gate_topk_counted": (c_int, [P, P, c_int64, c_int, c_int, c_int, P, P, P, P, c_int, c_int,
-                                       c_int, c_int, c_int, c_int, c_int, c_uint64, P, P, P, P, P,
-                                       P, P, P, c_int, c_int64, P]),
-    "dice_route_permute_counted": (c_int, [P, P, c_int64, c_int, c_int, P, c_int, P, c_int64, P,
-                                           P, P, P, P]),
     "dice_cond_decide": (c_int, [P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int, c_uint64,
                                  P, P, P, P, P, P, P]),
     "dice_route_permute": (c_int, [P, P, c_int64, c_int, c_int, P, c_int, P, c_int64, P, P, P,
@@ -52,8 +51,8 @@ SIGNATURES = {
     "dice_cache_assemble": (c_int, [P, P, P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P, P, P]),
     "dice_gemm": (c_int, [c_int, P, c_int64, P, c_int, c_int, P, c_int64, P, c_int64, P, c_int64,
                           P]),
-    "dice_expert_gemm2_pairs": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, P, P, c_int,
-                                        c_int64, P, P, P, P]),
+    "dice_expert_gemm2_pairs": (c_int, [P, c_int64, P, c_int, c_int, c_int, P, P, c_int64, P, P,
+                                        c_int, c_int64, P, P, P, P]),
     "dice_gemm_consume": (c_int, [P, c_int64, P, c_int, c_int, P, c_int64, P, P, c_int, P,
                                   c_int64, P, c_int64, P]),
     "dice_consume_rows": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, P]),
@@ -118,7 +117,7 @@ def check(rc: int, what: str) -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches count)
-KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_route_permute_counted": 2,
+KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_gate_route_state_words": 0,
                     "dice_grouped_ffn": 2, "dice_event_create": 0, "dice_event_destroy": 0,
                     "dice_event_record": 0, "dice_event_elapsed_ms": 0,
                     "dice_permute_max_rows": 0, "dice_permute_scratch_ints": 0,

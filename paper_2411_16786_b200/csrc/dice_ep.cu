@@ -229,7 +229,7 @@ int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* 
   if (rc) return rc;
   // GEMM1 (+ the rank's shared GEMM1 in the same launch), then GEMM2 whose
   // epilogue stores every finished row into its home rank's pair rows
-  rc = dice_expert_gemm1_with_dense(x_perm, max_rows, w1_t, El, hp, ep, tile_offsets, hbuf,
+  rc = dice_expert_gemm1_with_dense(x_perm, max_rows, 0, w1_t, El, hp, ep, tile_offsets, hbuf,
                                     A2, A2 != nullptr ? M2 : 0, B2, N2, out2, stream);
   if (rc) return rc;
   GemmProblem q{};

@@ -230,7 +230,7 @@ struct PairCfg {
 // Direct bf16 epilogue: this lane owns one row and 32 consecutive columns.
 template <int EPI>
 __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_t (&r)[32],
-                                                int64_t row, int col0) {
+                                                int64_t row, int col0, int64_t pair_row) {
   uint32_t w[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -242,7 +242,7 @@ __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_
   __nv_bfloat16* out = a.out_bf16 + row * a.ld_bf16;
   if constexpr (EPI == EPI_STORE_PAIR) {
     // (token, slot) pair of this expert row -> the layer's pair rows [s][t]
-    const int p = a.row_pair[row];
+    const int p = a.row_pair[pair_row];
     if (p < 0) return;                       // padding row of an expert group
     const int64_t t = p / a.top_k;
     const int s = p - (int)t * a.top_k;
@@ -349,7 +349,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int prob, n_blk, m_tile;   // N-fastest: resident tiles share A rows
         locate(tile, prob, n_blk, m_tile);
         const int g = prob == 0 ? find_group(sh->group_off, groups, m_tile) : 0;
-        const int a_row = m_tile * kPairM + rank * BM;
+        const int a_row = (prob == 0 && args.a_group_stride > 0)
+                              ? (int)(g * args.a_group_stride) +
+                                    (m_tile - sh->group_off[g]) * kPairM + rank * BM
+                              : m_tile * kPairM + rank * BM;
         const int b_row = g * (prob == 0 ? args.N : args2.N) + n_blk * TN + rank * (BN / 2);
         const CUtensorMap* mA = prob == 0 ? &tmA : &tmA2;
         const CUtensorMap* mB = prob == 0 ? &tmB : &tmB2;
@@ -414,6 +417,16 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int acc = C::kAccBufs == 2 ? (local & 1) : 0;
       const uint32_t acc_phase = C::kAccBufs == 2 ? ((local >> 1) & 1) : (local & 1);
       const int row0 = m_tile * kPairM + rank * BM + sub * 32;
+      // STORE_PAIR over capacity-strided expert regions: the row -> pair map
+      // entry of this lane's row
+      int64_t pair_row0 = row0;
+      if constexpr (EPI == EPI_STORE_PAIR) {
+        if (ar.pair_group_stride > 0) {
+          const int g = find_group(sh->group_off, groups, m_tile);
+          pair_row0 = g * ar.pair_group_stride + (int64_t)(m_tile - sh->group_off[g]) * kPairM +
+                      rank * BM + sub * 32;
+        }
+      }
       if constexpr (kResidPF) {   // first chunk's residual while the MMAs run
         if (grp * 32 < TN && n_blk * TN + grp * 32 < ar.N)
           resid_prefetch(ar, rbuf, lane, row0, rl, n_blk * TN + grp * 32);
@@ -430,7 +443,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (col0 >= ar.N) continue;  // warp-uniform
         if constexpr (DIRECT) {
           const int64_t row = row0 + lane;
-          if (row < rl) epilogue_direct<EPI>(ar, r, row, col0);
+          if (row < rl) epilogue_direct<EPI>(ar, r, row, col0, pair_row0 + lane);
           continue;
         }
 #pragma unroll

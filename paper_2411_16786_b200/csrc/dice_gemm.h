@@ -52,6 +52,12 @@ struct GemmArgs {
   const float* residual;
   int64_t ld_res;
   int stages;            // operand ring depth actually used (set by the host)
+  // grouped GEMMs over capacity-strided expert regions (the fused router
+  // writes expert e's permuted rows at e * stride): A rows of group g's tile j
+  // start at g * a_group_stride + 256 j (0: tiles are contiguous, row 256 m);
+  // STORE_PAIR's row -> pair map is indexed the same way with pair_group_stride
+  int64_t a_group_stride;
+  int64_t pair_group_stride;
   // CONSUME: pair_rows bf16 [k, n_tokens, ld_bf16-wide rows], pair_gates f32 [n, k]
   // STORE_PAIR: row -> pair map, source gates / ids of the pairs [n, k], the
   // cache gates / ids they are persisted to

@@ -229,16 +229,46 @@ struct DecideArgs {
   uint8_t* write;
 };
 
-// Permute counting fused into the gate launch (single-GPU engine): per block of
-// 32 tokens the number of active pairs per expert (the permute's per-chunk
-// counts) and the run counters (active pairs; remote pairs of the byte plan,
-// cluster.py:75-90), so the permute needs no counting pass of its own.
-struct CountArgs {
-  int32_t* chunk_counts;   // [ceil(n / 32), 8]; null: no counting
-  long long* counters;     // [2] (+=)
+// Token permute fused into the router launch (single-GPU engine, E = 8): one
+// block = 32 tokens. After the gate and the conditional-communication
+// decision, the block's active pairs are grouped by expert (warp match ranks
+// in pair order t*k+s, routed_rows' grouping, model.py:263-275, up to the
+// within-expert order, which changes no value), the per-expert offsets of the
+// earlier blocks come from a decoupled look-back over the blocks' published
+// counts, and the block copies its tokens' bf16 rows (rounded from the fp32 u
+// it already holds for the gate, the same rounding as the local GEMM's bf16
+// output) straight to their permuted positions. Expert e's rows live in a
+// fixed-capacity region [e*cap, (e+1)*cap) (cap >= tokens), so no position
+// depends on another expert's total; the last block writes the 256-row tile
+// prefix and marks the padding rows of every region. Counters: active pairs
+// and remote pairs of the byte plan (cluster.py:75-90).
+constexpr int kRowTileR = 256;   // expert regions padded to the CTA-pair GEMM's 256-row tile
+
+struct RouteArgs {
+  uint16_t* x_perm;             // [E * cap, hp] bf16; null: gate only
+  int64_t cap;                  // rows per expert region (multiple of 256)
+  int32_t* pos;                 // [n, k] row of each pair, -1 inactive
+  int32_t* row_pair;            // [E * cap] pair of each row, -1 on padding rows
+  int32_t* tile_offsets;        // [E + 1] 256-row tile prefix
+  long long* counters;          // [2] (+=) active pairs, remote pairs
   int devices;
   int64_t rows_total;
+  unsigned long long* lookback; // [blocks * 8] (generation, status, value)
+  unsigned* epoch;              // [2] generation, finished blocks
 };
+
+__device__ __forceinline__ unsigned long long lb_pack(unsigned gen, unsigned status,
+                                                      unsigned value) {
+  return ((unsigned long long)gen << 32) | ((unsigned long long)status << 30) | value;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // TokenCache.decide for token t (policies.py:159-186): cadence, mask redraw,
 // active / write masks (strict: also refresh reduced pairs whose expert changed)
@@ -294,32 +324,39 @@ __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, i
 // E = 8: warp per FOUR rows. Each W_gate float4 (4 columns of one expert) now
 // feeds four rows (two FFMA2 row pairs), halving the L1 wavefronts per row, and
 // the 4 x 8 partial logits transpose-reduce to exactly one (row, expert) per
-// lane (lane = 8 row + e). Rows are loaded in CH-chunk batches.
+// lane (lane = 8 row + e). Rows are loaded in CH-chunk batches. One block = 8
+// warps = 32 tokens. With r.x_perm set, the block also permutes its pairs
+// (RouteArgs); the bf16 rows are staged in dynamic shared memory.
 template <int CH>
 __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
     const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
     int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
-    int32_t* status, int step, int layer, const DecideArgs d, const CountArgs c) {
-  __shared__ int s_cnt[8];
+    int32_t* status, int step, int layer, const DecideArgs d, const RouteArgs r) {
+  extern __shared__ __align__(16) uint16_t s_rows[];   // [32, hp] bf16 (routing only)
+  __shared__ int s_wcnt[8][8];       // per (warp, expert): count, then exclusive prefix
+  __shared__ int s_base[8];
+  __shared__ int s_tot[8];
+  __shared__ int s_pos[32 * 8];
   __shared__ unsigned long long s_red[2];
-  if (c.chunk_counts != nullptr) {   // (block-uniform) one block = 32 tokens
-    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  const bool route = r.x_perm != nullptr;    // block-uniform
+  if (route) {
+    if (threadIdx.x < 64) s_wcnt[threadIdx.x >> 3][threadIdx.x & 7] = 0;
     if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
-    __syncthreads();
   }
   pdl_enter();
   constexpr int E = 8;
   const int lane = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  const int64_t quads = (n + 3) / 4;
-  for (int64_t q = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5); q < quads;
-       q += (int64_t)gridDim.x * warps) {
-    const int64_t t0 = 4 * q;
-    const int row = lane >> 3;             // 0..3
-    const int e_me = lane & 7;             // expert held by this lane after the reduce
-    const int64_t t = t0 + row;
-    const bool row_ok = t < n;
-    const int slot = e_me;
+  const int warp = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * 8 + warp;   // this warp's quad of tokens
+  const int64_t t0 = 4 * q;
+  const int row = lane >> 3;             // 0..3
+  const int e_me = lane & 7;             // expert held by this lane after the reduce
+  const int64_t t = t0 + row;
+  const bool row_ok = t < n;
+  const int slot = e_me;
+  bool valid = false;                    // (t, slot) is an active pair
+  int my_e = 0;
+  if (t0 < n) {
     int32_t d_last = 0, d_cid = -1;
     uint8_t d_primed = 1, d_red = 0;
     const bool d_lane = d.on && d.strategy != DICE_COND_OFF && row_ok && slot < k;
@@ -349,6 +386,15 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
       for (int j = 0; j < CH; ++j) {
         const int c = base + 128 * j + lane * 4;
         if (c >= hp) break;
+        if (route) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(x[i][j].x, x[i][j].y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(x[i][j].z, x[i][j].w);
+            *reinterpret_cast<uint2*>(s_rows + (int64_t)(warp * 4 + i) * hp + c) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+          }
+        }
         const float2 p0 = make_float2(x[0][j].x, x[1][j].x), p1 = make_float2(x[0][j].y, x[1][j].y);
         const float2 p2 = make_float2(x[0][j].z, x[1][j].z), p3 = make_float2(x[0][j].w, x[1][j].w);
         const float2 r0 = make_float2(x[2][j].x, x[3][j].x), r1 = make_float2(x[2][j].y, x[3][j].y);
@@ -395,7 +441,6 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
     if (scores != nullptr && row_ok) scores[t * E + e_me] = sc;
     const unsigned rowmask = 0xFFu << rowbase;
     float psum = 0.f, my_s = 0.f;
-    int my_e = 0;
     for (int j = 0; j < k; ++j) {
       const unsigned m = __ballot_sync(0xffffffffu, rank == j) & rowmask;
       const int src = __ffs(m) - 1;
@@ -430,24 +475,97 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
         my_act = act;
       }
     }
-    if (c.chunk_counts != nullptr) {
-      const bool valid = slot < k && row_ok && my_act;
-      bool remote = false;
-      if (valid && c.devices > 1)
-        remote = (int)((t * c.devices) / c.rows_total) != my_e / (E / c.devices);
-      if (valid) atomicAdd(&s_cnt[my_e], 1);
-      const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
-      const unsigned nr = __popc(__ballot_sync(0xffffffffu, remote));
-      if (lane == 0 && nv) atomicAdd(&s_red[0], (unsigned long long)nv);
-      if (lane == 0 && nr) atomicAdd(&s_red[1], (unsigned long long)nr);
+    valid = slot < k && row_ok && my_act;
+  }
+  if (!route) return;
+  // ---------------------------------------------------------- permute
+  const unsigned peers = __match_any_sync(0xffffffffu, valid ? my_e : -1);
+  const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
+  __syncthreads();                       // s_wcnt zeroed by every warp's view
+  if (valid && rank_in_warp == 0) s_wcnt[warp][my_e] = __popc(peers);
+  {
+    bool remote = false;
+    if (valid && r.devices > 1)
+      remote = (int)((t * r.devices) / r.rows_total) != my_e / (E / r.devices);
+    const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
+    const unsigned nr = __popc(__ballot_sync(0xffffffffu, remote));
+    if (lane == 0 && nv) atomicAdd(&s_red[0], (unsigned long long)nv);
+    if (lane == 0 && nr) atomicAdd(&s_red[1], (unsigned long long)nr);
+  }
+  __syncthreads();
+  const bool last_block = blockIdx.x == gridDim.x - 1;
+  if (threadIdx.x < E) {
+    const int e = threadIdx.x;
+    unsigned acc = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { const int c = s_wcnt[w][e]; s_wcnt[w][e] = (int)acc; acc += c; }
+    // decoupled look-back over the earlier blocks' published counts
+    const unsigned gen = *reinterpret_cast<volatile unsigned*>(&r.epoch[0]);
+    unsigned long long* mine = r.lookback + (int64_t)blockIdx.x * 8 + e;
+    unsigned excl = 0;
+    if (blockIdx.x == 0) {
+      st_release_u64(mine, lb_pack(gen, 2, acc));
+    } else {
+      st_release_u64(mine, lb_pack(gen, 1, acc));
+      for (int64_t j = (int64_t)blockIdx.x - 1; j >= 0;) {
+        const unsigned long long v = ld_acquire_u64(r.lookback + j * 8 + e);
+        const unsigned st = (unsigned)(v >> 30) & 3u;
+        if ((unsigned)(v >> 32) != gen || st == 0) { __nanosleep(20); continue; }
+        excl += (unsigned)(v & 0x3FFFFFFFu);
+        if (st == 2) break;
+        --j;
+      }
+      st_release_u64(mine, lb_pack(gen, 2, excl + acc));
+    }
+    s_base[e] = (int)(e * r.cap) + (int)excl;
+    s_tot[e] = (int)(excl + acc);
+  }
+  __syncthreads();
+  if (t0 < n && slot < k && row_ok) {
+    const int p = valid ? s_base[my_e] + s_wcnt[warp][my_e] + rank_in_warp : -1;
+    r.pos[t * k + slot] = p;
+    if (valid) r.row_pair[p] = (int32_t)(t * k + slot);
+    s_pos[(warp * 4 + row) * k + slot] = p;
+  } else if (slot < k) {
+    s_pos[(warp * 4 + row) * k + slot] = -1;
+  }
+  __syncthreads();
+  // copy the staged bf16 rows to their permuted positions (a warp per pair)
+  const int vec = hp / 8;
+  for (int qq = warp; qq < 32 * k; qq += 8) {
+    const int p = s_pos[qq];
+    if (p < 0) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(s_rows + (int64_t)(qq / k) * hp);
+    uint4* dst = reinterpret_cast<uint4*>(r.x_perm + (int64_t)p * hp);
+    for (int c = lane; c < vec; c += 32) dst[c] = src[c];
+  }
+  if (threadIdx.x == 0) {
+    if (s_red[0]) atomicAdd(reinterpret_cast<unsigned long long*>(&r.counters[0]), s_red[0]);
+    if (s_red[1]) atomicAdd(reinterpret_cast<unsigned long long*>(&r.counters[1]), s_red[1]);
+  }
+  if (last_block) {
+    // totals of every expert: tile prefix and the padding rows of each region
+    if (threadIdx.x == 0) {
+      int tiles = 0;
+      for (int e = 0; e < E; ++e) {
+        r.tile_offsets[e] = tiles;
+        tiles += (s_tot[e] + kRowTileR - 1) / kRowTileR;
+      }
+      r.tile_offsets[E] = tiles;
+    }
+    for (int e = 0; e < E; ++e) {
+      const int64_t b0 = e * r.cap + s_tot[e];
+      const int64_t b1 = e * r.cap + (s_tot[e] + kRowTileR - 1) / kRowTileR * kRowTileR;
+      for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) r.row_pair[i] = -1;
     }
   }
-  if (c.chunk_counts != nullptr) {
-    __syncthreads();
-    if (threadIdx.x < 8) c.chunk_counts[(int64_t)blockIdx.x * 8 + threadIdx.x] = s_cnt[threadIdx.x];
-    if (threadIdx.x == 0 && c.counters != nullptr) {
-      if (s_red[0]) atomicAdd(reinterpret_cast<unsigned long long*>(&c.counters[0]), s_red[0]);
-      if (s_red[1]) atomicAdd(reinterpret_cast<unsigned long long*>(&c.counters[1]), s_red[1]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&r.epoch[1], 1u) == gridDim.x - 1) {   // the last block to finish
+      r.epoch[1] = 0;
+      __threadfence();
+      atomicAdd(&r.epoch[0], 1u);
     }
   }
 }
@@ -1063,11 +1181,11 @@ namespace {
 int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
                      int32_t* ids, float* gates, float* scores, int32_t* status, int step,
                      int layer, const DecideArgs& d, cudaStream_t s,
-                     const CountArgs& c = CountArgs{nullptr, nullptr, 1, 1}) {
+                     const RouteArgs& ra = RouteArgs{}) {
   if (E < 1 || E > 64 || k < 1 || k > E || hp % 64 != 0) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
-  // the fused permute counting lives in the E = 8 row-quad kernel only
-  if (c.chunk_counts != nullptr && (E != 8 || k > 8)) return DICE_ERR_CONTRACT;
+  // the fused permute lives in the E = 8 row-quad kernel only
+  if (ra.x_perm != nullptr && (E != 8 || k > 8)) return DICE_ERR_CONTRACT;
   const size_t smem = (size_t)E * hp * sizeof(float);
   const int threads = 512;
   int64_t want = ((n + 1) / 2 + 15) / 16;
@@ -1075,8 +1193,18 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
   if (E == 8 && k <= 8) {
     const int64_t gw = ((n + 3) / 4 + 7) / 8;     // 8 warps per block, four rows each
     const int grid = (int)(gw < 1 ? 1 : gw);
-    launch_pdl(gate4_topk_kernel<3>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp, k, ids,
-               gates, scores, status, step, layer, d, c);
+    const size_t rsmem = ra.x_perm != nullptr ? (size_t)32 * hp * sizeof(uint16_t) : 0;
+    if (rsmem > 0) {
+      static size_t attr = 0;
+      if (rsmem > attr) {
+        if (cudaFuncSetAttribute(gate4_topk_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)rsmem) != cudaSuccess)
+          return DICE_ERR_CUDA;
+        attr = rsmem;
+      }
+    }
+    launch_pdl(gate4_topk_kernel<3>, dim3(grid), dim3(256), rsmem, s, u, w_gate_t, n, hp, k, ids,
+               gates, scores, status, step, layer, d, ra);
     return launch_ok();
   }
   if (E == 16 && k <= 16) {
@@ -1134,45 +1262,45 @@ int dice_gate_topk_decide(const float* u, const float* w_gate_t, int64_t n, int 
                           (cudaStream_t)stream);
 }
 
-int dice_gate_topk_counted(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
-                           int32_t* ids, float* gates, float* scores, int32_t* status, int step,
-                           int layer, int decide, int force, int refresh_interval, int strategy,
-                           int strict, uint64_t random_key, int32_t* last_refresh,
-                           uint8_t* primed, uint8_t* reduced, const int32_t* cached_ids,
-                           uint8_t* active, uint8_t* write, int32_t* chunk_counts,
-                           int64_t* counters, int devices, int64_t rows_total, void* stream) {
-  if (decide && (refresh_interval < 1 || strategy < 0 || strategy > 3)) return DICE_ERR_CONFIG;
-  if (chunk_counts == nullptr || devices < 1 || E % devices != 0 || rows_total < 1)
-    return DICE_ERR_CONTRACT;
-  const DecideArgs d{decide ? 1 : 0, step, force, refresh_interval, strategy, strict, random_key,
-                     last_refresh, primed, reduced, cached_ids, active, write};
-  const CountArgs c{chunk_counts, reinterpret_cast<long long*>(counters), devices, rows_total};
-  return gate_topk_launch(u, w_gate_t, n, hp, E, k, ids, gates, scores, status, step, layer, d,
-                          (cudaStream_t)stream, c);
+int64_t dice_gate_route_state_words(int64_t n) {
+  // per block of 32 tokens 8 look-back words, + 1 word of launch generation
+  return (n + 31) / 32 * 8 + 1;
 }
 
-int dice_route_permute_counted(const int32_t* ids, const uint8_t* active, int64_t n, int k, int E,
-                               const uint16_t* u16, int hp, uint16_t* x_perm, int64_t max_rows,
-                               int32_t* pos, int32_t* tile_offsets, const int32_t* chunk_counts,
-                               int32_t* row_pair, void* stream) {
-  if (E != 8 || k < 1 || hp % 64 != 0 || chunk_counts == nullptr) return DICE_ERR_CONTRACT;
-  if (kPermBlock % (32 * k) != 0) return DICE_ERR_CONTRACT;
-  if (max_rows < dice_permute_max_rows(n, k, E)) return DICE_ERR_CONTRACT;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int64_t P = n * k;
-  const int blocks = (int)((P + kPermBlock - 1) / kPermBlock);
-  if (blocks == 0) {
-    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (E + 1), s);
+int dice_gate_route(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
+                    int32_t* ids, float* gates, float* scores, int32_t* status, int step,
+                    int layer, int decide, int force, int refresh_interval, int strategy,
+                    int strict, uint64_t random_key, int32_t* last_refresh, uint8_t* primed,
+                    uint8_t* reduced, const int32_t* cached_ids, uint8_t* active,
+                    uint8_t* write, uint16_t* x_perm, int64_t cap, int32_t* pos,
+                    int32_t* row_pair, int32_t* tile_offsets, int64_t* counters, int devices,
+                    int64_t rows_total, uint64_t* route_state, void* stream) {
+  if (decide && (refresh_interval < 1 || strategy < 0 || strategy > 3)) return DICE_ERR_CONFIG;
+  if (E != 8 || k < 1 || k > 8 || x_perm == nullptr || pos == nullptr || row_pair == nullptr ||
+      tile_offsets == nullptr || counters == nullptr || route_state == nullptr || cap < n ||
+      cap % kRowTileR != 0 || devices < 1 || E % devices != 0 || rows_total < 1 ||
+      32 * (int64_t)hp * 2 > 200 * 1024 || cap * E > INT32_MAX)
+    return DICE_ERR_CONTRACT;
+  if (n == 0) {
+    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (E + 1), (cudaStream_t)stream);
     return launch_ok();
   }
-  const int count_rows = (int)((n + 31) / 32);
-  launch_pdl(permute_scatter_kernel, dim3(blocks), dim3(kPermBlock), 0, s, ids, active, n, k, E,
-             pos, chunk_counts, tile_offsets, 1, kRowTile, row_pair, count_rows,
-             kPermBlock / (32 * k));
-  if (x_perm != nullptr)
-    launch_pdl(permute_gather_kernel, dim3(grid_for(P * 32, 256)), dim3(256), 0, s, pos, P, u16, k,
-               hp, x_perm);
-  return launch_ok();
+  const DecideArgs d{decide ? 1 : 0, step, force, refresh_interval, strategy, strict, random_key,
+                     last_refresh, primed, reduced, cached_ids, active, write};
+  const int64_t blocks = (n + 31) / 32;
+  RouteArgs ra{};
+  ra.x_perm = x_perm;
+  ra.cap = cap;
+  ra.pos = pos;
+  ra.row_pair = row_pair;
+  ra.tile_offsets = tile_offsets;
+  ra.counters = reinterpret_cast<long long*>(counters);
+  ra.devices = devices;
+  ra.rows_total = rows_total;
+  ra.lookback = reinterpret_cast<unsigned long long*>(route_state);
+  ra.epoch = reinterpret_cast<unsigned*>(route_state + blocks * 8);
+  return gate_topk_launch(u, w_gate_t, n, hp, E, k, ids, gates, scores, status, step, layer, d,
+                          (cudaStream_t)stream, ra);
 }
 
 int dice_cond_decide(const int32_t* ids, int64_t n, int k, int step, int force, int refresh_interval,
@@ -1210,17 +1338,22 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
                               (cudaStream_t)stream, row_pair);
 }
 
-int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, const uint16_t* w1_t,
-                                 int E, int hp, int ep, const int32_t* tile_offsets,
-                                 uint16_t* hbuf, const uint16_t* A2, int64_t M2,
-                                 const uint16_t* B2, int N2, uint16_t* out2, void* stream) {
+int dice_expert_gemm1_with_dense(const uint16_t* x_perm, int64_t max_rows, int64_t group_stride,
+                                 const uint16_t* w1_t, int E, int hp, int ep,
+                                 const int32_t* tile_offsets, uint16_t* hbuf, const uint16_t* A2,
+                                 int64_t M2, const uint16_t* B2, int N2, uint16_t* out2,
+                                 void* stream) {
   if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0 ||
-      M2 < 0 || M2 > INT_MAX || N2 % 64 != 0)
+      M2 < 0 || M2 > INT_MAX || N2 % 64 != 0 || group_stride < 0 || group_stride % kRowTile != 0)
     return DICE_ERR_CONTRACT;
   GemmProblem p{};
-  p.A = x_perm; p.A_rows = max_rows; p.B = w1_t; p.M = (int)max_rows; p.N = ep; p.K = hp;
+  // group_stride > 0: expert e's rows at e * group_stride of x_perm (E * group_stride
+  // rows); the GELU output hbuf stays tile-compact (max_rows rows)
+  p.A = x_perm; p.A_rows = group_stride > 0 ? E * group_stride : max_rows; p.B = w1_t;
+  p.M = (int)max_rows; p.N = ep; p.K = hp;
   p.num_groups = E; p.group_tile_offsets = tile_offsets; p.max_m_tiles = (int)(max_rows / kRowTile);
   p.epi_kind = EPI_GELU_BF16;
+  p.epi.a_group_stride = group_stride;
   p.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(hbuf); p.epi.ld_bf16 = ep;
   GemmProblem q{};
   q.A = A2; q.A_rows = M2; q.B = B2; q.M = (int)M2; q.N = N2; q.K = hp;
@@ -1245,11 +1378,11 @@ int dice_expert_gemm2(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2
 
 int dice_expert_gemm2_pairs(const uint16_t* hbuf, int64_t max_rows, const uint16_t* w2_t, int E,
                             int hp, int ep, const int32_t* tile_offsets, const int32_t* row_pair,
-                            const float* gates, const int32_t* ids, int k, int64_t n,
-                            uint16_t* pair_rows, float* cache_gates, int32_t* cache_ids,
-                            void* stream) {
+                            int64_t pair_group_stride, const float* gates, const int32_t* ids,
+                            int k, int64_t n, uint16_t* pair_rows, float* cache_gates,
+                            int32_t* cache_ids, void* stream) {
   if (E < 1 || E > kMaxGroups || hp % 64 != 0 || ep % 64 != 0 || max_rows % kRowTile != 0 ||
-      k < 1 || n < 0 || row_pair == nullptr || pair_rows == nullptr ||
+      k < 1 || n < 0 || row_pair == nullptr || pair_rows == nullptr || pair_group_stride < 0 ||
       (cache_gates != nullptr && gates == nullptr) || (cache_ids != nullptr && ids == nullptr))
     return DICE_ERR_CONTRACT;
   GemmProblem q{};
@@ -1258,6 +1391,7 @@ int dice_expert_gemm2_pairs(const uint16_t* hbuf, int64_t max_rows, const uint16
   q.epi_kind = EPI_STORE_PAIR;
   q.epi.out_bf16 = reinterpret_cast<__nv_bfloat16*>(pair_rows); q.epi.ld_bf16 = hp;
   q.epi.row_pair = row_pair;
+  q.epi.pair_group_stride = pair_group_stride;
   q.epi.pair_gates = gates;
   q.epi.pair_ids = ids;
   q.epi.cache_gates = cache_gates;

@@ -92,28 +92,21 @@ def splitmix_bits(seed, start, count, device="cuda"):
     return out
 
 
+def _decide_args(decide):
+    if decide is None:
+        return (0, 0, 1, 0, 0, 0, None, None, None, None, None, None)
+    (force, R, strat, strict, key, last, primed, reduced, cached, active, write) = decide
+    return (1, int(force), R, strat, int(strict), key & 0xFFFFFFFFFFFFFFFF, _ptr(last),
+            _ptr(primed), _ptr(reduced), _ptr(cached), _ptr(active), _ptr(write))
+
+
 def gate_topk(u32, w_gate_t, k, ids, gates, scores=None, status=None, step=0, layer=0,
-              decide=None, count=None):
+              decide=None):
     """Fused gate (softmax + stable top-k); ``decide`` = TokenCache.decide_args(...)
-    also runs the conditional-communication decision in the same kernel;
-    ``count`` = (chunk_counts, counters, devices, rows_total) also runs the
-    permute's counting pass (E = 8; then route_permute(chunk_counts=...))."""
+    also runs the conditional-communication decision in the same kernel."""
     n, hp = u32.shape
     E = w_gate_t.shape[0]
     _need(u32, torch.float32, "gate u")
-    if count is not None:
-        chunk_counts, counters, devices, rows_total = count
-        _need(chunk_counts, torch.int32, "chunk_counts")
-        if decide is None:
-            args = (0, 0, 1, 0, 0, 0, None, None, None, None, None, None)
-        else:
-            (force, R, strat, strict, key, last, primed, reduced, cached, active, write) = decide
-            args = (1, int(force), R, strat, int(strict), key & 0xFFFFFFFFFFFFFFFF, _ptr(last),
-                    _ptr(primed), _ptr(reduced), _ptr(cached), _ptr(active), _ptr(write))
-        _lib.call("dice_gate_topk_counted", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids),
-                  _ptr(gates), _ptr(scores), _ptr(status), step, layer, *args,
-                  _ptr(chunk_counts), _ptr(counters), devices, rows_total, _stream())
-        return
     if decide is None:
         _lib.call("dice_gate_topk", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids),
                   _ptr(gates), _ptr(scores), _ptr(status), step, layer, _stream())
@@ -123,6 +116,28 @@ def gate_topk(u32, w_gate_t, k, ids, gates, scores=None, status=None, step=0, la
               _ptr(gates), _ptr(scores), _ptr(status), step, layer, int(force), R, strat,
               int(strict), key & 0xFFFFFFFFFFFFFFFF, _ptr(last), _ptr(primed), _ptr(reduced),
               _ptr(cached), _ptr(active), _ptr(write), _stream())
+
+
+def route_state_words(n):
+    return int(_lib.load().dice_gate_route_state_words(n))
+
+
+def gate_route(u32, w_gate_t, k, ids, gates, x_perm, cap, pos, row_pair, tile_offsets, counters,
+               state, scores=None, status=None, step=0, layer=0, decide=None, devices=1,
+               rows_total=None):
+    """Gate + conditional-communication decision + token permute in one launch
+    (E = 8): x_perm bf16 [E*cap, hp], expert e's rows from e*cap (dice_gate_route)."""
+    n, hp = u32.shape
+    E = w_gate_t.shape[0]
+    _need(u32, torch.float32, "gate u")
+    _need(x_perm, torch.bfloat16, "x_perm")
+    _need(state, torch.int64, "route state")
+    if x_perm.shape[0] < E * cap or state.numel() < route_state_words(n):
+        raise ContractError("gate_route: x_perm / route state too small")
+    _lib.call("dice_gate_route", _ptr(u32), _ptr(w_gate_t), n, hp, E, k, _ptr(ids), _ptr(gates),
+              _ptr(scores), _ptr(status), step, layer, *_decide_args(decide), _ptr(x_perm), cap,
+              _ptr(pos), _ptr(row_pair), _ptr(tile_offsets), _ptr(counters), devices,
+              n if rows_total is None else rows_total, _ptr(state), _stream())
 
 
 def cond_decide(ids, step, force, refresh_interval, strategy, strict, random_key, last, primed,
@@ -142,18 +157,11 @@ def permute_scratch_ints(n, k, E):
 
 
 def route_permute(ids, active, u16, x_perm, pos, tile_offsets, counters, scratch, E,
-                  devices=1, row0=0, rows_total=None, row_pair=None, chunk_counts=None):
+                  devices=1, row0=0, rows_total=None, row_pair=None):
     """row_pair (int32 [max_rows], optional): permuted row -> pair index t*k+s
-    (-1 on padding rows), for the expert GEMM2's pair-row stores. chunk_counts: the
-    per-32-token expert counts the gate launch produced (gate_topk(count=...));
-    the counting pass and its counters are then already done."""
+    (-1 on padding rows), for the expert GEMM2's pair-row stores."""
     n, k = ids.shape
     hp = u16.shape[1]
-    if chunk_counts is not None:
-        _lib.call("dice_route_permute_counted", _ptr(ids), _ptr(active), n, k, E, _ptr(u16), hp,
-                  _ptr(x_perm), x_perm.shape[0], _ptr(pos), _ptr(tile_offsets),
-                  _ptr(chunk_counts), _ptr(row_pair), _stream())
-        return
     _lib.call("dice_route_permute", _ptr(ids), _ptr(active), n, k, E, _ptr(u16), hp,
               _ptr(x_perm), x_perm.shape[0], _ptr(pos), _ptr(tile_offsets), _ptr(counters),
               devices, row0, n if rows_total is None else rows_total, _ptr(scratch),
@@ -167,14 +175,16 @@ def grouped_ffn(x_perm, w1_t, w2_t, E, tile_offsets, hbuf, y):
               _ptr(tile_offsets), _ptr(hbuf), _ptr(y), _stream())
 
 
-def expert_gemm1_with_shared(x_perm, w1_t, E, tile_offsets, hbuf, u16, ws1_t, hsh):
+def expert_gemm1_with_shared(x_perm, w1_t, E, tile_offsets, hbuf, u16, ws1_t, hsh,
+                             group_stride=0):
     """Grouped expert GEMM1 (+GELU) and the shared experts' GEMM1 (+GELU) in
-    one persistent launch (dice_expert_gemm1_with_dense)."""
-    max_rows, hp = x_perm.shape
-    ep = hbuf.shape[1]
-    _lib.call("dice_expert_gemm1_with_dense", _ptr(x_perm), max_rows, _ptr(w1_t), E, hp, ep,
-              _ptr(tile_offsets), _ptr(hbuf), _ptr(u16), u16.shape[0], _ptr(ws1_t), ws1_t.shape[0],
-              _ptr(hsh), _stream())
+    one persistent launch (dice_expert_gemm1_with_dense). group_stride > 0:
+    expert e's rows of x_perm start at e * group_stride (dice_gate_route)."""
+    max_rows, ep = hbuf.shape
+    hp = x_perm.shape[1]
+    _lib.call("dice_expert_gemm1_with_dense", _ptr(x_perm), max_rows, group_stride, _ptr(w1_t), E,
+              hp, ep, _ptr(tile_offsets), _ptr(hbuf), _ptr(u16), u16.shape[0], _ptr(ws1_t),
+              ws1_t.shape[0], _ptr(hsh), _stream())
 
 
 def expert_gemm2(hbuf, w2_t, E, tile_offsets, y):
@@ -185,7 +195,7 @@ def expert_gemm2(hbuf, w2_t, E, tile_offsets, y):
 
 
 def expert_gemm2_pairs(hbuf, w2_t, E, tile_offsets, row_pair, gates, ids, pair_rows,
-                       cache_gates=None, cache_ids=None):
+                       cache_gates=None, cache_ids=None, pair_group_stride=0):
     """Expert GEMM2 whose epilogue stores each row of pair p = t*k + s into
     pair_rows[s, t] (bf16 [k, n, hp]) and persists the pair's gate / expert id
     (dice_expert_gemm2_pairs)."""
@@ -196,8 +206,8 @@ def expert_gemm2_pairs(hbuf, w2_t, E, tile_offsets, row_pair, gates, ids, pair_r
     if tuple(pair_rows.shape) != (k, n, hp):
         raise ContractError(f"pair rows {tuple(pair_rows.shape)} != {(k, n, hp)}")
     _lib.call("dice_expert_gemm2_pairs", _ptr(hbuf), max_rows, _ptr(w2_t), E, hp, ep,
-              _ptr(tile_offsets), _ptr(row_pair), _ptr(gates), _ptr(ids), k, n, _ptr(pair_rows),
-              _ptr(cache_gates), _ptr(cache_ids), _stream())
+              _ptr(tile_offsets), _ptr(row_pair), pair_group_stride, _ptr(gates), _ptr(ids), k, n,
+              _ptr(pair_rows), _ptr(cache_gates), _ptr(cache_ids), _stream())
 
 
 def gemm_consume(A, B, residual, pair_rows, pair_gates, out_f32, out_bf16=None):

@@ -123,7 +123,9 @@ class GpuTimeline:
 
 
 class _Payload:
-    """Device buffers of one dispatch (DispatchPayload, schedules.py:48-57)."""
+    """Device buffers of one dispatch (DispatchPayload, schedules.py:48-57).
+    max_rows: rows of the expert-sorted buffer (tile-contiguous experts, or E
+    capacity regions of the fused router)."""
 
     def __init__(self, n, k, E, hp, max_rows, device):
         self.ids = torch.zeros(n, k, dtype=torch.int32, device=device)
@@ -185,6 +187,12 @@ class DeviceRunner:
         hp, ep = model.hp, model.ep
         self.n, self.k, self.E, self.S, self.hp, self.ep = n, k, E, S, hp, ep
         self.max_rows = ops.permute_max_rows(n, k, E)
+        # E = 8: the gate launch also permutes (dice_gate_route); expert e's
+        # rows live in a capacity region of cap rows (>= n: a token routes to
+        # an expert at most once)
+        self.fused_route = E == 8 and k <= 8
+        self.cap = (n + 255) // 256 * 256
+        perm_rows = max(E * self.cap, self.max_rows) if self.fused_route else self.max_rows
         f32, bf = torch.float32, torch.bfloat16
         self.x32 = torch.zeros(n, hp, dtype=f32, device=dev)
         self.x16 = torch.zeros(n, hp, dtype=bf, device=dev)
@@ -197,11 +205,11 @@ class DeviceRunner:
         self.scores = torch.empty(n, E, dtype=f32, device=dev) if record_routes else None
         L = cfg.num_layers
         if strategy is Strategy.SYNCHRONOUS:
-            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev)]
+            self.payloads = [_Payload(n, k, E, hp, perm_rows, dev)]
         elif strategy is Strategy.INTERWEAVED:
-            self.payloads = [_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(3)]
+            self.payloads = [_Payload(n, k, E, hp, perm_rows, dev) for _ in range(3)]
         else:
-            self.payloads = [[_Payload(n, k, E, hp, self.max_rows, dev) for _ in range(2)]
+            self.payloads = [[_Payload(n, k, E, hp, perm_rows, dev) for _ in range(2)]
                              for _ in range(L)]
         self.cache = None
         if policy.cond_strategy is not CondStrategy.OFF:
@@ -214,10 +222,8 @@ class DeviceRunner:
             self.pair_gates = torch.zeros(nslots, n, k, dtype=f32, device=dev)
             self.pair_ids = None
         self.scratch = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
-        # the permute's counting pass rides in the gate launch (E = 8 row-quad kernel)
-        self.gate_count = E == 8 and 32 % k == 0
-        self.chunk_counts = (torch.zeros((n + 31) // 32 * 8, dtype=torch.int32, device=dev)
-                             if self.gate_count else None)
+        self.route_state = (torch.zeros(ops.route_state_words(n), dtype=torch.int64, device=dev)
+                            if self.fused_route else None)
         self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
         self.status = torch.empty(4, dtype=torch.int32, device=dev)
         self.sync_layers = select_sync_layers(policy.sync_strategy, L, policy.explicit_layers)
@@ -375,12 +381,12 @@ class DeviceRunner:
             act = p.active
         else:
             act = None
-        with self._op("permute", step, layer):
-            ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
-                              self.counters[step, layer], self.scratch, self.E,
-                              devices=self.cluster.num_devices, row0=0, rows_total=self.n,
-                              row_pair=p.row_pair,
-                              chunk_counts=self.chunk_counts if self.gate_count else None)
+        if not self.fused_route:           # (else the gate launch permuted)
+            with self._op("permute", step, layer):
+                ops.route_permute(p.ids, act, self.u16, p.x_perm, p.pos, p.tiles,
+                                  self.counters[step, layer], self.scratch, self.E,
+                                  devices=self.cluster.num_devices, row0=0, rows_total=self.n,
+                                  row_pair=p.row_pair)
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
 
@@ -425,16 +431,17 @@ class DeviceRunner:
             e0.record()
         name = "grouped_ffn" if shared_layer is None else "grouped_ffn+shared_gemm1"
         rows, gates, ids = self._slot(p.layer)
+        stride = self.cap if self.fused_route else 0
         with self._op(name, p.gen, p.layer):
             if shared_layer is None:
                 ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
-                                             self.u16[:0], lw.w1_t, self.hsh)
+                                             self.u16[:0], lw.w1_t, self.hsh, group_stride=stride)
             else:
                 ops.expert_gemm1_with_shared(p.x_perm, lw.w1_t, self.E, p.tiles, self.hbuf,
                                              self.u16, self.model.layers[shared_layer].ws1_t,
-                                             self.hsh)
+                                             self.hsh, group_stride=stride)
             ops.expert_gemm2_pairs(self.hbuf, lw.w2_t, self.E, p.tiles, p.row_pair, p.gates,
-                                   p.ids, rows, gates, ids)
+                                   p.ids, rows, gates, ids, pair_group_stride=stride)
         if self.time_experts:
             e1.record()
             self._expert_events.append((e0, e1, p.gen, p.layer, shared_layer is not None))
@@ -486,11 +493,16 @@ class DeviceRunner:
             dec = None
             if self.cache is not None:
                 dec = self.cache.decide_args(layer, step, self.policy, sync, p.active, p.write)
-            with self._op("gate_decide", step, layer):
-                cnt = ((self.chunk_counts, self.counters[step, layer],
-                        self.cluster.num_devices, self.n) if self.gate_count else None)
-                ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
-                              self.status, step, layer, decide=dec, count=cnt)
+            with self._op("gate_route" if self.fused_route else "gate_decide", step, layer):
+                if self.fused_route:
+                    ops.gate_route(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, p.x_perm,
+                                   self.cap, p.pos, p.row_pair, p.tiles, self.counters[step, layer],
+                                   self.route_state, self.scores, self.status, step, layer,
+                                   decide=dec, devices=self.cluster.num_devices,
+                                   rows_total=self.n)
+                else:
+                    ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
+                                  self.status, step, layer, decide=dec)
             decided = dec is not None
             keep = self.record_filter(step, layer)
             if self.record_inputs:

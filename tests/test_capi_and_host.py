@@ -156,7 +156,11 @@ class _FakeOps:
     status_reset = splitmix_fill = gate_topk = cond_decide = route_permute = _noop
     grouped_ffn = cache_assemble = gemm = combine = denoise = pack_rows = _noop
     expert_gemm1_with_shared = expert_gemm2 = expert_gemm2_pairs = _noop
-    gemm_consume = consume_rows = _noop
+    gemm_consume = consume_rows = gate_route = _noop
+
+    @staticmethod
+    def route_state_words(n):
+        return (n + 31) // 32 * 8 + 1
 
 
 def _cpu_model(cfg):

@@ -277,36 +277,73 @@ def test_gemm_rejects_internal_epilogue_kinds():
             ops.gemm(epi, A, B, out_bf16=o)
 
 
-@pytest.mark.parametrize("n,k,devices", [(8192, 2, 2), (1000, 2, 1), (777, 1, 4), (300, 4, 8)])
-def test_gate_counted_permute_matches_count_kernel(n, k, devices):
-    """dice_gate_topk_counted + dice_route_permute_counted == dice_gate_topk +
-    dice_route_permute: ids, gates, positions, tile offsets, permuted rows and
-    the run counters (active / remote pairs under D simulated devices). (The
-    engine test covers the decide-masked path.)"""
+@pytest.mark.parametrize("n,k,devices,decide", [(8192, 2, 2, True), (1000, 2, 1, False),
+                                                (777, 1, 4, True), (300, 4, 8, False),
+                                                (37, 3, 1, True)])
+def test_gate_route_matches_gate_then_permute(n, k, devices, decide):
+    """dice_gate_route (gate + decide + permute in one launch, expert regions of
+    cap rows) == dice_gate_topk(_decide) + dice_route_permute: ids, gates, masks,
+    run counters and tile offsets identical; every active pair sits at the same
+    offset within its expert (pair order), with the same bf16 row; padding rows
+    map to no pair. Repeated launches (the look-back generation) agree."""
     E, hp = 8, 256
     g = torch.Generator(device=dev).manual_seed(n + k)
     u = torch.randn(n, hp, device=dev, generator=g)
     wg = torch.randn(E, hp, device=dev, generator=g) * 0.1
     u16 = u.to(torch.bfloat16)
-    max_rows = ops.permute_max_rows(n, k, E)
-    res = {}
-    for mode in ("count", "plain"):
-        ids = torch.empty(n, k, dtype=torch.int32, device=dev)
-        gates = torch.empty(n, k, device=dev)
-        cnt = torch.zeros(2, dtype=torch.int64, device=dev)
-        pos = torch.empty(n, k, dtype=torch.int32, device=dev)
-        tiles = torch.empty(E + 1, dtype=torch.int32, device=dev)
-        x_perm = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
-        if mode == "count":
-            cc = torch.zeros((n + 31) // 32 * 8, dtype=torch.int32, device=dev)
-            ops.gate_topk(u, wg, k, ids, gates, count=(cc, cnt, devices, n))
-            ops.route_permute(ids, None, u16, x_perm, pos, tiles, cnt, None, E, chunk_counts=cc)
-        else:
-            scr = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
-            ops.gate_topk(u, wg, k, ids, gates)
-            ops.route_permute(ids, None, u16, x_perm, pos, tiles, cnt, scr, E, devices=devices,
-                              rows_total=n)
-        torch.cuda.synchronize()
-        res[mode] = (ids, gates, pos, tiles, x_perm, cnt)
-    for a, b in zip(res["count"], res["plain"]):
-        assert torch.equal(a, b)
+    cap = (n + 255) // 256 * 256
+    state = torch.zeros(ops.route_state_words(n), dtype=torch.int64, device=dev)
+
+    def cache_state():
+        return dict(last=torch.full((n,), -10 ** 9, dtype=torch.int32, device=dev),
+                    primed=torch.zeros(n, dtype=torch.uint8, device=dev),
+                    red=torch.zeros(n, k, dtype=torch.uint8, device=dev),
+                    cid=torch.full((n, k), -1, dtype=torch.int32, device=dev))
+    st = {"route": cache_state(), "plain": cache_state()}
+    for step in range(3):
+        res = {}
+        for mode in ("route", "plain"):
+            ids = torch.empty(n, k, dtype=torch.int32, device=dev)
+            gates = torch.empty(n, k, device=dev)
+            act = torch.ones(n, k, dtype=torch.uint8, device=dev)
+            wr = torch.zeros(n, k, dtype=torch.uint8, device=dev)
+            cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+            pos = torch.empty(n, k, dtype=torch.int32, device=dev)
+            tiles = torch.empty(E + 1, dtype=torch.int32, device=dev)
+            c = st[mode]
+            dec = ((step == 0, 2, ops.COND_CODES["low_score"], False, 0, c["last"], c["primed"],
+                    c["red"], c["cid"], act, wr) if decide else None)
+            if mode == "route":
+                x_perm = torch.zeros(E * cap, hp, dtype=torch.bfloat16, device=dev)
+                row_pair = torch.full((E * cap,), 777, dtype=torch.int32, device=dev)
+                ops.gate_route(u, wg, k, ids, gates, x_perm, cap, pos, row_pair, tiles, cnt, state,
+                               step=step, decide=dec, devices=devices, rows_total=n)
+            else:
+                max_rows = ops.permute_max_rows(n, k, E)
+                x_perm = torch.zeros(max_rows, hp, dtype=torch.bfloat16, device=dev)
+                row_pair = torch.full((max_rows,), 777, dtype=torch.int32, device=dev)
+                scr = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+                ops.gate_topk(u, wg, k, ids, gates, step=step, decide=dec)
+                ops.route_permute(ids, act if decide else None, u16, x_perm, pos, tiles, cnt, scr,
+                                  E, devices=devices, rows_total=n, row_pair=row_pair)
+            torch.cuda.synchronize()
+            res[mode] = (ids, gates, act, wr, cnt, pos, tiles, x_perm, row_pair)
+        a, b = res["route"], res["plain"]
+        for x, y in zip(a[:5], b[:5]):
+            assert torch.equal(x, y)
+        assert torch.equal(a[6], b[6])
+        tiles = b[6].cpu().numpy()
+        pa, pb = a[5].cpu().numpy(), b[5].cpu().numpy()
+        idn = b[0].cpu().numpy()
+        assert np.array_equal(pa < 0, pb < 0)
+        v = pb >= 0
+        assert np.array_equal(pa[v] - idn[v] * cap, pb[v] - tiles[idn[v]] * 256)
+        assert torch.equal(a[7][torch.as_tensor(pa[v], device=dev).long()],
+                           b[7][torch.as_tensor(pb[v], device=dev).long()])
+        rpa = a[8].cpu().numpy()
+        pair_idx = np.nonzero(v.reshape(-1))[0]
+        assert np.array_equal(rpa[pa.reshape(-1)[pair_idx]], pair_idx)
+        for e in range(E):
+            cnt_e = int(((idn == e) & v).sum())
+            pad_end = (tiles[e + 1] - tiles[e]) * 256
+            assert (rpa[e * cap + cnt_e:e * cap + pad_end] == -1).all()

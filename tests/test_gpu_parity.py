@@ -461,10 +461,10 @@ def test_g_width_run_vs_reference():
 
 @pytest.mark.parametrize("strategy,devices", [("interweaved", 2), ("displaced", 4),
                                               ("synchronous", 1)])
-def test_gate_counted_permute_engine_bit_identical(strategy, devices):
-    """The permute's counting pass fused into the gate launch (per-32-token expert
-    counts + run counters) reproduces the separate count kernel bit for bit:
-    latents, bytes (remote-pair counters under D simulated devices) and pairs."""
+def test_gate_route_engine_bit_identical(strategy, devices):
+    """The permute fused into the gate launch (capacity regions, look-back
+    offsets) reproduces the separate permute kernels bit for bit: latents,
+    bytes (remote-pair counters under D simulated devices) and pairs."""
     cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=256,
                         expert_dim=512, num_tokens=200, batch=3, num_steps=6, step_size=1e-3)
     model = D.init_model(cfg, seed=13)
@@ -474,8 +474,8 @@ def test_gate_counted_permute_engine_bit_identical(strategy, devices):
     for g in ("1", "0"):
         r = D.DeviceRunner(model, x0, D.Strategy(strategy), pol,
                            D.ClusterConfig(num_devices=devices), 13)
-        assert r.gate_count
-        r.gate_count = g == "1"
+        assert r.fused_route
+        r.fused_route = g == "1"
         res = r.run()
         out[g] = (res.final.values.cpu(), res.dispatch_bytes, res.combine_bytes,
                   res.active_pairs, res.per_step_active_pairs)

@@ -16,6 +16,10 @@ for k in "256, .int.1, .bool.1" "192, .int.4, .bool.0" "192, .int.5, .bool.1, .i
       > $OUT/k$i.log 2>&1
   ncu -i $OUT/k$i.ncu-rep --page raw --csv > $OUT/k${i}_raw.csv 2>/dev/null
   ncu -i $OUT/k$i.ncu-rep --page details --csv > $OUT/k${i}_details.csv 2>/dev/null
+  if [ $i -ge 5 ]; then   # memory-bound kernels: keep the source-level view
+    ncu -i $OUT/k$i.ncu-rep --page source --csv --print-source sass > $OUT/k${i}_sass.csv 2>/dev/null
+  fi
   rm -f $OUT/k$i.ncu-rep
 done
+python tools/summarize_ncu.py $OUT > $OUT/ncu_summary.txt
 du -sh $OUT
