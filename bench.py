@@ -335,6 +335,8 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
     E experts, S shared, P active pairs of that (step, layer) from the device
     counters):
       gate_decide     4Rh (u) + 4Eh (W_gate) + 8Rk (ids, gates) + 5R + 3Rk (cache state)
+      gate_route      gate_decide + 2hP (bf16 rows to their permuted positions) + 8P (pos,
+                      row_pair)
       permute         4hP (row gather read + write, bf16) + 9Rk (ids, masks, positions)
       cache_assemble  2hP (fresh rows) + 2h(Rk - P) (cached rows) + 4Rh (combine slot) + 10Rk
                       (cache-row writes of refreshed pairs not counted: a lower bound)
@@ -363,6 +365,9 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
         P = float(cnt[step, layer, 0]) if layer >= 0 else 0.0
         if name == "gate_decide":
             work, kind = 4 * R * h + 4 * E * h + 8 * R * k + 5 * R + 3 * R * k, "hbm"
+        elif name == "gate_route":
+            work, kind = (4 * R * h + 4 * E * h + 8 * R * k + 5 * R + 3 * R * k
+                          + 2 * h * P + 8 * P), "hbm"
         elif name == "permute":
             work, kind = 4 * h * P + 9 * R * k, "hbm"
         elif name == "cache_assemble":
@@ -471,10 +476,14 @@ def run_gpu(args):
     expert_events = list(runner._expert_events)
     res = runner.finish()
     cnt = runner.counters.cpu().numpy()
-    exposed_ms = 0.0
+    exposed_ms = wait_ms = kern_ms = 0.0
     if world > 1:
-        exposed_ms = res.timeline["exposed_comm_seconds"] * 1e3 if res.timeline else 0.0
-        exposed_ms = float(allreduce([exposed_ms], dist.ReduceOp.MAX).item())
+        tl = res.timeline or {}
+        # max over ranks of (flag waits + exchange kernels) on the rank's stream
+        ex = allreduce([tl.get("exposed_comm_seconds", 0.0) * 1e3,
+                        tl.get("comm_wait_seconds", 0.0) * 1e3,
+                        tl.get("comm_kernel_seconds", 0.0) * 1e3], dist.ReduceOp.MAX)
+        exposed_ms, wait_ms, kern_ms = (float(v) for v in ex)
         cnt = allreduce(cnt, dist.ReduceOp.SUM).numpy()
     if world > 1:
         ms = float(allreduce([ms], dist.ReduceOp.MAX).item())
@@ -585,6 +594,9 @@ def run_gpu(args):
                    "l2": "inputs larger than L2: the bf16 weights are streamed every denoising step"},
         "moe_layer_us": ms_per_step * 1e3 / (cfg.num_steps * cfg.num_layers),
         "exposed_a2a_us": exposed_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
+        "a2a_parts_us": {"flag_waits": wait_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
+                         "send_and_regroup_kernels": kern_ms * 1e3 / (cfg.num_steps
+                                                                      * cfg.num_layers)},
         # the reference's logical buffer accounting (R*h*2 per occupied slot,
         # schedules.py:185) next to the physical bytes this rank's run holds
         "buffers": {"logical_peak_bytes": peak_logical, "device_bytes": device_bytes},

@@ -254,6 +254,19 @@ int dice_combine(const float* base, const float* rows, const float* gates, const
 int dice_denoise(float* x, uint16_t* x16, const float* y, float eta, int64_t n, int hp,
                  int32_t* status, int step, void* stream);
 
+/* Adjacent-step drift of one layer (step_similarity / _cosine, model.py:308-346):
+ * out f64 [4] = {sum a*b, sum a*a, sum b*b over the first `cols` columns of the
+ * n rows of a = prev (ld_prev) and b = cur (ld_cur), number of rows t with
+ * prev_top[t * top_stride] == cur_ids[t * k]} (top-1 routing agreement).
+ * Deterministic fixed-order fp64 reductions. roll != 0 then stores cur into
+ * prev and cur's top-1 into prev_top (a runner's previous-step buffers).
+ * partials: f64 [dice_similarity_partial_words()] scratch. */
+int64_t dice_similarity_partial_words(void);
+int dice_step_similarity(float* prev, const float* cur, int64_t n, int cols, int64_t ld_prev,
+                         int64_t ld_cur, int32_t* prev_top, int64_t top_stride,
+                         const int32_t* cur_ids, int k, int roll, double* partials, double* out,
+                         void* stream);
+
 /* f32 [n, ld_in] (first `cols` columns) -> bf16 [n, hp] and f32 [n, hp] padded copies. */
 int dice_pack_rows(const float* in, int64_t n, int cols, int64_t ld_in, int hp, float* out32,
                    uint16_t* out16, void* stream);
@@ -312,6 +325,24 @@ int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* 
                    int32_t* row_pair, const uint64_t* home_rows, const uint64_t* home_gates,
                    const uint64_t* home_ids, const int64_t* home_n, const uint16_t* A2,
                    int64_t M2, const uint16_t* B2, int N2, uint16_t* out2, void* stream);
+
+/* dice_ep_expert in two parts, so the exchange's receive-side regroup (a
+ * communication cost) is timed apart from the expert FFN:
+ * dice_ep_regroup: window rows -> x_perm grouped by local expert (256-row
+ * tiles, tile_offsets, row_pair = window entry of each row, -1 on padding);
+ * dice_ep_expert_ffn: grouped FFN on x_perm whose GEMM2 epilogue stores into
+ * the home ranks' pair rows (arguments as dice_ep_expert). */
+int dice_ep_regroup(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
+                    int64_t cap, int El, int hp, int32_t* ids_rx, int32_t* pos_rx,
+                    int32_t* tile_offsets, int32_t* scratch, uint16_t* x_perm, int32_t* row_pair,
+                    void* stream);
+int dice_ep_expert_ffn(const uint16_t* x_perm, int64_t max_rows, const void* rx_meta,
+                       int64_t cap, int D, int El, int hp, int ep, int k, const uint16_t* w1_t,
+                       const uint16_t* w2_t, const int32_t* tile_offsets, uint16_t* hbuf,
+                       const int32_t* row_pair, const uint64_t* home_rows,
+                       const uint64_t* home_gates, const uint64_t* home_ids,
+                       const int64_t* home_n, const uint16_t* A2, int64_t M2, const uint16_t* B2,
+                       int N2, uint16_t* out2, void* stream);
 
 #ifdef __cplusplus
 }

@@ -527,6 +527,29 @@ def run_schedule(g: Geometry, params: list, x0: np.ndarray, strategy: str,
     return res
 
 
+def step_similarity(inputs: list, routes: list):
+    """Adjacent-step drift (model.py:316-346): per layer, the mean over adjacent
+    step pairs of cos(u_s, u_{s+1}) (_cosine, 316-320: 1 if both norms are 0,
+    0 if one is) and of the top-1 routing agreement. Returns
+    (per_layer_cosine, per_layer_agreement) as fp64 arrays."""
+    steps, layers = len(inputs), len(inputs[0])
+    cos = np.zeros(layers)
+    agree = np.zeros(layers)
+    for layer in range(layers):
+        c, a = [], []
+        for s in range(steps - 1):
+            x, y = inputs[s][layer], inputs[s + 1][layer]
+            nx, ny = np.linalg.norm(x), np.linalg.norm(y)
+            if nx == 0.0 or ny == 0.0:
+                c.append(1.0 if nx == ny else 0.0)
+            else:
+                c.append(float(np.dot(x.ravel(), y.ravel()) / (nx * ny)))
+            a.append(float(np.mean(routes[s][layer].ids[:, 0] == routes[s + 1][layer].ids[:, 0])))
+        cos[layer] = np.mean(c)
+        agree[layer] = np.mean(a)
+    return cos, agree
+
+
 # --------------------------------------------------------------------- presets
 # Geometry presets for the BASELINE configs (SURVEY.md §8 preset table). The
 # reference only ships h=32/e=64 toys (model.py:93-99); widths are pinned here.

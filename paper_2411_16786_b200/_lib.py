@@ -58,6 +58,9 @@ SIGNATURES = {
     "dice_consume_rows": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, P]),
     "dice_combine": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P]),
     "dice_denoise": (c_int, [P, P, P, c_float, c_int64, c_int, P, c_int, P]),
+    "dice_similarity_partial_words": (c_int64, []),
+    "dice_step_similarity": (c_int, [P, P, c_int64, c_int, c_int64, c_int64, P, c_int64, P, c_int,
+                                     c_int, P, P, P]),
     "dice_pack_rows": (c_int, [P, c_int64, c_int, c_int64, c_int, P, P, P]),
     "dice_device_alloc": (c_int, [c_int64, ctypes.POINTER(c_void_p)]),
     "dice_device_free": (c_int, [P]),
@@ -73,6 +76,11 @@ SIGNATURES = {
                                P, P, c_int64, P, P, ctypes.POINTER(c_uint64),
                                ctypes.POINTER(c_uint64), ctypes.POINTER(c_uint64),
                                ctypes.POINTER(c_int64), P, c_int64, P, c_int, P, P]),
+    "dice_ep_regroup": (c_int, [P, P, P, c_int, c_int64, c_int, c_int, P, P, P, P, P, P, P]),
+    "dice_ep_expert_ffn": (c_int, [P, c_int64, P, c_int64, c_int, c_int, c_int, c_int, c_int, P,
+                                   P, P, P, P, ctypes.POINTER(c_uint64),
+                                   ctypes.POINTER(c_uint64), ctypes.POINTER(c_uint64),
+                                   ctypes.POINTER(c_int64), P, c_int64, P, c_int, P, P]),
 }
 
 _lock = threading.Lock()
@@ -124,11 +132,13 @@ KERNELS_PER_CALL = {"dice_route_permute": 3, "dice_gate_route_state_words": 0,
                     "dice_device_alloc": 0, "dice_device_free": 0, "dice_ipc_get_handle": 0,
                     "dice_ipc_open": 0, "dice_ipc_close": 0, "dice_stream_wait_eq": 0,
                     "dice_stream_write": 0, "dice_version": 0,
+                    "dice_similarity_partial_words": 0, "dice_step_similarity": 2,
                     # count + scatter + send
                     "dice_ep_dispatch": 3,
                     # receive ids + count + scatter + gather + GEMM1 + GEMM2 (the
                     # combine's peer stores ride in the GEMM2 epilogue)
-                    "dice_ep_expert": 6}
+                    "dice_ep_expert": 6,
+                    "dice_ep_regroup": 4, "dice_ep_expert_ffn": 2}
 launch_count = [0]
 
 

@@ -204,40 +204,49 @@ int dice_ep_dispatch(const int32_t* ids, const float* gates, const uint8_t* acti
   return cudaGetLastError() == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
 }
 
-// Receive side of one layer: group the rows every source rank stored in this
-// rank's window by local expert (256-row padded tiles), run the grouped
-// expert FFN, and let the expert GEMM2's epilogue store each output row into
-// its home rank's pair rows (with gate and expert id) over peer memory.
+// Receive side of one layer, part 1 (the exchange's regroup): group the rows
+// every source rank stored in this rank's window by local expert (256-row
+// padded tiles of x_perm, row_pair = window entry of each row, -1 on padding).
 // rx_rows [D*cap, hp], rx_meta [D*cap] (int4), rx_count [D] are this rank's
 // window for the layer.
-int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
-                   int64_t cap, int El, int hp, int ep, int k, const uint16_t* w1_t,
-                   const uint16_t* w2_t, int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets,
-                   int32_t* scratch, uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf,
-                   int32_t* row_pair, const uint64_t* home_rows, const uint64_t* home_gates,
-                   const uint64_t* home_ids, const int64_t* home_n, const uint16_t* A2,
-                   int64_t M2, const uint16_t* B2, int N2, uint16_t* out2, void* stream) {
-  if (D < 1 || D > kMaxRanks || hp % 64 != 0 || ep % 64 != 0 || El < 1 || k < 1 ||
-      row_pair == nullptr)
+int dice_ep_regroup(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
+                    int64_t cap, int El, int hp, int32_t* ids_rx, int32_t* pos_rx,
+                    int32_t* tile_offsets, int32_t* scratch, uint16_t* x_perm, int32_t* row_pair,
+                    void* stream) {
+  if (D < 1 || D > kMaxRanks || hp % 64 != 0 || El < 1 || row_pair == nullptr)
     return DICE_ERR_CONTRACT;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t total = (int64_t)D * cap;
   ep_rx_ids_kernel<<<(int)((total + 255) / 256 < 2368 ? (total + 255) / 256 : 2368), 256, 0, s>>>(
       static_cast<const int4*>(rx_meta), rx_count, D, cap, ids_rx);
-  int rc = permute_launch(ids_rx, nullptr, total, 1, El, 1, 256, El, rx_rows, hp, x_perm, pos_rx,
-                          tile_offsets, nullptr, 1, 0, total, scratch, s, row_pair);
-  if (rc) return rc;
-  // GEMM1 (+ the rank's shared GEMM1 in the same launch), then GEMM2 whose
-  // epilogue stores every finished row into its home rank's pair rows
-  rc = dice_expert_gemm1_with_dense(x_perm, max_rows, 0, w1_t, El, hp, ep, tile_offsets, hbuf,
-                                    A2, A2 != nullptr ? M2 : 0, B2, N2, out2, stream);
+  return permute_launch(ids_rx, nullptr, total, 1, El, 1, 256, El, rx_rows, hp, x_perm, pos_rx,
+                        tile_offsets, nullptr, 1, 0, total, scratch, s, row_pair);
+}
+
+// Part 2: the grouped expert FFN on the regrouped rows; GEMM1 (+ the rank's
+// shared GEMM1 in the same launch when A2 != NULL), then GEMM2 whose
+// epilogue stores every finished row into its home rank's pair rows (with
+// gate and expert id from the window metadata) over peer memory.
+int dice_ep_expert_ffn(const uint16_t* x_perm, int64_t max_rows, const void* rx_meta,
+                       int64_t cap, int D, int El, int hp, int ep, int k, const uint16_t* w1_t,
+                       const uint16_t* w2_t, const int32_t* tile_offsets, uint16_t* hbuf,
+                       const int32_t* row_pair, const uint64_t* home_rows,
+                       const uint64_t* home_gates, const uint64_t* home_ids,
+                       const int64_t* home_n, const uint16_t* A2, int64_t M2, const uint16_t* B2,
+                       int N2, uint16_t* out2, void* stream) {
+  if (D < 1 || D > kMaxRanks || hp % 64 != 0 || ep % 64 != 0 || El < 1 || k < 1 ||
+      row_pair == nullptr)
+    return DICE_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = dice_expert_gemm1_with_dense(x_perm, max_rows, 0, w1_t, El, hp, ep, tile_offsets, hbuf,
+                                        A2, A2 != nullptr ? M2 : 0, B2, N2, out2, stream);
   if (rc) return rc;
   GemmProblem q{};
   q.A = hbuf; q.A_rows = max_rows; q.B = w2_t; q.M = (int)max_rows; q.N = hp; q.K = ep;
   q.num_groups = El; q.group_tile_offsets = tile_offsets; q.max_m_tiles = (int)(max_rows / 256);
   q.epi_kind = EPI_STORE_SCATTER;
   q.epi.ld_bf16 = hp;
-  q.epi.row_pair = row_pair;
+  q.epi.row_pair = const_cast<int32_t*>(row_pair);
   q.epi.top_k = k;
   q.epi.scatter_meta = rx_meta;
   q.epi.scatter_cap = cap;
@@ -248,6 +257,23 @@ int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* 
     q.epi.scatter_n[r] = home_n[r];
   }
   return gemm_bf16(q, s);
+}
+
+// Both parts (regroup, then the FFN with the fused combine stores).
+int dice_ep_expert(const uint16_t* rx_rows, const void* rx_meta, const int32_t* rx_count, int D,
+                   int64_t cap, int El, int hp, int ep, int k, const uint16_t* w1_t,
+                   const uint16_t* w2_t, int32_t* ids_rx, int32_t* pos_rx, int32_t* tile_offsets,
+                   int32_t* scratch, uint16_t* x_perm, int64_t max_rows, uint16_t* hbuf,
+                   int32_t* row_pair, const uint64_t* home_rows, const uint64_t* home_gates,
+                   const uint64_t* home_ids, const int64_t* home_n, const uint16_t* A2,
+                   int64_t M2, const uint16_t* B2, int N2, uint16_t* out2, void* stream) {
+  if (ep % 64 != 0 || k < 1) return DICE_ERR_CONTRACT;
+  int rc = dice_ep_regroup(rx_rows, rx_meta, rx_count, D, cap, El, hp, ids_rx, pos_rx,
+                           tile_offsets, scratch, x_perm, row_pair, stream);
+  if (rc) return rc;
+  return dice_ep_expert_ffn(x_perm, max_rows, rx_meta, cap, D, El, hp, ep, k, w1_t, w2_t,
+                            tile_offsets, hbuf, row_pair, home_rows, home_gates, home_ids, home_n,
+                            A2, M2, B2, N2, out2, stream);
 }
 
 }  // extern "C"

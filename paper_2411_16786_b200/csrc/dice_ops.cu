@@ -261,12 +261,15 @@ __device__ __forceinline__ unsigned long long lb_pack(unsigned gen, unsigned sta
                                                       unsigned value) {
   return ((unsigned long long)gen << 32) | ((unsigned long long)status << 30) | value;
 }
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// The look-back words are self-contained (generation, status, count in one
+// 64-bit word; no other data is published through them), so relaxed
+// gpu-scope accesses suffice: no acquire (which would invalidate L1) is needed.
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -494,31 +497,54 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
   }
   __syncthreads();
   const bool last_block = blockIdx.x == gridDim.x - 1;
-  if (threadIdx.x < E) {
-    const int e = threadIdx.x;
-    unsigned acc = 0;
+  {
+    // warp w owns expert w: the block's count of the expert (exclusive prefix
+    // over the 8 warps back into s_wcnt), published at once as an aggregate;
+    // then a decoupled look-back whose 32 lanes read 32 predecessors per
+    // round (one L2 round trip finds the nearest inclusive prefix)
+    const int e = warp;
+    const int c = lane < 8 ? s_wcnt[lane][e] : 0;
+    int inc = c;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) { const int c = s_wcnt[w][e]; s_wcnt[w][e] = (int)acc; acc += c; }
-    // decoupled look-back over the earlier blocks' published counts
+    for (int off = 1; off < 8; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += y;
+    }
+    const unsigned acc = (unsigned)__shfl_sync(0xffffffffu, inc, 7);
+    if (lane < 8) s_wcnt[lane][e] = inc - c;
     const unsigned gen = *reinterpret_cast<volatile unsigned*>(&r.epoch[0]);
     unsigned long long* mine = r.lookback + (int64_t)blockIdx.x * 8 + e;
     unsigned excl = 0;
     if (blockIdx.x == 0) {
-      st_release_u64(mine, lb_pack(gen, 2, acc));
+      if (lane == 0) st_relaxed_u64(mine, lb_pack(gen, 2, acc));
     } else {
-      st_release_u64(mine, lb_pack(gen, 1, acc));
-      for (int64_t j = (int64_t)blockIdx.x - 1; j >= 0;) {
-        const unsigned long long v = ld_acquire_u64(r.lookback + j * 8 + e);
-        const unsigned st = (unsigned)(v >> 30) & 3u;
-        if ((unsigned)(v >> 32) != gen || st == 0) { __nanosleep(20); continue; }
-        excl += (unsigned)(v & 0x3FFFFFFFu);
-        if (st == 2) break;
-        --j;
+      if (lane == 0) st_relaxed_u64(mine, lb_pack(gen, 1, acc));
+      for (int64_t top = (int64_t)blockIdx.x - 1;;) {
+        const int64_t j = top - lane;
+        unsigned st = 2, val = 0;          // before block 0: an inclusive zero
+        if (j >= 0) {
+          const unsigned long long v = ld_relaxed_u64(r.lookback + j * 8 + e);
+          st = (unsigned)(v >> 32) == gen ? (unsigned)(v >> 30) & 3u : 0u;
+          val = (unsigned)(v & 0x3FFFFFFFu);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, st == 2);
+        const unsigned pend = __ballot_sync(0xffffffffu, st == 0);
+        const int stop = incl ? __ffs(incl) - 1 : 31;      // nearest inclusive lane
+        const unsigned upto = stop == 31 ? 0xffffffffu : (2u << stop) - 1u;
+        if (pend & upto) { __nanosleep(32); continue; }     // a needed aggregate is missing
+        unsigned part = lane <= stop ? val : 0u;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        excl += part;
+        if (incl) break;
+        top -= 32;
       }
-      st_release_u64(mine, lb_pack(gen, 2, excl + acc));
+      if (lane == 0) st_relaxed_u64(mine, lb_pack(gen, 2, excl + acc));
     }
-    s_base[e] = (int)(e * r.cap) + (int)excl;
-    s_tot[e] = (int)(excl + acc);
+    if (lane == 0) {
+      s_base[e] = (int)(e * r.cap) + (int)excl;
+      s_tot[e] = (int)(excl + acc);
+    }
   }
   __syncthreads();
   if (t0 < n && slot < k && row_ok) {
@@ -1091,6 +1117,90 @@ __global__ void pack_rows_kernel(const float* __restrict__ in, int64_t n, int co
 }
 
 
+// ------------------------------------------------------- step similarity
+// Adjacent-step drift of one layer's MoE input and its routing
+// (step_similarity / _cosine, model.py:308-346): fp64 sums dot(a, b), |a|^2,
+// |b|^2 over the first `cols` columns of n rows, and the number of rows whose
+// top-1 expert agrees (top_a[t * top_stride] vs ids_b[t * k]). Deterministic:
+// a fixed grid of kSimBlocks blocks, each thread owning a fixed set of
+// elements, fixed-order tree reductions, then one block summing the block
+// partials in block order. roll != 0 also stores b into a and b's top-1 into
+// top_a (the runner's previous-step buffers), after reading them.
+constexpr int kSimBlocks = 296;
+constexpr int kSimThreads = 256;
+
+__device__ __forceinline__ void sim_block_sum(double (&v)[4], double* s_red /*[4][8]*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v[j] += __shfl_down_sync(0xffffffffu, v[j], off);
+    if (lane == 0) s_red[j * 8 + warp] = v[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double acc = 0.0;
+    for (int w = 0; w < kSimThreads / 32; ++w) acc += s_red[threadIdx.x * 8 + w];
+    v[threadIdx.x] = acc;    // thread j holds sum j
+  }
+}
+
+__global__ void __launch_bounds__(kSimThreads) similarity_partial_kernel(
+    float* a, const float* b, int64_t n, int cols, int64_t lda, int64_t ldb, int32_t* top_a,
+    int64_t top_stride, const int32_t* __restrict__ ids_b, int k, int roll, double* part) {
+  __shared__ double s_red[4 * 8];
+  pdl_enter();
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool vec = (cols % 4 == 0) && (lda % 4 == 0) && (ldb % 4 == 0);
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    float* ar = a + t * lda;
+    const float* br = b + t * ldb;
+    if (vec) {
+      for (int c = threadIdx.x * 4; c < cols; c += kSimThreads * 4) {
+        const float4 x = *reinterpret_cast<const float4*>(ar + c);
+        const float4 y = *reinterpret_cast<const float4*>(br + c);
+        v[0] = fma((double)x.x, (double)y.x, v[0]); v[1] = fma((double)x.x, (double)x.x, v[1]);
+        v[2] = fma((double)y.x, (double)y.x, v[2]);
+        v[0] = fma((double)x.y, (double)y.y, v[0]); v[1] = fma((double)x.y, (double)x.y, v[1]);
+        v[2] = fma((double)y.y, (double)y.y, v[2]);
+        v[0] = fma((double)x.z, (double)y.z, v[0]); v[1] = fma((double)x.z, (double)x.z, v[1]);
+        v[2] = fma((double)y.z, (double)y.z, v[2]);
+        v[0] = fma((double)x.w, (double)y.w, v[0]); v[1] = fma((double)x.w, (double)x.w, v[1]);
+        v[2] = fma((double)y.w, (double)y.w, v[2]);
+        if (roll) *reinterpret_cast<float4*>(ar + c) = y;
+      }
+    } else {
+      for (int c = threadIdx.x; c < cols; c += kSimThreads) {
+        const double x = ar[c], y = br[c];
+        v[0] = fma(x, y, v[0]); v[1] = fma(x, x, v[1]); v[2] = fma(y, y, v[2]);
+        if (roll) ar[c] = br[c];
+      }
+    }
+    if (threadIdx.x == 0) {
+      const int32_t tb = ids_b[t * k];
+      v[3] += top_a[t * top_stride] == tb ? 1.0 : 0.0;
+      if (roll) top_a[t * top_stride] = tb;
+    }
+  }
+  sim_block_sum(v, s_red);
+  if (threadIdx.x < 4) part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = v[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kSimThreads) similarity_final_kernel(const double* part,
+                                                                       int parts, double* out) {
+  __shared__ double s_red[4 * 8];
+  pdl_enter();
+  double v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < parts; i += kSimThreads) acc += part[(int64_t)j * parts + i];
+    v[j] = acc;
+  }
+  sim_block_sum(v, s_red);
+  if (threadIdx.x < 4) out[threadIdx.x] = v[threadIdx.x];
+}
+
 static int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;
@@ -1517,6 +1627,26 @@ int dice_pack_rows(const float* in, int64_t n, int cols, int64_t ld_in, int hp, 
   if (n == 0) return DICE_OK;
   pack_rows_kernel<<<grid_for(n * hp, 256), 256, 0, (cudaStream_t)stream>>>(
       in, n, cols, ld_in, hp, out32, reinterpret_cast<__nv_bfloat16*>(out16));
+  return launch_ok();
+}
+
+int64_t dice_similarity_partial_words(void) { return 4 * (int64_t)kSimBlocks; }
+
+int dice_step_similarity(float* prev, const float* cur, int64_t n, int cols, int64_t ld_prev,
+                         int64_t ld_cur, int32_t* prev_top, int64_t top_stride,
+                         const int32_t* cur_ids, int k, int roll, double* partials, double* out,
+                         void* stream) {
+  if (n < 0 || cols < 0 || k < 1 || cols > ld_prev || cols > ld_cur) return DICE_ERR_CONTRACT;
+  if (out == nullptr || partials == nullptr) return DICE_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0)
+    return cudaMemsetAsync(out, 0, 4 * sizeof(double), s) == cudaSuccess ? DICE_OK : DICE_ERR_CUDA;
+  if (prev == nullptr || cur == nullptr || prev_top == nullptr || cur_ids == nullptr)
+    return DICE_ERR_CONTRACT;
+  launch_pdl(similarity_partial_kernel, dim3(kSimBlocks), dim3(kSimThreads), 0, s, prev, cur, n,
+             cols, ld_prev, ld_cur, prev_top, top_stride, cur_ids, k, roll, partials);
+  launch_pdl(similarity_final_kernel, dim3(1), dim3(kSimThreads), 0, s,
+             (const double*)partials, kSimBlocks, out);
   return launch_ok();
 }
 

@@ -318,6 +318,8 @@ class EPRunner:
         self.graph = None
         self._wait_events = []
         self._event_pool = []
+        self._comm_events = []
+        self._comm_pool = []
         self._expert_events = []
         self._expert_pool = []
         self.launches_per_run = 0
@@ -328,6 +330,24 @@ class EPRunner:
 
     def _peers(self):
         return range(self.world)
+
+    def _comm_begin(self):
+        """Graph-safe event before an exchange kernel (dispatch send / regroup):
+        on this single-stream rank they sit on the critical path, so their
+        time counts as exposed all-to-all time next to the flag waits."""
+        if not self.time_waits:
+            return None
+        i = len(self._comm_events)
+        if i >= len(self._comm_pool):
+            self._comm_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
+        a, b = self._comm_pool[i]
+        a.record()
+        return a, b
+
+    def _comm_end(self, evs):
+        if evs is not None:
+            evs[1].record()
+            self._comm_events.append(evs)
 
     def _timed_wait(self, addrs, value):
         if self.time_waits:
@@ -360,6 +380,7 @@ class EPRunner:
         self.peak_buffer_bytes = 0
         self.records, self.dispatch_log, self.combine_log = [], [], []
         self._wait_events = []
+        self._comm_events = []
         self._expert_events = []
 
     def _track(self, layer, kind="c"):
@@ -402,12 +423,14 @@ class EPRunner:
         rx_rows = _u64_array([g.rx_rows(d, layer, me) for d in self._peers()])
         rx_meta = _u64_array([g.rx_meta(d, layer, me) for d in self._peers()])
         rx_cnt = _u64_array([g.rx_count(d, layer, me) for d in self._peers()])
+        evs = self._comm_begin()
         _lib.call("dice_ep_dispatch", p.ids.data_ptr(), p.gates.data_ptr(),
                   None if act is None else act.data_ptr(),
                   self.n, self.k, self.E, D, me, self.u16.data_ptr(), self.hp,
                   self.pos_dest.data_ptr(), self.dest_off.data_ptr(),
                   self.counters[step, layer].data_ptr(), self.r0, self.cfg.total_rows,
                   self.scratch.data_ptr(), rx_rows, rx_meta, rx_cnt, ops._stream())
+        self._comm_end(evs)
         g.data("write", [("rx", d, layer, me) for d in self._peers()])
         g.write([g.flag("rx_ready", d, layer, me) for d in self._peers()], 1)
         p.layer, p.gen = layer, step
@@ -434,18 +457,23 @@ class EPRunner:
         gates = _u64_array([g.cx_gates(h, layer) for h in homes])
         ids = _u64_array([g.cx_ids(h, layer) for h in homes])
         hn = (ctypes.c_int64 * len(self.shard_n))(*self.shard_n)
+        evs = self._comm_begin()
+        _lib.call("dice_ep_regroup", g.rx_rows(me, layer, 0), g.rx_meta(me, layer, 0),
+                  g.rx_count(me, layer, 0), self.world, self.cap, self.El, self.hp,
+                  self.ids_rx.data_ptr(), self.pos_rx.data_ptr(), self.tiles.data_ptr(),
+                  self.scratch.data_ptr(), self.x_perm.data_ptr(), self.row_pair_rx.data_ptr(),
+                  ops._stream())
+        self._comm_end(evs)
         if self.time_experts:
             i = len(self._expert_events)
             if i >= len(self._expert_pool):
                 self._expert_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
             e0, e1 = self._expert_pool[i]
             e0.record()
-        _lib.call("dice_ep_expert", g.rx_rows(me, layer, 0), g.rx_meta(me, layer, 0),
-                  g.rx_count(me, layer, 0), self.world, self.cap, self.El, self.hp, self.ep,
-                  self.k, lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.ids_rx.data_ptr(),
-                  self.pos_rx.data_ptr(), self.tiles.data_ptr(), self.scratch.data_ptr(),
-                  self.x_perm.data_ptr(), self.max_rows, self.hbuf.data_ptr(),
-                  self.row_pair_rx.data_ptr(), rows, gates, ids, hn,
+        _lib.call("dice_ep_expert_ffn", self.x_perm.data_ptr(), self.max_rows,
+                  g.rx_meta(me, layer, 0), self.cap, self.world, self.El, self.hp, self.ep,
+                  self.k, lw.w1_t.data_ptr(), lw.w2_t.data_ptr(), self.tiles.data_ptr(),
+                  self.hbuf.data_ptr(), self.row_pair_rx.data_ptr(), rows, gates, ids, hn,
                   *self._shared_args(shared_layer), ops._stream())
         if self.time_experts:
             e1.record()
@@ -681,8 +709,12 @@ class EPRunner:
         per_step_total = [cfg.num_layers * cfg.total_rows * self.k] * cfg.num_steps
         timeline = None
         if self._wait_events:
-            timeline = {"exposed_comm_seconds":
-                        sum(a.elapsed_ms(b) for a, b in self._wait_events) * 1e-3}
+            waits = sum(a.elapsed_ms(b) for a, b in self._wait_events) * 1e-3
+            kernels = sum(a.elapsed_ms(b) for a, b in self._comm_events) * 1e-3
+            # single stream: the flag waits AND the exchange kernels (dispatch
+            # count / scatter / send, receive-side regroup) are on the critical path
+            timeline = {"exposed_comm_seconds": waits + kernels, "comm_wait_seconds": waits,
+                        "comm_kernel_seconds": kernels}
         return RunResult(
             final=ActivationBlock(values=self.x32[:, :cfg.hidden_dim].clone(),
                                   generated_step=cfg.num_steps),

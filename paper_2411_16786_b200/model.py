@@ -401,32 +401,57 @@ class StepSimilarity:
     mean_agreement: float
 
 
-def _cosine(a: torch.Tensor, b: torch.Tensor) -> float:
-    a = a.reshape(-1).double()
-    b = b.reshape(-1).double()
-    na, nb = torch.linalg.vector_norm(a).item(), torch.linalg.vector_norm(b).item()
-    if na == 0.0 or nb == 0.0:
-        return 1.0 if na == nb else 0.0
-    return float(torch.dot(a, b).item() / (na * nb))
-
-
-def step_similarity(inputs: list, routes: list) -> StepSimilarity:
-    """Adjacent-step cosine of each layer's MoE input and top-1 routing
-    agreement (model.py:323-346). inputs[s][l]: [rows, h]; routes[s][l]: RouteDecision."""
-    steps = len(inputs)
-    if steps < 2:
-        raise ContractError("step_similarity needs at least two recorded steps")
-    layers = len(inputs[0])
+def similarity_from_sums(sums, rows: int) -> StepSimilarity:
+    """StepSimilarity from the device sums f64 [layers, steps-1, 4] =
+    {a.b, |a|^2, |b|^2, top-1 agreements} of each adjacent step pair
+    (_cosine and the agreement mean, model.py:316-346)."""
+    sums = np.asarray(sums, dtype=np.float64)
+    layers, pairs = sums.shape[:2]
     cos = np.zeros(layers)
     agree = np.zeros(layers)
     for layer in range(layers):
         c_vals, a_vals = [], []
-        for s in range(steps - 1):
-            c_vals.append(_cosine(torch.as_tensor(inputs[s][layer]), torch.as_tensor(inputs[s + 1][layer])))
-            t0 = torch.as_tensor(routes[s][layer].expert_ids)[:, 0]
-            t1 = torch.as_tensor(routes[s + 1][layer].expert_ids)[:, 0].to(t0.device)
-            a_vals.append(float((t0 == t1).double().mean().item()))
+        for s in range(pairs):
+            dot, aa, bb, same = sums[layer, s]
+            na, nb = float(np.sqrt(aa)), float(np.sqrt(bb))
+            if na == 0.0 or nb == 0.0:
+                c_vals.append(1.0 if na == nb else 0.0)
+            else:
+                c_vals.append(float(dot / (na * nb)))
+            a_vals.append(float(same) / rows)
         cos[layer] = np.mean(c_vals)
         agree[layer] = np.mean(a_vals)
     return StepSimilarity(per_layer_cosine=cos, per_layer_agreement=agree,
                           mean_cosine=float(np.mean(cos)), mean_agreement=float(np.mean(agree)))
+
+
+def step_similarity(inputs: list, routes: list) -> StepSimilarity:
+    """Adjacent-step cosine of each layer's MoE input and top-1 routing
+    agreement (model.py:323-346), reduced on the device
+    (dice_step_similarity: fp64 sums in a fixed order, one D2H read).
+    inputs[s][l]: [rows, h]; routes[s][l]: RouteDecision."""
+    steps = len(inputs)
+    if steps < 2:
+        raise ContractError("step_similarity needs at least two recorded steps")
+    layers = len(inputs[0])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rows = int(torch.as_tensor(inputs[0][0]).shape[0])
+    sums = torch.empty(layers, steps - 1, 4, dtype=torch.float64, device=dev)
+    part = torch.empty(ops.similarity_partial_words(), dtype=torch.float64, device=dev)
+
+    def f32(v):
+        return torch.as_tensor(v).to(device=dev, dtype=torch.float32).contiguous()
+
+    def i32(r):
+        return torch.as_tensor(r.expert_ids).to(device=dev, dtype=torch.int32).contiguous()
+
+    for layer in range(layers):
+        a, ia = f32(inputs[0][layer]), i32(routes[0][layer])
+        for s in range(steps - 1):
+            b, ib = f32(inputs[s + 1][layer]), i32(routes[s + 1][layer])
+            if tuple(b.shape) != tuple(a.shape):
+                raise ContractError(f"step_similarity: input shapes {tuple(a.shape)} vs "
+                                    f"{tuple(b.shape)}")
+            ops.step_similarity(a, b, a.shape[1], ia, ib, sums[layer, s], part)
+            a, ia = b, ib
+    return similarity_from_sums(sums.cpu().numpy(), rows)

@@ -274,3 +274,25 @@ def pack_rows(src, hp, out32=None, out16=None):
     _need(src, torch.float32, "pack_rows src")
     _lib.call("dice_pack_rows", _ptr(src), n, cols, src.stride(0), hp, _ptr(out32), _ptr(out16),
               _stream())
+
+
+def similarity_partial_words():
+    return int(_lib.load().dice_similarity_partial_words())
+
+
+def step_similarity(prev, cur, cols, prev_top, cur_ids, out, partials, roll=False):
+    """out f64 [4] = {a.b, |a|^2, |b|^2, #rows with equal top-1} of prev / cur
+    (first ``cols`` columns); roll: then prev <- cur, prev_top <- cur's top-1.
+    prev_top: int32 [n] or the [n, k] ids of prev (its column 0 is read)."""
+    n = cur.shape[0]
+    _need(cur, torch.float32, "step_similarity cur")
+    _need(cur_ids, torch.int32, "step_similarity ids")
+    _need(out, torch.float64, "step_similarity out")
+    if prev.dtype != torch.float32 or prev.stride(1) != 1 or cur.stride(1) != 1:
+        raise ContractError("step_similarity: f32 row-major inputs expected")
+    if prev_top.dtype != torch.int32:
+        raise ContractError("step_similarity: int32 top-1 ids expected")
+    top_stride = prev_top.stride(0)
+    _lib.call("dice_step_similarity", _ptr(prev), _ptr(cur), n, int(cols), prev.stride(0),
+              cur.stride(0), _ptr(prev_top), top_stride, _ptr(cur_ids), cur_ids.shape[1],
+              int(bool(roll)), _ptr(partials), _ptr(out), _stream())

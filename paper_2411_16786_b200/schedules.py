@@ -33,7 +33,7 @@ import torch
 from . import ops
 from .cluster import ClusterConfig, build_placement
 from .errors import ContractError, NumericalDivergenceError
-from .model import ActivationBlock, RouteDecision, ToyModel, model_hash
+from .model import ActivationBlock, RouteDecision, ToyModel, model_hash, similarity_from_sums
 from .policies import (CondStrategy, PolicyConfig, TokenCache, is_sync_step,
                        select_sync_layers)
 
@@ -81,6 +81,7 @@ class RunResult:
     step_inputs: list | None = None
     step_routes: list | None = None
     gpu_seconds: float | None = None
+    similarity: object = None     # StepSimilarity of the run (track_similarity)
 
     @property
     def total_comm_bytes(self) -> int:
@@ -151,8 +152,13 @@ class DeviceRunner:
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *,
                  record_inputs: bool = False, record_routes: bool = False,
                  time_experts: bool = False, overlap: bool = False, timeline: bool = False,
-                 time_ops: bool = False, record_filter=None, record_outputs: bool = False):
-        """record_inputs / record_routes: per (step, layer) MoE inputs u and
+                 time_ops: bool = False, record_filter=None, record_outputs: bool = False,
+                 track_similarity: bool = False):
+        """track_similarity: accumulate step_similarity's sums on the device
+        during the run (each layer's previous-step MoE input and top-1 ids kept
+        in HBM, one fused compare-and-roll launch pair per stage; no host
+        copies) -> ``RunResult.similarity``.
+        record_inputs / record_routes: per (step, layer) MoE inputs u and
         routes (+ the conditional-communication masks in ``step_masks``), as
         run_sampling(record_*=True); ``record_filter(step, layer)`` limits the
         recorded inputs (others are None), ``record_outputs`` also records the
@@ -222,6 +228,15 @@ class DeviceRunner:
             self.pair_gates = torch.zeros(nslots, n, k, dtype=f32, device=dev)
             self.pair_ids = None
         self.scratch = torch.zeros(ops.permute_scratch_ints(n, k, E), dtype=torch.int32, device=dev)
+        self.track_similarity = track_similarity
+        if track_similarity:
+            self.sim_prev = torch.zeros(L, n, hp, dtype=f32, device=dev)
+            self.sim_top = torch.zeros(L, n, dtype=torch.int32, device=dev)
+            self.sim_sums = torch.zeros(L, max(cfg.num_steps - 1, 1), 4, dtype=torch.float64,
+                                        device=dev)
+            self.sim_sink = torch.zeros(4, dtype=torch.float64, device=dev)
+            self.sim_part = torch.empty(ops.similarity_partial_words(), dtype=torch.float64,
+                                        device=dev)
         self.route_state = (torch.zeros(ops.route_state_words(n), dtype=torch.int64, device=dev)
                             if self.fused_route else None)
         self.counters = torch.zeros(cfg.num_steps, L, 2, dtype=torch.int64, device=dev)
@@ -504,6 +519,12 @@ class DeviceRunner:
                     ops.gate_topk(self.u32, lw.w_gate_t, self.k, p.ids, p.gates, self.scores,
                                   self.status, step, layer, decide=dec)
             decided = dec is not None
+            if self.track_similarity:
+                with self._op("step_similarity", step, layer):
+                    ops.step_similarity(self.sim_prev[layer], self.u32, cfg.hidden_dim,
+                                        self.sim_top[layer], p.ids,
+                                        self.sim_sums[layer, step - 1] if step > 0
+                                        else self.sim_sink, self.sim_part, roll=True)
             keep = self.record_filter(step, layer)
             if self.record_inputs:
                 inputs_here.append(self.u32[:, :cfg.hidden_dim].cpu() if keep else None)
@@ -697,7 +718,9 @@ class DeviceRunner:
             per_step_active_pairs=per_step_active, per_step_total_pairs=per_step_total,
             step_inputs=self.step_inputs if self.record_inputs else None,
             step_routes=self.step_routes if self.record_routes else None,
-            gpu_seconds=gpu_seconds)
+            gpu_seconds=gpu_seconds,
+            similarity=(similarity_from_sums(self.sim_sums.cpu().numpy(), self.n)
+                        if self.track_similarity and cfg.num_steps > 1 else None))
 
     def run(self) -> RunResult:
         self.launch()
@@ -706,8 +729,12 @@ class DeviceRunner:
 
 def run_sampling(model: ToyModel, x0: ActivationBlock, strategy: Strategy,
                  policies: PolicyConfig, cluster: ClusterConfig, seed: int, *,
-                 record_inputs: bool = False, record_routes: bool = False) -> RunResult:
-    """Execute a full sampling run on the GPU (schedules.py:493-501)."""
+                 record_inputs: bool = False, record_routes: bool = False,
+                 track_similarity: bool = False) -> RunResult:
+    """Execute a full sampling run on the GPU (schedules.py:493-501).
+    track_similarity: step_similarity of the run's own MoE inputs and routes,
+    reduced on the device as it runs (RunResult.similarity)."""
     runner = DeviceRunner(model, x0, strategy, policies, cluster, seed,
-                          record_inputs=record_inputs, record_routes=record_routes)
+                          record_inputs=record_inputs, record_routes=record_routes,
+                          track_similarity=track_similarity)
     return runner.run()

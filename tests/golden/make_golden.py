@@ -322,10 +322,38 @@ def g_width():
         json.dump(meta, f, indent=1)
 
 
+def similarity():
+    """step_similarity (model.py:308-346) of the reference's own recorded MoE
+    inputs and routes: config 1 (S/2-8E2A widths, D=2; synchronous and full
+    DICE) and the reference's xl-toy preset (synchronous, D=4, the acceptance
+    criterion 9 trajectory, test_acceptance.py:282-293)."""
+    out, meta = {}, {}
+    c1 = ds.ModelConfig(num_layers=12, num_experts=8, num_shared=2, top_k=2, hidden_dim=384,
+                        expert_dim=1536, num_tokens=256, batch=4, num_steps=10, step_size=2e-4)
+    xl = ds.preset("xl-toy")
+    cases = [("c1_sync", c1, ds.Strategy.SYNCHRONOUS, ds.NEUTRAL, 2),
+             ("c1_dice", c1, ds.Strategy.INTERWEAVED, ds.dice_policy(), 2),
+             ("xltoy_sync", xl, ds.Strategy.SYNCHRONOUS, ds.NEUTRAL, 4)]
+    for name, cfg, strategy, pol, dev in cases:
+        model = ds.init_model(cfg, seed=0)
+        res = ds.run_sampling(model, ds.sample_x0(cfg, seed=0), strategy, pol,
+                              ds.ClusterConfig(num_devices=dev), 0, record_inputs=True,
+                              record_routes=True)
+        sim = dm.step_similarity(res.step_inputs, res.step_routes)
+        out[name + "_cosine"] = sim.per_layer_cosine
+        out[name + "_agreement"] = sim.per_layer_agreement
+        meta[name] = dict(config=cfg_dict(cfg), strategy=strategy.value, policy=pol_dict(pol),
+                          devices=dev, mean_cosine=sim.mean_cosine,
+                          mean_agreement=sim.mean_agreement)
+    np.savez_compressed(os.path.join(HERE, "similarity.npz"), **out)
+    with open(os.path.join(HERE, "similarity.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kat", "init", "gate", "cache", "runs", "placement", "config1",
-                             "xl_width", "g_width"]
-    fns = dict(kat=kat, init=init_and_layers, gate=gate_cases, cache=cache_sequences,
+                             "xl_width", "g_width", "similarity"]
+    fns = dict(similarity=similarity, kat=kat, init=init_and_layers, gate=gate_cases, cache=cache_sequences,
                runs=small_runs, placement=placement_bytes, config1=config1, xl_width=xl_width,
                g_width=g_width)
     for w in which:

@@ -200,3 +200,21 @@ def test_xl_width_runs_match_reference():
         assert (r.active_pairs, r.total_pairs) == (m["active_pairs"], m["total_pairs"])
         assert (r.dispatch_bytes, r.combine_bytes) == (m["dispatch_bytes"], m["combine_bytes"])
         assert r.peak_buffer_bytes == m["peak_buffer_bytes"]
+
+
+def test_step_similarity_matches_reference():
+    """f3: the oracle's step_similarity (model.py:316-346) on its own recorded
+    xl-toy synchronous trajectory reproduces the reference's per-layer cosines
+    and top-1 agreements (tests/golden/similarity.*, make_golden.similarity)."""
+    meta = json.load(open(os.path.join(G, "similarity.json")))["xltoy_sync"]
+    gold = load("similarity.npz")
+    c = meta["config"]
+    g = O.Geometry(**{k: c[k] for k in ("num_layers", "num_experts", "num_shared", "top_k",
+                                        "hidden_dim", "expert_dim", "num_tokens", "batch",
+                                        "num_steps", "step_size")})
+    res = O.run_schedule(g, O.init_params(g, 0), O.initial_latent(g, 0), O.SYNC, O.Policy(),
+                         meta["devices"], 0, record=True)
+    cos, agree = O.step_similarity(res.inputs, res.routes)
+    assert np.allclose(cos, gold["xltoy_sync_cosine"], rtol=0, atol=1e-13)
+    assert np.array_equal(agree, gold["xltoy_sync_agreement"])
+    assert abs(float(np.mean(cos)) - meta["mean_cosine"]) < 1e-13

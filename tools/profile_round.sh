@@ -8,8 +8,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start o
     --log-file $OUT/launches_steps6-7.csv python tools/profile_step.py > $OUT/launch.log 2>&1
 python tools/summarize_launches.py $OUT/launches_steps6-7.csv > $OUT/launch_summary.txt
 i=0
-for k in "256, .int.1, .bool.1" "192, .int.4, .bool.0" "192, .int.5, .bool.1, .int.2" "192, .int.3" \
-         "gate4_topk" "permute_scatter" "permute_gather"; do
+for k in "gemm_bf16_pair<.int.256, .int.1," "gemm_bf16_pair<.int.192, .int.4," \
+         "gemm_bf16_pair<.int.192, .int.5," "gemm_bf16_pair<.int.192, .int.3," "gate4_topk"; do
   i=$((i+1))
   timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
       --kernel-name-base demangled -k "regex:$k" -s 1 -c 1 -o $OUT/k$i python tools/profile_kernels.py \
