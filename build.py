@@ -25,13 +25,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT) -> str:
+    """defines / out: an experiment build (-D switches) written elsewhere
+    (loaded by the probes through DICE_LIB_PATH); the product build has none."""
+    if out == OUT and not defines and not force and not _stale():
         return OUT
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(os.path.dirname(out), src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -39,17 +41,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, OUT)
+    os.replace(tmp, out)
     for o in objs:
         os.remove(o)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--variant NAME -DSWITCH ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        d = os.path.join(ROOT, "build", "variants", name)
+        os.makedirs(d, exist_ok=True)
+        print(build(defines=[a[2:] for a in args if a.startswith("-D")],
+                    out=os.path.join(d, "_dice_b200.so")))
+    else:
+        print(build(force="--force" in args, verbose="-v" in args))

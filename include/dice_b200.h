@@ -134,14 +134,17 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
  * the tokens' rows, rounded to bf16 from the fp32 u (the bits the local GEMM
  * stores as its bf16 output), to their permuted rows. Expert e owns rows
  * [e*cap, (e+1)*cap) of x_perm (bf16 [E*cap, hp], cap >= n, a multiple of
- * 256); within an expert, rows follow pair order t*k+s (per-block offsets from
- * a decoupled look-back over the blocks' counts). Outputs pos int32 [n, k]
+ * 256); a block's rows of expert e follow pair order t*k+s and start at the
+ * offset one atomic add on the expert's row counter returned, so the order of
+ * the blocks within a region varies between launches (no value does: every
+ * expert-FFN output row depends on its own row only). Outputs pos int32 [n, k]
  * (-1 inactive), row_pair int32 [E*cap] (pair of each row, -1 on the padding
  * rows up to each expert's 256-row tile end), tile_offsets int32 [E+1] (256-row
  * tile prefix, for dice_expert_gemm1_with_dense(group_stride = cap)) and adds
  * dice_route_permute's counters. route_state: uint64
  * [dice_gate_route_state_words(n)], zero-filled once, then owned by these
- * launches (look-back words and a launch generation). */
+ * launches (a finished-block ticket and the per-expert row counters, reset by
+ * the last block of every launch). */
 int64_t dice_gate_route_state_words(int64_t n);
 int dice_gate_route(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
                     int32_t* ids, float* gates, float* scores, int32_t* status, int step,

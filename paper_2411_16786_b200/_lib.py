@@ -14,6 +14,8 @@ from .errors import (ConfigurationError, ContractError, NativeLibraryError, Nume
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_dice_b200.so")
+# experiment builds (tools/*_probe.py): another build of the same library
+LIB_PATH = os.environ.get("DICE_LIB_PATH", LIB_PATH)
 
 c_void_p, c_int, c_int64, c_uint64, c_double, c_float = (
     ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,

@@ -160,7 +160,7 @@ class _FakeOps:
 
     @staticmethod
     def route_state_words(n):
-        return (n + 31) // 32 * 8 + 1
+        return 5
 
 
 def _cpu_model(cfg):

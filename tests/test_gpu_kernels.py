@@ -8,6 +8,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import dice_oracle as O  # noqa: E402
 from paper_2411_16786_b200 import ops  # noqa: E402
+import paper_2411_16786_b200 as D  # noqa: E402
 
 dev = "cuda"
 
@@ -279,13 +280,16 @@ def test_gemm_rejects_internal_epilogue_kinds():
 
 @pytest.mark.parametrize("n,k,devices,decide", [(8192, 2, 2, True), (1000, 2, 1, False),
                                                 (777, 1, 4, True), (300, 4, 8, False),
-                                                (37, 3, 1, True)])
+                                                (37, 3, 1, True), (20000, 2, 1, True)])
 def test_gate_route_matches_gate_then_permute(n, k, devices, decide):
     """dice_gate_route (gate + decide + permute in one launch, expert regions of
     cap rows) == dice_gate_topk(_decide) + dice_route_permute: ids, gates, masks,
-    run counters and tile offsets identical; every active pair sits at the same
-    offset within its expert (pair order), with the same bf16 row; padding rows
-    map to no pair. Repeated launches (the look-back generation) agree."""
+    run counters and tile offsets identical; every expert region holds exactly
+    the expert's active pairs (blocks take their offsets in arrival order, in
+    pair order within a block), each row the pair's bf16 row, row_pair the
+    inverse of pos, padding rows map to no pair. Repeated launches (counters
+    reset by the last block) agree; 20000 rows = 625 blocks, more than one
+    resident wave."""
     E, hp = 8, 256
     g = torch.Generator(device=dev).manual_seed(n + k)
     u = torch.randn(n, hp, device=dev, generator=g)
@@ -337,13 +341,24 @@ def test_gate_route_matches_gate_then_permute(n, k, devices, decide):
         idn = b[0].cpu().numpy()
         assert np.array_equal(pa < 0, pb < 0)
         v = pb >= 0
-        assert np.array_equal(pa[v] - idn[v] * cap, pb[v] - tiles[idn[v]] * 256)
+        # the region of expert e holds rows [e*cap, e*cap + count_e): a permutation
+        off = pa[v] - idn[v] * cap
+        counts = np.bincount(idn[v], minlength=E)
+        assert (off >= 0).all() and (off < counts[idn[v]]).all()
+        for e in range(E):
+            oe = np.sort(off[idn[v] == e])
+            assert np.array_equal(oe, np.arange(counts[e]))
+            assert tiles[e + 1] - tiles[e] == (counts[e] + 255) // 256
         assert torch.equal(a[7][torch.as_tensor(pa[v], device=dev).long()],
                            b[7][torch.as_tensor(pb[v], device=dev).long()])
         rpa = a[8].cpu().numpy()
         pair_idx = np.nonzero(v.reshape(-1))[0]
         assert np.array_equal(rpa[pa.reshape(-1)[pair_idx]], pair_idx)
+        for e in range(E):   # padding up to the region's last 256-row tile
+            pad = rpa[e * cap + counts[e]: e * cap + (counts[e] + 255) // 256 * 256]
+            assert (pad == -1).all()
         for e in range(E):
             cnt_e = int(((idn == e) & v).sum())
             pad_end = (tiles[e + 1] - tiles[e]) * 256
             assert (rpa[e * cap + cnt_e:e * cap + pad_end] == -1).all()
+

@@ -530,8 +530,9 @@ def test_g_width_run_vs_reference():
 @pytest.mark.parametrize("strategy,devices", [("interweaved", 2), ("displaced", 4),
                                               ("synchronous", 1)])
 def test_gate_route_engine_bit_identical(strategy, devices):
-    """The permute fused into the gate launch (capacity regions, look-back
-    offsets) reproduces the separate permute kernels bit for bit: latents,
+    """The permute fused into the gate launch (capacity regions, block offsets
+    from atomic row counters) reproduces the separate permute kernels bit for
+    bit, and two runs of it agree bit for bit: latents,
     bytes (remote-pair counters under D simulated devices) and pairs."""
     cfg = D.ModelConfig(num_layers=4, num_experts=8, num_shared=2, top_k=2, hidden_dim=256,
                         expert_dim=512, num_tokens=200, batch=3, num_steps=6, step_size=1e-3)
@@ -539,13 +540,14 @@ def test_gate_route_engine_bit_identical(strategy, devices):
     x0 = D.sample_x0(cfg, 13)
     pol = D.dice_policy(refresh_interval=2, warmup=1, period=3)
     out = {}
-    for g in ("1", "0"):
+    for g in ("1", "0", "1b"):
         r = D.DeviceRunner(model, x0, D.Strategy(strategy), pol,
                            D.ClusterConfig(num_devices=devices), 13)
         assert r.fused_route
-        r.fused_route = g == "1"
+        r.fused_route = g != "0"
         res = r.run()
         out[g] = (res.final.values.cpu(), res.dispatch_bytes, res.combine_bytes,
                   res.active_pairs, res.per_step_active_pairs)
-    assert torch.equal(out["1"][0], out["0"][0])
-    assert out["1"][1:] == out["0"][1:]
+    for g in ("0", "1b"):
+        assert torch.equal(out["1"][0], out[g][0])
+        assert out["1"][1:] == out[g][1:]

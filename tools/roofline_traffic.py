@@ -21,10 +21,11 @@ import bench  # noqa: E402
 
 OUT = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "traffic")
 os.makedirs(OUT, exist_ok=True)
-REGEX = r"regex:gemm_bf16_pair<\(int\)(256, \(int\)1|192, \(int\)5),"
+REGEX = "regex:gemm_bf16_pair"
+COUNT = 12          # the first GEMM launches of the step: several grouped-FFN pairs
 rep = os.path.join(OUT, "ffn_pair")
 cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on",
-       "--profile-from-start", "off", "--kernel-name-base", "demangled", "-k", REGEX, "-c", "2",
+       "--profile-from-start", "off", "--kernel-name-base", "demangled", "-k", REGEX, "-c", str(COUNT),
        "-f", "-o", rep, sys.executable, os.path.join(ROOT, "tools", "profile_kernels.py")]
 subprocess.run(cmd, check=True, cwd=ROOT)
 raw = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "raw", "--csv"], check=True,
@@ -42,7 +43,7 @@ def col(name, r):
 def scale(name):
     u = units[hdr.index(name)]
     return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-            "usecond": 1e-6, "msecond": 1e-3}.get(u, 1)
+            "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}[u]
 
 
 kernels = []
@@ -54,12 +55,28 @@ for r in data:
                     "dram_write_bytes": wr, "duration_s": t,
                     "tensor_pipe_pct": col("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", r)
                     if "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed" in hdr else None})
-assert len(kernels) == 2, kernels
-total = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in kernels)
+import re  # noqa: E402
+
+
+def shape(name):
+    m = re.search(r"gemm_bf16_pair<(\d+), (\d+),", name)
+    return (int(m.group(1)), int(m.group(2))) if m else None
+
+
+# grouped-FFN pairs: the expert GEMM1 (256-wide tiles, GELU) directly followed by
+# the expert GEMM2 with the pair-row epilogue (EPI_STORE_PAIR = 5)
+pairs = [(a, b) for a, b in zip(kernels, kernels[1:])
+         if shape(a["kernel"]) == (256, 1) and shape(b["kernel"]) == (192, 5)]
+assert pairs, [k["kernel"] for k in kernels]
+per_pair = [a["dram_read_bytes"] + a["dram_write_bytes"] + b["dram_read_bytes"]
+            + b["dram_write_bytes"] for a, b in pairs]
+total = sum(per_pair) / len(per_pair)
 res = {"config": "xl256", "csrc_sha": bench.csrc_digest(),
        "traffic_bytes_per_launch_pair": total,
-       "capture": ("ncu --set full --clock-control none (cold caches), first grouped-FFN launch "
-                   "pair of step 7 of the bench workload (tools/profile_kernels.py)"),
+       "capture": (f"ncu --set full --clock-control none (cold caches): the first {COUNT} GEMM "
+                   f"launches of step 7 of the bench workload (tools/profile_kernels.py); mean "
+                   f"DRAM bytes over its {len(pairs)} grouped-FFN launch pairs"),
+       "per_pair_bytes": per_pair,
        "kernels": kernels}
 # gpurun brings back gpurun_out/ only: copy OUT/roofline_traffic.json to profiles/
 with open(os.path.join(OUT, "roofline_traffic.json"), "w") as f:
