@@ -476,14 +476,15 @@ def run_gpu(args):
     expert_events = list(runner._expert_events)
     res = runner.finish()
     cnt = runner.counters.cpu().numpy()
-    exposed_ms = wait_ms = kern_ms = 0.0
+    exposed_ms = wait_ms = kern_ms = join_ms = 0.0
     if world > 1:
         tl = res.timeline or {}
         # max over ranks of (flag waits + exchange kernels) on the rank's stream
         ex = allreduce([tl.get("exposed_comm_seconds", 0.0) * 1e3,
                         tl.get("comm_wait_seconds", 0.0) * 1e3,
-                        tl.get("comm_kernel_seconds", 0.0) * 1e3], dist.ReduceOp.MAX)
-        exposed_ms, wait_ms, kern_ms = (float(v) for v in ex)
+                        tl.get("comm_kernel_seconds", 0.0) * 1e3,
+                        tl.get("comm_join_seconds", 0.0) * 1e3], dist.ReduceOp.MAX)
+        exposed_ms, wait_ms, kern_ms, join_ms = (float(v) for v in ex)
         cnt = allreduce(cnt, dist.ReduceOp.SUM).numpy()
     if world > 1:
         ms = float(allreduce([ms], dist.ReduceOp.MAX).item())
@@ -594,9 +595,10 @@ def run_gpu(args):
                    "l2": "inputs larger than L2: the bf16 weights are streamed every denoising step"},
         "moe_layer_us": ms_per_step * 1e3 / (cfg.num_steps * cfg.num_layers),
         "exposed_a2a_us": exposed_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
-        "a2a_parts_us": {"flag_waits": wait_ms * 1e3 / (cfg.num_steps * cfg.num_layers),
-                         "send_and_regroup_kernels": kern_ms * 1e3 / (cfg.num_steps
-                                                                      * cfg.num_layers)},
+        "a2a_parts_us": {k_: v * 1e3 / (cfg.num_steps * cfg.num_layers) for k_, v in (
+            ("flag_waits", wait_ms),
+            ("main_stream_send_and_regroup_kernels", kern_ms),
+            ("waits_for_overlapped_sends", join_ms))},
         # the reference's logical buffer accounting (R*h*2 per occupied slot,
         # schedules.py:185) next to the physical bytes this rank's run holds
         "buffers": {"logical_peak_bytes": peak_logical, "device_bytes": device_bytes},

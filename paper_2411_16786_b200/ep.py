@@ -188,16 +188,22 @@ class EPGroup:
 
     # stream memops ---------------------------------------------------------
     trace = None   # optional list: the protocol simulation test records every op
+    stream = "main"   # the rank's stream the next ops are issued on (trace tag)
+
+    def stream_op(self, kind, stream, event_id):
+        """Record an event record / wait between the rank's two streams (test tracing)."""
+        if self.trace is not None:
+            self.trace.append((kind, stream, event_id, stream))
 
     def wait(self, addrs, value):
         if self.trace is not None:
-            self.trace.append(("wait", [int(a) for a in addrs], value))
+            self.trace.append(("wait", [int(a) for a in addrs], value, self.stream))
         arr = _u64_array(addrs)
         _lib.call("dice_stream_wait_eq", arr, len(addrs), value, ops._stream())
 
     def write(self, addrs, value):
         if self.trace is not None:
-            self.trace.append(("write", [int(a) for a in addrs], value))
+            self.trace.append(("write", [int(a) for a in addrs], value, self.stream))
         arr = _u64_array(addrs)
         _lib.call("dice_stream_write", arr, len(addrs), value, ops._stream())
 
@@ -205,7 +211,7 @@ class EPGroup:
         """Record a data access of a kernel (test tracing only); gen: the step
         whose combine a pair-row store writes / a consume expects."""
         if self.trace is not None:
-            self.trace.append((kind, regions, gen))
+            self.trace.append((kind, regions, gen, self.stream))
 
 
 class _EPPayload:
@@ -244,7 +250,14 @@ class EPRunner:
 
     def __init__(self, model: ToyModel, x0_shard: ActivationBlock, strategy: Strategy,
                  policy: PolicyConfig, cluster: ClusterConfig, seed: int, *, rank: int,
-                 world: int, pg=None, time_waits: bool = False, time_experts: bool = False):
+                 world: int, pg=None, time_waits: bool = False, time_experts: bool = False,
+                 overlap_dispatch: bool = True):
+        """overlap_dispatch: in asynchronous interweaved stages the dispatch
+        send (decide state ready -> group by destination -> P2P row stores ->
+        ready flags) runs on a second stream, overlapping the stage's expert
+        FFN and consume; the main stream joins it before the next local_block
+        GEMM overwrites the rows it reads (and the join's wait is counted as
+        exposed all-to-all time)."""
         cfg = model.config
         if cluster.num_devices != world:
             raise ConfigurationError(f"cluster.num_devices={cluster.num_devices} != world={world}")
@@ -268,6 +281,13 @@ class EPRunner:
         self.time_experts = time_experts
         dev = model.device
         self.dev = dev
+        self.cuda = str(dev).startswith("cuda")
+        self.overlap_dispatch = (overlap_dispatch and strategy is Strategy.INTERWEAVED
+                                 and world > 1)
+        self.comm = torch.cuda.Stream(device=dev) if self.overlap_dispatch and self.cuda else None
+        self._comm_pending = None       # event of the last send issued on the comm stream
+        self._uread = 0                 # sends issued (test tracing of the u16 reuse)
+        self._ev_id = 0
         k, E, S, hp, ep = cfg.top_k, cfg.num_experts, cfg.num_shared, model.hp, model.ep
         self.n, self.k, self.E, self.S, self.hp, self.ep = n, k, E, S, hp, ep
         self.shard_n = [shard_rows(cfg.total_rows, world, r)[1] - shard_rows(cfg.total_rows, world, r)[0]
@@ -299,8 +319,12 @@ class EPRunner:
         self.tiles = torch.empty(El + 1, dtype=torch.int32, device=dev)
         self.pos_dest = torch.empty(n, k, dtype=torch.int32, device=dev)
         self.dest_off = torch.empty(world + 1, dtype=torch.int32, device=dev)
-        sc = max(ops.permute_scratch_ints(n, k, world), ops.permute_scratch_ints(total, 1, El))
-        self.scratch = torch.zeros(sc, dtype=torch.int32, device=dev)
+        # the dispatch (possibly on the comm stream) and the receive-side regroup
+        # (main stream) each own their permute scratch
+        self.scratch = torch.zeros(ops.permute_scratch_ints(total, 1, El), dtype=torch.int32,
+                                   device=dev)
+        self.scratch_tx = torch.zeros(ops.permute_scratch_ints(n, k, world), dtype=torch.int32,
+                                      device=dev)
         self.hsh = torch.empty(n, max(S, 1) * ep, dtype=bf, device=dev)
         # displaced: the dispatch in the windows and the new one coexist per layer
         per_layer = 2 if strategy is Strategy.DISPLACED else 1
@@ -320,6 +344,8 @@ class EPRunner:
         self._event_pool = []
         self._comm_events = []
         self._comm_pool = []
+        self._join_events = []
+        self._pool_next = 0
         self._expert_events = []
         self._expert_pool = []
         self.launches_per_run = 0
@@ -331,13 +357,59 @@ class EPRunner:
     def _peers(self):
         return range(self.world)
 
+    # ---------------------------------------------------------- comm stream
+    def _send_overlapped(self, step, layer, p, decided):
+        """The asynchronous stage's dispatch on the comm stream, ordered after
+        the gate (main) by an event."""
+        g = self.grp
+        self._ev_id += 1
+        fork = self._ev_id
+        g.stream_op("record", "main", fork)
+        g.stream_op("wait_event", "comm", fork)
+        if self.cuda:
+            ev = torch.cuda.Event()
+            ev.record()
+            self.comm.wait_event(ev)
+        g.stream = "comm"
+        try:
+            if self.cuda:
+                with torch.cuda.stream(self.comm):
+                    self._send(step, layer, p, force=False, decided=decided, timed=False)
+                    done = torch.cuda.Event()
+                    done.record()
+            else:
+                self._send(step, layer, p, force=False, decided=decided, timed=False)
+                done = None
+        finally:
+            g.stream = "main"
+        self._ev_id += 1
+        g.stream_op("record", "comm", self._ev_id)
+        self._comm_pending = (done, self._ev_id)
+
+    def _join_comm(self):
+        """Main waits for the outstanding comm-stream send (its rows are read
+        from u16 / the payload, which the main stream is about to reuse)."""
+        if self._comm_pending is None:
+            return
+        done, eid = self._comm_pending
+        self._comm_pending = None
+        self.grp.stream_op("wait_event", "main", eid)
+        if not self.cuda:
+            return
+        evs = self._comm_begin()
+        torch.cuda.current_stream().wait_event(done)
+        if evs is not None:
+            evs[1].record()
+            self._join_events.append(evs)
+
     def _comm_begin(self):
         """Graph-safe event before an exchange kernel (dispatch send / regroup):
         on this single-stream rank they sit on the critical path, so their
         time counts as exposed all-to-all time next to the flag waits."""
         if not self.time_waits:
             return None
-        i = len(self._comm_events)
+        i = self._pool_next
+        self._pool_next += 1
         if i >= len(self._comm_pool):
             self._comm_pool.append((ops.DeviceEvent(), ops.DeviceEvent()))
         a, b = self._comm_pool[i]
@@ -381,7 +453,10 @@ class EPRunner:
         self.records, self.dispatch_log, self.combine_log = [], [], []
         self._wait_events = []
         self._comm_events = []
+        self._join_events = []
+        self._pool_next = 0
         self._expert_events = []
+        self._comm_pending = None
 
     def _track(self, layer, kind="c"):
         self.occupied.add((kind, layer))
@@ -406,7 +481,7 @@ class EPRunner:
         return pair[0]
 
     # ------------------------------------------------------------- exchange
-    def _send(self, step, layer, p: _EPPayload, force, decided=False):
+    def _send(self, step, layer, p: _EPPayload, force, decided=False, timed=True):
         """decide (unless the gate launch already took it) + dispatch all-to-all
         send of layer `layer`."""
         g, me, D = self.grp, self.rank, self.world
@@ -418,20 +493,23 @@ class EPRunner:
         else:
             act = None
         # my regions in every destination window must have been consumed
-        self._timed_wait([g.flag("rx_free", me, layer, d) for d in self._peers()], 1)
+        wait = self._timed_wait if timed else g.wait
+        wait([g.flag("rx_free", me, layer, d) for d in self._peers()], 1)
         g.write([g.flag("rx_free", me, layer, d) for d in self._peers()], 0)
         rx_rows = _u64_array([g.rx_rows(d, layer, me) for d in self._peers()])
         rx_meta = _u64_array([g.rx_meta(d, layer, me) for d in self._peers()])
         rx_cnt = _u64_array([g.rx_count(d, layer, me) for d in self._peers()])
-        evs = self._comm_begin()
+        evs = self._comm_begin() if timed else None
         _lib.call("dice_ep_dispatch", p.ids.data_ptr(), p.gates.data_ptr(),
                   None if act is None else act.data_ptr(),
                   self.n, self.k, self.E, D, me, self.u16.data_ptr(), self.hp,
                   self.pos_dest.data_ptr(), self.dest_off.data_ptr(),
                   self.counters[step, layer].data_ptr(), self.r0, self.cfg.total_rows,
-                  self.scratch.data_ptr(), rx_rows, rx_meta, rx_cnt, ops._stream())
+                  self.scratch_tx.data_ptr(), rx_rows, rx_meta, rx_cnt, ops._stream())
         self._comm_end(evs)
         g.data("write", [("rx", d, layer, me) for d in self._peers()])
+        self._uread += 1
+        g.data("uread", [], gen=self._uread)       # the send kernel read u16 / the payload
         g.write([g.flag("rx_ready", d, layer, me) for d in self._peers()], 1)
         p.layer, p.gen = layer, step
         self.dispatch_log.append((step, layer))
@@ -540,6 +618,8 @@ class EPRunner:
         for layer in range(cfg.num_layers):
             lw = self.model.layers[layer]
             hin32, hin16 = (self.x32, self.x16) if layer == 0 else (self.h32, self.h16)
+            self._join_comm()      # the previous stage's send read u16 / its payload
+            self.grp.data("uwrite", [], gen=self._uread)   # local_block overwrites u16
             ops.gemm(ops.EPI_GELU_RESID, hin16, lw.w_mix_t, out_f32=self.u32,
                      out_bf16=self.u16, residual=hin32)
             sync = self._stage_is_sync(step, layer)
@@ -587,7 +667,10 @@ class EPRunner:
                 self._track(layer, "d")
             else:
                 gen = self.slot_gen[layer]
-                self._send(step, layer, p, force=False, decided=decided)
+                if self.overlap_dispatch:
+                    self._send_overlapped(step, layer, p, decided)
+                else:
+                    self._send(step, layer, p, force=False, decided=decided)
                 prev, self.pending = self.pending, p
                 merged = self.merge_gemm1 and prev is not None
                 if prev is not None:
@@ -640,6 +723,7 @@ class EPRunner:
         self._reset_state(x0_device)
         for step in range(self.cfg.num_steps):
             self._run_step(step)
+        self._join_comm()
         self._drain()
         self.launches_per_run = _lib.launch_count[0] - c0
 
@@ -711,10 +795,13 @@ class EPRunner:
         if self._wait_events:
             waits = sum(a.elapsed_ms(b) for a, b in self._wait_events) * 1e-3
             kernels = sum(a.elapsed_ms(b) for a, b in self._comm_events) * 1e-3
-            # single stream: the flag waits AND the exchange kernels (dispatch
-            # count / scatter / send, receive-side regroup) are on the critical path
-            timeline = {"exposed_comm_seconds": waits + kernels, "comm_wait_seconds": waits,
-                        "comm_kernel_seconds": kernels}
+            joins = sum(a.elapsed_ms(b) for a, b in self._join_events) * 1e-3
+            # on the main stream: the flag waits, the exchange kernels issued on
+            # it (blocking stages' dispatch, every receive-side regroup) and the
+            # waits for the overlapped sends of the comm stream
+            timeline = {"exposed_comm_seconds": waits + kernels + joins,
+                        "comm_wait_seconds": waits, "comm_kernel_seconds": kernels,
+                        "comm_join_seconds": joins}
         return RunResult(
             final=ActivationBlock(values=self.x32[:, :cfg.hidden_dim].clone(),
                                   generated_step=cfg.num_steps),

@@ -61,3 +61,27 @@ def test_gpu_arm_line():
     q = line["quality"]
     assert q["dice_latent_mse_vs_sync"] >= 0 and q["speedup_dice_vs_sync"] > 0
     assert line["buffers"]["device_bytes"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_expert_parallel_line():
+    """--gpus 2 spawns its two ranks itself (on one GPU when only one is
+    visible): the line reports n_gpus 2, the exposed all-to-all time and its
+    parts (flag waits, main-stream exchange kernels, waits for the overlapped
+    comm-stream sends)."""
+    env = dict(os.environ)
+    import torch
+    if torch.cuda.device_count() < 2:
+        env["DICE_BENCH_SAME_DEVICE"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "tiny",
+                        "--gpus", "2", "--steps", "2", "--warmup", "3"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    parts = line["a2a_parts_us"]
+    assert set(parts) == {"flag_waits", "main_stream_send_and_regroup_kernels",
+                          "waits_for_overlapped_sends"}
+    assert line["exposed_a2a_us"] >= parts["main_stream_send_and_regroup_kernels"] > 0

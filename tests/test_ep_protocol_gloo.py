@@ -1,7 +1,9 @@
 """CPU, world_size 2 and 4 over gloo: the expert-parallel exchange protocol
 (EPRunner host control flow, IPC-handle rendezvous through torch.distributed,
 ready/free flag handshakes) is simulated under many random interleavings of
-the ranks' stream operations. Checks: no deadlock; every receive region is
+the ranks' stream operations (each rank's main stream and, for the
+interweaved schedule, its comm stream carrying the overlapped dispatch sends,
+joined only by event records / waits). Checks: no deadlock; every receive region is
 written exactly once before it is read and read before it is rewritten; every
 consume of a home's pair rows finds, from every expert rank, the combine of
 exactly the step it consumes (stored and signalled; never a newer one) — no
@@ -63,28 +65,41 @@ def initial_flags(logs):
 
 
 def simulate(logs, seed):
+    """Random interleaving of every (rank, stream) op queue: a rank's main
+    stream and its comm stream (overlapped dispatch sends) run concurrently,
+    ordered only by their event records / waits."""
     rng = random.Random(seed)
     flags = initial_flags(logs)
     init = dict(flags)
     full = set()            # receive regions holding unread data
     cx = {}                 # pair-row region -> (step of its combine, signalled)
-    pcs = [0] * len(logs)
-    traces = [lg["trace"] for lg in logs]
+    queues = {}
+    for r, lg in enumerate(logs):
+        for op in lg["trace"]:
+            queues.setdefault((r, op[3]), []).append(op)
+    pcs = {q: 0 for q in queues}
+    recorded = set()        # (rank, event id)
+    ureads = set()          # (rank, send number) whose u16 read has executed
     steps = 0
     while True:
         ready = []
-        for r, tr in enumerate(traces):
-            if pcs[r] >= len(tr):
+        for q, tr in queues.items():
+            if pcs[q] >= len(tr):
                 continue
-            op = tr[pcs[r]]
+            op = tr[pcs[q]]
             if op[0] == "wait" and not all(flags[a] == op[2] for a in op[1]):
                 continue
-            ready.append(r)
+            if op[0] == "wait_event" and (q[0], op[2]) not in recorded:
+                continue
+            ready.append(q)
         if not ready:
             break
-        r = rng.choice(ready)
-        op = traces[r][pcs[r]]
-        if op[0] == "write":                      # flag write (stream memop)
+        q = rng.choice(ready)
+        r = q[0]
+        op = queues[q][pcs[q]]
+        if op[0] == "record":
+            recorded.add((r, op[2]))
+        elif op[0] == "write":                    # flag write (stream memop)
             for a in op[1]:
                 assert a in flags, hex(a)
                 flags[a] = op[2]
@@ -103,13 +118,18 @@ def simulate(logs, seed):
             for reg in map(tuple, op[1]):
                 assert reg in cx and not cx[reg][1], f"rank {r}: {reg} arrives without a store"
                 cx[reg] = (cx[reg][0], True)
+        elif op[0] == "uread":                    # a send kernel read u16 / its payload
+            ureads.add((r, op[2]))
+        elif op[0] == "uwrite":                   # local_block overwrites u16
+            assert op[2] == 0 or (r, op[2]) in ureads, \
+                f"rank {r}: u16 overwritten before send {op[2]} read it"
         elif op[0] == "consume":                  # home reads its pair rows
             for reg in map(tuple, op[1]):
                 got = cx.get(reg)
                 assert got == (op[2], True), f"rank {r} consumes {reg}: has {got}, wants step {op[2]}"
-        pcs[r] += 1
+        pcs[q] += 1
         steps += 1
-    done = all(pcs[r] >= len(t) for r, t in enumerate(traces))
+    done = all(pcs[q] >= len(t) for q, t in queues.items())
     assert done, f"deadlock: pcs={pcs}"
     assert not full, f"unread regions at the end: {sorted(full)[:4]}"
     assert all(arrived for _, arrived in cx.values())
@@ -132,7 +152,7 @@ def test_exchange_protocol_random_interleavings(world, strategy, policy):
         fixed = []
         for op in lg["trace"]:
             if op[0] == "write" and op[1] and not isinstance(op[1][0], int):
-                fixed.append(("kwrite", op[1], op[2]))
+                fixed.append(("kwrite", op[1], op[2], op[3]))
             else:
                 fixed.append(op)
         lg["trace"] = fixed
@@ -145,6 +165,8 @@ def test_exchange_protocol_random_interleavings(world, strategy, policy):
            "deep": O.Policy(sync_strategy=O.SYNC_DEEP)}[policy]
     ref = O.run_schedule(g, O.init_params(g, 3), O.initial_latent(g, 3), strategy, pol, world, 3)
     assert recs[0] == [tuple(t) for t in ref.staleness]
+    if strategy == "interweaved":   # the overlapped dispatch really uses the comm stream
+        assert any(op[3] == "comm" for lg in logs for op in lg["trace"])
     for seed in range(40):
         simulate(logs, seed)
 
