@@ -20,7 +20,8 @@ teacher-forced on the GPU's own recorded values (SURVEY.md §8c protocol):
   schedules.py:372-397, policies.py:188-208), recomputed in fp64 from the
   GPU's u / ids, within rel-L2 <= 5e-3 and max |err| <= 1e-2 * max |ref|
   (measured: ~1e-3 both)
-  (bf16 GEMM operands, fp32 accumulation and residual).
+  (bf16 GEMM operands, fp32 accumulation and residual); at the G widths the
+  fp64 recomputation covers the first 1024 rows (rows are independent).
 """
 import numpy as np
 import pytest
@@ -42,9 +43,19 @@ def _tie_band(scores, k):
     return np.min(top[:, :-1] - top[:, 1:], axis=1) < TAU
 
 
-@pytest.fixture(scope="module")
-def bench_run():
-    cfg = D.preset("xl2-8e2a", batch=32, num_steps=9)
+GEOMETRIES = {   # name -> (preset, overrides): 8192 rows each
+    "xl256": ("xl2-8e2a", dict(batch=32, num_tokens=256)),
+    "xl512": ("xl2-8e2a", dict(batch=8, num_tokens=1024)),
+    "g512": ("g-16e2a", dict(batch=8, num_tokens=1024)),
+}
+CHECK_ROWS = {"xl256": None, "xl512": None, "g512": 1024}
+
+
+@pytest.fixture(scope="module", params=sorted(GEOMETRIES))
+def bench_run(request):
+    name = request.param
+    preset, over = GEOMETRIES[name]
+    cfg = D.preset(preset, num_steps=9, **over)
     assert cfg.total_rows == 8192
     model = D.init_model(cfg, seed=0)
     x0 = D.sample_x0(cfg, 1000)
@@ -54,12 +65,14 @@ def bench_run():
                        record_routes=True, record_outputs=True,
                        record_filter=lambda s, l: (s, l) in keep)
     res = r.run()
-    g = O.Geometry(**{**O.PRESETS["xl2-8e2a"], "batch": 32, "num_steps": 9})
-    return cfg, g, r, res, keep
+    g = O.Geometry(**{**O.PRESETS[preset], **over, "num_steps": 9})
+    yield cfg, g, r, res, keep, CHECK_ROWS[name]
+    del r, model
+    torch.cuda.empty_cache()
 
 
 def test_teacher_forced_routing_bit_exact_at_bench_geometry(bench_run):
-    cfg, g, r, res, keep = bench_run
+    cfg, g, r, res, keep, _ = bench_run
     excluded = 0
     for (s, l) in sorted(keep):
         u = res.step_inputs[s][l].numpy().astype(np.float64)
@@ -77,7 +90,7 @@ def test_teacher_forced_routing_bit_exact_at_bench_geometry(bench_run):
 
 
 def test_cond_masks_exact_at_bench_geometry(bench_run):
-    cfg, g, r, res, keep = bench_run
+    cfg, g, r, res, keep, _ = bench_run
     pol = O.dice_defaults()
     cache = O.CadenceCache(cfg.num_layers, cfg.total_rows, cfg.top_k, 1)
     sync_set = O.sync_layer_set(pol.sync_strategy, cfg.num_layers)
@@ -91,9 +104,12 @@ def test_cond_masks_exact_at_bench_geometry(bench_run):
             assert np.array_equal(gact, act) and np.array_equal(gwr, wr), (s, l)
             checked += 1
             async_stages += not force
-    assert checked == cfg.num_steps * cfg.num_layers and async_stages == 2 * 14
-    # the run's pair counters agree with the replayed masks
-    assert res.per_step_active_pairs[7] == 14 * 8192 * 2 + 14 * 8192
+    n_deep = len(sync_set)
+    n_shallow = cfg.num_layers - n_deep
+    assert checked == cfg.num_steps * cfg.num_layers and async_stages == 2 * n_shallow
+    # the run's pair counters agree with the replayed masks (step 7: deep layers
+    # move both slots, shallow layers only slot 0 behind the LowScore cadence)
+    assert res.per_step_active_pairs[7] == n_deep * 8192 * 2 + n_shallow * 8192
 
 
 def _oracle_layer(g, l):
@@ -109,37 +125,42 @@ def _check(h_gpu, h_ref, what):
 
 
 def test_teacher_forced_sync_stage_outputs_at_bench_geometry(bench_run):
-    cfg, g, r, res, keep = bench_run
+    cfg, g, r, res, keep, nrow = bench_run
+    sl = slice(0, nrow)
     for (s, l) in ((0, 0), (8, L_DEEP)):
         p = _oracle_layer(g, l)
-        u = res.step_inputs[s][l].numpy().astype(np.float64)
-        route = O.forced_route(u, p.w_gate, res.step_routes[s][l].expert_ids.numpy())
+        u = res.step_inputs[s][l].numpy().astype(np.float64)[sl]
+        route = O.forced_route(u, p.w_gate, res.step_routes[s][l].expert_ids.numpy()[sl])
         rows = O.expert_rows(p, u, route)
         h_ref = u + O.weighted_combine(rows, O.shared_sum(p, u), route.gates)
-        _check(r.step_outputs[s][l].numpy().astype(np.float64), h_ref, f"sync stage ({s},{l})")
+        _check(r.step_outputs[s][l].numpy().astype(np.float64)[sl], h_ref,
+               f"sync stage ({s},{l})")
 
 
 def test_teacher_forced_stale_cached_stage_at_bench_geometry(bench_run):
     """Stage (8, L_ASYNC) consumes dispatch (7, L_ASYNC): slot 0 fresh at step 7,
     slot 1 cached from the forced refresh at step 6 (LowScore, R=5), each with
     the gate stored with its row; plus the shared experts on u(8)."""
-    cfg, g, r, res, keep = bench_run
+    cfg, g, r, res, keep, nrow = bench_run
+    sl = slice(0, nrow)
     l = L_ASYNC
     assert [(x.layer, x.used_step, x.generated_step) for x in res.staleness_records
             if x.layer == l and x.used_step == 8] == [(l, 8, 7)]
     p = _oracle_layer(g, l)
     pol = O.dice_defaults()
-    cache = O.CadenceCache(1, cfg.total_rows, cfg.top_k, cfg.hidden_dim)
+    n = cfg.total_rows if nrow is None else nrow
+    cache = O.CadenceCache(1, n, cfg.top_k, cfg.hidden_dim)
     rows = gates = None
     for s, force in ((6, True), (7, False)):
-        u = res.step_inputs[s][l].numpy().astype(np.float64)
-        route = O.forced_route(u, p.w_gate, res.step_routes[s][l].expert_ids.numpy())
+        u = res.step_inputs[s][l].numpy().astype(np.float64)[sl]
+        route = O.forced_route(u, p.w_gate, res.step_routes[s][l].expert_ids.numpy()[sl])
         act, wr = cache.decide(0, s, route.ids, pol, force)
         fresh = O.expert_rows(p, u, route, act)
         rows, gates = cache.assemble(0, fresh, route, act, wr)
-    u8 = res.step_inputs[8][l].numpy().astype(np.float64)
+    u8 = res.step_inputs[8][l].numpy().astype(np.float64)[sl]
     h_ref = u8 + O.weighted_combine(rows, O.shared_sum(p, u8), gates)
-    _check(r.step_outputs[8][l].numpy().astype(np.float64), h_ref, "stale cached stage (8, 3)")
+    _check(r.step_outputs[8][l].numpy().astype(np.float64)[sl], h_ref,
+           "stale cached stage (8, 3)")
 
 
 # ------------------------------------------------------------- divergence
