@@ -199,95 +199,6 @@ __device__ __forceinline__ void epilogue_gelu_resid_pf(const GemmArgs& a, const 
   }
 }
 
-// f32-output epilogues (GELU_RESID, CONSUME, STORE_F32) straight from TMEM
-// with the 16x256b load shape: four adjacent threads hold 8 consecutive
-// columns of a row, so every residual / pair-row load and every f32 store of
-// a warp instruction covers whole 32-byte sectors of 8 rows, with no shared
-// memory transpose (the smem goes to the operand ring). A warp's 32 TMEM lanes
-// are read as two 16-lane halves; the chunk's global loads are issued before
-// its TMEM loads so their latencies overlap.
-template <int EPI>
-__device__ __forceinline__ void epilogue_f32_row16(const GemmArgs& a, uint32_t taddr, int lane,
-                                                   int64_t row0, int row_limit, int col0) {
-  const int q = lane & 3, rr = lane >> 2;
-  constexpr int KF = 2;
-#pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    float2 res[2][4];
-    uint32_t prw[KF][2][4];
-    float pg[KF][2];
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int64_t row = row0 + hh * 16 + half * 8 + rr;
-      if (row >= row_limit) continue;
-      if constexpr (EPI == EPI_GELU_RESID || EPI == EPI_CONSUME) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          res[half][j] = __ldg(reinterpret_cast<const float2*>(a.residual + row * a.ld_res +
-                                                               col0 + 8 * j + 2 * q));
-      }
-      if constexpr (EPI == EPI_CONSUME) {
-#pragma unroll
-        for (int s = 0; s < KF; ++s) {
-          if (s < a.top_k) {
-            pg[s][half] = __ldg(a.pair_gates + row * a.top_k + s);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              prw[s][half][j] = __ldg(reinterpret_cast<const uint32_t*>(
-                  a.pair_rows + ((int64_t)s * a.n_tokens + row) * a.N + col0 + 8 * j + 2 * q));
-          }
-        }
-      }
-    }
-    uint32_t v[16];
-    tmem_ld_16x256b_x4(taddr + ((uint32_t)(hh * 16) << 16), v);
-    tmem_ld_wait();
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int64_t row = row0 + hh * 16 + half * 8 + rr;
-      if (row >= row_limit) continue;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = col0 + 8 * j + 2 * q;
-        float2 x = make_float2(__uint_as_float(v[4 * j + 2 * half]),
-                               __uint_as_float(v[4 * j + 2 * half + 1]));
-        if constexpr (EPI == EPI_GELU_RESID) {
-          x = gelu_erf2(x);
-          x.x += res[half][j].x;
-          x.y += res[half][j].y;
-        }
-        if constexpr (EPI == EPI_CONSUME) {
-          // (shared + g_0 row_0) + g_1 row_1 ..., each product and sum rounded,
-          // then the residual (combine_outputs model.py:295-297, _consume
-          // schedules.py:317)
-#pragma unroll
-          for (int s = 0; s < KF; ++s) {
-            if (s < a.top_k) {
-              const uint32_t w = prw[s][half][j];
-              x.x = __fadd_rn(x.x, __fmul_rn(pg[s][half], __uint_as_float(w << 16)));
-              x.y = __fadd_rn(x.y, __fmul_rn(pg[s][half], __uint_as_float(w & 0xFFFF0000u)));
-            }
-          }
-          for (int s = KF; s < a.top_k; ++s) {
-            const float g = __ldg(a.pair_gates + row * a.top_k + s);
-            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(
-                a.pair_rows + ((int64_t)s * a.n_tokens + row) * a.N + col));
-            x.x = __fadd_rn(x.x, __fmul_rn(g, __uint_as_float(w << 16)));
-            x.y = __fadd_rn(x.y, __fmul_rn(g, __uint_as_float(w & 0xFFFF0000u)));
-          }
-          x.x = __fadd_rn(res[half][j].x, x.x);
-          x.y = __fadd_rn(res[half][j].y, x.y);
-        }
-        if (a.out_f32 != nullptr) *reinterpret_cast<float2*>(a.out_f32 + row * a.ld_f32 + col) = x;
-        if (a.out_bf16 != nullptr) {
-          __nv_bfloat162 b = __floats2bfloat162_rn(x.x, x.y);
-          *reinterpret_cast<__nv_bfloat162*>(a.out_bf16 + row * a.ld_bf16 + col) = b;
-        }
-      }
-    }
-  }
-}
-
 // --------------------------------------------------------- CTA-pair kernel
 // cta_group::2: a cluster of two CTAs computes a 256 x BN tile. Each CTA
 // stages its own 128 rows of A and half (BN/2 rows) of B, so per-CTA operand
@@ -368,8 +279,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   // args2.num_m_tiles > 0: a second, dense problem with the same K and epilogue
   // kind runs in the same persistent launch; its tiles follow the first's
   // (one launch and one wave tail for two independent GEMMs)
-  constexpr bool kF32Epi = EPI == EPI_GELU_RESID || EPI == EPI_CONSUME || EPI == EPI_STORE_F32;
-  constexpr bool kResidPF = EPI == EPI_GELU_RESID && !DIRECT;
+  constexpr bool kResidPF = EPI == EPI_GELU_RESID;
   using C = PairCfg<BN, DIRECT, NSUB, kResidPF>;
   constexpr int TN = C::kTN;
   const int kStages = args.stages;   // <= C::kStages (host-clamped)
@@ -527,12 +437,6 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int ci = grp; ci < TN / 32; ci += kEpiGroups) {
         const int col_in_tile = ci * 32;
         const int col0 = n_blk * TN + col_in_tile;
-        if constexpr (DIRECT && kF32Epi) {
-          if (col0 >= ar.N) continue;  // warp-uniform
-          epilogue_f32_row16<EPI>(ar, tmem_base + ((uint32_t)(sub * 32) << 16) + acc * TN +
-                                          col_in_tile, lane, row0, rl, col0);
-          continue;
-        }
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * TN + col_in_tile, r);
         tmem_ld_wait();
@@ -651,7 +555,7 @@ template <int BN, int EPI, bool DIRECT, int NSUB = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
                 const CUtensorMap* tb2 = nullptr, const GemmArgs* a2 = nullptr) {
-  using C = PairCfg<BN, DIRECT, NSUB, EPI == EPI_GELU_RESID && !DIRECT>;
+  using C = PairCfg<BN, DIRECT, NSUB, EPI == EPI_GELU_RESID>;
   static bool attr_done = false;
   if (!attr_done) {
     if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -686,13 +590,6 @@ int dispatch_wide(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
   }
 }
 
-// f32-output epilogues from TMEM with the 16x256b shape (no smem staging)
-#ifdef DICE_XP_F32_STAGED
-constexpr bool kF32Row16 = false;
-#else
-constexpr bool kF32Row16 = true;
-#endif
-
 template <int BN>
 int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                   int max_tiles, cudaStream_t s) {
@@ -701,9 +598,9 @@ int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
     case EPI_GELU_BF16: return launch_pair<BN, EPI_GELU_BF16, true>(ta, tb, a, max_tiles, s);
     case EPI_STORE_PAIR: return launch_pair<BN, EPI_STORE_PAIR, true>(ta, tb, a, max_tiles, s);
     case EPI_STORE_SCATTER: return launch_pair<BN, EPI_STORE_SCATTER, true>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, kF32Row16>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, kF32Row16>(ta, tb, a, max_tiles, s);
-    case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, kF32Row16>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false>(ta, tb, a, max_tiles, s);
+    case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false>(ta, tb, a, max_tiles, s);
     default: return DICE_ERR_CONTRACT;
   }
 }

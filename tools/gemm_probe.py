@@ -18,8 +18,12 @@ def bench(M, N, K, epi, reps=20, label=""):
     o16 = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
     o32 = torch.empty(M, N, device=dev) if epi in (2, 3, 4) else None
     res = torch.randn(M, N, device=dev) if epi in (3, 4) else None
-    add = torch.randn(M, N, device=dev) if epi == 4 else None
-    run = lambda: ops.gemm(epi, A, B, out_f32=o32, out_bf16=o16, residual=res, addend=add)
+    if epi == 4:   # shared GEMM2 + consume over two slots of pair rows
+        rows = (torch.randn(2, M, N, device=dev) * 0.1).to(torch.bfloat16)
+        gates = torch.rand(M, 2, device=dev)
+        run = lambda: ops.gemm_consume(A, B, res, rows, gates, o32, o16)
+    else:
+        run = lambda: ops.gemm(epi, A, B, out_f32=o32, out_bf16=o16, residual=res)
     for _ in range(3):
         run()
     ts = []
