@@ -129,8 +129,8 @@ int dice_route_permute(const int32_t* ids, const uint8_t* active, int64_t n, int
                        int32_t* row_pair, void* stream);
 
 /* Router + conditional-communication decision + token permute in ONE launch
- * (single-GPU engine, E = 8, k <= 8): dice_gate_topk(_decide) (decide = 0 / 1)
- * whose blocks of 32 tokens also group their active pairs by expert and copy
+ * (single-GPU engine, E = 8 or 16, k <= E): dice_gate_topk(_decide) (decide = 0 / 1)
+ * whose blocks of 256/E tokens also group their active pairs by expert and copy
  * the tokens' rows, rounded to bf16 from the fp32 u (the bits the local GEMM
  * stores as its bf16 output), to their permuted rows. Expert e owns rows
  * [e*cap, (e+1)*cap) of x_perm (bf16 [E*cap, hp], cap >= n, a multiple of

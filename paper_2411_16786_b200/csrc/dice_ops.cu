@@ -322,37 +322,41 @@ __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, i
     decide_token(t, k, ids, d);
 }
 
-// E = 8: warp per FOUR rows. Each W_gate float4 (4 columns of one expert) now
-// feeds four rows (two FFMA2 row pairs), halving the L1 wavefronts per row, and
-// the 4 x 8 partial logits transpose-reduce to exactly one (row, expert) per
-// lane (lane = 8 row + e). Rows are loaded in CH-chunk batches. One block = 8
-// warps = 32 tokens. With r.x_perm set, the block also permutes its pairs
-// (RouteArgs); the bf16 rows are staged in dynamic shared memory.
-template <int CH>
+// Router, warp per RPW = 32 / E rows (E = 8: four rows, E = 16: two). Each
+// W_gate float4 (4 columns of one expert) feeds the warp's rows as FFMA2 row
+// pairs (E = 8: halving the L1 wavefronts per row), and the RPW x E partial
+// logits transpose-reduce to exactly one (row, expert) per lane
+// (lane = E row + e). Rows are loaded in CH-chunk batches. One block = 8
+// warps = TPB = 8 RPW tokens. With r.x_perm set, the block also permutes its
+// pairs (RouteArgs); the bf16 rows are staged in dynamic shared memory.
+template <int E, int CH>
 __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
     const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
     int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
     int32_t* status, int step, int layer, const DecideArgs d, const RouteArgs r) {
-  extern __shared__ __align__(16) uint16_t s_rows[];   // [32, hp] bf16 (routing only)
-  __shared__ int s_wcnt[8][8];       // per (warp, expert): count, then exclusive prefix
-  __shared__ int s_base[8];
-  __shared__ int s_tot[8];
+  static_assert(E == 8 || E == 16, "router handles E = 8 or 16");
+  constexpr int RPW = 32 / E;            // rows per warp
+  constexpr int NP = RPW / 2;            // FFMA2 row pairs per warp
+  constexpr int TPB = 8 * RPW;           // tokens per block
+  extern __shared__ __align__(16) uint16_t s_rows[];   // [TPB, hp] bf16 (routing only)
+  __shared__ int s_wcnt[8][E];       // per (warp, expert): count, then exclusive prefix
+  __shared__ int s_base[E];
+  __shared__ int s_tot[E];
   __shared__ int s_fin;
-  __shared__ int s_pos[32 * 8];
+  __shared__ int s_pos[TPB * E];
   __shared__ unsigned long long s_red[2];
   const bool route = r.x_perm != nullptr;    // block-uniform
   if (route) {
-    if (threadIdx.x < 64) s_wcnt[threadIdx.x >> 3][threadIdx.x & 7] = 0;
+    for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) s_wcnt[i / E][i % E] = 0;
     if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
   }
   pdl_enter();
-  constexpr int E = 8;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t q = (int64_t)blockIdx.x * 8 + warp;   // this warp's quad of tokens
-  const int64_t t0 = 4 * q;
-  const int row = lane >> 3;             // 0..3
-  const int e_me = lane & 7;             // expert held by this lane after the reduce
+  const int64_t q = (int64_t)blockIdx.x * 8 + warp;   // this warp's group of rows
+  const int64_t t0 = RPW * q;
+  const int row = lane / E;              // 0..RPW-1
+  const int e_me = lane % E;             // expert held by this lane after the reduce
   const int64_t t = t0 + row;
   const bool row_ok = t < n;
   const int slot = e_me;
@@ -368,19 +372,21 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
       d_red = d.reduced[t * k + slot];
       if (d.strict) d_cid = d.cached_ids[t * k + slot];
     }
-    const float* rp[4];
+    const float* rp[RPW];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) rp[i] = u + (t0 + i < n ? t0 + i : t0) * hp;
-    float2 a01[E], a23[E];
+    for (int i = 0; i < RPW; ++i) rp[i] = u + (t0 + i < n ? t0 + i : t0) * hp;
+    float2 acc[NP][E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) { a01[e] = make_float2(0.f, 0.f); a23[e] = a01[e]; }
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[pp][e] = make_float2(0.f, 0.f);
     for (int base = 0; base < hp; base += 128 * CH) {
-      float4 x[4][CH];
+      float4 x[RPW][CH];
 #pragma unroll
       for (int j = 0; j < CH; ++j) {
         const int c = base + 128 * j + lane * 4;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < RPW; ++i)
           x[i][j] = c < hp ? ldg_stream_f4(rp[i] + c)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -390,50 +396,56 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
         if (c >= hp) break;
         if (route) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < RPW; ++i) {
             __nv_bfloat162 lo = __floats2bfloat162_rn(x[i][j].x, x[i][j].y);
             __nv_bfloat162 hi = __floats2bfloat162_rn(x[i][j].z, x[i][j].w);
-            *reinterpret_cast<uint2*>(s_rows + (int64_t)(warp * 4 + i) * hp + c) =
+            *reinterpret_cast<uint2*>(s_rows + (int64_t)(warp * RPW + i) * hp + c) =
                 make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
           }
         }
-        const float2 p0 = make_float2(x[0][j].x, x[1][j].x), p1 = make_float2(x[0][j].y, x[1][j].y);
-        const float2 p2 = make_float2(x[0][j].z, x[1][j].z), p3 = make_float2(x[0][j].w, x[1][j].w);
-        const float2 r0 = make_float2(x[2][j].x, x[3][j].x), r1 = make_float2(x[2][j].y, x[3][j].y);
-        const float2 r2 = make_float2(x[2][j].z, x[3][j].z), r3 = make_float2(x[2][j].w, x[3][j].w);
+        float2 p[NP][4];
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          const float4 a = x[2 * pp][j], b = x[2 * pp + 1][j];
+          p[pp][0] = make_float2(a.x, b.x); p[pp][1] = make_float2(a.y, b.y);
+          p[pp][2] = make_float2(a.z, b.z); p[pp][3] = make_float2(a.w, b.w);
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const float4 w = __ldg(reinterpret_cast<const float4*>(wt + (int64_t)e * hp + c));
-          a01[e] = __ffma2_rn(p0, make_float2(w.x, w.x), a01[e]);
-          a23[e] = __ffma2_rn(r0, make_float2(w.x, w.x), a23[e]);
-          a01[e] = __ffma2_rn(p1, make_float2(w.y, w.y), a01[e]);
-          a23[e] = __ffma2_rn(r1, make_float2(w.y, w.y), a23[e]);
-          a01[e] = __ffma2_rn(p2, make_float2(w.z, w.z), a01[e]);
-          a23[e] = __ffma2_rn(r2, make_float2(w.z, w.z), a23[e]);
-          a01[e] = __ffma2_rn(p3, make_float2(w.w, w.w), a01[e]);
-          a23[e] = __ffma2_rn(r3, make_float2(w.w, w.w), a23[e]);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) acc[pp][e] = __ffma2_rn(p[pp][0], make_float2(w.x, w.x), acc[pp][e]);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) acc[pp][e] = __ffma2_rn(p[pp][1], make_float2(w.y, w.y), acc[pp][e]);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) acc[pp][e] = __ffma2_rn(p[pp][2], make_float2(w.z, w.z), acc[pp][e]);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) acc[pp][e] = __ffma2_rn(p[pp][3], make_float2(w.w, w.w), acc[pp][e]);
         }
       }
     }
-    float a[32];
+    float a[32];                           // index = row * E + e
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      a[e] = a01[e].x; a[8 + e] = a01[e].y; a[16 + e] = a23[e].x; a[24 + e] = a23[e].y;
-    }
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        a[(2 * pp) * E + e] = acc[pp][e].x;
+        a[(2 * pp + 1) * E + e] = acc[pp][e].y;
+      }
     tr_level<32>(a, lane, 16); tr_level<16>(a, lane, 8); tr_level<8>(a, lane, 4);
     tr_level<4>(a, lane, 2); tr_level<2>(a, lane, 1);
-    const float logit = a[0];              // row (lane >> 3), expert (lane & 7)
+    const float logit = a[0];              // row (lane / E), expert (lane % E)
     const bool bad = !isfinite(logit) && row_ok;
     if (__any_sync(0xffffffffu, bad) && lane == 0) record_nonfinite(status, step, layer);
     float mx = logit;
 #pragma unroll
-    for (int off = 1; off < 8; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    for (int off = 1; off < E; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     const float ex = expf(logit - mx);
     float sum = ex;
 #pragma unroll
-    for (int off = 1; off < 8; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    for (int off = 1; off < E; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
     const float sc = ex / sum;
-    const int rowbase = row * 8;
+    const int rowbase = row * E;
     int rank = 0;
 #pragma unroll
     for (int qe = 0; qe < E; ++qe) {
@@ -441,14 +453,14 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
       rank += (sq > sc) || (sq == sc && qe < e_me);
     }
     if (scores != nullptr && row_ok) scores[t * E + e_me] = sc;
-    const unsigned rowmask = 0xFFu << rowbase;
+    const unsigned rowmask = (E == 32 ? 0xFFFFFFFFu : ((1u << E) - 1u)) << rowbase;
     float psum = 0.f, my_s = 0.f;
     for (int j = 0; j < k; ++j) {
       const unsigned m = __ballot_sync(0xffffffffu, rank == j) & rowmask;
       const int src = __ffs(m) - 1;
       const float sj = __shfl_sync(0xffffffffu, sc, src);
       psum += sj;
-      if (slot == j) { my_s = sj; my_e = src & 7; }
+      if (slot == j) { my_s = sj; my_e = src % E; }
     }
     if (slot < k && row_ok) {
       ids[t * k + slot] = my_e;
@@ -495,17 +507,17 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
     if (lane == 0 && nr) atomicAdd(&s_red[1], (unsigned long long)nr);
   }
   __syncthreads();
-  {
-    // warp w owns expert w: the block's count of the expert (exclusive prefix
-    // over the 8 warps back into s_wcnt) and ONE atomic add on the expert's
-    // row counter, whose return value is the block's offset in the region.
-    // Blocks take their offsets in arrival order, so the order of rows within
-    // an expert region varies between launches; every row's expert-FFN output
-    // depends on that row alone, so no value does. (Offsets in block order
-    // need the predecessors' counts: a look-back chain measured 14 us slower
-    // at 8192 rows, a grid-wide count barrier 5 us slower and only valid
-    // while every block is resident.)
-    const int e = warp;
+#pragma unroll
+  for (int e = warp; e < E; e += 8) {
+    // warp w owns experts w, w + 8, ...: the block's count of the expert
+    // (exclusive prefix over the 8 warps back into s_wcnt) and ONE atomic add
+    // on the expert's row counter, whose return value is the block's offset in
+    // the region. Blocks take their offsets in arrival order, so the order of
+    // rows within an expert region varies between launches; every row's
+    // expert-FFN output depends on that row alone, so no value does. (Offsets
+    // in block order need the predecessors' counts: a look-back chain measured
+    // 14 us slower at 8192 rows, a grid-wide count barrier 5 us slower and
+    // only valid while every block is resident.)
     const int c = lane < 8 ? s_wcnt[lane][e] : 0;
     int inc = c;
 #pragma unroll
@@ -513,10 +525,10 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
       const int y = __shfl_up_sync(0xffffffffu, inc, off);
       if (lane >= off) inc += y;
     }
-    const unsigned acc = (unsigned)__shfl_sync(0xffffffffu, inc, 7);
+    const unsigned acc_e = (unsigned)__shfl_sync(0xffffffffu, inc, 7);
     if (lane < 8) s_wcnt[lane][e] = inc - c;
     unsigned base = 0;
-    if (lane == 0 && acc) base = atomicAdd(&r.state[1 + e], acc);
+    if (lane == 0 && acc_e) base = atomicAdd(&r.state[1 + e], acc_e);
     if (lane == 0) s_base[e] = (int)(e * r.cap) + (int)base;
   }
   __syncthreads();
@@ -524,9 +536,9 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
     const int p = valid ? s_base[my_e] + s_wcnt[warp][my_e] + rank_in_warp : -1;
     r.pos[t * k + slot] = p;
     if (valid) r.row_pair[p] = (int32_t)(t * k + slot);
-    s_pos[(warp * 4 + row) * k + slot] = p;
+    s_pos[(warp * RPW + row) * k + slot] = p;
   } else if (slot < k) {
-    s_pos[(warp * 4 + row) * k + slot] = -1;
+    s_pos[(warp * RPW + row) * k + slot] = -1;
   }
   // the staged rows were written through the generic proxy; the bulk copies
   // below read them through the async proxy
@@ -535,7 +547,7 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
   // copy the staged bf16 rows to their permuted positions: one bulk async
   // copy (TMA engine, smem -> global) per active pair, issued by one thread
   // per pair; the issuing threads wait until their copies have read smem
-  for (int qq = threadIdx.x; qq < 32 * k; qq += blockDim.x) {
+  for (int qq = threadIdx.x; qq < TPB * k; qq += blockDim.x) {
     const int p = s_pos[qq];
     if (p < 0) continue;
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
@@ -579,154 +591,6 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
   if (threadIdx.x <= E) r.state[threadIdx.x] = 0;
 }
 
-// Warp per row pair, no shared-memory prologue: W_gate is read through L1
-// (37 KB per SM, coalesced 512-byte lines per expert), every lane issues all of
-// its 16-byte row loads before any math (u was just written by the local_block
-// GEMM and is L2-resident), and 2 x 16 lanes finish the rows' softmax / top-k.
-// d.on: the token's conditional-communication state is prefetched alongside
-// the row loads and its decision (decide_token's semantics) is taken by the k
-// slot lanes right after the top-k, so the decision adds no memory round trip.
-template <int E, int CH, int MINB>
-__global__ void __launch_bounds__(256, MINB) gate_topk_fast_kernel(
-    const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
-    int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
-    int32_t* status, int step, int layer, const DecideArgs d) {
-  pdl_enter();
-  static_assert(E == 8 || E == 16, "fast gate handles E = 8 or 16");
-  constexpr int V = 2 * E;
-  constexpr int DUP = E == 8 ? 2 : 1;   // lanes holding the same (row, expert)
-  const int lane = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  const int64_t pairs = (n + 1) / 2;
-  for (int64_t q = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5); q < pairs;
-       q += (int64_t)gridDim.x * warps) {
-    const int64_t t0 = 2 * q;
-    const bool has1 = t0 + 1 < n;
-    const int row = lane >> 4;                      // 0 or 1
-    const int64_t t = t0 + row;
-    const bool row_ok = row == 0 || has1;
-    const int slot = lane & 15;
-    // decision state prefetch (independent of the gate)
-    int32_t d_last = 0, d_cid = -1;
-    uint8_t d_primed = 1, d_red = 0;
-    const bool d_lane = d.on && d.strategy != DICE_COND_OFF && row_ok && slot < k;
-    if (d_lane) {
-      d_last = d.last[t];
-      d_primed = d.primed[t];
-      d_red = d.reduced[t * k + slot];
-      if (d.strict) d_cid = d.cached_ids[t * k + slot];
-    }
-    const float* r0 = u + t0 * hp;
-    const float* r1 = u + (has1 ? t0 + 1 : t0) * hp;
-    float a[32];
-    float2 acc[E];   // (row 0, row 1) partial logits per expert, packed FFMA2
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
-    for (int base = 0; base < hp; base += 128 * CH) {
-      float4 xs[CH], ys[CH];
-#pragma unroll
-      for (int j = 0; j < CH; ++j) {
-        const int c = base + 128 * j + lane * 4;
-        if (c < hp) {
-          xs[j] = __ldg(reinterpret_cast<const float4*>(r0 + c));
-          ys[j] = __ldg(reinterpret_cast<const float4*>(r1 + c));
-        } else {
-          xs[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          ys[j] = xs[j];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < CH; ++j) {
-        const int c = base + 128 * j + lane * 4;
-        if (c >= hp) break;
-        const float4 x = xs[j], y = ys[j];
-        const float2 p0 = make_float2(x.x, y.x), p1 = make_float2(x.y, y.y);
-        const float2 p2 = make_float2(x.z, y.z), p3 = make_float2(x.w, y.w);
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const float4 w = __ldg(reinterpret_cast<const float4*>(wt + (int64_t)e * hp + c));
-          acc[e] = __ffma2_rn(p0, make_float2(w.x, w.x), acc[e]);
-          acc[e] = __ffma2_rn(p1, make_float2(w.y, w.y), acc[e]);
-          acc[e] = __ffma2_rn(p2, make_float2(w.z, w.z), acc[e]);
-          acc[e] = __ffma2_rn(p3, make_float2(w.w, w.w), acc[e]);
-        }
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) { a[e] = acc[e].x; a[E + e] = acc[e].y; }
-#pragma unroll
-    for (int i = 2 * E; i < 32; ++i) a[i] = 0.f;
-    // transpose-reduce: V values -> 1 value per lane
-    if constexpr (V == 32) {
-      tr_level<32>(a, lane, 16); tr_level<16>(a, lane, 8); tr_level<8>(a, lane, 4);
-      tr_level<4>(a, lane, 2); tr_level<2>(a, lane, 1);
-    } else {
-      tr_level<16>(a, lane, 16); tr_level<8>(a, lane, 8); tr_level<4>(a, lane, 4);
-      tr_level<2>(a, lane, 2);
-      a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
-    }
-    const float logit = a[0];
-    const int e_me = (lane & 15) / DUP;             // expert held by this lane
-    // non-finite MoE input shows up as a non-finite logit (model.py:212-213)
-    const bool bad = !isfinite(logit) && row_ok;
-    if (__any_sync(0xffffffffu, bad) && lane == 0) record_nonfinite(status, step, layer);
-    // softmax within the row group (offsets 1..8 cover the 16 lanes of a row)
-    float mx = logit;
-#pragma unroll
-    for (int off = DUP; off < 16; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const float ex = expf(logit - mx);
-    float sum = ex;
-#pragma unroll
-    for (int off = DUP; off < 16; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-    const float sc = ex / sum;
-    // rank = #experts with a higher score, or an equal score and a lower id
-    const int rowbase = row * 16;
-    int rank = 0;
-#pragma unroll
-    for (int qe = 0; qe < E; ++qe) {
-      const float sq = __shfl_sync(0xffffffffu, sc, rowbase + qe * DUP);
-      rank += (sq > sc) || (sq == sc && qe < e_me);
-    }
-    const bool primary = (lane % DUP) == 0;
-    if (scores != nullptr && primary && row_ok) scores[t * E + e_me] = sc;
-    const unsigned rowmask = row == 0 ? 0x0000ffffu : 0xffff0000u;
-    float psum = 0.f, my_s = 0.f;
-    int my_e = 0;
-    for (int j = 0; j < k; ++j) {
-      const unsigned m = __ballot_sync(0xffffffffu, primary && rank == j) & rowmask;
-      const int src = __ffs(m) - 1;
-      const float sj = __shfl_sync(0xffffffffu, sc, src);
-      psum += sj;
-      if (slot == j) { my_s = sj; my_e = (src & 15) / DUP; }
-    }
-    if (slot < k && row_ok) {
-      ids[t * k + slot] = my_e;
-      gates[t * k + slot] = my_s / psum;
-    }
-    if (d.on && slot < k && row_ok) {
-      // TokenCache.decide for (t, slot) (policies.py:159-186; decide_token)
-      if (d.strategy == DICE_COND_OFF) {
-        d.active[t * k + slot] = 1;
-        d.write[t * k + slot] = 0;
-      } else {
-        const bool due = d.force || !d_primed || (step - d_last) >= d.R;
-        bool red = d_red != 0;
-        if (due) {
-          if (d.strategy == DICE_COND_LOW_SCORE) red = slot >= 1;
-          else if (d.strategy == DICE_COND_HIGH_SCORE) red = slot == 0;
-          else red = slot != (int)(splitmix_at(d.key, (uint64_t)t + 1) % (uint64_t)k);
-          d.reduced[t * k + slot] = red;
-          if (slot == 0) { d.last[t] = step; d.primed[t] = 1; }
-        }
-        bool act = !red || due;
-        bool wr = red && due;
-        if (d.strict && red && !due && my_e != d_cid) { act = true; wr = true; }
-        d.active[t * k + slot] = act;
-        d.write[t * k + slot] = wr;
-      }
-    }
-  }
-}
 
 // ------------------------------------------------------------- permute
 // Pairs are visited in token-major order p = t*k + s; within an expert the
@@ -1277,38 +1141,31 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
                      const RouteArgs& ra = RouteArgs{}) {
   if (E < 1 || E > 64 || k < 1 || k > E || hp % 64 != 0) return DICE_ERR_CONTRACT;
   if (n == 0) return DICE_OK;
-  // the fused permute lives in the E = 8 row-quad kernel only
-  if (ra.x_perm != nullptr && (E != 8 || k > 8)) return DICE_ERR_CONTRACT;
+  // the fused permute lives in the E = 8 / 16 router kernel only
+  if (ra.x_perm != nullptr && ((E != 8 && E != 16) || k > E)) return DICE_ERR_CONTRACT;
   const size_t smem = (size_t)E * hp * sizeof(float);
   const int threads = 512;
   int64_t want = ((n + 1) / 2 + 15) / 16;
   if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
-  if (E == 8 && k <= 8) {
-    const int64_t gw = ((n + 3) / 4 + 7) / 8;     // 8 warps per block, four rows each
+  if ((E == 8 || E == 16) && k <= E) {
+    // 8 warps per block: four rows per warp at E = 8, two at E = 16
+    const int rpw = 32 / E;
+    const int64_t gw = ((n + rpw - 1) / rpw + 7) / 8;
     const int grid = (int)(gw < 1 ? 1 : gw);
-    const size_t rsmem = ra.x_perm != nullptr ? (size_t)32 * hp * sizeof(uint16_t) : 0;
+    const size_t rsmem = ra.x_perm != nullptr ? (size_t)8 * rpw * hp * sizeof(uint16_t) : 0;
+    auto kern = E == 8 ? gate4_topk_kernel<8, 3> : gate4_topk_kernel<16, 3>;
     if (rsmem > 0) {
-      static size_t attr = 0;
-      if (rsmem > attr) {
-        if (cudaFuncSetAttribute(gate4_topk_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)rsmem) != cudaSuccess)
+      static size_t attr[2] = {0, 0};
+      size_t& a = attr[E == 8 ? 0 : 1];
+      if (rsmem > a) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem) !=
+            cudaSuccess)
           return DICE_ERR_CUDA;
-        attr = rsmem;
+        a = rsmem;
       }
     }
-    launch_pdl(gate4_topk_kernel<3>, dim3(grid), dim3(256), rsmem, s, u, w_gate_t, n, hp, k, ids,
-               gates, scores, status, step, layer, d, ra);
-    return launch_ok();
-  }
-  if (E == 16 && k <= 16) {
-    const int64_t gw = ((n + 1) / 2 + 7) / 8;     // 8 warps per block, a row pair each
-    const int grid = (int)(gw < 1 ? 1 : gw);
-    if (hp / 128 <= 9)   // 16-byte loads in flight per lane and row
-      launch_pdl(gate_topk_fast_kernel<16, 9, 2>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp,
-                 k, ids, gates, scores, status, step, layer, d);
-    else
-      launch_pdl(gate_topk_fast_kernel<16, 4, 2>, dim3(grid), dim3(256), 0, s, u, w_gate_t, n, hp,
-                 k, ids, gates, scores, status, step, layer, d);
+    launch_pdl(kern, dim3(grid), dim3(256), rsmem, s, u, w_gate_t, n, hp, k, ids, gates, scores,
+               status, step, layer, d, ra);
     return launch_ok();
   }
   const int grid = (int)(want < 2 * 148 ? (want < 1 ? 1 : want) : 2 * 148);
@@ -1356,10 +1213,10 @@ int dice_gate_topk_decide(const float* u, const float* w_gate_t, int64_t n, int 
 }
 
 int64_t dice_gate_route_state_words(int64_t n) {
-  // finished-block ticket + 8 per-expert row counters (uint32), zero between
-  // launches (the last block resets them)
+  // finished-block ticket + up to 16 per-expert row counters (uint32), zero
+  // between launches (the last block resets them)
   (void)n;
-  return 5;
+  return 9;
 }
 
 int dice_gate_route(const float* u, const float* w_gate_t, int64_t n, int hp, int E, int k,
@@ -1371,10 +1228,10 @@ int dice_gate_route(const float* u, const float* w_gate_t, int64_t n, int hp, in
                     int32_t* row_pair, int32_t* tile_offsets, int64_t* counters, int devices,
                     int64_t rows_total, uint64_t* route_state, void* stream) {
   if (decide && (refresh_interval < 1 || strategy < 0 || strategy > 3)) return DICE_ERR_CONFIG;
-  if (E != 8 || k < 1 || k > 8 || x_perm == nullptr || pos == nullptr || row_pair == nullptr ||
+  if ((E != 8 && E != 16) || k < 1 || k > E || x_perm == nullptr || pos == nullptr || row_pair == nullptr ||
       tile_offsets == nullptr || counters == nullptr || route_state == nullptr || cap < n ||
       cap % kRowTileR != 0 || devices < 1 || E % devices != 0 || rows_total < 1 ||
-      32 * (int64_t)hp * 2 > 200 * 1024 || cap * E > INT32_MAX)
+      (int64_t)(256 / E) * hp * 2 > 200 * 1024 || cap * E > INT32_MAX)
     return DICE_ERR_CONTRACT;
   if (n == 0) {
     cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (E + 1), (cudaStream_t)stream);

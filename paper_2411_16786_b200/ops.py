@@ -126,7 +126,7 @@ def gate_route(u32, w_gate_t, k, ids, gates, x_perm, cap, pos, row_pair, tile_of
                state, scores=None, status=None, step=0, layer=0, decide=None, devices=1,
                rows_total=None):
     """Gate + conditional-communication decision + token permute in one launch
-    (E = 8): x_perm bf16 [E*cap, hp], expert e's rows from e*cap (dice_gate_route)."""
+    (E = 8 or 16): x_perm bf16 [E*cap, hp], expert e's rows from e*cap (dice_gate_route)."""
     n, hp = u32.shape
     E = w_gate_t.shape[0]
     _need(u32, torch.float32, "gate u")

@@ -193,10 +193,10 @@ class DeviceRunner:
         hp, ep = model.hp, model.ep
         self.n, self.k, self.E, self.S, self.hp, self.ep = n, k, E, S, hp, ep
         self.max_rows = ops.permute_max_rows(n, k, E)
-        # E = 8: the gate launch also permutes (dice_gate_route); expert e's
-        # rows live in a capacity region of cap rows (>= n: a token routes to
-        # an expert at most once)
-        self.fused_route = E == 8 and k <= 8
+        # E = 8 / 16: the gate launch also permutes (dice_gate_route); expert
+        # e's rows live in a capacity region of cap rows (>= n: a token routes
+        # to an expert at most once)
+        self.fused_route = E in (8, 16) and k <= E
         self.cap = (n + 255) // 256 * 256
         perm_rows = max(E * self.cap, self.max_rows) if self.fused_route else self.max_rows
         f32, bf = torch.float32, torch.bfloat16

@@ -278,19 +278,20 @@ def test_gemm_rejects_internal_epilogue_kinds():
             ops.gemm(epi, A, B, out_bf16=o)
 
 
-@pytest.mark.parametrize("n,k,devices,decide", [(8192, 2, 2, True), (1000, 2, 1, False),
-                                                (777, 1, 4, True), (300, 4, 8, False),
-                                                (37, 3, 1, True), (20000, 2, 1, True)])
-def test_gate_route_matches_gate_then_permute(n, k, devices, decide):
+@pytest.mark.parametrize("E,n,k,devices,decide", [
+    (8, 8192, 2, 2, True), (8, 1000, 2, 1, False), (8, 777, 1, 4, True), (8, 300, 4, 8, False),
+    (8, 37, 3, 1, True), (8, 20000, 2, 1, True), (16, 8192, 2, 8, True), (16, 1001, 2, 1, False),
+    (16, 333, 5, 4, True), (16, 17, 16, 2, True), (16, 20000, 2, 1, True)])
+def test_gate_route_matches_gate_then_permute(E, n, k, devices, decide):
     """dice_gate_route (gate + decide + permute in one launch, expert regions of
     cap rows) == dice_gate_topk(_decide) + dice_route_permute: ids, gates, masks,
     run counters and tile offsets identical; every expert region holds exactly
     the expert's active pairs (blocks take their offsets in arrival order, in
     pair order within a block), each row the pair's bf16 row, row_pair the
     inverse of pos, padding rows map to no pair. Repeated launches (counters
-    reset by the last block) agree; 20000 rows = 625 blocks, more than one
-    resident wave."""
-    E, hp = 8, 256
+    reset by the last block) agree; 20000 rows = 625 (E = 8) / 1250 (E = 16)
+    blocks, more than one resident wave."""
+    hp = 256 if E == 8 else 320
     g = torch.Generator(device=dev).manual_seed(n + k)
     u = torch.randn(n, hp, device=dev, generator=g)
     wg = torch.randn(E, hp, device=dev, generator=g) * 0.1
