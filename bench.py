@@ -344,6 +344,13 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
       local_gemm      2Rh^2;  shared_gemm1 / shared_gemm2_consume 2RhSe each;  grouped_ffn 4heP
       (grouped_ffn+shared_gemm1: the expert FFN launches that also carry the stage's
        shared GEMM1, 4heP + 2RhSe)
+    A GEMM also moves algorithmic bytes (operands once, epilogue inputs / outputs):
+      local_gemm      2Rh (A) + 2h^2 (W_mix) + 4Rh (residual) + 6Rh (u f32 + bf16)
+      shared_gemm1    2Rh + 2hSe + 2RSe
+      shared_gemm2_consume  2RSe + 2hSe + 4Rh (u) + 2kRh (token-cache rows) + 4Rk + 6Rh
+      grouped_ffn     2hP + 2Ehe + 2eP (GEMM1) + 2eP + 2Ehe + 2hP + 8P (GEMM2)
+    and is bound by whichever roofline takes longer: `bound` names it, `frac` is the
+    binding roofline's time over the measured time (tensor_frac / hbm_frac: each one).
     """
     import torch
     r = D.DeviceRunner(model, x0, D.Strategy.INTERWEAVED, policy, cluster, seed, time_ops=True,
@@ -376,27 +383,44 @@ def op_breakdown(D, model, x0, policy, cluster, seed, cfg, args):
             work, kind = 14 * R * h, "hbm"
         elif name == "local_gemm":
             work, kind = 2.0 * R * h * h, "tensor"
-        elif name in ("shared_gemm1", "shared_gemm2_consume"):
+            byts = 12.0 * R * h + 2.0 * h * h
+        elif name == "shared_gemm1":
             work, kind = 2.0 * R * h * S * e, "tensor"
+            byts = 2.0 * R * h + 2.0 * h * S * e + 2.0 * R * S * e
+        elif name == "shared_gemm2_consume":
+            work, kind = 2.0 * R * h * S * e, "tensor"
+            byts = 2.0 * R * S * e + 2.0 * h * S * e + 10.0 * R * h + 2.0 * k * R * h + 4.0 * R * k
         elif name.startswith("grouped_ffn"):
             work, kind = 4.0 * h * e * P + (2.0 * R * h * S * e if "shared" in name else 0.0), "tensor"
+            byts = 4.0 * h * P + 4.0 * E * h * e + 4.0 * e * P + 8.0 * P
+            if "shared" in name:
+                byts += 2.0 * R * h + 2.0 * h * S * e + 2.0 * R * S * e
         else:
             continue
-        a = agg.setdefault(name, [0.0, 0, 0.0, kind])
+        if kind == "hbm":
+            byts = work
+        a = agg.setdefault(name, [0.0, 0, 0.0, kind, 0.0])
         a[0] += ms
         a[1] += 1
         a[2] += work
+        a[4] += byts
     total_ms = sum(v[0] for v in agg.values())
     out = {}
-    for name, (ms, calls, work, kind) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
-        rate = work / (ms * 1e-3)
+    for name, (ms, calls, work, kind, byts) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        sec = ms * 1e-3
+        hbm_frac = byts / (hbm * 1e9) / sec
         if kind == "hbm":
-            achieved, unit, peak = rate / 1e9, "GB/s", hbm
-        else:
-            achieved, unit, peak = rate / 1e12, "TFLOP/s", peak_tf
+            out[name] = {"us_per_call": ms * 1e3 / calls, "calls": calls, "share": ms / total_ms,
+                         "bound": "hbm", "achieved": byts / sec / 1e9, "unit": "GB/s",
+                         "peak": hbm, "frac": hbm_frac}
+            continue
+        tensor_frac = work / (peak_tf * 1e12) / sec
+        bound = "hbm" if hbm_frac > tensor_frac else "tensor"
         out[name] = {"us_per_call": ms * 1e3 / calls, "calls": calls, "share": ms / total_ms,
-                     "bound": kind, "achieved": achieved, "unit": unit, "peak": peak,
-                     "frac": achieved / peak}
+                     "bound": bound, "achieved": work / sec / 1e12, "unit": "TFLOP/s",
+                     "peak": peak_tf, "achieved_gbs": byts / sec / 1e9, "hbm_peak": hbm,
+                     "tensor_frac": tensor_frac, "hbm_frac": hbm_frac,
+                     "frac": max(tensor_frac, hbm_frac)}
     return out
 
 
