@@ -242,7 +242,11 @@ struct DecideArgs {
 // depends on another expert's total; the last block writes the 256-row tile
 // prefix and marks the padding rows of every region. Counters: active pairs
 // and remote pairs of the byte plan (cluster.py:75-90).
-constexpr int kRowTileR = 256;   // expert regions padded to the CTA-pair GEMM's 256-row tile
+constexpr int kRowTileR = 256;
+#ifndef DICE_ROUTER_WPB
+#define DICE_ROUTER_WPB 8
+#endif
+constexpr int kRouterWarps = DICE_ROUTER_WPB;   // warps per router block   // expert regions padded to the CTA-pair GEMM's 256-row tile
 
 struct RouteArgs {
   uint16_t* x_perm;             // [E * cap, hp] bf16; null: gate only
@@ -329,17 +333,17 @@ __global__ void cond_decide_kernel(const int32_t* __restrict__ ids, int64_t n, i
 // (lane = E row + e). Rows are loaded in CH-chunk batches. One block = 8
 // warps = TPB = 8 RPW tokens. With r.x_perm set, the block also permutes its
 // pairs (RouteArgs); the bf16 rows are staged in dynamic shared memory.
-template <int E, int CH>
-__global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
+template <int E, int CH, int WPB>
+__global__ void __launch_bounds__(32 * WPB, 2) gate4_topk_kernel(
     const float* __restrict__ u, const float* __restrict__ wt, int64_t n, int hp, int k,
     int32_t* __restrict__ ids, float* __restrict__ gates, float* __restrict__ scores,
     int32_t* status, int step, int layer, const DecideArgs d, const RouteArgs r) {
   static_assert(E == 8 || E == 16, "router handles E = 8 or 16");
   constexpr int RPW = 32 / E;            // rows per warp
   constexpr int NP = RPW / 2;            // FFMA2 row pairs per warp
-  constexpr int TPB = 8 * RPW;           // tokens per block
+  constexpr int TPB = WPB * RPW;         // tokens per block
   extern __shared__ __align__(16) uint16_t s_rows[];   // [TPB, hp] bf16 (routing only)
-  __shared__ int s_wcnt[8][E];       // per (warp, expert): count, then exclusive prefix
+  __shared__ int s_wcnt[WPB][E];     // per (warp, expert): count, then exclusive prefix
   __shared__ int s_base[E];
   __shared__ int s_tot[E];
   __shared__ int s_fin;
@@ -347,13 +351,13 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
   __shared__ unsigned long long s_red[2];
   const bool route = r.x_perm != nullptr;    // block-uniform
   if (route) {
-    for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) s_wcnt[i / E][i % E] = 0;
+    for (int i = threadIdx.x; i < WPB * E; i += blockDim.x) s_wcnt[i / E][i % E] = 0;
     if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
   }
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t q = (int64_t)blockIdx.x * 8 + warp;   // this warp's group of rows
+  const int64_t q = (int64_t)blockIdx.x * WPB + warp;   // this warp's group of rows
   const int64_t t0 = RPW * q;
   const int row = lane / E;              // 0..RPW-1
   const int e_me = lane % E;             // expert held by this lane after the reduce
@@ -508,9 +512,9 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
   }
   __syncthreads();
 #pragma unroll
-  for (int e = warp; e < E; e += 8) {
-    // warp w owns experts w, w + 8, ...: the block's count of the expert
-    // (exclusive prefix over the 8 warps back into s_wcnt) and ONE atomic add
+  for (int e = warp; e < E; e += WPB) {
+    // warp w owns experts w, w + WPB, ...: the block's count of the expert
+    // (exclusive prefix over the warps back into s_wcnt) and ONE atomic add
     // on the expert's row counter, whose return value is the block's offset in
     // the region. Blocks take their offsets in arrival order, so the order of
     // rows within an expert region varies between launches; every row's
@@ -518,15 +522,15 @@ __global__ void __launch_bounds__(256, 2) gate4_topk_kernel(
     // in block order need the predecessors' counts: a look-back chain measured
     // 14 us slower at 8192 rows, a grid-wide count barrier 5 us slower and
     // only valid while every block is resident.)
-    const int c = lane < 8 ? s_wcnt[lane][e] : 0;
+    const int c = lane < WPB ? s_wcnt[lane][e] : 0;
     int inc = c;
 #pragma unroll
-    for (int off = 1; off < 8; off <<= 1) {
+    for (int off = 1; off < WPB; off <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, inc, off);
       if (lane >= off) inc += y;
     }
-    const unsigned acc_e = (unsigned)__shfl_sync(0xffffffffu, inc, 7);
-    if (lane < 8) s_wcnt[lane][e] = inc - c;
+    const unsigned acc_e = (unsigned)__shfl_sync(0xffffffffu, inc, WPB - 1);
+    if (lane < WPB) s_wcnt[lane][e] = inc - c;
     unsigned base = 0;
     if (lane == 0 && acc_e) base = atomicAdd(&r.state[1 + e], acc_e);
     if (lane == 0) s_base[e] = (int)(e * r.cap) + (int)base;
@@ -1148,12 +1152,13 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
   int64_t want = ((n + 1) / 2 + 15) / 16;
   if (smem > 200 * 1024) return DICE_ERR_CONTRACT;
   if ((E == 8 || E == 16) && k <= E) {
-    // 8 warps per block: four rows per warp at E = 8, two at E = 16
+    // kRouterWarps warps per block: four rows per warp at E = 8, two at E = 16
+    constexpr int WPB = kRouterWarps;
     const int rpw = 32 / E;
-    const int64_t gw = ((n + rpw - 1) / rpw + 7) / 8;
+    const int64_t gw = ((n + rpw - 1) / rpw + WPB - 1) / WPB;
     const int grid = (int)(gw < 1 ? 1 : gw);
-    const size_t rsmem = ra.x_perm != nullptr ? (size_t)8 * rpw * hp * sizeof(uint16_t) : 0;
-    auto kern = E == 8 ? gate4_topk_kernel<8, 3> : gate4_topk_kernel<16, 3>;
+    const size_t rsmem = ra.x_perm != nullptr ? (size_t)WPB * rpw * hp * sizeof(uint16_t) : 0;
+    auto kern = E == 8 ? gate4_topk_kernel<8, 3, WPB> : gate4_topk_kernel<16, 3, WPB>;
     if (rsmem > 0) {
       static size_t attr[2] = {0, 0};
       size_t& a = attr[E == 8 ? 0 : 1];
@@ -1164,8 +1169,8 @@ int gate_topk_launch(const float* u, const float* w_gate_t, int64_t n, int hp, i
         a = rsmem;
       }
     }
-    launch_pdl(kern, dim3(grid), dim3(256), rsmem, s, u, w_gate_t, n, hp, k, ids, gates, scores,
-               status, step, layer, d, ra);
+    launch_pdl(kern, dim3(grid), dim3(32 * WPB), rsmem, s, u, w_gate_t, n, hp, k, ids, gates,
+               scores, status, step, layer, d, ra);
     return launch_ok();
   }
   const int grid = (int)(want < 2 * 148 ? (want < 1 ? 1 : want) : 2 * 148);
