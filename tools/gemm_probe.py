@@ -71,6 +71,11 @@ if __name__ == "__main__":
         bench(8192, 4608, 1152, 0, label="8192x4608x1152 epi=0")
         bench(8192, 1152, 2304, 0, label="8192x1152x2304 epi=0")
         raise SystemExit
+    if "--consume" in __import__("sys").argv:
+        for M in (8192, 9472):
+            for epi in (0, 2, 4):
+                bench(M, 1152, 9216, epi, label=f"consume shape M={M} epi={epi}")
+        raise SystemExit
     if "--bn" in __import__("sys").argv:
         bench(16384, 4608, 4608, 0, label="16k x 4608 x 4608")
         bench(16384, 4608, 1152, 0, label="16k x 4608 x 1152")
