@@ -340,8 +340,10 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int num_pairs = gridDim.x >> 1;
   const int n_items = pair < num_tiles ? (num_tiles - 1 - pair) / num_pairs + 1 : 0;
 
+  // producer (warp 0) and MMA issuer (warp 1 of the even CTA): converged
+  // loops, one elected lane issues (elect_one)
   if (warp == 0) {
-    if (lane == 0) {
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0; it < n_items; ++it) {
@@ -358,18 +360,22 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const CUtensorMap* mB = prob == 0 ? &tmB : &tmB2;
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0), C::kStageBytes);
-          tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
+          if (elect_one()) {
+            mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0),
+                                          C::kStageBytes);
+            tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
 #pragma unroll
-          for (int sub = 0; sub < NSUB; ++sub)
-            tma_load_2d_pair(smB + stage * C::kBBytes + sub * C::kSubBBytes, mB, &sh->full[stage],
-                             kb * BK, b_row + sub * BN);
+            for (int sub = 0; sub < NSUB; ++sub)
+              tma_load_2d_pair(smB + stage * C::kBBytes + sub * C::kSubBBytes, mB,
+                               &sh->full[stage], kb * BK, b_row + sub * BN);
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(kPairM, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -385,19 +391,23 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::kABytes);
           const uint32_t b_base = smem_u32(smB + stage * C::kBBytes);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            const uint64_t ad = umma_desc_sw128(a_base + k * UMMA_K * 2);
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              const uint64_t ad = umma_desc_sw128(a_base + k * UMMA_K * 2);
 #pragma unroll
-            for (int sub = 0; sub < NSUB; ++sub)
-              umma_bf16_pair(d_tmem + sub * BN, ad,
-                             umma_desc_sw128(b_base + sub * C::kSubBBytes + k * UMMA_K * 2), idesc,
-                             (kb != k0 || k != 0) ? 1u : 0u);
+              for (int sub = 0; sub < NSUB; ++sub)
+                umma_bf16_pair(d_tmem + sub * BN, ad,
+                               umma_desc_sw128(b_base + sub * C::kSubBBytes + k * UMMA_K * 2),
+                               idesc, (kb != k0 || k != 0) ? 1u : 0u);
+            }
+            umma_commit_pair(&sh->empty[stage]);
           }
-          umma_commit_pair(&sh->empty[stage]);
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit_pair(&sh->tfull[acc]);
+        if (elect_one()) umma_commit_pair(&sh->tfull[acc]);
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {

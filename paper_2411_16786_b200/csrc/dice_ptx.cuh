@@ -101,6 +101,19 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// One lane of the converged warp. The producer and MMA warps run their loops
+// converged and let one elected lane issue: the descriptors then live in
+// uniform registers and the tcgen05.mma / TMA instructions issue back to back
+// (issued from a lane == 0 branch, every instruction was wrapped in an
+// ELECT / R2UR.BROADCAST loop that throttled the MMA issue: 67 % tensor-pipe
+// activity on the N = 1152 GEMMs instead of 94 %).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .b32 r;\n\t.reg .pred e;\n\telect.sync r|e, 0xffffffff;\n\t"
+               "selp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+  return p != 0;
+}
+
 // ----------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
