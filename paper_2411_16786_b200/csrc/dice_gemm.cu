@@ -203,17 +203,15 @@ __device__ __forceinline__ void epilogue_gelu_resid_pf(const GemmArgs& a, const 
 // cta_group::2: a cluster of two CTAs computes a 256 x BN tile. Each CTA
 // stages its own 128 rows of A and half (BN/2 rows) of B, so per-CTA operand
 // traffic per MMA FLOP is 2/3 of the single-CTA 128 x BN tile; the even CTA
-// issues the pair MMAs and both CTAs drain their 128 TMEM lanes.
-// NSUB > 1: a 256 x (NSUB*BN) tile of NSUB accumulators sharing each staged A
-// block (per-SM operand bytes per MMA cycle fall from 8192/BN + 32 to
-// 8192/(NSUB*BN) + 32), single-buffered in TMEM.
-template <int BN, bool DIRECT, int NSUB, bool RESID_PF = false>
+// issues the pair MMAs and both CTAs drain their 128 TMEM lanes. TMEM holds
+// two BN-column accumulators, so the epilogue of tile i overlaps the MMAs of
+// tile i + 1.
+template <int BN, bool DIRECT, bool RESID_PF = false>
 struct PairCfg {
-  static constexpr int kTN = NSUB * BN;
-  static constexpr int kAccBufs = NSUB == 1 ? 2 : 1;
+  static constexpr int kTN = BN;
+  static constexpr int kAccBufs = 2;
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kSubBBytes = (BN / 2) * BK * 2;
-  static constexpr int kBBytes = NSUB * kSubBBytes;
+  static constexpr int kBBytes = (BN / 2) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // bf16-only epilogues store straight from registers (64 contiguous bytes of
   // one row per lane, whole sectors), so their smem goes to the operand ring
@@ -271,7 +269,7 @@ __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_
   for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
 
-template <int BN, int EPI, bool DIRECT, int NSUB>
+template <int BN, int EPI, bool DIRECT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const GemmArgs args, const __grid_constant__ CUtensorMap tmA2,
@@ -280,7 +278,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   // kind runs in the same persistent launch; its tiles follow the first's
   // (one launch and one wave tail for two independent GEMMs)
   constexpr bool kResidPF = EPI == EPI_GELU_RESID;
-  using C = PairCfg<BN, DIRECT, NSUB, kResidPF>;
+  using C = PairCfg<BN, DIRECT, kResidPF>;
   constexpr int TN = C::kTN;
   const int kStages = args.stages;   // <= C::kStages (host-clamped)
   constexpr int kPairM = 2 * BM;
@@ -364,10 +362,7 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0),
                                           C::kStageBytes);
             tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
-#pragma unroll
-            for (int sub = 0; sub < NSUB; ++sub)
-              tma_load_2d_pair(smB + stage * C::kBBytes + sub * C::kSubBBytes, mB,
-                               &sh->full[stage], kb * BK, b_row + sub * BN);
+            tma_load_2d_pair(smB + stage * C::kBBytes, mB, &sh->full[stage], kb * BK, b_row);
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -394,12 +389,9 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k) {
-              const uint64_t ad = umma_desc_sw128(a_base + k * UMMA_K * 2);
-#pragma unroll
-              for (int sub = 0; sub < NSUB; ++sub)
-                umma_bf16_pair(d_tmem + sub * BN, ad,
-                               umma_desc_sw128(b_base + sub * C::kSubBBytes + k * UMMA_K * 2),
-                               idesc, (kb != k0 || k != 0) ? 1u : 0u);
+              umma_bf16_pair(d_tmem, umma_desc_sw128(a_base + k * UMMA_K * 2),
+                             umma_desc_sw128(b_base + k * UMMA_K * 2), idesc,
+                             (kb != k0 || k != 0) ? 1u : 0u);
             }
             umma_commit_pair(&sh->empty[stage]);
           }
@@ -561,14 +553,14 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int EPI, bool DIRECT, int NSUB = 1>
+template <int BN, int EPI, bool DIRECT>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
                 const CUtensorMap* tb2 = nullptr, const GemmArgs* a2 = nullptr) {
-  using C = PairCfg<BN, DIRECT, NSUB, EPI == EPI_GELU_RESID>;
+  using C = PairCfg<BN, DIRECT, EPI == EPI_GELU_RESID>;
   static bool attr_done = false;
   if (!attr_done) {
-    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kSmemBytes) != cudaSuccess)
       return DICE_ERR_CUDA;
     attr_done = true;
@@ -582,22 +574,9 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
   aa.stages = C::kStages;
   GemmArgs bb{};
   if (a2 != nullptr) bb = *a2;
-  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT, NSUB>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
+  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
              ta, tb, aa, a2 != nullptr ? *ta2 : ta, a2 != nullptr ? *tb2 : tb, bb);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
-}
-
-// 256 x 384 tiles (two 192-column accumulators) for N % 384 == 0
-int dispatch_wide(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                  int max_tiles, cudaStream_t s) {
-  switch (epi) {
-    case EPI_STORE_BF16: return launch_pair<192, EPI_STORE_BF16, true, 2>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_BF16: return launch_pair<192, EPI_GELU_BF16, true, 2>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_PAIR: return launch_pair<192, EPI_STORE_PAIR, true, 2>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_SCATTER:
-      return launch_pair<192, EPI_STORE_SCATTER, true, 2>(ta, tb, a, max_tiles, s);
-    default: return DICE_ERR_CONTRACT;
-  }
 }
 
 template <int BN>
@@ -618,33 +597,20 @@ int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
 }  // namespace
 
 struct TileChoice {
-  int bn;        // MMA N per accumulator
-  int tile_n;    // output columns per tile (bn, or 384 for the wide tiles)
-  bool wide;
+  int bn;        // MMA N per accumulator = output columns per tile
+  int tile_n;
 };
 
 // Every GEMM runs on the CTA-pair kernel (256-row tiles: the permute pads
-// expert groups to 256 rows). Tile width: 256 when N allows, else 192 / 128;
-// N = 1152-class long-K bf16 GEMMs take 256 x 384 tiles (measured, XL shapes:
-// 16384x1152x4608 1148 -> 1348 TF/s) when the wave count does not lose what
-// the wider tile gains (its single TMEM buffer exposes each tile's epilogue,
-// so only for the register-direct bf16 epilogues).
+// expert groups to 256 rows) with two TMEM accumulators. Tile width: 256 when
+// N allows, else 192 / 128. (256 x 384 tiles of two accumulators sharing each
+// staged A block won while the MMA issue was the bottleneck; with the
+// converged issue loop the double-buffered 256 x 192 tile is faster at
+// N = 1152: 1452 vs 1370 TF/s at 16384 x 1152 x 4608.)
 TileChoice choose_tile(const GemmProblem& p) {
   TileChoice c{};
   c.bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
-  c.wide = false;
-  if (c.bn == 192 && p.N % 384 == 0) {
-    const int64_t m_tiles = p.group_tile_offsets != nullptr ? p.max_m_tiles : (p.M + 255) / 256;
-    const int pairs = num_sms() / 2;
-    auto wave_eff = [&](int64_t tiles) {
-      return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs);
-    };
-    const bool direct_epi = p.epi_kind == EPI_STORE_BF16 || p.epi_kind == EPI_GELU_BF16 ||
-                            p.epi_kind == EPI_STORE_PAIR || p.epi_kind == EPI_STORE_SCATTER;
-    const double narrow = wave_eff(m_tiles * (p.N / 192));
-    c.wide = direct_epi && p.K >= 2048 && 1.15 * wave_eff(m_tiles * (p.N / 384)) >= narrow;
-  }
-  c.tile_n = c.wide ? 384 : c.bn;
+  c.tile_n = c.bn;
   return c;
 }
 
@@ -675,14 +641,12 @@ int prepare(const GemmProblem& p, const TileChoice& tc, CUtensorMap* ta, CUtenso
 int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   const TileChoice tc = choose_tile(p);
   const int bn = tc.bn;
-  const bool wide = tc.wide;
   CUtensorMap ta, tb;
   GemmArgs a;
   int rc = prepare(p, tc, &ta, &tb, &a);
   if (rc) return rc;
   const int max_tiles = a.num_m_tiles * a.num_n_blocks;
   if (max_tiles == 0) return 0;
-  if (wide) return dispatch_wide(p.epi_kind, ta, tb, a, max_tiles, stream);
   if (bn == 256) return dispatch_pair<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
   if (bn == 192) return dispatch_pair<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
   return dispatch_pair<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
@@ -696,8 +660,7 @@ int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t st
   const TileChoice c1 = choose_tile(p1), c2 = choose_tile(p2);
   const bool ok = p1.K == p2.K && p1.epi_kind == p2.epi_kind &&
                   (p1.epi_kind == EPI_STORE_BF16 || p1.epi_kind == EPI_GELU_BF16) &&
-                  p2.group_tile_offsets == nullptr && !c1.wide &&
-                  !c2.wide && c1.bn == c2.bn &&
+                  p2.group_tile_offsets == nullptr && c1.bn == c2.bn &&
                   (c1.bn == 256 || c1.bn == 192);
   if (!ok) {
     const int rc = gemm_bf16(p1, stream);

@@ -88,7 +88,7 @@ def test_ep_xl_widths_matches_single_gpu(geometry):
     2 shared; 4 layers, 3 steps, full DICE policy; 2 ranks) and at the G-16E2A
     widths (h=1664 padded to 1792, e=6656, 16 experts; 4 ranks of 4 experts):
     the run over peer memory reproduces the single-GPU engine bit-exactly — the
-    bench geometry's tile shapes (256x384 expert GEMM2 with the combine stored
+    bench geometry's tile shapes (256x192 expert GEMM2 with the combine stored
     into the peers' windows by its epilogue, dual GEMM1 launches) on both sides."""
     if geometry == "xl":
         world = 2
