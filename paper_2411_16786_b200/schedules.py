@@ -564,7 +564,17 @@ class DeviceRunner:
                 self._consume(layer, step, self.slot_gen[layer], gemm1_done=merged)
             if self.record_outputs:
                 outputs_here.append(self.h32[:, :cfg.hidden_dim].cpu() if keep else None)
-        self._flush_pending(side=self.strategy is Strategy.INTERWEAVED)
+        if (self.strategy is Strategy.INTERWEAVED and self.pending is not None
+                and step + 1 < cfg.num_steps):
+            # the reference flushes the last layer's dispatch at the end of the
+            # step (schedules.py:443); the combine slot is claimed here, and the
+            # expert FFN itself runs at the next step's first asynchronous stage,
+            # inside that stage's shared-GEMM1 launch (or before a synchronous
+            # stage): the same values, since the FFN depends on the dispatched
+            # rows only and layer L-1 is consumed no earlier than step s+1
+            self._track("c", self.pending.layer)
+        else:
+            self._flush_pending(side=self.strategy is Strategy.INTERWEAVED)
         self._mark(f"denoise s{step}")
         with self._op("denoise", step, -1):
             ops.denoise(self.x32, self.x16, self.h32, cfg.step_size, self.status, step)
