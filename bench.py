@@ -595,6 +595,38 @@ def run_gpu(args):
                                                        / np.linalg.norm(finals["sync"]))
         quality["speedup_dice_vs_sync"] = quality["sync_ms_per_run"] / ms_per_step
         quality["policy_of_value"] = conf["policy"]
+    elif not args.no_quality and world > 1:
+        # the north-star comparison on the same box: the synchronous expert-parallel
+        # path (every stage blocks on its dispatch and combine, schedules.py:319-345)
+        # timed the same way (device events, max over ranks), and the latent MSE of
+        # this run vs it over all ranks' row shards
+        from paper_2411_16786_b200.ep import EPRunner
+        r = EPRunner(model, x0, D.Strategy.SYNCHRONOUS, D.NEUTRAL, cluster, seed, rank=rank,
+                     world=world)
+        if not args.eager:
+            r.capture()
+        final_sync = r.sample(x0_host).clone().numpy().astype(np.float64)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, min(args.steps, 3))
+        ev0.record()
+        for _ in range(reps):
+            r.launch()
+        ev1.record()
+        barrier()
+        r.finish()
+        sync_ms = float(allreduce([ev0.elapsed_time(ev1) / reps], dist.ReduceOp.MAX).item())
+        d = final_dice - final_sync
+        sq = allreduce([float(np.sum(d * d)), float(np.sum(final_sync * final_sync)),
+                        float(d.size)], dist.ReduceOp.SUM)
+        del r
+        torch.cuda.empty_cache()
+        quality = {"sync_ep_ms_per_run": sync_ms,
+                   "dice_latent_mse_vs_sync": float(sq[0] / sq[2]),
+                   "dice_rel_l2_vs_sync": float(np.sqrt(sq[0] / sq[1])),
+                   "speedup_dice_vs_sync": sync_ms / ms_per_step,
+                   "policy_of_value": conf["policy"],
+                   "note": f"synchronous expert parallelism on the same {world} ranks"}
 
     if rank != 0:
         if world > 1:

@@ -85,3 +85,7 @@ def test_gpu_arm_expert_parallel_line():
     assert set(parts) == {"flag_waits", "main_stream_send_and_regroup_kernels",
                           "waits_for_overlapped_sends"}
     assert line["exposed_a2a_us"] >= parts["main_stream_send_and_regroup_kernels"] > 0
+    # the synchronous expert-parallel path timed on the same ranks (north-star ratio)
+    q = line["quality"]
+    assert q["sync_ep_ms_per_run"] > 0 and q["speedup_dice_vs_sync"] > 0
+    assert q["dice_latent_mse_vs_sync"] >= 0
