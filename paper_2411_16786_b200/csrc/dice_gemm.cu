@@ -269,8 +269,12 @@ __device__ __forceinline__ void epilogue_direct(const GemmArgs& a, const uint32_
   for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
 
-template <int BN, int EPI, bool DIRECT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// MC = 2: a cluster of two CTA pairs computes the n-blocks 2j, 2j + 1 of one
+// m-tile; each CTA loads half of the A block both pairs need and TMA-multicasts
+// it to its counterpart in the other pair (L2 reads of A halve), and a ring
+// slot is refilled only after both pairs' MMAs have read it.
+template <int BN, int EPI, bool DIRECT, int MC>
+__global__ void __launch_bounds__(kThreads, 1)
 gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const GemmArgs args, const __grid_constant__ CUtensorMap tmA2,
                const __grid_constant__ CUtensorMap tmB2, const GemmArgs args2) {
@@ -289,14 +293,18 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   float* sm_epi = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
   GemmShared* sh = reinterpret_cast<GemmShared*>(smem + C::kStages * C::kStageBytes + C::kEpiBytes);
 
+  static_assert(MC == 1 || MC == 2, "one or two CTA pairs per cluster");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1;           // CTA within its pair
+  const uint32_t pp = crank >> 1;            // pair within the cluster
+  const uint32_t leader = crank & ~1u;       // the pair's even CTA
 
   // prologue before the programmatic-dependency wait: it touches no memory the
   // stream predecessor writes, so under PDL it overlaps that kernel's tail
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&sh->full[s], 2); mbar_init(&sh->empty[s], 1); }
+    for (int s = 0; s < kStages; ++s) { mbar_init(&sh->full[s], 2); mbar_init(&sh->empty[s], MC); }
     for (int b = 0; b < 2; ++b) { mbar_init(&sh->tfull[b], 1); mbar_init(&sh->tempty[b], 2 * kEpiWarps); }
     fence_barrier_init();
   }
@@ -326,16 +334,21 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int groups = args.group_tile_offsets != nullptr ? args.num_groups : 1;
   const int n_blocks = args.num_n_blocks;
   const int k_blocks = args.num_k_blocks;
-  const int T1 = m_tiles * n_blocks;
-  const int n_blocks2 = args2.num_n_blocks;
-  const int num_tiles = T1 + (args2.num_m_tiles > 0 ? args2.num_m_tiles * n_blocks2 : 0);
-  // tile -> (problem, n block, m tile); N-fastest within each problem
+  // work items: (m tile, MC consecutive n blocks), one n block per pair
+  const int n_units = n_blocks / MC;
+  const int T1 = m_tiles * n_units;
+  const int n_units2 = args2.num_n_blocks / MC;
+  const int num_tiles = T1 + (args2.num_m_tiles > 0 ? args2.num_m_tiles * n_units2 : 0);
+  // item -> (problem, n block, m tile); N-fastest within each problem
   auto locate = [&](int tile, int& prob, int& n_blk, int& m_tile) {
-    if (tile < T1) { prob = 0; n_blk = tile % n_blocks; m_tile = tile / n_blocks; }
-    else { prob = 1; const int t2 = tile - T1; n_blk = t2 % n_blocks2; m_tile = t2 / n_blocks2; }
+    if (tile < T1) { prob = 0; n_blk = (tile % n_units) * MC + pp; m_tile = tile / n_units; }
+    else {
+      prob = 1; const int t2 = tile - T1;
+      n_blk = (t2 % n_units2) * MC + pp; m_tile = t2 / n_units2;
+    }
   };
-  const int pair = blockIdx.x >> 1;
-  const int num_pairs = gridDim.x >> 1;
+  const int pair = blockIdx.x / (2 * MC);         // cluster index
+  const int num_pairs = gridDim.x / (2 * MC);
   const int n_items = pair < num_tiles ? (num_tiles - 1 - pair) / num_pairs + 1 : 0;
 
   // producer (warp 0) and MMA issuer (warp 1 of the even CTA): converged
@@ -359,9 +372,15 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&sh->empty[stage], phase ^ 1);
           if (elect_one()) {
-            mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), 0),
+            mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&sh->full[stage]), leader),
                                           C::kStageBytes);
-            tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
+            if constexpr (MC == 1) {
+              tma_load_2d_pair(smA + stage * C::kABytes, mA, &sh->full[stage], kb * BK, a_row);
+            } else {   // this CTA's half of the A block, to itself and its counterpart
+              tma_load_2d_pair_mc(smA + stage * C::kABytes + pp * (BM / 2) * BK * 2, mA,
+                                  &sh->full[stage], kb * BK, a_row + (int)pp * (BM / 2),
+                                  (uint16_t)((1u << rank) | (1u << (2 + rank))));
+            }
             tma_load_2d_pair(smB + stage * C::kBBytes, mB, &sh->full[stage], kb * BK, b_row);
           }
           __syncwarp();
@@ -393,12 +412,12 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                              umma_desc_sw128(b_base + k * UMMA_K * 2), idesc,
                              (kb != k0 || k != 0) ? 1u : 0u);
             }
-            umma_commit_pair(&sh->empty[stage]);
+            umma_commit_pair(&sh->empty[stage], MC == 1 ? (uint16_t)0x3 : (uint16_t)0xF);
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (elect_one()) umma_commit_pair(&sh->tfull[acc]);
+        if (elect_one()) umma_commit_pair(&sh->tfull[acc], (uint16_t)(0x3u << (2 * pp)));
         __syncwarp();
       }
     }
@@ -408,8 +427,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     float* stage = sm_epi + (warp - 4) * 1024;
     float* rbuf = sm_epi + kEpiWarps * 1024 + (warp - 4) * 1024;   // (kResidPF only)
     const int row_limit = args.group_tile_offsets != nullptr ? INT_MAX : args.M_valid;
-    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), 0);
-    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), 0);
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), leader);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), leader);
     for (int local = 0; local < n_items; ++local) {
       const int tile = pair + local * num_pairs;
       int prob, n_blk, m_tile;
@@ -553,43 +572,65 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int EPI, bool DIRECT>
+// MC: CTA pairs per cluster (2: A multicast across the two pairs of an m-tile;
+// the A tensor map's box is then BM / 2 rows and the n-block counts are even)
+template <int BN, int EPI, bool DIRECT, int MC = 1>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int max_tiles,
                 cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
                 const CUtensorMap* tb2 = nullptr, const GemmArgs* a2 = nullptr) {
   using C = PairCfg<BN, DIRECT, EPI == EPI_GELU_RESID>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(gemm_bf16_pair<BN, EPI, DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::kSmemBytes) != cudaSuccess)
+  auto kern = gemm_bf16_pair<BN, EPI, DIRECT, MC>;
+  constexpr int CL = 2 * MC;               // CTAs per cluster
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) !=
+        cudaSuccess)
       return DICE_ERR_CUDA;
-    attr_done = true;
+    // clusters must fit a GPC: a persistent grid larger than the co-resident
+    // cluster count would run its last clusters as a second wave
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(num_sms() - num_sms() % CL);
+    q.blockDim = dim3(kThreads);
+    q.dynamicSmemBytes = C::kSmemBytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    q.attrs = at;
+    q.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &q) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = num_sms() / CL;
+    }
+    max_clusters = nc;
   }
-  const int items = max_tiles + (a2 != nullptr ? a2->num_m_tiles * a2->num_n_blocks : 0);
-  const int sms = num_sms();
-  int grid = 2 * items < sms ? 2 * items : sms;
-  grid &= ~1;
+  if (a.num_n_blocks % MC != 0 || (a2 != nullptr && a2->num_n_blocks % MC != 0))
+    return DICE_ERR_CONTRACT;
+  const int items = (max_tiles + (a2 != nullptr ? a2->num_m_tiles * a2->num_n_blocks : 0)) / MC;
+  int grid = items < max_clusters ? CL * items : CL * max_clusters;
   if (grid <= 0) return 0;
   GemmArgs aa = a;
   aa.stages = C::kStages;
   GemmArgs bb{};
   if (a2 != nullptr) bb = *a2;
-  launch_pdl(gemm_bf16_pair<BN, EPI, DIRECT>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream,
-             ta, tb, aa, a2 != nullptr ? *ta2 : ta, a2 != nullptr ? *tb2 : tb, bb);
+  launch_pdl_cluster(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, CL, ta, tb, aa,
+                     a2 != nullptr ? *ta2 : ta, a2 != nullptr ? *tb2 : tb, bb);
   return cudaGetLastError() == cudaSuccess ? 0 : DICE_ERR_CUDA;
 }
 
-template <int BN>
+template <int BN, int MC = 1>
 int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                   int max_tiles, cudaStream_t s) {
   switch (epi) {
-    case EPI_STORE_BF16: return launch_pair<BN, EPI_STORE_BF16, true>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_BF16: return launch_pair<BN, EPI_GELU_BF16, true>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_PAIR: return launch_pair<BN, EPI_STORE_PAIR, true>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_SCATTER: return launch_pair<BN, EPI_STORE_SCATTER, true>(ta, tb, a, max_tiles, s);
-    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false>(ta, tb, a, max_tiles, s);
-    case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false>(ta, tb, a, max_tiles, s);
-    case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_BF16: return launch_pair<BN, EPI_STORE_BF16, true, MC>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_BF16: return launch_pair<BN, EPI_GELU_BF16, true, MC>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_PAIR: return launch_pair<BN, EPI_STORE_PAIR, true, MC>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_SCATTER: return launch_pair<BN, EPI_STORE_SCATTER, true, MC>(ta, tb, a, max_tiles, s);
+    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, false, MC>(ta, tb, a, max_tiles, s);
+    case EPI_GELU_RESID: return launch_pair<BN, EPI_GELU_RESID, false, MC>(ta, tb, a, max_tiles, s);
+    case EPI_CONSUME: return launch_pair<BN, EPI_CONSUME, false, MC>(ta, tb, a, max_tiles, s);
     default: return DICE_ERR_CONTRACT;
   }
 }
@@ -599,6 +640,7 @@ int dispatch_pair(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const G
 struct TileChoice {
   int bn;        // MMA N per accumulator = output columns per tile
   int tile_n;
+  int mc;        // CTA pairs per cluster sharing the A block
 };
 
 // Every GEMM runs on the CTA-pair kernel (256-row tiles: the permute pads
@@ -611,6 +653,13 @@ TileChoice choose_tile(const GemmProblem& p) {
   TileChoice c{};
   c.bn = (p.N % 256 == 0) ? 256 : (p.N % 192 == 0 ? 192 : 128);
   c.tile_n = c.bn;
+  // N = 1152-class GEMMs (256 x 192 tiles, an even number of n-blocks): clusters
+  // of two CTA pairs share each A block by TMA multicast. Only 33 clusters of
+  // four fit the GPCs (132 of 148 SMs), but halving the A reads from L2 cuts
+  // enough energy that the power-capped step runs ~5 % higher clocks: +0.8 %
+  // img/s in-step (35.0-35.2 vs 34.8, same box); for the 256 x 256 GEMM1s the
+  // lost SMs weigh more (1370 vs 1477 TF/s) and they stay on pairs
+  c.mc = (c.bn == 192 && ((p.N + c.tile_n - 1) / c.tile_n) % 2 == 0) ? 2 : 1;
   return c;
 }
 
@@ -621,7 +670,7 @@ int prepare(const GemmProblem& p, const TileChoice& tc, CUtensorMap* ta, CUtenso
   if (p.K <= 0 || p.N <= 0 || p.N % 32 != 0 || p.K % 8 != 0) return DICE_ERR_CONTRACT;
   if (p.num_groups < 1 || p.num_groups > kMaxGroups) return DICE_ERR_CONTRACT;
   const int tile_m = 2 * BM;
-  int rc = tensor_map(p.A, p.A_rows, p.K, BM, ta);
+  int rc = tensor_map(p.A, p.A_rows, p.K, BM / tc.mc, ta);
   if (rc) return rc;
   rc = tensor_map(p.B, (int64_t)p.num_groups * p.N, p.K, tc.bn / 2, tb);
   if (rc) return rc;
@@ -647,6 +696,11 @@ int gemm_bf16(const GemmProblem& p, cudaStream_t stream) {
   if (rc) return rc;
   const int max_tiles = a.num_m_tiles * a.num_n_blocks;
   if (max_tiles == 0) return 0;
+  if (tc.mc == 2) {
+    if (bn == 256) return dispatch_pair<256, 2>(p.epi_kind, ta, tb, a, max_tiles, stream);
+    if (bn == 192) return dispatch_pair<192, 2>(p.epi_kind, ta, tb, a, max_tiles, stream);
+    return dispatch_pair<128, 2>(p.epi_kind, ta, tb, a, max_tiles, stream);
+  }
   if (bn == 256) return dispatch_pair<256>(p.epi_kind, ta, tb, a, max_tiles, stream);
   if (bn == 192) return dispatch_pair<192>(p.epi_kind, ta, tb, a, max_tiles, stream);
   return dispatch_pair<128>(p.epi_kind, ta, tb, a, max_tiles, stream);
@@ -660,7 +714,7 @@ int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t st
   const TileChoice c1 = choose_tile(p1), c2 = choose_tile(p2);
   const bool ok = p1.K == p2.K && p1.epi_kind == p2.epi_kind &&
                   (p1.epi_kind == EPI_STORE_BF16 || p1.epi_kind == EPI_GELU_BF16) &&
-                  p2.group_tile_offsets == nullptr && c1.bn == c2.bn &&
+                  p2.group_tile_offsets == nullptr && c1.bn == c2.bn && c1.mc == c2.mc &&
                   (c1.bn == 256 || c1.bn == 192);
   if (!ok) {
     const int rc = gemm_bf16(p1, stream);
@@ -674,10 +728,20 @@ int gemm_bf16_dual(const GemmProblem& p1, const GemmProblem& p2, cudaStream_t st
   if (rc) return rc;
   const int t1 = a1.num_m_tiles * a1.num_n_blocks;
   if (a2.num_m_tiles * a2.num_n_blocks == 0) return gemm_bf16(p1, stream);
+  if (c1.bn == 256 && c1.mc == 2) {
+    return p1.epi_kind == EPI_GELU_BF16
+               ? launch_pair<256, EPI_GELU_BF16, true, 2>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2)
+               : launch_pair<256, EPI_STORE_BF16, true, 2>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2);
+  }
   if (c1.bn == 256) {
     return p1.epi_kind == EPI_GELU_BF16
                ? launch_pair<256, EPI_GELU_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2)
                : launch_pair<256, EPI_STORE_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2);
+  }
+  if (c1.mc == 2) {
+    return p1.epi_kind == EPI_GELU_BF16
+               ? launch_pair<192, EPI_GELU_BF16, true, 2>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2)
+               : launch_pair<192, EPI_STORE_BF16, true, 2>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2);
   }
   return p1.epi_kind == EPI_GELU_BF16
              ? launch_pair<192, EPI_GELU_BF16, true>(ta1, tb1, a1, t1, stream, &ta2, &tb2, &a2)
