@@ -16,7 +16,7 @@ def per_launch(M, N, K, epi, reps=20):
     o16 = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
     o32 = torch.empty(M, N, device=dev) if epi in (2, 3, 4) else None
     res = torch.randn(M, N, device=dev) if epi in (3, 4) else None
-    run = lambda: ops.gemm(epi, A, B, out_f32=o32, out_bf16=o16, residual=res, addend=res)
+    run = lambda: ops.gemm(epi, A, B, out_f32=o32, out_bf16=o16, residual=res)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
@@ -42,4 +42,3 @@ for M in (256, 2048, 8192):
     per_launch(M, 1152, 1152, 0)
 per_launch(8192, 1152, 1152, 3)
 per_launch(8192, 9216, 1152, 1)
-per_launch(8192, 1152, 9216, 4)
