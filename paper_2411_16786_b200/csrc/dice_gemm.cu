@@ -358,10 +358,13 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0; it < n_items; ++it) {
-        // items run last to first: in the dual launch the grouped expert tiles
-        // (whose hbuf the next launch, the expert GEMM2, reads) are written last
-        // and are still in L2 when it starts (+0.2 % img/s, three same-box pairs)
-        const int tile = num_tiles - 1 - (pair + it * num_pairs), k0 = 0, k1 = k_blocks;
+        // the dual launch (expert + shared GEMM1) runs its items last to first:
+        // the grouped expert tiles, whose hbuf the next launch (the expert GEMM2)
+        // reads first-to-last, are written last and are still in L2 when it
+        // starts (+0.2 % img/s over forward order in three same-box pairs, +0.2 %
+        // more over reversing every launch)
+        const int xi = pair + it * num_pairs;
+        const int tile = args2.num_m_tiles > 0 ? num_tiles - 1 - xi : xi, k0 = 0, k1 = k_blocks;
         int prob, n_blk, m_tile;   // N-fastest: resident tiles share A rows
         locate(tile, prob, n_blk, m_tile);
         const int g = prob == 0 ? find_group(sh->group_off, groups, m_tile) : 0;
@@ -433,7 +436,8 @@ gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sh->tempty[0]), leader);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&sh->tempty[1]), leader);
     for (int local = 0; local < n_items; ++local) {
-      const int tile = num_tiles - 1 - (pair + local * num_pairs);   // as the producer
+      const int xl = pair + local * num_pairs;                        // as the producer
+      const int tile = args2.num_m_tiles > 0 ? num_tiles - 1 - xl : xl;
       int prob, n_blk, m_tile;
       locate(tile, prob, n_blk, m_tile);
       const GemmArgs& ar = prob == 0 ? args : args2;
